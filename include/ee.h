@@ -1,0 +1,183 @@
+/*
+ * ee.h — C-ABI of libee.so, the B200 (sm_100a) early-exit hot path.
+ *
+ * The drop-in boundary for the reference's kernel plugin `eepipe.kernels`
+ * (`pkg/src/eepipe/kernels.py:1-41`) and for the raw-array inference math that
+ * the reference keeps outside that module (`eepipe/inference.py:118-229`).
+ * Granularity is fused hot-path ops rather than the reference's 11 float64
+ * micro-kernels; each entry point names the reference function(s) it
+ * replaces.
+ *
+ * Conventions:
+ *  - every pointer argument is a DEVICE pointer owned by the caller unless
+ *    stated; no allocation happens inside the library; workspaces are
+ *    caller-provided and sized by ee_workspace_bytes();
+ *  - every call is asynchronous on `stream` (a cudaStream_t passed as void*);
+ *  - activations on the residual stream are float32; weights, KV cache and
+ *    GEMV inputs use `dtype` (EE_F32 parity mode or EE_BF16 perf mode);
+ *  - results are deterministic and ROW-STABLE: the value computed for one row
+ *    does not depend on how many rows share the call (the reference's
+ *    `dot_rows` contract, `eepipe/_pykernels.py:14-17`, `115-121`), so batched
+ *    KV recomputation and pipelined inference agree bitwise;
+ *  - return code 0 = OK; otherwise an EE_E* code that the Python host maps to
+ *    the reference exception classes (`eepipe/errors.py:4-25`), with a
+ *    thread-local message from ee_last_error().
+ */
+#ifndef EE_H_
+#define EE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes -> eepipe.errors */
+#define EE_OK 0
+#define EE_ESHAPE 1     /* ShapeError */
+#define EE_ETOKEN 2     /* TokenError */
+#define EE_ENONFINITE 3 /* NonFiniteError */
+#define EE_ECONFIG 4    /* ConfigError */
+#define EE_ECUDA 5      /* RuntimeError (CUDA launch / runtime failure) */
+
+/* dtypes */
+#define EE_F32 0
+#define EE_BF16 1
+
+/* GEMV epilogues */
+#define EE_EPI_STORE 0    /* out[r, n] = v            (float32 out)          */
+#define EE_EPI_RESIDUAL 1 /* out[r, n] += v           (float32 residual)     */
+#define EE_EPI_GELU 2     /* out[r, n] = gelu_erf(v)  (dtype out)            */
+
+/* workspace ops for ee_workspace_bytes */
+#define EE_OP_ATTENTION 1
+#define EE_OP_EXIT_HEAD 2
+#define EE_OP_DECODER 3
+#define EE_OP_EXIT_HEAD_TRAIN 4
+
+const char* ee_last_error(void);
+int ee_abi_version(void);
+/* number of SMs of the current device (grid sizing), -1 on error */
+int ee_device_sms(void);
+
+size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, int64_t nh, int64_t s_max);
+
+/* Token + position embedding rows: out[r] = tok_emb[tok[r]] + pos_emb[pos[r]]
+ * (float32 out).  Replaces `_InferParams.embed` (eepipe/inference.py:187-191)
+ * and `embed_tokens` (eepipe/model.py:233-243).  Token ids are validated by
+ * the host (TokenError) before the call. */
+int ee_embed(const int32_t* tok, const int32_t* pos, int64_t m, const void* tok_emb,
+             const void* pos_emb, int64_t h, int dtype, float* out, void* stream);
+
+/* RMSNorm of (optionally gathered) float32 rows into a compact dtype buffer:
+ * out[i] = x[rows[i]] * (mean(x^2)+eps)^-1/2 * w  (w == NULL: plain cast).
+ * Replaces `rmsnorm_fwd` (eepipe/_pykernels.py:36-41). rows may be NULL. */
+int ee_rmsnorm_rows(const float* x, int64_t ldx, const int32_t* rows, int64_t m, int64_t h,
+                    const float* w, float eps, void* out, int dtype, void* stream);
+
+/* Row-stable GEMV/GEMM  v[r, n] = sum_k x[r, k] * W[n, k]  with a fused
+ * epilogue (EE_EPI_*).  W is (N, K) row-major ("K-major", i.e. the reference
+ * matrix transposed once at load).  x is (m, K) in `dtype`.
+ * Replaces `dot_rows` (eepipe/_pykernels.py:115-121) and its callers'
+ * elementwise tails (`x + dot_rows(..)`, `gelu_fwd(dot_rows(..))`,
+ * eepipe/inference.py:227-229). */
+int ee_gemv(const void* x, int64_t m, int64_t K, const void* W, int64_t N, int dtype, int epilogue,
+            void* out, int64_t ldo, void* stream);
+
+/* Fused Q/K/V projection with the KV-cache write in the epilogue:
+ * [q | k | v] = xn @ Wqkv^T,  q -> q_out (float32, m x h),
+ * k, v -> kcache/vcache[pos[r]] (dtype, layout (s_max, h)).
+ * Replaces the q/k/v `dot_rows` + `KVCache.fill` of `_layer_step`
+ * (eepipe/inference.py:219-226). */
+int ee_qkv_kvwrite(const void* xn, int64_t m, int64_t h, const void* Wqkv, int dtype, float* q_out,
+                   void* kcache, void* vcache, const int32_t* pos, void* stream);
+
+/* Multi-row causal decode attention: row r attends over cache positions
+ * 0..pos[r] of one layer (K/V of all rows already written).  Split-KV chunks
+ * are keyed by position only and merged in a fixed order (row-stable).
+ * q float32 (m, nh*dh); out dtype (m, nh*dh).  max_pos >= max(pos).
+ * Replaces `_attend_rows` (eepipe/inference.py:194-213). */
+int ee_decode_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_pos,
+                        const void* kcache, const void* vcache, int64_t nh, int64_t dh, int dtype,
+                        void* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Fused inference exit head: for each of the m rows of xn (already
+ * [normed and] cast, (m, h) dtype) computes logits = xn @ W^T over the
+ * vocabulary WITHOUT writing them (unless logits_dbg != NULL), with a split-V
+ * online (max, sum-exp, argmax) and a fixed-order merge, then
+ *   token[r] = argmax (lowest index wins ties),
+ *   conf[r]  = max softmax probability = 1 / sum exp(l - max),
+ *   fire[r]  = threshold < 1 && conf > threshold.
+ * *nonfinite is set to 1 if any logit was not finite (host raises
+ * NonFiniteError).  m <= 16 per call.  W is (V, h) row-major.
+ * Replaces `head_logits` + `exit_decision` (eepipe/inference.py:118-133,
+ * 175-185). */
+int ee_exit_head_infer(const void* xn, int64_t m, int64_t h, const void* W, int64_t V, int dtype,
+                       float threshold, int32_t* token, float* conf, uint8_t* fire,
+                       int32_t* nonfinite, float* logits_dbg, void* ws, size_t ws_bytes,
+                       void* stream);
+
+/* ---- decode layer chain (the KV-recompute kernel) -------------------- */
+
+typedef struct {
+    const float* attn_norm; /* (h) float32 */
+    const void* wqkv;       /* (3h, h) dtype: [wq^T; wk^T; wv^T] */
+    const void* wo;         /* (h, h)  dtype: wo^T */
+    const float* mlp_norm;  /* (h) float32 */
+    const void* w1;         /* (4h, h) dtype: w1^T */
+    const void* w2;         /* (h, 4h) dtype: w2^T */
+    void* kcache;           /* (s_max, h) dtype */
+    void* vcache;           /* (s_max, h) dtype */
+} ee_layer_t;
+
+typedef struct {
+    int64_t h, nh, s_max, max_rows;
+    int dtype;
+    float eps;
+    void* xn;   /* (max_rows, 4h) dtype scratch */
+    float* q;   /* (max_rows, h) float32 scratch */
+    void* attn; /* (max_rows, h) dtype scratch */
+    void* ws;   /* attention workspace (ee_workspace_bytes(EE_OP_ATTENTION, ...)) */
+    size_t ws_bytes;
+} ee_decoder_t;
+
+/* One transformer layer for the first m rows of x (float32, (m, h), updated
+ * in place), KV written at pos[r] before any row attends:
+ * RMSNorm -> QKV(+KV write) -> attention -> wo + residual -> RMSNorm ->
+ * w1 + GELU -> w2 + residual.  Replaces `_layer_step`
+ * (eepipe/inference.py:216-229). */
+int ee_decode_layer(const ee_decoder_t* dec, const ee_layer_t* layer, float* x, int64_t m,
+                    const int32_t* pos, int32_t max_pos, void* stream);
+
+/* Layers [0, n_layers) of `layers` in order over n_rows rows of x that are
+ * ordered by entry depth DESCENDING, so the rows a layer must advance (entry
+ * < layer) are always a suffix: layer i advances rows [n_rows - m_active[i],
+ * n_rows) (m_active[i] == 0 skips the layer).  This is the batched back-fill
+ * pass of KV recomputation (`run_pass` layer loop,
+ * eepipe/inference.py:316-326): one weight read per layer serves every
+ * deferred row plus the new one. */
+int ee_decode_layers(const ee_decoder_t* dec, const ee_layer_t* layers, int32_t n_layers,
+                     int64_t n_rows, const int32_t* m_active, float* x, const int32_t* pos,
+                     int32_t max_pos, void* stream);
+
+/* ---- training exit head (fused CE) ---------------------------------- */
+
+/* Weighted cross-entropy of one exit head and its gradients, without the
+ * (n, V) logits in HBM.  x (n, h) bf16 (already normed if the head has a
+ * norm), W (V, h) bf16, targets int64 (n).  Writes
+ *   *loss  = weight * mean_i CE_i (float32, device scalar),
+ *   dx     = d loss / d x  (n, h) float32,
+ *   dw_acc += d loss / d W (V, h) float32 (accumulated across microbatches).
+ * Replaces `run_head` matmul + `cross_entropy` fwd/bwd + the matmul backward
+ * (eepipe/model.py:219-230, eepipe/autodiff.py:158-179, 301-323,
+ * eepipe/_ckernels.pyx:130-167). */
+int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
+                       const int64_t* targets, float weight, float* loss, float* dx, float* dw_acc,
+                       void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EE_H_ */

@@ -1,0 +1,128 @@
+"""ctypes binding of libee.so (the C-ABI declared in include/ee.h).
+
+The product path has exactly one backend: the sm_100a CUDA library built
+in-tree.  There is no CPU fallback — if the library is missing or no CUDA
+device is present, every compute entry point raises.  Return codes map onto
+the reference exception classes (`eepipe/errors.py:4-25`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ConfigError, NonFiniteError, ShapeError, TokenError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libee.so")
+
+EE_OK, EE_ESHAPE, EE_ETOKEN, EE_ENONFINITE, EE_ECONFIG, EE_ECUDA = range(6)
+EE_F32, EE_BF16 = 0, 1
+EE_EPI_STORE, EE_EPI_RESIDUAL, EE_EPI_GELU = 0, 1, 2
+EE_OP_ATTENTION, EE_OP_EXIT_HEAD, EE_OP_DECODER, EE_OP_EXIT_HEAD_TRAIN = 1, 2, 3, 4
+
+_ERRORS = {EE_ESHAPE: ShapeError, EE_ETOKEN: TokenError, EE_ENONFINITE: NonFiniteError,
+           EE_ECONFIG: ConfigError, EE_ECUDA: RuntimeError}
+
+c_void_p, c_int64, c_int32, c_int, c_float, c_size_t = (
+    ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int, ctypes.c_float, ctypes.c_size_t)
+
+
+class EeLayer(ctypes.Structure):
+    _fields_ = [("attn_norm", c_void_p), ("wqkv", c_void_p), ("wo", c_void_p),
+                ("mlp_norm", c_void_p), ("w1", c_void_p), ("w2", c_void_p),
+                ("kcache", c_void_p), ("vcache", c_void_p)]
+
+
+class EeDecoder(ctypes.Structure):
+    _fields_ = [("h", c_int64), ("nh", c_int64), ("s_max", c_int64), ("max_rows", c_int64),
+                ("dtype", c_int), ("eps", c_float), ("xn", c_void_p), ("q", c_void_p),
+                ("attn", c_void_p), ("ws", c_void_p), ("ws_bytes", c_size_t)]
+
+
+# name -> (restype, argtypes); every symbol declared in include/ee.h
+SIGNATURES = {
+    "ee_last_error": (ctypes.c_char_p, []),
+    "ee_abi_version": (c_int, []),
+    "ee_device_sms": (c_int, []),
+    "ee_workspace_bytes": (c_size_t, [c_int, c_int64, c_int64, c_int64, c_int64, c_int64]),
+    "ee_embed": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int, c_void_p,
+                         c_void_p]),
+    "ee_rmsnorm_rows": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_float,
+                                c_void_p, c_int, c_void_p]),
+    "ee_gemv": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int, c_int, c_void_p,
+                        c_int64, c_void_p]),
+    "ee_qkv_kvwrite": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_void_p]),
+    "ee_decode_attention": (c_int, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                    c_int64, c_int64, c_int, c_void_p, c_void_p, c_size_t,
+                                    c_void_p]),
+    "ee_exit_head_infer": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int, c_float,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_size_t, c_void_p]),
+    "ee_decode_layer": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int32,
+                                c_void_p]),
+    "ee_decode_layers": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p,
+                                 c_void_p, c_int32, c_void_p]),
+    "ee_exit_head_train": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                   c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                   c_void_p]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and type the library.  Raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"libee.so not found at {path}; build it with "
+            "`python -m paper_2312_04916_b200.build_lib` (no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = ""):
+    if rc != EE_OK:
+        msg = _lib.ee_last_error().decode(errors="replace") if _lib is not None else ""
+        raise _ERRORS.get(rc, RuntimeError)(f"{what}: {msg}" if what else msg)
+
+
+def call(name: str, *args):
+    lib = load()
+    check(getattr(lib, name)(*args), name)
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2312_04916_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    load()
+
+
+def stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def dtype_code(torch_dtype):
+    import torch
+    if torch_dtype == torch.float32:
+        return EE_F32
+    if torch_dtype == torch.bfloat16:
+        return EE_BF16
+    raise ConfigError(f"unsupported compute dtype {torch_dtype}")

@@ -1,0 +1,74 @@
+// Shared device/host helpers for libee.so (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ee.h"
+
+typedef __nv_bfloat16 bf16;
+
+// ---- error plumbing (abi.cu) -------------------------------------------
+int ee_fail(int code, const char* fmt, ...);
+int ee_check_launch(const char* what);
+
+#define EE_REQUIRE(cond, code, ...)          \
+    do {                                     \
+        if (!(cond)) return ee_fail(code, __VA_ARGS__); \
+    } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- scalar conversions ---------------------------------------------------
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<bf16>(bf16 v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ bf16 from_f32<bf16>(float v) { return __float2bfloat16_rn(v); }
+
+// exact-erf GELU in float32 (eepipe/_pykernels.py:27-28)
+__device__ __forceinline__ float gelu_erf(float x) {
+    return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
+}
+
+// ---- memory helpers -------------------------------------------------------
+// Streaming 16-byte load: weights are read exactly once per pass, so keep
+// them out of L1 and hint a 256-byte L2 prefetch.
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Cached 16-byte load (activations re-read by every CTA).
+__device__ __forceinline__ uint4 ld_cached16(const void* p) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+// ---- tensor-core fragment MMA (bf16 x bf16 -> f32, m16n8k16) -------------
+__device__ __forceinline__ void mma_16816(float c[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// ---- host-side launch helpers (defined in the .cu files) -----------------
+int launch_rmsnorm_rows(const float* x, int64_t ldx, const int32_t* rows, int64_t m, int64_t h,
+                        const float* w, float eps, void* out, int dtype, cudaStream_t s);
+int launch_gemv(const void* x, int64_t m, int64_t K, const void* W, int64_t N, int dtype,
+                int epi, void* out, int64_t ldo, cudaStream_t s);
+int launch_qkv(const void* xn, int64_t m, int64_t h, const void* Wqkv, int dtype, float* q,
+               void* kc, void* vc, const int32_t* pos, cudaStream_t s);
+int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_pos,
+                     const void* kc, const void* vc, int64_t nh, int64_t dh, int dtype, void* out,
+                     void* ws, size_t ws_bytes, cudaStream_t s);
+size_t attention_ws_bytes(int64_t m, int64_t nh, int64_t dh, int64_t s_max);
+size_t exit_head_ws_bytes(int64_t m, int64_t V);

@@ -1,0 +1,97 @@
+// Row kernels: token+position embedding and RMSNorm(+gather, +cast).
+//
+// Both are HBM/L2-trivial (m <= a few rows at decode); they exist so that the
+// residual stream stays float32 while GEMV inputs are produced once, already
+// normalised and in the weight dtype.
+#include "ee_common.cuh"
+
+namespace {
+
+constexpr int kRowThreads = 256;
+
+// Fixed-order block sum: per-thread serial partials, then a fixed tree.
+__device__ __forceinline__ float block_sum_fixed(float v, float* sh) {
+    const int tid = threadIdx.x;
+    sh[tid] = v;
+    __syncthreads();
+    for (int s = kRowThreads / 2; s > 0; s >>= 1) {
+        if (tid < s) sh[tid] += sh[tid + s];
+        __syncthreads();
+    }
+    float r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRowThreads)
+k_embed(const int32_t* __restrict__ tok, const int32_t* __restrict__ pos,
+        const T* __restrict__ tok_emb, const T* __restrict__ pos_emb, int h,
+        float* __restrict__ out) {
+    const int r = blockIdx.x;
+    const T* te = tok_emb + (int64_t)tok[r] * h;
+    const T* pe = pos_emb + (int64_t)pos[r] * h;
+    float* o = out + (int64_t)r * h;
+    for (int k = threadIdx.x; k < h; k += kRowThreads) o[k] = to_f32(te[k]) + to_f32(pe[k]);
+}
+
+// y = x * (mean(x^2) + eps)^(-1/2) * w   (eepipe/_pykernels.py:36-41)
+template <typename TO>
+__global__ void __launch_bounds__(kRowThreads)
+k_rmsnorm_rows(const float* __restrict__ x, int64_t ldx, const int32_t* __restrict__ rows,
+               int h, const float* __restrict__ w, float eps, TO* __restrict__ out) {
+    __shared__ float sh[kRowThreads];
+    const int i = blockIdx.x;
+    const int src = rows ? rows[i] : i;
+    const float* xr = x + (int64_t)src * ldx;
+    TO* o = out + (int64_t)i * h;
+    if (w == nullptr) {
+        for (int k = threadIdx.x; k < h; k += kRowThreads) o[k] = from_f32<TO>(xr[k]);
+        return;
+    }
+    float ss = 0.f;
+    for (int k = threadIdx.x; k < h; k += kRowThreads) ss = fmaf(xr[k], xr[k], ss);
+    const float tot = block_sum_fixed(ss, sh);
+    const float inv = 1.0f / sqrtf(tot / (float)h + eps);
+    for (int k = threadIdx.x; k < h; k += kRowThreads) o[k] = from_f32<TO>(xr[k] * inv * w[k]);
+}
+
+}  // namespace
+
+int launch_rmsnorm_rows(const float* x, int64_t ldx, const int32_t* rows, int64_t m, int64_t h,
+                        const float* w, float eps, void* out, int dtype, cudaStream_t s) {
+    if (m == 0) return EE_OK;
+    EE_REQUIRE(m > 0 && h > 0 && ldx >= h, EE_ESHAPE, "rmsnorm_rows: bad shape m=%lld h=%lld",
+               (long long)m, (long long)h);
+    if (dtype == EE_BF16)
+        k_rmsnorm_rows<bf16><<<(unsigned)m, kRowThreads, 0, s>>>(x, ldx, rows, (int)h, w, eps,
+                                                                 (bf16*)out);
+    else if (dtype == EE_F32)
+        k_rmsnorm_rows<float><<<(unsigned)m, kRowThreads, 0, s>>>(x, ldx, rows, (int)h, w, eps,
+                                                                  (float*)out);
+    else
+        return ee_fail(EE_ECONFIG, "rmsnorm_rows: unknown dtype %d", dtype);
+    return ee_check_launch("rmsnorm_rows");
+}
+
+extern "C" int ee_rmsnorm_rows(const float* x, int64_t ldx, const int32_t* rows, int64_t m,
+                               int64_t h, const float* w, float eps, void* out, int dtype,
+                               void* stream) {
+    return launch_rmsnorm_rows(x, ldx, rows, m, h, w, eps, out, dtype, as_stream(stream));
+}
+
+extern "C" int ee_embed(const int32_t* tok, const int32_t* pos, int64_t m, const void* tok_emb,
+                        const void* pos_emb, int64_t h, int dtype, float* out, void* stream) {
+    if (m == 0) return EE_OK;
+    EE_REQUIRE(m > 0 && h > 0, EE_ESHAPE, "embed: bad shape");
+    cudaStream_t s = as_stream(stream);
+    if (dtype == EE_BF16)
+        k_embed<bf16><<<(unsigned)m, kRowThreads, 0, s>>>(tok, pos, (const bf16*)tok_emb,
+                                                          (const bf16*)pos_emb, (int)h, out);
+    else if (dtype == EE_F32)
+        k_embed<float><<<(unsigned)m, kRowThreads, 0, s>>>(tok, pos, (const float*)tok_emb,
+                                                           (const float*)pos_emb, (int)h, out);
+    else
+        return ee_fail(EE_ECONFIG, "embed: unknown dtype %d", dtype);
+    return ee_check_launch("embed");
+}

@@ -1,0 +1,1017 @@
+"""Early-exit generation on B200: KV recomputation and pipeline-based inference.
+
+Same API as the reference `eepipe.inference` (`eepipe/inference.py`):
+`exit_decision`, `KVCache`, `DeferredToken`, `GenerationTrace`,
+`generate_kv_recompute`, `generate_pipeline`, `greedy_reference`,
+`compare_modes`, `default_stage_times`, `full_pass_units`.  The math runs in
+libee.so (include/ee.h); this module is the host control logic: which rows
+advance through which layers, where heads are evaluated, when a pass stops,
+and the KV fill-mask discipline.
+
+Design (B200-first):
+
+* Weights are packed once per (model, dtype) into HBM in the layout the
+  kernels stream: per layer Wqkv (3h, h), Wo (h, h), W1 (4h, h), W2 (h, 4h)
+  K-major; head matrices stay (V, h).  KV cache is one (L, 2, s_max, h)
+  tensor.  Residual rows are float32; weights/KV/GEMV inputs are float32
+  (parity mode) or bf16 (perf mode).
+* A pass keeps its rows in one device buffer ordered by entry depth
+  DESCENDING, so the rows that advance at layer l (entry < l) are a suffix
+  and the new token's row is simply appended — deferred hidden states never
+  move between passes (the reference's `DeferredToken.hidden`).
+* One C-ABI call advances a whole span of layers between head taps
+  (`ee_decode_layers`); the host synchronises only at taps where the decide
+  row's exit decision gates the rest of the pass (`run_pass` early stop,
+  `eepipe/inference.py:324-326`).
+* The fill mask of `KVCache` is kept on the host (positions are host-known
+  control data) with the reference's refill / unfilled-read errors
+  (`eepipe/inference.py:58-70`); the K/V values live only in HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import time
+from dataclasses import dataclass, field
+from queue import Queue
+
+import numpy as np
+
+from . import _lib
+from ._lib import EE_EPI_GELU, EE_EPI_RESIDUAL, call, ptr, stream_ptr
+from .errors import ConfigError, NonFiniteError, TokenError
+from .model import NORM_EPS, EarlyExitModel, HeadDesc, ModelConfig, StagePartition
+from .schedule import inference_latency
+
+_UNSUPPORTED_HEADS = ("layer+embed",)
+_EMIT_TIMEOUT = 120.0
+_HEAD_MAX_ROWS = 16
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# Records (eepipe/inference.py:76-115)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class DeferredToken:
+    """A generated token whose deep-layer KV entries are still missing.
+    ``hidden`` is the device row index of its residual state (the state
+    itself never leaves HBM)."""
+
+    position: int
+    exit_layer: int
+    hidden: int
+
+
+@dataclass
+class GenerationTrace:
+    prompt: list
+    threshold: float
+    mode: str
+    tokens: list = field(default_factory=list)
+    exit_layers: list = field(default_factory=list)
+    exit_stages: list = field(default_factory=list)
+    confidences: list = field(default_factory=list)  # per token: {head_key: float}
+    latencies: list = field(default_factory=list)  # modeled, per token
+    total_latency: float = 0.0
+    baseline_latency: float = 0.0
+    measured_latencies: list = field(default_factory=list)  # seconds, per token (host clock)
+    measured_total: float = 0.0
+
+    @property
+    def speedup(self):
+        return self.baseline_latency / self.total_latency if self.total_latency else 1.0
+
+    @property
+    def mean_exit_layer(self):
+        return float(np.mean(self.exit_layers)) if self.exit_layers else 0.0
+
+    def records(self):
+        for i, tok in enumerate(self.tokens):
+            yield {
+                "position": len(self.prompt) + i,
+                "token": int(tok),
+                "exit_layer": self.exit_layers[i],
+                "exit_stage": self.exit_stages[i] if self.exit_stages else None,
+                "confidence": self.confidences[i],
+                "latency": self.latencies[i] if i < len(self.latencies) else None,
+                "measured_latency": (self.measured_latencies[i]
+                                     if i < len(self.measured_latencies) else None),
+            }
+
+
+def exit_decision(logits, threshold):
+    """Greedy decision at one exit (`eepipe/inference.py:118-133`):
+    confidence = max softmax probability, token = argmax (lowest index wins),
+    fire only on a strict crossing.  Evaluated on the GPU in float64; the
+    generation paths use the fused kernel instead (`ee_exit_head_infer`)."""
+    torch = _torch()
+    _lib.require_cuda()
+    z = torch.as_tensor(np.asarray(logits, dtype=np.float64).ravel()
+                        if not isinstance(logits, torch.Tensor) else logits.reshape(-1))
+    z = z.to(device="cuda", dtype=torch.float64)
+    if not bool(torch.isfinite(z).all()):
+        raise NonFiniteError("non-finite exit logits")
+    if not 0.0 < threshold <= 1.0:
+        raise ConfigError("threshold must lie in (0, 1]")
+    p = torch.softmax(z, dim=0)
+    token = int(torch.argmax(p))
+    conf = float(p[token])
+    return threshold < 1.0 and conf > threshold, token, conf
+
+
+# ---------------------------------------------------------------------------
+# KV cache (eepipe/inference.py:40-73)
+# ---------------------------------------------------------------------------
+
+
+class KVCache:
+    """Per-layer key/value store in HBM with a monotone host-side fill mask.
+
+    Layout: one (n_layers, 2, max_positions, num_heads*head_dim) tensor.
+    `fill` raises ConfigError on a refill, `view` on a read below an unfilled
+    position — the reference's KV-ordering guard."""
+
+    def __init__(self, layer_indices, max_positions, num_heads, head_dim, dtype=None,
+                 device=None):
+        torch = _torch()
+        self.layer_indices = list(layer_indices)
+        self._slot = {l: i for i, l in enumerate(self.layer_indices)}
+        self.max_positions = max_positions
+        self.num_heads, self.head_dim = num_heads, head_dim
+        self.data = torch.zeros((len(self.layer_indices), 2, max_positions, num_heads * head_dim),
+                                dtype=dtype or torch.float32, device=device or "cuda")
+        self.mask = np.zeros((len(self.layer_indices), max_positions), dtype=bool)
+
+    def k(self, layer):
+        return self.data[self._slot[layer], 0]
+
+    def v(self, layer):
+        return self.data[self._slot[layer], 1]
+
+    def fill(self, layer, position, k, v):
+        s = self._slot[layer]
+        if self.mask[s, position]:
+            raise ConfigError(f"KV at layer {layer}, position {position} already filled")
+        self.data[s, 0, position] = _torch().as_tensor(np.asarray(k)).reshape(-1).to(self.data)
+        self.data[s, 1, position] = _torch().as_tensor(np.asarray(v)).reshape(-1).to(self.data)
+        self.mask[s, position] = True
+
+    def view(self, layer, upto):
+        s = self._slot[layer]
+        if not self.mask[s, :upto].all():
+            raise ConfigError(f"reading unfilled KV at layer {layer} below {upto}")
+        shape = (upto, self.num_heads, self.head_dim)
+        return self.data[s, 0, :upto].reshape(shape), self.data[s, 1, :upto].reshape(shape)
+
+    def complete(self, upto):
+        return bool(self.mask[:, :upto].all())
+
+    def reset(self):
+        self.mask[:] = False
+
+    # bulk bookkeeping for kernel-side writes: layers [a, b) (slots), rows at
+    # `positions` written, each row then reads [0, pos] (max_pos covers all)
+    def mark_written(self, slot_a, slot_b, positions, max_pos):
+        block = self.mask[slot_a:slot_b]
+        if block[:, positions].any():
+            bad = np.argwhere(block[:, positions])[0]
+            raise ConfigError(f"KV at layer {self.layer_indices[slot_a + bad[0]]}, position "
+                              f"{positions[bad[1]]} already filled")
+        block[:, positions] = True
+        if not block[:, :max_pos + 1].all():
+            raise ConfigError(f"reading unfilled KV at layer {self.layer_indices[slot_a]} "
+                              f"below {max_pos + 1}")
+
+
+def _check_context(cfg: ModelConfig, needed):
+    if needed > cfg.max_seq_len:
+        raise TokenError(f"context of {needed} positions exceeds max_seq_len {cfg.max_seq_len}")
+
+
+def default_stage_times(part: StagePartition):
+    """`eepipe/inference.py:239-243`."""
+    per = part.config.num_layers // part.num_stages
+    return [per * 1.0 + 0.5 * len(st.heads) for st in part.stages]
+
+
+def full_pass_units(cfg: ModelConfig, num_heads_total):
+    """`eepipe/inference.py:246-248`."""
+    return cfg.num_layers * 1.0 + 0.5 * num_heads_total
+
+
+# ---------------------------------------------------------------------------
+# Device engine: packed weights + KV + scratch for a layer span and heads
+# ---------------------------------------------------------------------------
+
+
+def _resolve_dtype(params, dtype):
+    torch = _torch()
+    if dtype is None:
+        first = next(iter(params.values())).data
+        if isinstance(first, np.ndarray):
+            return torch.float32  # parity mode for reference-drawn weights
+        return torch.float32 if first.dtype == torch.float32 else torch.bfloat16
+    if isinstance(dtype, str):
+        dtype = {"fp32": torch.float32, "float32": torch.float32, "bf16": torch.bfloat16,
+                 "bfloat16": torch.bfloat16}[dtype]
+    return dtype
+
+
+class _Head:
+    __slots__ = ("desc", "W", "norm", "pre_norm", "w1t", "w2t", "V")
+
+
+class _PinnedRing:
+    """Host->device staging of small int32 control arrays through a ring of
+    pinned buffers; a buffer is rewritten only after the copy that last used
+    it has executed (its event), so asynchronous uploads never race."""
+
+    def __init__(self, cap, n=8):
+        torch = _torch()
+        self.cap = cap
+        self.bufs = [torch.zeros(cap, dtype=torch.int32).pin_memory() for _ in range(n)]
+        self.events = [None] * n
+        self.i = 0
+
+    def put(self, arr, dst, stream):
+        torch = _torch()
+        arr = np.asarray(arr, dtype=np.int32)
+        n = arr.size
+        if n > self.cap or n > dst.numel():
+            raise ConfigError("control block overflow")
+        i = self.i
+        self.i = (i + 1) % len(self.bufs)
+        if self.events[i] is not None:
+            self.events[i].synchronize()
+        b = self.bufs[i]
+        b[:n] = torch.from_numpy(arr)
+        dst[:n].copy_(b[:n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.events[i] = ev
+
+
+class Engine:
+    """HBM-resident state of one inference worker (the whole model for KV
+    recomputation, or one pipeline stage).  Built once per (params, dtype,
+    device) and reused across generate calls."""
+
+    def __init__(self, params, heads, cfg: ModelConfig, layer_indices, has_embedding, dtype,
+                 device=None, max_rows=8):
+        torch = _torch()
+        _lib.require_cuda()
+        self.device = torch.device(device or "cuda:0")
+        self.cfg = cfg
+        self.dtype = dtype
+        self.dcode = _lib.dtype_code(dtype)
+        self.layer_indices = list(layer_indices)
+        self.h = h = cfg.hidden_dim
+        self.nh = cfg.num_heads
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.current_stream(self.device)
+
+            def dev(name, dt=None):
+                a = params[name].data
+                t = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
+                return t.to(device=self.device, dtype=dt or dtype)
+
+            self.tok_emb = dev("tok_emb").contiguous() if has_embedding else None
+            self.pos_emb = dev("pos_emb").contiguous() if has_embedding else None
+            self.kv = KVCache(self.layer_indices, cfg.max_seq_len, cfg.num_heads,
+                              h // cfg.num_heads, dtype, self.device)
+            self.packed = []
+            self.layers_c = (_lib.EeLayer * max(1, len(self.layer_indices)))()
+            for i, l in enumerate(self.layer_indices):
+                p = f"layer{l}."
+                wqkv = torch.cat([dev(p + "wq").t(), dev(p + "wk").t(), dev(p + "wv").t()], 0)
+                lw = {
+                    "attn_norm": dev(p + "attn_norm", torch.float32).contiguous(),
+                    "wqkv": wqkv.contiguous(),
+                    "wo": dev(p + "wo").t().contiguous(),
+                    "mlp_norm": dev(p + "mlp_norm", torch.float32).contiguous(),
+                    "w1": dev(p + "w1").t().contiguous(),
+                    "w2": dev(p + "w2").t().contiguous(),
+                }
+                self.packed.append(lw)
+                c = self.layers_c[i]
+                for k in ("attn_norm", "wqkv", "wo", "mlp_norm", "w1", "w2"):
+                    setattr(c, k, lw[k].data_ptr())
+                c.kcache = self.kv.k(l).data_ptr()
+                c.vcache = self.kv.v(l).data_ptr()
+            self.heads = []
+            for hd in heads:
+                if hd.kind in _UNSUPPORTED_HEADS:
+                    raise ConfigError(
+                        f"head kind {hd.kind!r} is not supported for cached inference")
+                e = _Head()
+                e.desc = hd
+                e.W = dev(hd.param_names["out"]).contiguous()
+                e.V = e.W.shape[0]
+                e.norm = (dev(hd.param_names["norm"], torch.float32).contiguous()
+                          if "norm" in hd.param_names else None)
+                e.pre_norm = e.w1t = e.w2t = None
+                if hd.kind == "mlp+embed":
+                    e.pre_norm = dev(hd.param_names["pre_norm"], torch.float32).contiguous()
+                    e.w1t = dev(hd.param_names["w1"]).t().contiguous()
+                    e.w2t = dev(hd.param_names["w2"]).t().contiguous()
+                self.heads.append(e)
+            vmax = max([e.V for e in self.heads], default=1)
+            self.head_ws = torch.zeros(
+                _lib.load().ee_workspace_bytes(_lib.EE_OP_EXIT_HEAD, _HEAD_MAX_ROWS, h, vmax, 0, 0),
+                dtype=torch.uint8, device=self.device)
+            self.head_xn = torch.empty((_HEAD_MAX_ROWS, h), dtype=dtype, device=self.device)
+            self.head_x = torch.empty((_HEAD_MAX_ROWS, h), dtype=torch.float32, device=self.device)
+            self.head_mid = torch.empty((_HEAD_MAX_ROWS, 4 * h), dtype=dtype, device=self.device)
+            self.max_slots = 256
+            self.r_tok = torch.zeros((self.max_slots, _HEAD_MAX_ROWS), dtype=torch.int32,
+                                     device=self.device)
+            self.r_conf = torch.zeros((self.max_slots, _HEAD_MAX_ROWS), dtype=torch.float32,
+                                      device=self.device)
+            self.r_fire = torch.zeros((self.max_slots, _HEAD_MAX_ROWS), dtype=torch.uint8,
+                                      device=self.device)
+            self.r_bad = torch.zeros((self.max_slots,), dtype=torch.int32, device=self.device)
+            self.h_tok = torch.zeros_like(self.r_tok, device="cpu").pin_memory()
+            self.h_conf = torch.zeros_like(self.r_conf, device="cpu").pin_memory()
+            self.h_fire = torch.zeros_like(self.r_fire, device="cpu").pin_memory()
+            self.h_bad = torch.zeros_like(self.r_bad, device="cpu").pin_memory()
+            self.max_rows = 0
+            self._grow(max_rows)
+        # accounting for bench.py: kernels launched and host<->device bytes
+        self.launches = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    # -- scratch -------------------------------------------------------------
+    def _grow(self, rows):
+        torch = _torch()
+        if rows <= self.max_rows:
+            return
+        rows = max(rows, 2 * self.max_rows)
+        h, cfg = self.h, self.cfg
+        self._x_old = getattr(self, "x", None)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self.x = torch.zeros((rows, h), dtype=torch.float32, device=self.device)
+            self.xn = torch.empty((rows, 4 * h), dtype=self.dtype, device=self.device)
+            self.q = torch.empty((rows, h), dtype=torch.float32, device=self.device)
+            self.attn = torch.empty((rows, h), dtype=self.dtype, device=self.device)
+            wsb = _lib.load().ee_workspace_bytes(_lib.EE_OP_ATTENTION, rows, h, 0, cfg.num_heads,
+                                                 cfg.max_seq_len)
+            self.attn_ws = torch.zeros(wsb, dtype=torch.uint8, device=self.device)
+            # control block: positions (rows) + gather lists, staged via pinned memory
+            self.ctrl_cap = 4 * rows + 64 * _HEAD_MAX_ROWS + 64
+            self.ctrl = torch.zeros(self.ctrl_cap, dtype=torch.int32, device=self.device)
+            self.ring = _PinnedRing(self.ctrl_cap)
+            self.tokbuf = torch.zeros(2 * rows, dtype=torch.int32, device=self.device)
+            if self.max_rows:
+                old = self._x_old
+                self.x[:old.shape[0]].copy_(old)
+            self.dec = _lib.EeDecoder(h=h, nh=cfg.num_heads, s_max=cfg.max_seq_len,
+                                      max_rows=rows, dtype=self.dcode, eps=NORM_EPS,
+                                      xn=self.xn.data_ptr(), q=self.q.data_ptr(),
+                                      attn=self.attn.data_ptr(), ws=self.attn_ws.data_ptr(),
+                                      ws_bytes=wsb)
+        self.max_rows = rows
+        self._x_old = None
+
+    # -- primitives ------------------------------------------------------------
+    def upload_ctrl(self, arr):
+        self.ring.put(arr, self.ctrl, self.stream)
+        self.h2d_bytes += 4 * len(arr)
+
+    def ctrl_ptr(self, off):
+        return ctypes.c_void_p(self.ctrl.data_ptr() + 4 * off)
+
+    def embed_rows(self, tokens, positions, row0):
+        """x[row0:row0+m] = tok_emb[tokens] + pos_emb[positions]."""
+        torch = _torch()
+        tokens = np.asarray(tokens, dtype=np.int64)
+        if tokens.size and (tokens.min() < 0 or tokens.max() >= self.cfg.vocab_size):
+            raise TokenError("token id out of vocabulary range")
+        m = len(tokens)
+        self._grow(max(row0 + m, (m + 1) // 2))
+        stage = np.concatenate([tokens, np.asarray(positions, dtype=np.int64)])
+        self.ring.put(stage, self.tokbuf, self.stream)
+        self.h2d_bytes += 4 * len(stage)
+        self.launches += 1
+        dbuf = self.tokbuf
+        call("ee_embed", ptr(dbuf), ctypes.c_void_p(dbuf.data_ptr() + 4 * m), m,
+             ptr(self.tok_emb), ptr(self.pos_emb), self.h, self.dcode,
+             ctypes.c_void_p(self.x.data_ptr() + 4 * row0 * self.h), stream_ptr(self.stream))
+
+    def eval_head(self, e: _Head, rows_ptr, m, threshold, slot):
+        """Fused head on m gathered rows of x; results into result slot."""
+        h = self.h
+        s = stream_ptr(self.stream)
+        xsrc = self.x
+        if e.desc.kind == "mlp+embed":
+            # x' = x + GELU(RMSNorm(x; pre_norm) @ w1) @ w2   (eepipe/inference.py:178-182)
+            call("ee_rmsnorm_rows", ptr(self.x), h, rows_ptr, m, h, None, NORM_EPS,
+                 ptr(self.head_x), _lib.EE_F32, s)
+            call("ee_rmsnorm_rows", ptr(self.head_x), h, None, m, h, ptr(e.pre_norm), NORM_EPS,
+                 ptr(self.head_xn), self.dcode, s)
+            call("ee_gemv", ptr(self.head_xn), m, h, ptr(e.w1t), 4 * h, self.dcode, EE_EPI_GELU,
+                 ptr(self.head_mid), 4 * h, s)
+            call("ee_gemv", ptr(self.head_mid), m, 4 * h, ptr(e.w2t), h, self.dcode,
+                 EE_EPI_RESIDUAL, ptr(self.head_x), h, s)
+            xsrc, rows_ptr = self.head_x, None
+            self.launches += 4
+        call("ee_rmsnorm_rows", ptr(xsrc), h, rows_ptr, m, h, ptr(e.norm), NORM_EPS,
+             ptr(self.head_xn), self.dcode, s)
+        self.launches += 2
+        call("ee_exit_head_infer", ptr(self.head_xn), m, h, ptr(e.W), e.V, self.dcode,
+             float(threshold),
+             ctypes.c_void_p(self.r_tok.data_ptr() + 4 * _HEAD_MAX_ROWS * slot),
+             ctypes.c_void_p(self.r_conf.data_ptr() + 4 * _HEAD_MAX_ROWS * slot),
+             ctypes.c_void_p(self.r_fire.data_ptr() + _HEAD_MAX_ROWS * slot),
+             ctypes.c_void_p(self.r_bad.data_ptr() + 4 * slot), None,
+             ptr(self.head_ws), self.head_ws.numel(), s)
+
+    def fetch_results(self, nslots):
+        """D2H of the first nslots result slots, then synchronise."""
+        if nslots == 0:
+            return
+        for d, hst in ((self.r_tok, self.h_tok), (self.r_conf, self.h_conf),
+                       (self.r_fire, self.h_fire), (self.r_bad, self.h_bad)):
+            hst[:nslots].copy_(d[:nslots], non_blocking=True)
+        self.d2h_bytes += nslots * (9 * _HEAD_MAX_ROWS + 4)
+        self.stream.synchronize()
+        if bool(self.h_bad[:nslots].any()):
+            raise NonFiniteError("non-finite exit logits")
+
+    def run_layers(self, la, lb, n_rows, m_active, max_pos, pos_off):
+        """Slots [la, lb) of this engine's layers over rows [0, n_rows)."""
+        n = lb - la
+        if n <= 0:
+            return
+        arr = (ctypes.c_int32 * n)(*m_active)
+        layers = ctypes.c_void_p(ctypes.addressof(self.layers_c) +
+                                 la * ctypes.sizeof(_lib.EeLayer))
+        self.launches += 7 * sum(1 for v in m_active if v)
+        call("ee_decode_layers", ctypes.byref(self.dec), layers, n, n_rows, arr, ptr(self.x),
+             self.ctrl_ptr(pos_off), int(max_pos), stream_ptr(self.stream))
+
+
+_ENGINE_CACHE_ATTR = "_ee_engines"
+
+
+def _engine_for(owner, params, heads, cfg, layer_indices, has_embedding, dtype, device=None):
+    """Engines are cached on the owning object (model or stage spec)."""
+    torch = _torch()
+    dt = _resolve_dtype(params, dtype)
+    dev = torch.device(device or "cuda:0")
+    cache = owner.__dict__.setdefault(_ENGINE_CACHE_ATTR, {})
+    key = (dt, str(dev), tuple(layer_indices), tuple(hd.key for hd in heads))
+    eng = cache.get(key)
+    if eng is None:
+        eng = Engine(params, heads, cfg, layer_indices, has_embedding, dt, dev)
+        cache[key] = eng
+    return eng
+
+
+# ---------------------------------------------------------------------------
+# KV recomputation (single worker) — eepipe/inference.py:256-381
+# ---------------------------------------------------------------------------
+
+
+class _PassRunner:
+    """Executes one `run_pass` of the reference on the engine."""
+
+    def __init__(self, eng: Engine, threshold, conf_log):
+        self.e = eng
+        self.thr = threshold
+        self.conf_log = conf_log
+        self.L = eng.cfg.num_layers
+        taps = {}
+        for hi, e in enumerate(eng.heads):
+            taps.setdefault(e.desc.layer_index, []).append(hi)
+        self.taps = taps  # tap -> head indices in (tap, is_final) order
+
+    def run(self, n, pos, entry, decide_row, forced):
+        """Rows [0, n) of engine.x with positions/entries ordered by entry
+        descending.  Returns (decision (token, exit_layer) | None, depth)."""
+        e, L = self.e, self.L
+        # control block: positions, then per-tap gather lists
+        ctrl = list(pos)
+        lists = {}
+        for tap in sorted(self.taps):
+            rows = [r for r in range(n)
+                    if (tap > entry[r] or (tap == 0 and entry[r] == 0))
+                    and (r == decide_row or entry[r] > 0)]
+            if rows:
+                lists[tap] = (len(ctrl), rows)
+                ctrl.extend(rows)
+        e.upload_ctrl(ctrl)
+        max_pos = max(pos)
+        slots = []  # (slot, head idx, rows) in evaluation order
+        decision = None
+        checked = 0  # slots whose results have been fetched
+
+        def eval_tap(tap):
+            if tap not in lists:
+                return False
+            off, rows = lists[tap]
+            gates = False
+            for hi in self.taps[tap]:
+                for c0 in range(0, len(rows), _HEAD_MAX_ROWS):
+                    chunk = rows[c0:c0 + _HEAD_MAX_ROWS]
+                    slot = len(slots)
+                    if slot >= e.max_slots:
+                        raise ConfigError("too many head evaluations in one pass")
+                    e.eval_head(e.heads[hi], e.ctrl_ptr(off + c0), len(chunk), self.thr, slot)
+                    slots.append((slot, hi, chunk))
+                    gates |= decide_row in chunk
+            return gates
+
+        def decide_from(upto):
+            nonlocal decision, checked
+            e.fetch_results(upto)
+            for slot, hi, chunk in slots[checked:upto]:
+                hd = e.heads[hi].desc
+                for j, r in enumerate(chunk):
+                    if r == decide_row and decision is None:
+                        tok = int(e.h_tok[slot, j])
+                        if hd.is_final:
+                            decision = (tok, L)
+                        elif bool(e.h_fire[slot, j]):
+                            decision = (tok, hd.layer_index)
+            checked = upto
+
+        def stop_here(tap):
+            return decision is not None and not forced and decision[1] == tap and tap < L
+
+        gates = eval_tap(0)
+        if gates and not forced:
+            decide_from(len(slots))
+            if decision is not None and decision[1] == 0:
+                self._log(slots, pos)
+                return decision, 0
+        stops = sorted(t for t in self.taps if t >= 1) or [L]
+        if stops[-1] != L:
+            stops.append(L)
+        la = 1
+        depth = L
+        for tap in stops:
+            # layers la..tap, grouped into runs with a constant active suffix
+            l = la
+            while l <= tap:
+                m_act = sum(1 for r in range(n) if entry[r] < l)
+                l2 = l
+                while l2 + 1 <= tap and sum(1 for r in range(n) if entry[r] < l2 + 1) == m_act:
+                    l2 += 1
+                if m_act:
+                    e.run_layers(l - 1, l2, n, [m_act] * (l2 - l + 1), max_pos, 0)
+                    act_pos = pos[n - m_act:]
+                    e.kv.mark_written(l - 1, l2, act_pos, max(act_pos))
+                l = l2 + 1
+            la = tap + 1
+            gates = eval_tap(tap)
+            if gates and not forced and decision is None:
+                decide_from(len(slots))
+                if stop_here(tap):
+                    depth = tap
+                    break
+        if checked < len(slots):
+            decide_from(len(slots))
+        self._log(slots, pos)
+        return decision, depth
+
+    def _log(self, slots, pos):
+        e = self.e
+        for slot, hi, chunk in slots:
+            key = e.heads[hi].desc.key
+            for j, r in enumerate(chunk):
+                self.conf_log.setdefault(pos[r], {})[key] = float(e.h_conf[slot, j])
+
+
+def generate_kv_recompute(model: EarlyExitModel, prompt, threshold, max_new_tokens,
+                          max_deferred=4, *, dtype=None, device=None) -> GenerationTrace:
+    """Incremental decoding that batches deferred early-exit tokens into the
+    current pass to recompute their missing KV entries
+    (`eepipe/inference.py:256-381`).  ``dtype`` selects fp32 parity mode or
+    bf16 perf mode (default: fp32 for host float64 weights, else the weights'
+    dtype)."""
+    if max_deferred < 1:
+        raise ConfigError("max_deferred must be at least 1")
+    prompt = [int(t) for t in prompt]
+    if not prompt:
+        raise ConfigError("prompt must be non-empty")
+    if not 0.0 < threshold <= 1.0:
+        raise ConfigError("threshold must lie in (0, 1]")
+    cfg = model.config
+    _check_context(cfg, len(prompt) + max_new_tokens)
+    L = cfg.num_layers
+    eng = _engine_for(model, model.params, model.heads, cfg, range(1, L + 1), True, dtype, device)
+    torch = _torch()
+    with torch.cuda.device(eng.device), torch.cuda.stream(eng.stream):
+        return _kv_recompute(eng, model, prompt, threshold, max_new_tokens, max_deferred)
+
+
+def _kv_recompute(eng, model, prompt, threshold, max_new_tokens, max_deferred):
+    cfg = model.config
+    L = cfg.num_layers
+    eng.kv.reset()
+    trace = GenerationTrace(prompt, threshold, "recompute")
+    conf_log: dict = {}
+    runner = _PassRunner(eng, threshold, conf_log)
+    units = full_pass_units(cfg, len(model.heads))
+    pass_depths = []
+    t_start = time.perf_counter()
+    t_last = t_start
+
+    # Prefill: every prompt row at full depth; its last row decides token 1.
+    t0 = len(prompt)
+    eng._grow(max(t0, max_deferred + 1))
+    eng.embed_rows(prompt, range(t0), 0)
+    decision, _ = runner.run(t0, list(range(t0)), [0] * t0, t0 - 1, True)
+    pass_depths.append(L)
+
+    deferred: list[DeferredToken] = []  # rows 0..len-1 of eng.x, entry descending
+    position = t0 - 1
+    for i in range(max_new_tokens):
+        token, exit_layer = decision
+        trace.tokens.append(token)
+        trace.exit_layers.append(exit_layer)
+        now = time.perf_counter()
+        trace.measured_latencies.append(now - t_last)
+        t_last = now
+        if i == max_new_tokens - 1:
+            break
+        position += 1
+        forced = len(deferred) >= max_deferred
+        n = len(deferred) + 1
+        eng.embed_rows([token], [position], n - 1)
+        pos = [d.position for d in deferred] + [position]
+        ent = [d.exit_layer for d in deferred] + [0]
+        decision, depth = runner.run(n, pos, ent, n - 1, forced)
+        pass_depths.append(depth)
+        if depth < L:
+            deferred = [DeferredToken(d.position, max(d.exit_layer, depth), r)
+                        for r, d in enumerate(deferred)]
+            deferred.append(DeferredToken(position, depth, n - 1))
+        else:
+            deferred = []
+        if len(deferred) > max_deferred:
+            raise RuntimeError("deferred list overflow")  # internal bug guard
+
+    flush_cost = 0.0
+    if deferred:  # complete the remaining KV entries and deep-exit confidences
+        runner.run(len(deferred), [d.position for d in deferred],
+                   [d.exit_layer for d in deferred], None, True)
+        flush_cost = units
+    eng.stream.synchronize()
+    trace.measured_total = time.perf_counter() - t_start
+
+    gen = len(trace.tokens)
+    if gen and not eng.kv.complete(t0 + gen - 1):
+        raise ConfigError("KV fill mask incomplete after generation")
+    trace.confidences = [conf_log.get(t0 - 1 + i, {}) for i in range(gen)]
+    trace.latencies = [units * d / L for d in pass_depths[:gen]]
+    trace.total_latency = sum(trace.latencies) + flush_cost
+    trace.baseline_latency = units * gen
+    return trace
+
+
+# ---------------------------------------------------------------------------
+# Pipeline mode — eepipe/inference.py:389-539
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class _FwdMsg:
+    rows: object  # device tensor (m, h) float32
+    positions: list
+    decide_pos: int
+    emitted: bool
+    ready: object = None  # CUDA event recorded on the sender's stream
+    stop: bool = False
+
+
+@dataclass
+class _EmitMsg:
+    position: int
+    token: int
+    exit_layer: int
+    exit_stage: int
+
+
+class _InferStage:
+    """One pipeline stage: own layers, heads, KV cache and CUDA stream;
+    strict FIFO position order (`eepipe/inference.py:406-463`)."""
+
+    def __init__(self, spec, cfg, threshold, q_in, q_out, emit_q, conf_log, lock, dtype, device):
+        torch = _torch()
+        heads = [hd for _, hd in spec.heads]
+        self.spec = spec
+        self.cfg = cfg
+        self.threshold = threshold
+        self.eng = _engine_for(spec, spec.params, heads, cfg, spec.layer_indices,
+                               spec.has_embedding, dtype, device)
+        self.eng.kv.reset()
+        with torch.cuda.device(self.eng.device):
+            self.stream = torch.cuda.Stream(self.eng.device)
+        self.eng.stream = self.stream
+        self.heads_at = {}
+        for local, hd in spec.heads:
+            hi = next(i for i, e in enumerate(self.eng.heads) if e.desc.key == hd.key)
+            self.heads_at.setdefault(local, []).append(hi)
+        self.q_in, self.q_out, self.emit_q = q_in, q_out, emit_q
+        self.conf_log, self.lock = conf_log, lock
+        self.exception = None
+
+    def _check_heads(self, msg, local, n):
+        e = self.eng
+        if local not in self.heads_at or msg.decide_pos not in msg.positions:
+            return
+        r = msg.positions.index(msg.decide_pos)
+        e.upload_ctrl(list(msg.positions) + [r])
+        for k, hi in enumerate(self.heads_at[local]):
+            e.eval_head(e.heads[hi], e.ctrl_ptr(n), 1, self.threshold, k)
+        e.fetch_results(len(self.heads_at[local]))
+        for k, hi in enumerate(self.heads_at[local]):
+            hd = e.heads[hi].desc
+            conf = float(e.h_conf[k, 0])
+            with self.lock:
+                self.conf_log.setdefault(msg.decide_pos, {})[hd.key] = conf
+            if not msg.emitted and (bool(e.h_fire[k, 0]) or hd.is_final):
+                self.emit_q.put(_EmitMsg(msg.decide_pos, int(e.h_tok[k, 0]), hd.layer_index,
+                                         self.spec.index))
+                msg.emitted = True
+
+    def run(self):
+        torch = _torch()
+        try:
+            with torch.cuda.device(self.eng.device), torch.cuda.stream(self.stream):
+                e = self.eng
+                while True:
+                    msg = self.q_in.get()
+                    if msg.stop:
+                        if self.q_out is not None:
+                            self.q_out.put(msg)
+                        return
+                    if msg.ready is not None:
+                        self.stream.wait_event(msg.ready)
+                    n = len(msg.positions)
+                    e._grow(n)
+                    e.x[:n].copy_(msg.rows, non_blocking=True)
+                    msg.rows.record_stream(self.stream)
+                    e.upload_ctrl(list(msg.positions))
+                    self._check_heads(msg, 0, n)
+                    max_pos = max(msg.positions)
+                    local = 1
+                    stops = sorted(k for k in self.heads_at if k >= 1)
+                    nloc = len(self.spec.layer_indices)
+                    if not stops or stops[-1] != nloc:
+                        stops.append(nloc)
+                    for stop in stops:
+                        if stop >= local:
+                            e.upload_ctrl(list(msg.positions))
+                            e.run_layers(local - 1, stop, n, [n] * (stop - local + 1), max_pos, 0)
+                            e.kv.mark_written(local - 1, stop, list(msg.positions), max_pos)
+                            self._check_heads(msg, stop, n)
+                            local = stop + 1
+                    if self.q_out is not None:
+                        out = e.x[:n].clone()
+                        ev = torch.cuda.Event()
+                        ev.record(self.stream)
+                        self.q_out.put(_FwdMsg(out, msg.positions, msg.decide_pos, msg.emitted,
+                                               ev))
+        except BaseException as exc:  # surfaced by the coordinator
+            self.exception = exc
+            self.emit_q.put(exc)
+
+
+def generate_pipeline(part: StagePartition, prompt, threshold, max_new_tokens, stage_times=None,
+                      *, dtype=None, devices=None) -> GenerationTrace:
+    """Pipeline-based early-exit inference (`eepipe/inference.py:466-539`).
+
+    One worker thread per stage, each with its own CUDA stream (and its own
+    GPU when ``devices`` lists several): stage s processes positions strictly
+    in order; the emitted token's pass continues to the last stage filling KV
+    while stage 1 already runs the next token.  For the multi-process
+    NCCL/NVLink variant (one process per GPU) see `pipeline_infer.py`."""
+    torch = _torch()
+    if part.num_stages < 2:
+        raise ConfigError("pipeline inference needs at least 2 stages")
+    prompt = [int(t) for t in prompt]
+    if not prompt:
+        raise ConfigError("prompt must be non-empty")
+    if not 0.0 < threshold <= 1.0:
+        raise ConfigError("threshold must lie in (0, 1]")
+    cfg = part.config
+    _check_context(cfg, len(prompt) + max_new_tokens)
+    _lib.require_cuda()
+    if devices is None:
+        devices = ["cuda:0"] * part.num_stages
+    conf_log: dict = {}
+    lock = threading.Lock()
+    queues = [Queue() for _ in range(part.num_stages)]
+    emit_q: Queue = Queue()
+    stages = []
+    for i, spec in enumerate(part.stages):
+        q_out = queues[i + 1] if i + 1 < part.num_stages else None
+        stages.append(_InferStage(spec, cfg, threshold, queues[i], q_out, emit_q, conf_log, lock,
+                                  dtype, devices[i % len(devices)]))
+    threads = [threading.Thread(target=s.run, daemon=True, name=f"infer-stage-{s.spec.index}")
+               for s in stages]
+    for t in threads:
+        t.start()
+
+    first = stages[0].eng
+    t0 = len(prompt)
+    trace = GenerationTrace(prompt, threshold, "pipeline")
+
+    def embedded(tokens, positions):
+        with torch.cuda.device(first.device), torch.cuda.stream(first.stream):
+            first._grow(len(tokens))
+            first.embed_rows(tokens, positions, 0)
+            rows = first.x[:len(tokens)].clone()
+            ev = torch.cuda.Event()
+            ev.record(first.stream)
+        return rows, ev
+
+    t_start = time.perf_counter()
+    t_last = t_start
+    rows, ev = embedded(prompt, list(range(t0)))
+    queues[0].put(_FwdMsg(rows, list(range(t0)), t0 - 1, False, ev))
+    position = t0 - 1
+    try:
+        for i in range(max_new_tokens):
+            emit = emit_q.get(timeout=_EMIT_TIMEOUT)
+            if isinstance(emit, BaseException):
+                raise emit
+            trace.tokens.append(emit.token)
+            trace.exit_layers.append(emit.exit_layer)
+            trace.exit_stages.append(emit.exit_stage)
+            now = time.perf_counter()
+            trace.measured_latencies.append(now - t_last)
+            t_last = now
+            if i == max_new_tokens - 1:
+                break
+            position += 1
+            rows, ev = embedded([emit.token], [position])
+            queues[0].put(_FwdMsg(rows, [position], position, False, ev))
+    finally:
+        queues[0].put(_FwdMsg(None, [], -1, True, None, stop=True))
+        for t in threads:
+            t.join(timeout=_EMIT_TIMEOUT)
+    for s in stages:
+        if s.exception is not None:
+            raise s.exception
+    for s in stages:
+        s.stream.synchronize()
+    trace.measured_total = time.perf_counter() - t_start
+
+    gen = len(trace.tokens)
+    if gen:
+        for s in stages:
+            if not s.eng.kv.complete(t0 + gen - 1):
+                raise ConfigError("KV fill mask incomplete after generation")
+    trace.confidences = [conf_log.get(t0 - 1 + i, {}) for i in range(gen)]
+    times = stage_times if stage_times is not None else default_stage_times(part)
+    lat = inference_latency(trace.exit_stages, times)
+    trace.latencies = lat["pipeline_per_token"]
+    trace.total_latency = lat["pipeline_total"]
+    trace.baseline_latency = lat["sequential_total"]
+    return trace
+
+
+# ---------------------------------------------------------------------------
+# Reference decoding and mode comparison — eepipe/inference.py:547-613
+# ---------------------------------------------------------------------------
+
+
+def greedy_reference(model: EarlyExitModel, prompt, max_new_tokens, *, dtype=None, device=None):
+    """Full-prefix recomputation for every token with the final head only and
+    a fresh cache each step (the uncached oracle of `eepipe/inference.py
+    :547-569`), run on the same kernels."""
+    cfg = model.config
+    prompt = [int(t) for t in prompt]
+    _check_context(cfg, len(prompt) + max_new_tokens)
+    final = [hd for hd in model.heads if hd.is_final]
+    L = cfg.num_layers
+    eng = _engine_for(model, model.params, final, cfg, range(1, L + 1), True, dtype, device)
+    runner = _PassRunner(eng, 1.0, {})
+    toks = list(prompt)
+    out = []
+    torch = _torch()
+    with torch.cuda.device(eng.device), torch.cuda.stream(eng.stream):
+        for _ in range(max_new_tokens):
+            eng.kv.reset()
+            n = len(toks)
+            eng._grow(n)
+            eng.embed_rows(toks, range(n), 0)
+            decision, _ = runner.run(n, list(range(n)), [0] * n, n - 1, True)
+            out.append(decision[0])
+            toks.append(decision[0])
+    return out
+
+
+def compare_modes(model: EarlyExitModel, part: StagePartition, prompts, thresholds,
+                  max_new_tokens, max_deferred=4, *, dtype=None):
+    """Both inference methods over the prompt set; ``divergences`` is empty
+    when tokens, exit layers and confidences agree bitwise."""
+    report = {"divergences": [], "runs": []}
+    for p_idx, prompt in enumerate(prompts):
+        for thr in thresholds:
+            pipe = generate_pipeline(part, prompt, thr, max_new_tokens, dtype=dtype)
+            reco = generate_kv_recompute(model, prompt, thr, max_new_tokens, max_deferred,
+                                         dtype=dtype)
+            problem = None
+            if pipe.tokens != reco.tokens:
+                problem = next(i for i, (a, b) in enumerate(zip(pipe.tokens, reco.tokens))
+                               if a != b)
+            elif pipe.exit_layers != reco.exit_layers:
+                problem = "exit layers"
+            elif pipe.confidences != reco.confidences:
+                problem = "confidences"
+            if problem is not None:
+                report["divergences"].append({
+                    "prompt": p_idx, "threshold": thr, "first_diff": problem,
+                    "pipeline": pipe.tokens, "recompute": reco.tokens})
+                continue
+            report["runs"].append({
+                "prompt": p_idx, "threshold": thr, "tokens": list(pipe.tokens),
+                "mean_exit_layer": pipe.mean_exit_layer,
+                "pipeline_latency": pipe.total_latency, "pipeline_speedup": pipe.speedup,
+                "recompute_latency": reco.total_latency, "recompute_speedup": reco.speedup})
+    return report
+
+
+# ---------------------------------------------------------------------------
+# Parity/debug helpers (used by tests and the smoke check)
+# ---------------------------------------------------------------------------
+
+
+def prefill_taps(model: EarlyExitModel, tokens, *, dtype=None, device=None):
+    """Hidden states of every prompt row at every tap 0..L (a fresh cache),
+    as float32 numpy arrays — the GPU counterpart of running `_layer_step`
+    layer by layer over a prompt."""
+    torch = _torch()
+    cfg = model.config
+    L = cfg.num_layers
+    eng = _engine_for(model, model.params, model.heads, cfg, range(1, L + 1), True, dtype, device)
+    n = len(tokens)
+    taps = []
+    with torch.cuda.device(eng.device), torch.cuda.stream(eng.stream):
+        eng.kv.reset()
+        eng._grow(n)
+        eng.embed_rows(list(tokens), range(n), 0)
+        eng.upload_ctrl(list(range(n)))
+        taps.append(eng.x[:n].cpu().numpy().copy())
+        for l in range(1, L + 1):
+            eng.run_layers(l - 1, l, n, [n], n - 1, 0)
+            eng.kv.mark_written(l - 1, l, list(range(n)), n - 1)
+            taps.append(eng.x[:n].cpu().numpy().copy())
+    return taps
+
+
+def head_logits(model: EarlyExitModel, head_key, rows, threshold=1.0, *, dtype=None, device=None):
+    """Run one head's fused kernel on given float32 hidden rows (m <= 16)
+    with the debug logits dump enabled.  Returns (logits (m, V) float32,
+    tokens, confidences, fires) as numpy arrays."""
+    torch = _torch()
+    cfg = model.config
+    L = cfg.num_layers
+    eng = _engine_for(model, model.params, model.heads, cfg, range(1, L + 1), True, dtype, device)
+    hi = next(i for i, e in enumerate(eng.heads) if e.desc.key == head_key)
+    e = eng.heads[hi]
+    rows = np.asarray(rows, dtype=np.float32).reshape(-1, cfg.hidden_dim)
+    m = rows.shape[0]
+    if m > _HEAD_MAX_ROWS:
+        raise ConfigError(f"at most {_HEAD_MAX_ROWS} rows per head call")
+    with torch.cuda.device(eng.device), torch.cuda.stream(eng.stream):
+        eng._grow(m)
+        eng.x[:m].copy_(torch.from_numpy(rows))
+        eng.upload_ctrl(list(range(m)))
+        dbg = torch.zeros((m, e.V), dtype=torch.float32, device=eng.device)
+        h = eng.h
+        s = stream_ptr(eng.stream)
+        # same sequence as Engine.eval_head, plus the logits dump
+        xsrc, rows_ptr = eng.x, eng.ctrl_ptr(0)
+        if e.desc.kind == "mlp+embed":
+            call("ee_rmsnorm_rows", ptr(eng.x), h, rows_ptr, m, h, None, NORM_EPS,
+                 ptr(eng.head_x), _lib.EE_F32, s)
+            call("ee_rmsnorm_rows", ptr(eng.head_x), h, None, m, h, ptr(e.pre_norm), NORM_EPS,
+                 ptr(eng.head_xn), eng.dcode, s)
+            call("ee_gemv", ptr(eng.head_xn), m, h, ptr(e.w1t), 4 * h, eng.dcode, EE_EPI_GELU,
+                 ptr(eng.head_mid), 4 * h, s)
+            call("ee_gemv", ptr(eng.head_mid), m, 4 * h, ptr(e.w2t), h, eng.dcode,
+                 EE_EPI_RESIDUAL, ptr(eng.head_x), h, s)
+            xsrc, rows_ptr = eng.head_x, None
+        call("ee_rmsnorm_rows", ptr(xsrc), h, rows_ptr, m, h, ptr(e.norm), NORM_EPS,
+             ptr(eng.head_xn), eng.dcode, s)
+        call("ee_exit_head_infer", ptr(eng.head_xn), m, h, ptr(e.W), e.V, eng.dcode,
+             float(threshold), ptr(eng.r_tok), ptr(eng.r_conf), ptr(eng.r_fire), ptr(eng.r_bad),
+             ptr(dbg), ptr(eng.head_ws), eng.head_ws.numel(), s)
+        eng.fetch_results(1)
+        out = dbg.cpu().numpy()
+    return (out, eng.h_tok[0, :m].numpy().copy(), eng.h_conf[0, :m].numpy().copy(),
+            eng.h_fire[0, :m].numpy().astype(bool))

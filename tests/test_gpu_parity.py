@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference golden
+vectors and the float64 oracle.
+
+Tolerances (north star): fp32 parity mode — identical greedy tokens and exit
+layers, confidences within 1e-5 relative; bf16 perf mode — exit-head
+logits/confidence within 1e-3 relative (norm-wise for logits).
+"""
+import numpy as np
+import pytest
+
+import ee_oracle as O
+from helpers import (arrays, c1_config, gold, mlp_config, oracle_inputs, small_config,
+                     tap0_config)
+from paper_2312_04916_b200 import inference as I
+from paper_2312_04916_b200.errors import ConfigError, TokenError
+from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model, partition
+
+pytestmark = pytest.mark.gpu
+
+CONF_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return build_model(c1_config(), 0)
+
+
+@pytest.fixture(scope="module")
+def small():
+    return build_model(small_config(), 7)
+
+
+def _close_conf(ours, ref, rtol=CONF_RTOL):
+    assert len(ours) == len(ref)
+    for a, b in zip(ours, ref):
+        assert set(a) == set(b)
+        for k in a:
+            assert a[k] == pytest.approx(b[k], rel=rtol), (k, a[k], b[k])
+
+
+def _same_decisions(tr, ref):
+    assert tr.tokens == ref["tokens"]
+    assert tr.exit_layers == ref["exit_layers"]
+
+
+# ---- kernel-level parity on C1 (fp32) ----------------------------------------
+
+def test_c1_prefill_taps_match_reference(c1):
+    a = arrays()
+    taps = I.prefill_taps(c1, gold()["c1_prompt"], dtype="fp32")
+    for l in range(5):
+        ref = a[f"c1_tap{l}"]
+        err = np.abs(taps[l] - ref).max() / np.abs(ref).max()
+        assert err < 1e-5, (l, err)
+
+
+def test_c1_head_logits_match_reference(c1):
+    a = arrays()
+    for key, tap in (("exit_l1", 1), ("exit_l2", 2), ("final", 4)):
+        ref = a[f"c1_logits_{key}"]
+        lg, tok, conf, _ = I.head_logits(c1, key, a[f"c1_tap{tap}"][-1:], dtype="fp32")
+        assert np.abs(lg[0] - ref).max() / np.abs(ref).max() < 1e-5
+        _, rtok, rconf = O.exit_decision(ref, 1.0)
+        assert tok[0] == rtok
+        assert conf[0] == pytest.approx(rconf, rel=CONF_RTOL)
+
+
+# ---- end-to-end generation parity -------------------------------------------
+
+@pytest.mark.parametrize("tag,thr", [("thr08", 0.8), ("thr_force", 0.99 / 1024)])
+def test_c1_kv_recompute_matches_reference(c1, tag, thr):
+    ref = gold()[f"c1_{tag}"]
+    tr = I.generate_kv_recompute(c1, gold()["c1_prompt"], thr, 8, dtype="fp32")
+    _same_decisions(tr, ref)
+    _close_conf(tr.confidences, ref["confidences"])
+    assert tr.latencies == ref["latencies"]
+
+
+def test_small_modes_match_reference_and_each_other(small):
+    g = gold()
+    prompt = g["small_prompts"][0]
+    part = partition(small, 4)
+    for run in g["small_runs"]:
+        thr = run["threshold"]
+        if "recompute" in run:
+            tr = I.generate_kv_recompute(small, prompt, thr, 12, run["max_deferred"], dtype="fp32")
+            _same_decisions(tr, run["recompute"])
+            _close_conf(tr.confidences, run["recompute"]["confidences"])
+            assert tr.latencies == run["recompute"]["latencies"]
+        else:
+            tr = I.generate_pipeline(part, prompt, thr, 12, dtype="fp32")
+            _same_decisions(tr, run["pipeline"])
+            assert tr.exit_stages == run["pipeline"]["exit_stages"]
+            _close_conf(tr.confidences, run["pipeline"]["confidences"])
+            assert tr.latencies == run["pipeline"]["latencies"]
+
+
+def test_mixed_exit_layers_match_reference(small):
+    g = gold()
+    prompt = g["small_prompts"][0]
+    part = partition(small, 4)
+    for run in g["small_mixed"]:
+        if "recompute" in run:
+            tr = I.generate_kv_recompute(small, prompt, 0.015775, 16, run["max_deferred"],
+                                         dtype="fp32")
+            ref = run["recompute"]
+        else:
+            tr = I.generate_pipeline(part, prompt, 0.015775, 16, dtype="fp32")
+            ref = run["pipeline"]
+        _same_decisions(tr, ref)
+        _close_conf(tr.confidences, ref["confidences"])
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_gpu_modes_bitwise_equal(small, dtype):
+    """Row-stable kernels: pipeline and recompute agree BITWISE on the GPU
+    (tokens, exit layers, confidence dicts), like the reference's own test
+    (tests/test_inference.py:106-114)."""
+    prompt = gold()["small_prompts"][0]
+    part = partition(small, 4)
+    for thr in (1.0, 6.0 / 64, 0.99 / 64, 0.015775):
+        for md in (1, 2, 4):
+            pipe = I.generate_pipeline(part, prompt, thr, 12, dtype=dtype)
+            reco = I.generate_kv_recompute(small, prompt, thr, 12, md, dtype=dtype)
+            assert pipe.tokens == reco.tokens
+            assert pipe.exit_layers == reco.exit_layers
+            assert pipe.confidences == reco.confidences
+
+
+def test_greedy_reference_matches(small):
+    g = gold()
+    for p, ref in zip(g["small_prompts"], g["small_greedy"]):
+        assert I.greedy_reference(small, p, 10, dtype="fp32") == ref
+        assert I.generate_kv_recompute(small, p, 1.0, 10, dtype="fp32").tokens == ref
+
+
+def test_mlp_and_tap0_heads(small):
+    g = gold()
+    mm = build_model(mlp_config(), 0)
+    assert I.generate_kv_recompute(mm, [3, 1, 4], 1.0, 6, dtype="fp32").tokens == g["mlp_tokens"]
+    tr = I.generate_kv_recompute(mm, [3, 1, 4], 0.99 / 64, 6, dtype="fp32")
+    _same_decisions(tr, g["mlp_force"])
+    _close_conf(tr.confidences, g["mlp_force"]["confidences"])
+    tp = I.generate_pipeline(partition(mm, 2), [3, 1, 4], 0.99 / 64, 6, dtype="fp32")
+    _same_decisions(tp, g["mlp_pipe_force"])
+    mt = build_model(tap0_config(), 7)
+    tr = I.generate_kv_recompute(mt, g["small_prompts"][0], 0.99 / 64, 10, dtype="fp32")
+    _same_decisions(tr, g["tap0_reco"])
+    _close_conf(tr.confidences, g["tap0_reco"]["confidences"])
+    tp = I.generate_pipeline(partition(mt, 4), g["small_prompts"][0], 0.99 / 64, 10, dtype="fp32")
+    _same_decisions(tp, g["tap0_pipe"])
+    _close_conf(tp.confidences, g["tap0_pipe"]["confidences"])
+
+
+def test_max_deferred_one_forces_full_fill(small):
+    g = gold()["small_md1_14"]
+    tr = I.generate_kv_recompute(small, gold()["small_prompts"][0], 0.99 / 64, 14, 1, dtype="fp32")
+    _same_decisions(tr, g)
+    full = max(tr.latencies)
+    for i in range(1, len(tr.latencies) - 1):
+        if tr.latencies[i] < full:
+            assert tr.latencies[i + 1] == full
+
+
+def test_errors(small):
+    part = partition(small, 4)
+    with pytest.raises(TokenError):
+        I.generate_kv_recompute(small, [0] * 48, 1.0, 4)
+    with pytest.raises(TokenError):
+        I.generate_pipeline(part, [0] * 48, 1.0, 4)
+    with pytest.raises(ConfigError):
+        I.generate_kv_recompute(small, [], 1.0, 4)
+    with pytest.raises(ConfigError):
+        I.generate_kv_recompute(small, [1], 1.0, 4, max_deferred=0)
+    with pytest.raises(ConfigError):
+        I.generate_pipeline(partition(small, 1), [1, 2, 3], 1.0, 4)
+    with pytest.raises(TokenError):
+        I.generate_kv_recompute(small, [64], 1.0, 2)
+    cfg = ModelConfig(4, 32, 4, 64, 32, exits=(ExitSpec(2, "layer+embed", 0.5),))
+    with pytest.raises(ConfigError):
+        I.generate_kv_recompute(build_model(cfg, 0), [1, 2], 1.0, 4)
+
+
+def test_exit_decision_kats_on_gpu():
+    fire, tok, conf = I.exit_decision(np.zeros(4), 0.25)
+    assert conf == pytest.approx(0.25) and not fire and tok == 0
+    z = np.zeros(8)
+    z[3] = 30.0
+    fire, tok, conf = I.exit_decision(z, 0.8)
+    assert fire and tok == 3 and conf > 0.999999
+
+
+# ---- row stability of the raw kernels ------------------------------------------
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_head_kernel_row_stable(small, dtype):
+    rng = np.random.default_rng(0)
+    rows = rng.normal(size=(7, 32)).astype(np.float32)
+    full = I.head_logits(small, "final", rows, dtype=dtype)
+    for i in range(7):
+        one = I.head_logits(small, "final", rows[i:i + 1], dtype=dtype)
+        assert np.array_equal(full[0][i], one[0][0])
+        assert full[1][i] == one[1][0] and full[2][i] == one[2][0]
+
+
+# ---- bf16 at 7B width -------------------------------------------------------------
+
+def test_bf16_exit_head_7b_width():
+    """Exit-head logits/confidence at h=4096, V=50304 in bf16 within 1e-3
+    relative of the float64 oracle (weights and rows rounded to bf16 first,
+    so the tolerance measures the kernel, not the input rounding)."""
+    import torch
+    cfg = ModelConfig(1, 4096, 32, 50304, 16, exits=(ExitSpec(1, "minimalistic", 0.1),))
+    m = build_model(cfg, 0, init="device", dtype=torch.bfloat16)
+    rng = np.random.default_rng(3)
+    rows = (rng.normal(size=(5, 4096)) * 1.0).astype(np.float32)
+    lg, tok, conf, _ = I.head_logits(m, "exit_l1", rows, dtype="bf16")
+    W = m.params["exit_l1.out"].data.float().cpu().numpy().astype(np.float64)
+    xb = torch.from_numpy(rows).bfloat16().float().numpy().astype(np.float64)
+    ref = xb @ W.T
+    rel = np.linalg.norm(lg - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert rel.max() < 1e-3, rel
+    for i in range(5):
+        _, rtok, rconf = O.exit_decision(ref[i], 1.0)
+        assert conf[i] == pytest.approx(rconf, rel=1e-3)
+        if tok[i] != rtok:  # near-tie: report, allowed only within tolerance
+            assert abs(ref[i][tok[i]] - ref[i][rtok]) < 1e-3 * abs(ref[i][rtok])
