@@ -64,6 +64,13 @@ __device__ __forceinline__ void unit_partial(const float (*tile)[kMaxCols], int 
 }
 
 __device__ __forceinline__ void combine(float& m1, float& s1, int& i1, float m2, float s2, int i2) {
+    if (s2 == 0.f) return;  // empty partial (no units for this thread)
+    if (s1 == 0.f) {
+        m1 = m2;
+        s1 = s2;
+        i1 = i2;
+        return;
+    }
     const float M = fmaxf(m1, m2);
     const float s = s1 * expf(m1 - M) + s2 * expf(m2 - M);
     const int i = (m1 > m2) ? i1 : ((m2 > m1) ? i2 : min(i1, i2));

@@ -389,22 +389,28 @@ class Engine:
     def ctrl_ptr(self, off):
         return ctypes.c_void_p(self.ctrl.data_ptr() + 4 * off)
 
-    def embed_rows(self, tokens, positions, row0):
-        """x[row0:row0+m] = tok_emb[tokens] + pos_emb[positions]."""
-        torch = _torch()
+    def embed_rows(self, tokens, positions, row0, out=None, staging=None):
+        """x[row0:row0+m] = tok_emb[tokens] + pos_emb[positions]  (or into
+        ``out`` with a separate (ring, device buffer) ``staging`` pair, for an
+        embedder running beside the stage worker that owns ``x``)."""
         tokens = np.asarray(tokens, dtype=np.int64)
         if tokens.size and (tokens.min() < 0 or tokens.max() >= self.cfg.vocab_size):
             raise TokenError("token id out of vocabulary range")
         m = len(tokens)
-        self._grow(max(row0 + m, (m + 1) // 2))
+        if out is None:
+            self._grow(max(row0 + m, (m + 1) // 2))
+            dst = ctypes.c_void_p(self.x.data_ptr() + 4 * row0 * self.h)
+            ring, dbuf = self.ring, self.tokbuf
+        else:
+            dst = ptr(out)
+            ring, dbuf = staging
         stage = np.concatenate([tokens, np.asarray(positions, dtype=np.int64)])
-        self.ring.put(stage, self.tokbuf, self.stream)
+        ring.put(stage, dbuf, _torch().cuda.current_stream(self.device))
         self.h2d_bytes += 4 * len(stage)
         self.launches += 1
-        dbuf = self.tokbuf
         call("ee_embed", ptr(dbuf), ctypes.c_void_p(dbuf.data_ptr() + 4 * m), m,
-             ptr(self.tok_emb), ptr(self.pos_emb), self.h, self.dcode,
-             ctypes.c_void_p(self.x.data_ptr() + 4 * row0 * self.h), stream_ptr(self.stream))
+             ptr(self.tok_emb), ptr(self.pos_emb), self.h, self.dcode, dst,
+             stream_ptr(_torch().cuda.current_stream(self.device)))
 
     def eval_head(self, e: _Head, rows_ptr, m, threshold, slot):
         """Fused head on m gathered rows of x; results into result slot."""
@@ -827,14 +833,20 @@ def generate_pipeline(part: StagePartition, prompt, threshold, max_new_tokens, s
     first = stages[0].eng
     t0 = len(prompt)
     trace = GenerationTrace(prompt, threshold, "pipeline")
+    # the coordinator embeds on its own stream with its own staging buffers
+    # (stage 1's worker owns first.x and first.ring)
+    with torch.cuda.device(first.device):
+        emb_stream = torch.cuda.Stream(first.device)
+        cap = 2 * max(t0, 1) + 16
+        staging = (_PinnedRing(cap), torch.zeros(cap, dtype=torch.int32, device=first.device))
 
     def embedded(tokens, positions):
-        with torch.cuda.device(first.device), torch.cuda.stream(first.stream):
-            first._grow(len(tokens))
-            first.embed_rows(tokens, positions, 0)
-            rows = first.x[:len(tokens)].clone()
+        with torch.cuda.device(first.device), torch.cuda.stream(emb_stream):
+            rows = torch.empty((len(tokens), cfg.hidden_dim), dtype=torch.float32,
+                               device=first.device)
+            first.embed_rows(tokens, positions, 0, out=rows, staging=staging)
             ev = torch.cuda.Event()
-            ev.record(first.stream)
+            ev.record(emb_stream)
         return rows, ev
 
     t_start = time.perf_counter()
