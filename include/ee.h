@@ -44,6 +44,9 @@ extern "C" {
 /* dtypes */
 #define EE_F32 0
 #define EE_BF16 1
+/* bf16 weights in the TILED layout produced by ee_pack_tiled (activations and
+ * KV cache stay plain bf16): the TMA-fed GEMV path, K % 512 == 0 */
+#define EE_BF16_TILED 2
 
 /* GEMV epilogues */
 #define EE_EPI_STORE 0    /* out[r, n] = v            (float32 out)          */
@@ -62,6 +65,14 @@ int ee_abi_version(void);
 int ee_device_sms(void);
 
 size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, int64_t nh, int64_t s_max);
+
+/* HBM weight layout for the TMA-fed GEMV.  A (N, K) row-major bf16 matrix is
+ * re-laid out as [N/16 tiles][K/512 stages][16 rows][512] (zero rows pad N;
+ * 16-byte chunk c of row r stored at chunk c ^ (r & 7)), so each pipeline
+ * stage is one contiguous 16 KB bulk copy.  ee_tiled_weight_bytes returns 0
+ * when the shape is not packable (K % 512 != 0).  One-time, at load. */
+size_t ee_tiled_weight_bytes(int64_t N, int64_t K);
+int ee_pack_tiled(const void* W, int64_t N, int64_t K, void* out, void* stream);
 
 /* Token + position embedding rows: out[r] = tok_emb[tok[r]] + pos_emb[pos[r]]
  * (float32 out).  Replaces `_InferParams.embed` (eepipe/inference.py:187-191)
@@ -102,10 +113,11 @@ int ee_decode_attention(const float* q, int64_t m, const int32_t* pos, int32_t m
                         const void* kcache, const void* vcache, int64_t nh, int64_t dh, int dtype,
                         void* out, void* ws, size_t ws_bytes, void* stream);
 
-/* Fused inference exit head: for each of the m rows of xn (already
- * [normed and] cast, (m, h) dtype) computes logits = xn @ W^T over the
- * vocabulary WITHOUT writing them (unless logits_dbg != NULL), with a split-V
- * online (max, sum-exp, argmax) and a fixed-order merge, then
+/* Fused inference exit head: gathers the float32 residual rows x[rows[i]]
+ * (rows may be NULL), applies the head's RMSNorm (norm_w; NULL for a
+ * minimalistic exit), computes logits = xn @ W^T over the vocabulary WITHOUT
+ * writing them (unless logits_dbg != NULL, (m, V) float32), with a split-V
+ * (max, sum-exp, argmax) per vocabulary tile and a fixed-order merge, then
  *   token[r] = argmax (lowest index wins ties),
  *   conf[r]  = max softmax probability = 1 / sum exp(l - max),
  *   fire[r]  = threshold < 1 && conf > threshold.
@@ -113,7 +125,8 @@ int ee_decode_attention(const float* q, int64_t m, const int32_t* pos, int32_t m
  * NonFiniteError).  m <= 16 per call.  W is (V, h) row-major.
  * Replaces `head_logits` + `exit_decision` (eepipe/inference.py:118-133,
  * 175-185). */
-int ee_exit_head_infer(const void* xn, int64_t m, int64_t h, const void* W, int64_t V, int dtype,
+int ee_exit_head_infer(const float* x, int64_t ldx, const int32_t* rows, int64_t m, int64_t h,
+                       const float* norm_w, float eps, const void* W, int64_t V, int dtype,
                        float threshold, int32_t* token, float* conf, uint8_t* fire,
                        int32_t* nonfinite, float* logits_dbg, void* ws, size_t ws_bytes,
                        void* stream);

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libee.so")
 
 EE_OK, EE_ESHAPE, EE_ETOKEN, EE_ENONFINITE, EE_ECONFIG, EE_ECUDA = range(6)
-EE_F32, EE_BF16 = 0, 1
+EE_F32, EE_BF16, EE_BF16_TILED = 0, 1, 2
 EE_EPI_STORE, EE_EPI_RESIDUAL, EE_EPI_GELU = 0, 1, 2
 EE_OP_ATTENTION, EE_OP_EXIT_HEAD, EE_OP_DECODER, EE_OP_EXIT_HEAD_TRAIN = 1, 2, 3, 4
 
@@ -46,6 +46,8 @@ SIGNATURES = {
     "ee_abi_version": (c_int, []),
     "ee_device_sms": (c_int, []),
     "ee_workspace_bytes": (c_size_t, [c_int, c_int64, c_int64, c_int64, c_int64, c_int64]),
+    "ee_tiled_weight_bytes": (c_size_t, [c_int64, c_int64]),
+    "ee_pack_tiled": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "ee_embed": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int, c_void_p,
                          c_void_p]),
     "ee_rmsnorm_rows": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_float,
@@ -57,9 +59,9 @@ SIGNATURES = {
     "ee_decode_attention": (c_int, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                     c_int64, c_int64, c_int, c_void_p, c_void_p, c_size_t,
                                     c_void_p]),
-    "ee_exit_head_infer": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int, c_float,
-                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                   c_size_t, c_void_p]),
+    "ee_exit_head_infer": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p,
+                                   c_float, c_void_p, c_int64, c_int, c_float, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "ee_decode_layer": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int32,
                                 c_void_p]),
     "ee_decode_layers": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p,

@@ -1,6 +1,7 @@
 // libee.so: error handling, versioning and workspace sizing of the C-ABI.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "ee_common.cuh"
 
@@ -24,6 +25,26 @@ extern "C" const char* ee_last_error(void) { return g_err; }
 
 extern "C" int ee_abi_version(void) { return 1; }
 
+bool ee_pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("EE_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+int ee_sm_count() {
+    static int n = 0;
+    if (n <= 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 extern "C" int ee_device_sms(void) {
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return -1;
@@ -39,7 +60,7 @@ extern "C" size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, in
         case EE_OP_ATTENTION:
             return attention_ws_bytes(m, nh, nh > 0 ? h / nh : 0, s_max);
         case EE_OP_EXIT_HEAD:
-            return exit_head_ws_bytes(m, V);
+            return exit_head_ws_bytes(m, h, V);
         case EE_OP_DECODER:
             return attention_ws_bytes(m, nh, nh > 0 ? h / nh : 0, s_max);
         case EE_OP_EXIT_HEAD_TRAIN:

@@ -4,21 +4,42 @@
 // hidden axis as reshape(nh, dh) (eepipe/inference.py:207, 225), scale
 // 1/sqrt(dh).  Work is split into KV chunks of kChunk positions keyed by
 // POSITION ONLY (chunk c covers [64c, 64c+64) ∩ [0, p]), one CTA per
-// (head, row, chunk).  Each CTA writes (max, sum-exp, acc[dh]); the last CTA
-// of a (row, head) to finish merges the chunks in ascending order.  Nothing
-// depends on how many rows share the launch, so the result is row-stable.
-//
-// Bytes: K and V rows of the prefix are read once per (row, head); for the
-// rows of one recompute pass the shared prefix is L2-resident after the first
-// row touches it.
+// (head, row, chunk), 4 warps:
+//   scores: warp w takes positions j ≡ w (mod 4); each lane owns 4
+//           consecutive head dims (one 8-B bf16 / 16-B fp32 load per
+//           position), fixed xor-butterfly per score;
+//   P·V:    warp w accumulates the same positions, lane owns 4 dims;
+//           the 4 warp partials are summed in warp order.
+// Each CTA writes (max, sum-exp, acc[dh]); the last CTA of a (row, head)
+// merges the chunks in ascending order.  Nothing depends on how many rows
+// share the launch, so the result is row-stable.
 #include "ee_common.cuh"
 
 namespace {
 
 constexpr int kChunk = 64;
 constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerLaunch = 64;
+constexpr int kMaxDh = 256;
 
+__device__ __forceinline__ void load4(const float* p, float v[4]) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    v[0] = u.x;
+    v[1] = u.y;
+    v[2] = u.z;
+    v[3] = u.w;
+}
+__device__ __forceinline__ void load4(const bf16* p, float v[4]) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+    const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+    v[0] = fa.x;
+    v[1] = fa.y;
+    v[2] = fb.x;
+    v[3] = fb.y;
+}
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -36,12 +57,14 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos,
               const T* __restrict__ kc, const T* __restrict__ vc, int nh, int dh, float scale,
               T* __restrict__ out, float* __restrict__ part, int* __restrict__ ctr,
               int chunks_cap) {
-    extern __shared__ float sm[];
-    float* qs = sm;           // [dh]
-    float* sc = sm + dh;      // [kChunk]
+    __shared__ __align__(16) float qs[kMaxDh];
+    __shared__ float sc[kChunk];
+    __shared__ __align__(16) float red[kWarps][kMaxDh];
     __shared__ float s_m, s_l;
     __shared__ int s_last;
 
+    pdl_trigger_dev();
+    pdl_wait_dev();
     const int hh = blockIdx.x, r = blockIdx.y, c = blockIdx.z;
     const int h = nh * dh;
     const int p = pos[r];
@@ -54,12 +77,38 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos,
 
     const int j0 = c * kChunk;
     const int nj = min(kChunk, p + 1 - j0);
-    for (int jj = warp; jj < nj; jj += kThreads / 32) {
-        const T* kr = kc + (int64_t)(j0 + jj) * h + hh * dh;
-        float s = 0.f;
-        for (int d = lane; d < dh; d += 32) s = fmaf(qs[d], to_f32(kr[d]), s);
-        s = warp_sum(s);
-        if (lane == 0) sc[jj] = s * scale;
+    const T* kbase = kc + (int64_t)j0 * h + hh * dh;
+    const T* vbase = vc + (int64_t)j0 * h + hh * dh;
+
+    // scores: warp w owns positions w, w+4, ... (16 per warp for a full chunk);
+    // all K loads of a group of 8 positions are issued before any reduction
+    // so the warp has 8 independent requests in flight.
+    for (int j8 = warp; j8 < nj; j8 += 8 * kWarps) {
+        float s[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] = 0.f;
+        for (int d = lane * 4; d < dh; d += 128) {
+            float kv[8][4];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int jj = j8 + u * kWarps;
+                if (jj < nj) load4(kbase + (int64_t)jj * h + d, kv[u]);
+                else kv[u][0] = kv[u][1] = kv[u][2] = kv[u][3] = 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                s[u] = fmaf(qs[d], kv[u][0], s[u]);
+                s[u] = fmaf(qs[d + 1], kv[u][1], s[u]);
+                s[u] = fmaf(qs[d + 2], kv[u][2], s[u]);
+                s[u] = fmaf(qs[d + 3], kv[u][3], s[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float v = warp_sum(s[u]);
+            const int jj = j8 + u * kWarps;
+            if (lane == 0 && jj < nj) sc[jj] = v * scale;
+        }
     }
     __syncthreads();
     if (warp == 0) {
@@ -80,17 +129,43 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos,
     }
     __syncthreads();
 
+    // P·V: warp w over positions j ≡ w (mod 4), lane owns dims [4*lane + 128*i, +4)
+    for (int d = lane * 4; d < dh; d += 128) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        for (int j8 = warp; j8 < nj; j8 += 8 * kWarps) {
+            float vv[8][4];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int jj = j8 + u * kWarps;
+                if (jj < nj) load4(vbase + (int64_t)jj * h + d, vv[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int jj = j8 + u * kWarps;
+                if (jj < nj) {
+                    const float pj = sc[jj];
+                    a0 = fmaf(pj, vv[u][0], a0);
+                    a1 = fmaf(pj, vv[u][1], a1);
+                    a2 = fmaf(pj, vv[u][2], a2);
+                    a3 = fmaf(pj, vv[u][3], a3);
+                }
+            }
+        }
+        red[warp][d] = a0;
+        red[warp][d + 1] = a1;
+        red[warp][d + 2] = a2;
+        red[warp][d + 3] = a3;
+    }
+    __syncthreads();
+
     const int64_t slot = ((int64_t)r * nh + hh) * chunks_cap;
     const int stride = dh + 2;
     for (int d = tid; d < dh; d += kThreads) {
-        const T* vcol = vc + (int64_t)j0 * h + hh * dh + d;
-        float a = 0.f;
-        for (int jj = 0; jj < nj; ++jj) a = fmaf(sc[jj], to_f32(vcol[(int64_t)jj * h]), a);
-        if (nchunks == 1) {
+        const float a = ((red[0][d] + red[1][d]) + red[2][d]) + red[3][d];
+        if (nchunks == 1)
             out[(int64_t)r * h + hh * dh + d] = from_f32<T>(a / s_l);
-        } else {
+        else
             part[(slot + c) * stride + 2 + d] = a;
-        }
     }
     if (nchunks == 1) return;
     if (tid == 0) {
@@ -136,6 +211,9 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
                      void* ws, size_t ws_bytes, cudaStream_t s) {
     if (m == 0) return EE_OK;
     EE_REQUIRE(m > 0 && nh > 0 && dh > 0 && max_pos >= 0, EE_ESHAPE, "attention: bad shape");
+    EE_REQUIRE(dh % 4 == 0 && dh <= kMaxDh, EE_ESHAPE,
+               "attention: head_dim must be a multiple of 4 and <= %d (got %lld)", kMaxDh,
+               (long long)dh);
     const int chunks = max_pos / kChunk + 1;
     const size_t cbytes = counters_bytes(nh);
     EE_REQUIRE(ws != nullptr && ws_bytes >= cbytes, EE_ESHAPE, "attention: workspace too small");
@@ -144,26 +222,26 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
     EE_REQUIRE(chunks_cap >= chunks, EE_ESHAPE,
                "attention: workspace holds %lld chunks, need %d (max_pos %d)",
                (long long)chunks_cap, chunks, max_pos);
+    dtype = act_dtype(dtype);
     int* ctr = (int*)ws;
     float* part = (float*)((char*)ws + cbytes);
     const float scale = 1.0f / sqrtf((float)dh);
-    const size_t shm = (size_t)(dh + kChunk) * sizeof(float);
     const int64_t h = nh * dh;
     for (int64_t r0 = 0; r0 < m; r0 += kRowsPerLaunch) {
         const int64_t mr = m - r0 < kRowsPerLaunch ? m - r0 : kRowsPerLaunch;
         const dim3 grid((unsigned)nh, (unsigned)mr, (unsigned)chunks);
+        cudaError_t e;
         if (dtype == EE_BF16)
-            k_attn_decode<bf16><<<grid, kThreads, shm, s>>>(
-                q + r0 * h, pos + r0, (const bf16*)kc, (const bf16*)vc, (int)nh, (int)dh, scale,
-                (bf16*)out + r0 * h, part, ctr, (int)chunks_cap);
+            e = launch_ex(k_attn_decode<bf16>, grid, dim3(kThreads), 0, s, q + r0 * h, pos + r0,
+                          (const bf16*)kc, (const bf16*)vc, (int)nh, (int)dh, scale,
+                          (bf16*)out + r0 * h, part, ctr, (int)chunks_cap);
         else if (dtype == EE_F32)
-            k_attn_decode<float><<<grid, kThreads, shm, s>>>(
-                q + r0 * h, pos + r0, (const float*)kc, (const float*)vc, (int)nh, (int)dh, scale,
-                (float*)out + r0 * h, part, ctr, (int)chunks_cap);
+            e = launch_ex(k_attn_decode<float>, grid, dim3(kThreads), 0, s, q + r0 * h, pos + r0,
+                          (const float*)kc, (const float*)vc, (int)nh, (int)dh, scale,
+                          (float*)out + r0 * h, part, ctr, (int)chunks_cap);
         else
             return ee_fail(EE_ECONFIG, "attention: unknown dtype %d", dtype);
-        int rc = ee_check_launch("decode_attention");
-        if (rc) return rc;
+        if (e != cudaSuccess) return ee_fail(EE_ECUDA, "attention launch: %s", cudaGetErrorString(e));
     }
     return EE_OK;
 }

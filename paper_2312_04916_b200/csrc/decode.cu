@@ -19,21 +19,16 @@ extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, float
     const int64_t h = D->h;
     const int dt = D->dtype;
     int rc;
-    // h1 = rmsnorm(x, attn_norm)                          eepipe/inference.py:218
+    // 7 PDL-chained kernels; the TMA GEMVs prefetch their weights while the
+    // preceding (small) kernel runs
     if ((rc = launch_rmsnorm_rows(x, h, nullptr, m, h, L->attn_norm, D->eps, D->xn, dt, s))) return rc;
-    // q, k, v = h1 @ wq|wk|wv ; K/V of every row written   eepipe/inference.py:219-226
     if ((rc = launch_qkv(D->xn, m, h, L->wqkv, dt, D->q, L->kcache, L->vcache, pos, s))) return rc;
-    // a = attend(q) over cache[0..pos]                     eepipe/inference.py:226
     if ((rc = launch_attention(D->q, m, pos, max_pos, L->kcache, L->vcache, D->nh, h / D->nh, dt,
                                D->attn, D->ws, D->ws_bytes, s)))
         return rc;
-    // x = x + a @ wo                                       eepipe/inference.py:227
     if ((rc = launch_gemv(D->attn, m, h, L->wo, h, dt, EE_EPI_RESIDUAL, x, h, s))) return rc;
-    // h2 = rmsnorm(x, mlp_norm)                            eepipe/inference.py:228
     if ((rc = launch_rmsnorm_rows(x, h, nullptr, m, h, L->mlp_norm, D->eps, D->attn, dt, s))) return rc;
-    // u = gelu(h2 @ w1)                                    eepipe/inference.py:229
     if ((rc = launch_gemv(D->attn, m, h, L->w1, 4 * h, dt, EE_EPI_GELU, D->xn, 4 * h, s))) return rc;
-    // x = x + u @ w2                                       eepipe/inference.py:229
     return launch_gemv(D->xn, m, 4 * h, L->w2, h, dt, EE_EPI_RESIDUAL, x, h, s);
 }
 

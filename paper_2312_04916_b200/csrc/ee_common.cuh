@@ -71,4 +71,38 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
                      const void* kc, const void* vc, int64_t nh, int64_t dh, int dtype, void* out,
                      void* ws, size_t ws_bytes, cudaStream_t s);
 size_t attention_ws_bytes(int64_t m, int64_t nh, int64_t dh, int64_t s_max);
-size_t exit_head_ws_bytes(int64_t m, int64_t V);
+size_t exit_head_ws_bytes(int64_t m, int64_t h, int64_t V);
+
+// ---- programmatic dependent launch ----------------------------------------
+// Every kernel of the decode chain is launched with programmatic stream
+// serialization: it may start while its predecessor drains, does its
+// independent prologue (weight streaming, barrier init), then waits with
+// griddepcontrol.wait before touching the predecessor's outputs.
+__device__ __forceinline__ void pdl_wait_dev() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger_dev() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+bool ee_pdl_enabled();  // EE_PDL=0 disables (debug)
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = ee_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+int ee_sm_count();  // cached per process
+
+
+// ---- tiled bf16 weight layout (pack.cu) -------------------------------------
+constexpr int kTiledKS = 512;  // k elements per tile stage
+// activation / KV dtype for a weight dtype (tiled bf16 weights -> bf16)
+static inline int act_dtype(int dt) { return dt == EE_F32 ? EE_F32 : (dt == EE_BF16_TILED ? EE_BF16 : dt); }

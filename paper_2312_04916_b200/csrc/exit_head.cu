@@ -1,70 +1,52 @@
-// Fused inference exit head: [norm already applied] -> logits over the
-// vocabulary -> split-V online (max, sum-exp, argmax) -> fixed-order merge ->
-// (token, confidence, fire).  Logits never touch HBM (optional debug dump).
+// Fused inference exit head:
+//   [gather rows] -> [RMSNorm] -> logits over the vocabulary -> split-V
+//   (max, sum-exp, argmax) per 16-row vocabulary tile -> fixed-order merge ->
+//   (token, confidence, fire).  Logits never touch HBM (optional debug dump).
 //
 // Restates `head_logits` + `exit_decision` (eepipe/inference.py:118-133,
 // 175-185):  m = max(l); p = exp(l - m) / sum; token = argmax (lowest index
 // wins); conf = p[token] = 1 / sum exp(l - m); fire = thr < 1 && conf > thr.
 //
-// Work unit = 16 vocabulary rows x full h (bf16 tensor-core GEMV core) or
-// 8 rows (fp32 SIMT).  Units are handed out dynamically to warps of a
-// persistent grid (load balance across 148 SMs with no tail); each unit's
-// partial depends only on the unit, so the result is deterministic and
-// row-stable.  The last CTA to finish merges the partials in unit order with
-// a fixed-shape tree.
+// bf16: the TMA-bulk-fed GEMV body (gemv_tma.cuh) with the RMSNorm fused in
+// its prologue and a softmax-partial epilogue; tiles are statically
+// round-robined over a persistent grid, the last CTA to finish merges the
+// per-tile partials in tile order with a fixed-shape tree (deterministic,
+// row-stable).  fp32 (parity mode): RMSNorm launch + SIMT dot products with
+// the same partial/merge scheme.
 #include <algorithm>
 
 #include "gemv_core.cuh"
+#include "gemv_tma.cuh"
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
 constexpr int kMaxCols = 16;
-constexpr int kUnroll = 4;
 
 struct HeadWs {
-    int* unit_ctr;
     int* done_ctr;
     int* flag;
+    int* unit_ctr;
     float* pm;
     float* ps;
     int* pi;
+    float* xn;  // fp32 path: normalised rows (kMaxCols x h)
 };
 
 __host__ __device__ inline HeadWs head_ws(void* base, int64_t units) {
     HeadWs w;
     char* b = (char*)base;
-    w.unit_ctr = (int*)b;
-    w.done_ctr = (int*)(b + 4);
-    w.flag = (int*)(b + 8);
+    w.done_ctr = (int*)b;
+    w.flag = (int*)(b + 4);
+    w.unit_ctr = (int*)(b + 8);
     w.pm = (float*)(b + 256);
     w.ps = w.pm + units * kMaxCols;
     w.pi = (int*)(w.ps + units * kMaxCols);
+    w.xn = (float*)(w.pi + units * kMaxCols);
     return w;
 }
 
-// Serial (max, argmax, sum-exp) of one column over a unit's rows, ascending n.
-template <int R>
-__device__ __forceinline__ void unit_partial(const float (*tile)[kMaxCols], int c, int n0, int V,
-                                             float& mx, float& sum, int& idx, bool& bad) {
-    mx = -INFINITY;
-    idx = n0;
-    const int nr = min(R, V - n0);
-    for (int i = 0; i < nr; ++i) {
-        const float v = tile[i][c];
-        bad |= !isfinite(v);
-        if (v > mx) {
-            mx = v;
-            idx = n0 + i;
-        }
-    }
-    sum = 0.f;
-    for (int i = 0; i < nr; ++i) sum += expf(tile[i][c] - mx);
-}
-
 __device__ __forceinline__ void combine(float& m1, float& s1, int& i1, float m2, float s2, int i2) {
-    if (s2 == 0.f) return;  // empty partial (no units for this thread)
+    if (s2 == 0.f) return;  // empty partial
     if (s1 == 0.f) {
         m1 = m2;
         s1 = s2;
@@ -79,23 +61,24 @@ __device__ __forceinline__ void combine(float& m1, float& s1, int& i1, float m2,
     i1 = i;
 }
 
-// Last CTA: fixed-order merge of all unit partials for each column.
+// Fixed-order merge of all unit partials for each column (nthreads threads).
+template <int NT>
 __device__ void merge_and_decide(const HeadWs& w, int64_t units, int m, float thr, int32_t* token,
-                                 float* conf, uint8_t* fire, int32_t* nonfinite) {
-    __shared__ float sm_m[kThreads], sm_s[kThreads];
-    __shared__ int sm_i[kThreads];
-    const int tid = threadIdx.x;
+                                 float* conf, uint8_t* fire, int32_t* nonfinite, int tid,
+                                 void (*sync)()) {
+    __shared__ float sm_m[NT], sm_s[NT];
+    __shared__ int sm_i[NT];
     for (int c = 0; c < m; ++c) {
         float M = -INFINITY, S = 0.f;
         int I = 0x7fffffff;
-        for (int64_t u = tid; u < units; u += kThreads)
+        for (int64_t u = tid; u < units; u += NT)
             combine(M, S, I, __ldcg(w.pm + u * kMaxCols + c), __ldcg(w.ps + u * kMaxCols + c),
                     __ldcg(w.pi + u * kMaxCols + c));
         sm_m[tid] = M;
         sm_s[tid] = S;
         sm_i[tid] = I;
-        __syncthreads();
-        for (int s = kThreads / 2; s > 0; s >>= 1) {
+        sync();
+        for (int s = NT / 2; s > 0; s >>= 1) {
             if (tid < s) {
                 float a = sm_m[tid], b = sm_s[tid];
                 int i = sm_i[tid];
@@ -104,7 +87,7 @@ __device__ void merge_and_decide(const HeadWs& w, int64_t units, int m, float th
                 sm_s[tid] = b;
                 sm_i[tid] = i;
             }
-            __syncthreads();
+            sync();
         }
         if (tid == 0) {
             const float cf = 1.0f / sm_s[0];
@@ -112,15 +95,92 @@ __device__ void merge_and_decide(const HeadWs& w, int64_t units, int m, float th
             conf[c] = cf;
             fire[c] = (thr < 1.0f && cf > thr) ? 1 : 0;
         }
-        __syncthreads();
+        sync();
     }
     if (tid == 0) {
         *nonfinite = __ldcg(w.flag);
         *w.flag = 0;
-        *w.unit_ctr = 0;
         *w.done_ctr = 0;
+        *w.unit_ctr = 0;
     }
 }
+
+__device__ void sync_consumers() { tma_gemv::consumers_sync(); }
+__device__ void sync_block() { __syncthreads(); }
+
+// ---- bf16: epilogue for the TMA body ---------------------------------------
+struct HeadEpi {
+    HeadWs w;
+    int V, m;
+    float thr;
+    int32_t *token, *nonfinite;
+    float* conf;
+    uint8_t* fire;
+    float* dbg;
+    bool bad;
+
+    __device__ void tile(const float* red, int n0, int r0, int N, int mm, int cols) {
+        using namespace tma_gemv;
+        const int tid = threadIdx.x;
+        const int nr = min(kRows, V - n0);
+        auto val = [&](int i, int c) {
+            const int o = i * kMaxCols + c;
+            return ((red[o] + red[kRows * kMaxCols + o]) + red[2 * kRows * kMaxCols + o]) +
+                   red[3 * kRows * kMaxCols + o];
+        };
+        if (tid < m) {
+            const int c = tid;
+            float mx = -INFINITY;
+            int idx = n0;
+            for (int i = 0; i < nr; ++i) {
+                const float v = val(i, c);
+                bad |= !isfinite(v);
+                if (v > mx) {
+                    mx = v;
+                    idx = n0 + i;
+                }
+            }
+            float sum = 0.f;
+            for (int i = 0; i < nr; ++i) sum += expf(val(i, c) - mx);
+            const int64_t u = n0 / kRows;
+            w.pm[u * kMaxCols + c] = mx;
+            w.ps[u * kMaxCols + c] = sum;
+            w.pi[u * kMaxCols + c] = idx;
+        }
+        if (dbg) {
+            for (int i = tid; i < kRows * m; i += kConsumers * 32) {
+                const int row = i & 15, c = i >> 4;
+                if (row < nr) dbg[(int64_t)c * V + n0 + row] = val(row, c);
+            }
+        }
+    }
+
+    __device__ void finish() {
+        using namespace tma_gemv;
+        __shared__ int s_last;
+        if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(w.flag, 1);
+        __threadfence();
+        consumers_sync();
+        if (threadIdx.x == 0) s_last = (atomicAdd(w.done_ctr, 1) == (int)gridDim.x - 1);
+        consumers_sync();
+        if (!s_last) return;
+        __threadfence();
+        const int64_t units = (V + kRows - 1) / kRows;
+        merge_and_decide<kConsumers * 32>(w, units, m, thr, token, conf, fire, nonfinite,
+                                          threadIdx.x, sync_consumers);
+    }
+};
+
+template <int NB>
+__global__ void __launch_bounds__(tma_gemv::kThreads)
+k_exit_head_tma(const bf16* __restrict__ W, int V, int K, const bf16* __restrict__ X, int m,
+                HeadEpi epi) {
+    tma_gemv::gemv_body<NB>(W, V, K, X, K, m, epi);
+}
+
+// ---- fp32 parity path --------------------------------------------------------
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
 
 __device__ __forceinline__ int grab_unit(int* ctr) {
     int u = 0;
@@ -128,70 +188,16 @@ __device__ __forceinline__ int grab_unit(int* ctr) {
     return __shfl_sync(0xffffffffu, u, 0);
 }
 
-__device__ __forceinline__ bool finish_cta(const HeadWs& w) {
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(w.done_ctr, 1) == (int)gridDim.x - 1);
-    __syncthreads();
-    if (s_last) __threadfence();
-    return s_last;
-}
-
-template <int NB>
+template <typename TW>
 __global__ void __launch_bounds__(kThreads)
-k_exit_head_bf16(const bf16* __restrict__ X, int m, int64_t K, const bf16* __restrict__ W, int V,
-                 float thr, int32_t* token, float* conf, uint8_t* fire, int32_t* nonfinite,
-                 float* logits_dbg, void* ws) {
-    __shared__ float tiles[kWarps][16][kMaxCols];
-    const int64_t units = (V + 15) / 16;
-    const HeadWs w = head_ws(ws, units);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float (*tile)[kMaxCols] = tiles[warp];
-    bool bad = false;
-    for (int u = grab_unit(w.unit_ctr); u < units; u = grab_unit(w.unit_ctr)) {
-        float acc[NB][4];
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.f;
-        const int n0 = u * 16;
-        warp_tile_bf16<NB, kUnroll>(W, K, n0, V, X, K, 0, m, 0, 1, acc);
-        {
-            const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb) {
-                tile[g][nb * 8 + 2 * t] = acc[nb][0];
-                tile[g][nb * 8 + 2 * t + 1] = acc[nb][1];
-                tile[g + 8][nb * 8 + 2 * t] = acc[nb][2];
-                tile[g + 8][nb * 8 + 2 * t + 1] = acc[nb][3];
-            }
-        }
-        __syncwarp();
-        if (lane < m) {
-            float mx, sum;
-            int idx;
-            unit_partial<16>(tile, lane, n0, V, mx, sum, idx, bad);
-            w.pm[(int64_t)u * kMaxCols + lane] = mx;
-            w.ps[(int64_t)u * kMaxCols + lane] = sum;
-            w.pi[(int64_t)u * kMaxCols + lane] = idx;
-        }
-        if (logits_dbg) {
-            for (int i = lane; i < 16 * m; i += 32) {
-                const int row = i & 15, c = i >> 4;
-                if (n0 + row < V) logits_dbg[(int64_t)c * V + n0 + row] = tile[row][c];
-            }
-        }
-        __syncwarp();
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(w.flag, 1);
-    if (finish_cta(w)) merge_and_decide(w, units, m, thr, token, conf, fire, nonfinite);
-}
-
-__global__ void __launch_bounds__(kThreads)
-k_exit_head_f32(const float* __restrict__ X, int m, int64_t K, const float* __restrict__ W, int V,
+k_exit_head_simt(const float* __restrict__ X, int m, int64_t K, const TW* __restrict__ W, int V,
                 float thr, int32_t* token, float* conf, uint8_t* fire, int32_t* nonfinite,
                 float* logits_dbg, void* ws) {
     constexpr int RW = 8, RX = 4;
     __shared__ float tiles[kWarps][RW][kMaxCols];
+    __shared__ int s_last;
+    pdl_trigger_dev();
+    pdl_wait_dev();
     const int64_t units = (V + RW - 1) / RW;
     const HeadWs w = head_ws(ws, units);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -216,9 +222,19 @@ k_exit_head_f32(const float* __restrict__ X, int m, int64_t K, const float* __re
         }
         __syncwarp();
         if (lane < m) {
-            float mx, sum;
-            int idx;
-            unit_partial<RW>(tile, lane, n0, V, mx, sum, idx, bad);
+            const int nr = min(RW, V - n0);
+            float mx = -INFINITY;
+            int idx = n0;
+            for (int i = 0; i < nr; ++i) {
+                const float v = tile[i][lane];
+                bad |= !isfinite(v);
+                if (v > mx) {
+                    mx = v;
+                    idx = n0 + i;
+                }
+            }
+            float sum = 0.f;
+            for (int i = 0; i < nr; ++i) sum += expf(tile[i][lane] - mx);
             w.pm[(int64_t)u * kMaxCols + lane] = mx;
             w.ps[(int64_t)u * kMaxCols + lane] = sum;
             w.pi[(int64_t)u * kMaxCols + lane] = idx;
@@ -232,53 +248,95 @@ k_exit_head_f32(const float* __restrict__ X, int m, int64_t K, const float* __re
         __syncwarp();
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(w.flag, 1);
-    if (finish_cta(w)) merge_and_decide(w, units, m, thr, token, conf, fire, nonfinite);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(w.done_ctr, 1) == (int)gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    merge_and_decide<kThreads>(w, units, m, thr, token, conf, fire, nonfinite, threadIdx.x,
+                               sync_block);
 }
 
 }  // namespace
 
-// Workspace: 256 B of counters + (max, sum, idx) per (unit, column).  Sized
-// for the fp32 unit (8 rows), which is the larger count.  Zero once at
+// Workspace: 256 B of counters + (max, sum, idx) per (unit, column) for the
+// smaller fp32 unit (8 rows) + kMaxCols normalised fp32 rows.  Zero once at
 // allocation; every call leaves the counters zeroed.
-size_t exit_head_ws_bytes(int64_t /*m*/, int64_t V) {
+size_t exit_head_ws_bytes(int64_t /*m*/, int64_t h, int64_t V) {
     const int64_t units = (V + 7) / 8;
-    return 256 + (size_t)units * kMaxCols * 12;
+    return 256 + (size_t)units * kMaxCols * 12 + (size_t)kMaxCols * h * 4;
 }
 
-extern "C" int ee_exit_head_infer(const void* xn, int64_t m, int64_t h, const void* W, int64_t V,
-                                  int dtype, float threshold, int32_t* token, float* conf,
-                                  uint8_t* fire, int32_t* nonfinite, float* logits_dbg, void* ws,
-                                  size_t ws_bytes, void* stream) {
+extern "C" int ee_exit_head_infer(const float* x, int64_t ldx, const int32_t* rows, int64_t m,
+                                  int64_t h, const float* norm_w, float eps, const void* W,
+                                  int64_t V, int dtype, float threshold, int32_t* token,
+                                  float* conf, uint8_t* fire, int32_t* nonfinite,
+                                  float* logits_dbg, void* ws, size_t ws_bytes, void* stream) {
     if (m == 0) return EE_OK;
     EE_REQUIRE(m > 0 && m <= kMaxCols, EE_ESHAPE, "exit_head: 1 <= m <= %d rows per call (m=%lld)",
                kMaxCols, (long long)m);
     EE_REQUIRE(h > 0 && V > 0 && V < (1ll << 30), EE_ESHAPE, "exit_head: bad shape");
     EE_REQUIRE(threshold > 0.f && threshold <= 1.f, EE_ECONFIG, "threshold must lie in (0, 1]");
-    EE_REQUIRE(ws != nullptr && ws_bytes >= exit_head_ws_bytes(m, V), EE_ESHAPE,
+    EE_REQUIRE(ws != nullptr && ws_bytes >= exit_head_ws_bytes(m, h, V), EE_ESHAPE,
                "exit_head: workspace too small");
     cudaStream_t s = as_stream(stream);
-    int sms = ee_device_sms();
-    if (sms <= 0) sms = 148;
-    if (dtype == EE_BF16) {
-        EE_REQUIRE(h % 8 == 0, EE_ESHAPE, "exit_head bf16 needs h %% 8 == 0");
+    const int sms = ee_sm_count();
+    if (dtype == EE_BF16_TILED) {
+        EE_REQUIRE(h % kTiledKS == 0, EE_ESHAPE, "exit_head tiled needs h %% %d == 0", kTiledKS);
         const int64_t units = (V + 15) / 16;
-        const unsigned grid = (unsigned)std::min<int64_t>((units + kWarps - 1) / kWarps, (int64_t)sms * 4);
-        if (m <= 8)
-            k_exit_head_bf16<1><<<grid, kThreads, 0, s>>>((const bf16*)xn, (int)m, h, (const bf16*)W,
-                                                          (int)V, threshold, token, conf, fire,
-                                                          nonfinite, logits_dbg, ws);
-        else
-            k_exit_head_bf16<2><<<grid, kThreads, 0, s>>>((const bf16*)xn, (int)m, h, (const bf16*)W,
-                                                          (int)V, threshold, token, conf, fire,
-                                                          nonfinite, logits_dbg, ws);
-    } else if (dtype == EE_F32) {
+        HeadWs w = head_ws(ws, (V + 7) / 8);
+        HeadEpi epi{w, (int)V, (int)m, threshold, token, nonfinite, conf, fire, logits_dbg, false};
+        // gather + RMSNorm (or plain cast) of the evaluated rows -> bf16 (m, h)
+        int rc = launch_rmsnorm_rows(x, ldx, rows, m, h, norm_w, eps, w.xn, EE_BF16, s);
+        if (rc) return rc;
+        const bf16* xn = (const bf16*)w.xn;
+        const int nb = m <= 8 ? 1 : 2;
+        const size_t smem = tma_gemv::smem_bytes(nb);
+        const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / (smem + 1024)));
+        const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sms * per_sm);
+        static int conf_smem[2][16] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaError_t e;
+        if (nb == 1) {
+            if ((int)smem > conf_smem[0][dev & 15]) {
+                cudaFuncSetAttribute(k_exit_head_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                conf_smem[0][dev & 15] = (int)smem;
+            }
+            e = launch_ex(k_exit_head_tma<1>, dim3(grid), dim3(tma_gemv::kThreads), smem, s,
+                          (const bf16*)W, (int)V, (int)h, xn, (int)m, epi);
+        } else {
+            if ((int)smem > conf_smem[1][dev & 15]) {
+                cudaFuncSetAttribute(k_exit_head_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                conf_smem[1][dev & 15] = (int)smem;
+            }
+            e = launch_ex(k_exit_head_tma<2>, dim3(grid), dim3(tma_gemv::kThreads), smem, s,
+                          (const bf16*)W, (int)V, (int)h, xn, (int)m, epi);
+        }
+        if (e != cudaSuccess) return ee_fail(EE_ECUDA, "exit_head launch: %s", cudaGetErrorString(e));
+        return EE_OK;
+    }
+    if (dtype == EE_F32 || dtype == EE_BF16) {
+        // SIMT path: parity mode (fp32) and small row-major bf16 heads
+        HeadWs w = head_ws(ws, (V + 7) / 8);
+        int rc = launch_rmsnorm_rows(x, ldx, rows, m, h, norm_w, eps, w.xn, EE_F32, s);
+        if (rc) return rc;
         const int64_t units = (V + 7) / 8;
         const unsigned grid = (unsigned)std::min<int64_t>((units + kWarps - 1) / kWarps, (int64_t)sms * 4);
-        k_exit_head_f32<<<grid, kThreads, 0, s>>>((const float*)xn, (int)m, h, (const float*)W,
-                                                  (int)V, threshold, token, conf, fire, nonfinite,
-                                                  logits_dbg, ws);
-    } else {
-        return ee_fail(EE_ECONFIG, "exit_head: unknown dtype %d", dtype);
+        cudaError_t e;
+        if (dtype == EE_F32)
+            e = launch_ex(k_exit_head_simt<float>, dim3(grid), dim3(kThreads), 0, s,
+                          (const float*)w.xn, (int)m, h, (const float*)W, (int)V, threshold, token,
+                          conf, fire, nonfinite, logits_dbg, ws);
+        else
+            e = launch_ex(k_exit_head_simt<bf16>, dim3(grid), dim3(kThreads), 0, s,
+                          (const float*)w.xn, (int)m, h, (const bf16*)W, (int)V, threshold, token,
+                          conf, fire, nonfinite, logits_dbg, ws);
+        if (e != cudaSuccess) return ee_fail(EE_ECUDA, "exit_head launch: %s", cudaGetErrorString(e));
+        return EE_OK;
     }
-    return ee_check_launch("exit_head_infer");
+    return ee_fail(EE_ECONFIG, "exit_head: unknown dtype %d", dtype);
 }

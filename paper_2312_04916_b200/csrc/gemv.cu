@@ -1,10 +1,16 @@
-// Backbone GEMVs with fused epilogues (store / residual / GELU / QKV+KV-write).
+// Backbone GEMVs with fused epilogues.
 //
-// Grid: x over 16-row weight tiles (bf16) or 8-row tiles (fp32), y over
-// activation-row groups.  A CTA = 8 warps splitting K in interleaved 32-wide
-// blocks; the 8 partial tiles are summed in warp order (fixed), so results
-// are deterministic and independent of m.
+// EE_BF16_TILED (perf mode, weights packed by ee_pack_tiled, K % 512 == 0):
+//   the TMA-bulk-fed persistent kernel of gemv_tma.cuh, launched with
+//   programmatic dependent launch (weights stream before the dependency on
+//   the previous kernel resolves).
+// EE_BF16 (row-major weights, any K % 8 == 0): LDG + mma.sync kernel.
+// EE_F32 (parity mode): SIMT FFMA kernel.
+// All are row-stable: each output's reduction order depends only on (n, k).
+#include <algorithm>
+
 #include "gemv_core.cuh"
+#include "gemv_tma.cuh"
 
 namespace {
 
@@ -13,7 +19,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kUnroll = 4;
 constexpr int kF32RW = 8, kF32RX = 4;
 
-// ---- epilogues -----------------------------------------------------------
+// ---- element-wise epilogue functors --------------------------------------
 struct EpiStore {
     float* out;
     int64_t ldo;
@@ -56,12 +62,41 @@ struct EpiQKV {  // q, k, v = dot_rows(h1, wq|wk|wv); KVCache.fill (inference.py
     }
 };
 
-// ---- kernels -------------------------------------------------------------
+// Adapter: sum the 4 consumer-warp partial tiles in fixed order, apply Fn.
+template <class Fn>
+struct TileApply {
+    Fn fn;
+    __device__ void tile(const float* red, int n0, int r0, int N, int m, int cols) {
+        using namespace tma_gemv;
+        for (int i = threadIdx.x; i < kRows * cols; i += kConsumers * 32) {
+            const int row = i & 15, col = i >> 4;
+            const int o = row * kMaxCols + col;
+            const float v = ((red[o] + red[kRows * kMaxCols + o]) + red[2 * kRows * kMaxCols + o]) +
+                            red[3 * kRows * kMaxCols + o];
+            const int n = n0 + row, r = r0 + col;
+            if (n < N && r < m) fn(n, r, v);
+        }
+    }
+    __device__ void finish() {}
+};
+
+// ---- TMA-fed kernel (tiled weights) ------------------------------------------
+template <int NB, class Fn>
+__global__ void __launch_bounds__(tma_gemv::kThreads)
+k_gemv_tma(const bf16* __restrict__ W, int N, int K, const bf16* __restrict__ X, int64_t ldx,
+           int m, Fn fn) {
+    TileApply<Fn> epi{fn};
+    tma_gemv::gemv_body<NB>(W, N, K, X, ldx, m, epi);
+}
+
+// ---- LDG kernels (row-major bf16, fp32 parity mode) ----------------------------
 template <int NB, class Epi>
 __global__ void __launch_bounds__(kThreads)
 k_gemv_bf16(const bf16* __restrict__ W, int N, int64_t K, const bf16* __restrict__ X,
             int64_t ldx, int m, Epi epi) {
     __shared__ float red[kWarps][16][8 * NB];
+    pdl_trigger_dev();
+    pdl_wait_dev();
     const int warp = threadIdx.x >> 5;
     const int n0 = blockIdx.x * 16, r0 = blockIdx.y * 8 * NB;
     float acc[NB][4];
@@ -85,6 +120,8 @@ __global__ void __launch_bounds__(kThreads)
 k_gemv_f32(const float* __restrict__ W, int N, int64_t K, const float* __restrict__ X,
            int64_t ldx, int m, Epi epi) {
     __shared__ float red[kWarps][kF32RW][kF32RX];
+    pdl_trigger_dev();
+    pdl_wait_dev();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * kF32RW, r0 = blockIdx.y * kF32RX;
     float acc[kF32RW][kF32RX];
@@ -110,29 +147,71 @@ k_gemv_f32(const float* __restrict__ W, int N, int64_t K, const float* __restric
     }
 }
 
+// ---- launchers ------------------------------------------------------------
+template <int NB, class Fn>
+int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K, Fn fn,
+               cudaStream_t s) {
+    auto kern = k_gemv_tma<NB, Fn>;
+    const size_t smem = tma_gemv::smem_bytes(NB);
+    static bool configured[16] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!configured[dev & 15]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured[dev & 15] = true;
+    }
+    const int64_t tiles = (N + tma_gemv::kRows - 1) / tma_gemv::kRows;
+    const int64_t groups = (m + 8 * NB - 1) / (8 * NB);
+    const int64_t items = tiles * groups;
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
+    const unsigned grid = (unsigned)std::min<int64_t>(items, (int64_t)ee_sm_count() * per_sm);
+    cudaError_t e = launch_ex(kern, dim3(grid), dim3(tma_gemv::kThreads), smem, s,
+                              (const bf16*)W, (int)N, (int)K, X, ldx, (int)m, fn);
+    if (e != cudaSuccess) return ee_fail(EE_ECUDA, "gemv_tma launch: %s", cudaGetErrorString(e));
+    return EE_OK;
+}
+
+template <class Fn>
+int run_tma(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K, Fn fn,
+            cudaStream_t s) {
+    EE_REQUIRE(K % kTiledKS == 0, EE_ESHAPE, "tiled gemv needs K %% %d == 0 (K=%lld)", kTiledKS,
+               (long long)K);
+    if (m <= 8) return run_tma_nb<1>(X, ldx, m, W, N, K, fn, s);
+    return run_tma_nb<2>(X, ldx, m, W, N, K, fn, s);
+}
+
 template <class Epi>
 int run_bf16(const void* x, int64_t m, int64_t K, const void* W, int64_t N, Epi epi,
              cudaStream_t s) {
     EE_REQUIRE(K % 8 == 0, EE_ESHAPE, "bf16 gemv needs K %% 8 == 0 (K=%lld)", (long long)K);
     const unsigned gx = (unsigned)((N + 15) / 16);
-    if (m <= 8) {
-        k_gemv_bf16<1, Epi><<<dim3(gx, 1), kThreads, 0, s>>>((const bf16*)W, (int)N, K,
-                                                             (const bf16*)x, K, (int)m, epi);
-    } else {
-        const unsigned gy = (unsigned)((m + 15) / 16);
-        k_gemv_bf16<2, Epi><<<dim3(gx, gy), kThreads, 0, s>>>((const bf16*)W, (int)N, K,
-                                                              (const bf16*)x, K, (int)m, epi);
-    }
-    return ee_check_launch("gemv_bf16");
+    cudaError_t e;
+    if (m <= 8)
+        e = launch_ex(k_gemv_bf16<1, Epi>, dim3(gx, 1), dim3(kThreads), 0, s, (const bf16*)W,
+                      (int)N, K, (const bf16*)x, K, (int)m, epi);
+    else
+        e = launch_ex(k_gemv_bf16<2, Epi>, dim3(gx, (unsigned)((m + 15) / 16)), dim3(kThreads), 0,
+                      s, (const bf16*)W, (int)N, K, (const bf16*)x, K, (int)m, epi);
+    if (e != cudaSuccess) return ee_fail(EE_ECUDA, "gemv_bf16 launch: %s", cudaGetErrorString(e));
+    return EE_OK;
 }
 
 template <class Epi>
 int run_f32(const void* x, int64_t m, int64_t K, const void* W, int64_t N, Epi epi,
             cudaStream_t s) {
     const dim3 grid((unsigned)((N + kF32RW - 1) / kF32RW), (unsigned)((m + kF32RX - 1) / kF32RX));
-    k_gemv_f32<Epi><<<grid, kThreads, 0, s>>>((const float*)W, (int)N, K, (const float*)x, K,
-                                              (int)m, epi);
-    return ee_check_launch("gemv_f32");
+    cudaError_t e = launch_ex(k_gemv_f32<Epi>, grid, dim3(kThreads), 0, s, (const float*)W, (int)N,
+                              K, (const float*)x, K, (int)m, epi);
+    if (e != cudaSuccess) return ee_fail(EE_ECUDA, "gemv_f32 launch: %s", cudaGetErrorString(e));
+    return EE_OK;
+}
+
+template <class Epi>
+int run_any(int dtype, const void* x, int64_t m, int64_t K, const void* W, int64_t N, Epi epi,
+            cudaStream_t s) {
+    if (dtype == EE_BF16_TILED) return run_tma((const bf16*)x, K, m, W, N, K, epi, s);
+    if (dtype == EE_BF16) return run_bf16(x, m, K, W, N, epi, s);
+    return ee_fail(EE_ECONFIG, "gemv: unknown dtype %d", dtype);
 }
 
 }  // namespace
@@ -140,23 +219,21 @@ int run_f32(const void* x, int64_t m, int64_t K, const void* W, int64_t N, Epi e
 int launch_gemv(const void* x, int64_t m, int64_t K, const void* W, int64_t N, int dtype, int epi,
                 void* out, int64_t ldo, cudaStream_t s) {
     if (m == 0 || N == 0) return EE_OK;
-    EE_REQUIRE(m > 0 && K > 0 && N > 0 && N < (1ll << 31), EE_ESHAPE,
+    EE_REQUIRE(m > 0 && K > 0 && N > 0 && N < (1ll << 31) && K < (1ll << 30), EE_ESHAPE,
                "gemv: bad shape m=%lld K=%lld N=%lld", (long long)m, (long long)K, (long long)N);
     EE_REQUIRE(m <= 65535 * 16, EE_ESHAPE, "gemv: too many rows");
-    if (dtype == EE_BF16) {
-        switch (epi) {
-            case EE_EPI_STORE: return run_bf16(x, m, K, W, N, EpiStore{(float*)out, ldo}, s);
-            case EE_EPI_RESIDUAL: return run_bf16(x, m, K, W, N, EpiResidual{(float*)out, ldo}, s);
-            case EE_EPI_GELU: return run_bf16(x, m, K, W, N, EpiGelu<bf16>{(bf16*)out, ldo}, s);
-        }
-    } else if (dtype == EE_F32) {
+    if (dtype == EE_F32) {
         switch (epi) {
             case EE_EPI_STORE: return run_f32(x, m, K, W, N, EpiStore{(float*)out, ldo}, s);
             case EE_EPI_RESIDUAL: return run_f32(x, m, K, W, N, EpiResidual{(float*)out, ldo}, s);
             case EE_EPI_GELU: return run_f32(x, m, K, W, N, EpiGelu<float>{(float*)out, ldo}, s);
         }
-    } else {
-        return ee_fail(EE_ECONFIG, "gemv: unknown dtype %d", dtype);
+        return ee_fail(EE_ECONFIG, "gemv: unknown epilogue %d", epi);
+    }
+    switch (epi) {
+        case EE_EPI_STORE: return run_any(dtype, x, m, K, W, N, EpiStore{(float*)out, ldo}, s);
+        case EE_EPI_RESIDUAL: return run_any(dtype, x, m, K, W, N, EpiResidual{(float*)out, ldo}, s);
+        case EE_EPI_GELU: return run_any(dtype, x, m, K, W, N, EpiGelu<bf16>{(bf16*)out, ldo}, s);
     }
     return ee_fail(EE_ECONFIG, "gemv: unknown epilogue %d", epi);
 }
@@ -165,11 +242,9 @@ int launch_qkv(const void* xn, int64_t m, int64_t h, const void* Wqkv, int dtype
                void* kc, void* vc, const int32_t* pos, cudaStream_t s) {
     if (m == 0) return EE_OK;
     EE_REQUIRE(m > 0 && h > 0, EE_ESHAPE, "qkv: bad shape");
-    if (dtype == EE_BF16)
-        return run_bf16(xn, m, h, Wqkv, 3 * h, EpiQKV<bf16>{q, (bf16*)kc, (bf16*)vc, pos, (int)h}, s);
     if (dtype == EE_F32)
         return run_f32(xn, m, h, Wqkv, 3 * h, EpiQKV<float>{q, (float*)kc, (float*)vc, pos, (int)h}, s);
-    return ee_fail(EE_ECONFIG, "qkv: unknown dtype %d", dtype);
+    return run_any(dtype, xn, m, h, Wqkv, 3 * h, EpiQKV<bf16>{q, (bf16*)kc, (bf16*)vc, pos, (int)h}, s);
 }
 
 extern "C" int ee_gemv(const void* x, int64_t m, int64_t K, const void* W, int64_t N, int dtype,

@@ -100,13 +100,13 @@ __device__ __forceinline__ void store_frag(float (*tile)[8 * NB], const float (&
 // fp32 SIMT tile: RW weight rows x RX activation rows, lanes over
 // k = 32*(w0 + j*wstep) + lane.  Result reduced over the warp with a fixed
 // xor butterfly (every lane ends with the full warp sum).
-template <int RW, int RX>
-__device__ __forceinline__ void warp_tile_f32(const float* __restrict__ W, int64_t K, int n0,
+template <int RW, int RX, typename TW = float>
+__device__ __forceinline__ void warp_tile_f32(const TW* __restrict__ W, int64_t K, int n0,
                                               int N, const float* __restrict__ X, int64_t ldx,
                                               int r0, int m, int w0, int wstep,
                                               float (&acc)[RW][RX]) {
     const int lane = threadIdx.x & 31;
-    const float* wr[RW];
+    const TW* wr[RW];
     const float* xr[RX];
 #pragma unroll
     for (int i = 0; i < RW; ++i) wr[i] = W + (int64_t)min(n0 + i, N - 1) * K;
@@ -118,7 +118,7 @@ __device__ __forceinline__ void warp_tile_f32(const float* __restrict__ W, int64
         for (int j = 0; j < RX; ++j) xv[j] = __ldg(xr[j] + k);
 #pragma unroll
         for (int i = 0; i < RW; ++i) {
-            const float wv = __ldg(wr[i] + k);
+            const float wv = to_f32<TW>(wr[i][k]);
 #pragma unroll
             for (int j = 0; j < RX; ++j) acc[i][j] = fmaf(wv, xv[j], acc[i][j]);
         }

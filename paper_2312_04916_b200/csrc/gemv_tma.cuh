@@ -1,0 +1,223 @@
+// TMA-bulk-fed, row-stable GEMV for bf16 weights in the tiled layout
+// (pack.cu) on sm_100a.
+//
+//   v[r, n] = sum_k x[r, k] * W[n, k]     (x: bf16 rows, W: tiled bf16)
+//
+// Structure (persistent CTA, 5 warps, 2 CTAs per SM):
+//   warp 4, one elected lane = producer.  Streams the CTA's weight tiles
+//     through a ring of kStages shared-memory stages; a stage is one 16 x 512
+//     bf16 block = ONE 16 KB bulk async copy
+//     (`cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes`,
+//     SASS UBLKCP) completing on the stage's `wfull` mbarrier.  Weights never
+//     depend on the previous kernel, so the producer fills the whole ring
+//     BEFORE `griddepcontrol.wait`: under programmatic dependent launch the
+//     next GEMV's weights stream in while the previous kernel drains.  After
+//     the wait it also copies the stage's chunk of the activation rows
+//     (`xfull` mbarrier), so consumers never touch global memory.
+//   warps 0..3 = consumers: wait wfull[s] and xfull[s], build m16n8k16
+//     fragments with 16-B LDS (weights XOR-swizzled per row by the packer,
+//     activations padded: both conflict-free), mma.sync into fp32, release
+//     empty[s].  The 16 k-blocks of a stage are split round-robin over the 4
+//     warps and the 4 partial tiles are summed in warp order, so the
+//     reduction order of every output depends only on (n, k), never on the
+//     number of rows m (row-stable, the `dot_rows` contract of
+//     eepipe/_pykernels.py:14-17).
+#pragma once
+
+#include "ee_common.cuh"
+
+namespace tma_gemv {
+
+constexpr int kConsumers = 4;
+constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr int kRows = 16;
+constexpr int kStages = 4;
+constexpr int KS = kTiledKS;                  // 512 k per stage
+constexpr int kWBytes = kRows * KS * 2;       // 16 KB weight block per stage
+constexpr int kXPitch = KS * 2 + 16;          // padded activation row
+constexpr int kMaxCols = 16;                  // activation rows per work item (NB = 2)
+
+__host__ __device__ constexpr int stage_bytes(int NB) { return kWBytes + 8 * NB * kXPitch; }
+__host__ inline size_t smem_bytes(int NB) {
+    return (size_t)kStages * stage_bytes(NB) + 3 * kStages * 8 +
+           (size_t)kConsumers * kRows * kMaxCols * 4 + 64;
+}
+
+// ---- PTX wrappers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+}
+__device__ __forceinline__ uint4 lds16(uint32_t addr) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(addr));
+    return r;
+}
+
+// Work item i -> tile = i % tiles, column group = i / tiles; a CTA takes
+// items blockIdx.x, +gridDim.x, ...  Epi provides tile(red, n0, r0, N, m,
+// cols) and finish(), both called by the 128 consumer threads.
+// K must be a multiple of 512, W in the tiled layout.
+template <int NB, class Epi>
+__device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int K,
+                                          const bf16* __restrict__ X, int64_t ldx, int m,
+                                          Epi& epi) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int cols = 8 * NB;
+    constexpr int sbytes = stage_bytes(NB);
+    uint8_t* ring = smem;
+    uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + kStages * sbytes);
+    uint64_t* xfull = wfull + kStages;
+    uint64_t* empty = xfull + kStages;
+    float* red = reinterpret_cast<float*>(empty + kStages);  // [kConsumers][16][kMaxCols]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles = (N + kRows - 1) / kRows;
+    const int groups = (m + cols - 1) / cols;
+    const int items = tiles * groups;
+    const int nks = K / KS;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&wfull[s], 1);
+            mbar_init(&xfull[s], 1);
+            mbar_init(&empty[s], kConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_trigger_dev();
+
+    if (warp == kConsumers) {
+        // ---------------- producer (one lane) ----------------
+        if (lane != 0) return;
+        const int my_items =
+            items > (int)blockIdx.x ? (items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        const int total = my_items * nks;
+        auto issue_w = [&](int q) {
+            const int it = (int)blockIdx.x + (q / nks) * (int)gridDim.x;
+            const int ks = q % nks;
+            const int slot = q % kStages;
+            mbar_expect_tx(&wfull[slot], kWBytes);
+            bulk_g2s(ring + slot * sbytes, W + ((int64_t)(it % tiles) * nks + ks) * (kRows * KS),
+                     kWBytes, &wfull[slot]);
+        };
+        auto issue_x = [&](int q) {
+            const int it = (int)blockIdx.x + (q / nks) * (int)gridDim.x;
+            const int ks = q % nks;
+            const int slot = q % kStages;
+            const int r0 = (it / tiles) * cols;
+            const int mr = min(cols, m - r0);
+            uint8_t* dst = ring + slot * sbytes + kWBytes;
+            mbar_expect_tx(&xfull[slot], (uint32_t)(mr * KS * 2));
+            for (int r = 0; r < mr; ++r)
+                bulk_g2s(dst + r * kXPitch, X + (int64_t)(r0 + r) * ldx + (int64_t)ks * KS, KS * 2,
+                         &xfull[slot]);
+        };
+        // 1) weights for the first ring's worth of stages, before the
+        //    dependency on the previous kernel is resolved
+        const int pre = min(total, kStages);
+        for (int q = 0; q < pre; ++q) issue_w(q);
+        // 2) activations are produced by the previous kernel
+        pdl_wait_dev();
+        for (int q = 0; q < pre; ++q) issue_x(q);
+        // 3) steady state
+        for (int q = pre; q < total; ++q) {
+            mbar_wait(&empty[q % kStages], ((q / kStages) - 1) & 1);
+            issue_w(q);
+            issue_x(q);
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    pdl_wait_dev();  // epilogues read/write buffers shared with the predecessor
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t ring_u32 = smem_u32(ring);
+    int q = 0;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int tile = it % tiles;
+        const int grp = it / tiles;
+        const int n0 = tile * kRows;
+        const int r0 = grp * cols;
+        const int mr = min(cols, m - r0);
+        float acc[NB][4];
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.f;
+        // activation rows >= mr were not copied: read row mr-1 instead
+        // (columns are independent inside the MMA; those outputs are dropped)
+        uint32_t xoff[NB];
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) xoff[nb] = kWBytes + min(nb * 8 + g, mr - 1) * kXPitch + t * 16;
+        const uint32_t wa = g * (KS * 2), wb = (g + 8) * (KS * 2);
+
+        for (int ks = 0; ks < nks; ++ks, ++q) {
+            const int slot = q % kStages;
+            const uint32_t par = (q / kStages) & 1;
+            mbar_wait(&wfull[slot], par);
+            mbar_wait(&xfull[slot], par);
+            const uint32_t st = ring_u32 + slot * sbytes;
+#pragma unroll
+            for (int i = 0; i < KS / 32 / kConsumers; ++i) {
+                const int kb = warp + i * kConsumers;
+                const uint32_t sw = (uint32_t)(((kb * 4 + t) ^ g) * 16);  // swizzled chunk
+                const uint4 a = lds16(st + wa + sw);
+                const uint4 b = lds16(st + wb + sw);
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    const uint4 x = lds16(st + xoff[nb] + kb * 64);
+                    mma_16816(acc[nb], a.x, b.x, a.y, b.y, x.x, x.y);
+                    mma_16816(acc[nb], a.z, b.z, a.w, b.w, x.z, x.w);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+        // cross-warp reduction in fixed warp order, then the epilogue
+        float* rw = red + warp * kRows * kMaxCols;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+            rw[g * kMaxCols + nb * 8 + 2 * t] = acc[nb][0];
+            rw[g * kMaxCols + nb * 8 + 2 * t + 1] = acc[nb][1];
+            rw[(g + 8) * kMaxCols + nb * 8 + 2 * t] = acc[nb][2];
+            rw[(g + 8) * kMaxCols + nb * 8 + 2 * t + 1] = acc[nb][3];
+        }
+        consumers_sync();
+        epi.tile(red, n0, r0, N, m, cols);
+        consumers_sync();
+    }
+    epi.finish();
+}
+
+}  // namespace tma_gemv

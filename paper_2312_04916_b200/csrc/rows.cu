@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(kRowThreads)
 k_embed(const int32_t* __restrict__ tok, const int32_t* __restrict__ pos,
         const T* __restrict__ tok_emb, const T* __restrict__ pos_emb, int h,
         float* __restrict__ out) {
+    pdl_trigger_dev();
+    pdl_wait_dev();
     const int r = blockIdx.x;
     const T* te = tok_emb + (int64_t)tok[r] * h;
     const T* pe = pos_emb + (int64_t)pos[r] * h;
@@ -41,6 +43,8 @@ __global__ void __launch_bounds__(kRowThreads)
 k_rmsnorm_rows(const float* __restrict__ x, int64_t ldx, const int32_t* __restrict__ rows,
                int h, const float* __restrict__ w, float eps, TO* __restrict__ out) {
     __shared__ float sh[kRowThreads];
+    pdl_trigger_dev();
+    pdl_wait_dev();
     const int i = blockIdx.x;
     const int src = rows ? rows[i] : i;
     const float* xr = x + (int64_t)src * ldx;
@@ -63,15 +67,18 @@ int launch_rmsnorm_rows(const float* x, int64_t ldx, const int32_t* rows, int64_
     if (m == 0) return EE_OK;
     EE_REQUIRE(m > 0 && h > 0 && ldx >= h, EE_ESHAPE, "rmsnorm_rows: bad shape m=%lld h=%lld",
                (long long)m, (long long)h);
+    cudaError_t e;
+    dtype = act_dtype(dtype);
     if (dtype == EE_BF16)
-        k_rmsnorm_rows<bf16><<<(unsigned)m, kRowThreads, 0, s>>>(x, ldx, rows, (int)h, w, eps,
-                                                                 (bf16*)out);
+        e = launch_ex(k_rmsnorm_rows<bf16>, dim3((unsigned)m), dim3(kRowThreads), 0, s, x, ldx, rows,
+                      (int)h, w, eps, (bf16*)out);
     else if (dtype == EE_F32)
-        k_rmsnorm_rows<float><<<(unsigned)m, kRowThreads, 0, s>>>(x, ldx, rows, (int)h, w, eps,
-                                                                  (float*)out);
+        e = launch_ex(k_rmsnorm_rows<float>, dim3((unsigned)m), dim3(kRowThreads), 0, s, x, ldx,
+                      rows, (int)h, w, eps, (float*)out);
     else
         return ee_fail(EE_ECONFIG, "rmsnorm_rows: unknown dtype %d", dtype);
-    return ee_check_launch("rmsnorm_rows");
+    if (e != cudaSuccess) return ee_fail(EE_ECUDA, "rmsnorm_rows launch: %s", cudaGetErrorString(e));
+    return EE_OK;
 }
 
 extern "C" int ee_rmsnorm_rows(const float* x, int64_t ldx, const int32_t* rows, int64_t m,
@@ -85,13 +92,16 @@ extern "C" int ee_embed(const int32_t* tok, const int32_t* pos, int64_t m, const
     if (m == 0) return EE_OK;
     EE_REQUIRE(m > 0 && h > 0, EE_ESHAPE, "embed: bad shape");
     cudaStream_t s = as_stream(stream);
+    cudaError_t e;
+    dtype = act_dtype(dtype);
     if (dtype == EE_BF16)
-        k_embed<bf16><<<(unsigned)m, kRowThreads, 0, s>>>(tok, pos, (const bf16*)tok_emb,
-                                                          (const bf16*)pos_emb, (int)h, out);
+        e = launch_ex(k_embed<bf16>, dim3((unsigned)m), dim3(kRowThreads), 0, s, tok, pos,
+                      (const bf16*)tok_emb, (const bf16*)pos_emb, (int)h, out);
     else if (dtype == EE_F32)
-        k_embed<float><<<(unsigned)m, kRowThreads, 0, s>>>(tok, pos, (const float*)tok_emb,
-                                                           (const float*)pos_emb, (int)h, out);
+        e = launch_ex(k_embed<float>, dim3((unsigned)m), dim3(kRowThreads), 0, s, tok, pos,
+                      (const float*)tok_emb, (const float*)pos_emb, (int)h, out);
     else
         return ee_fail(EE_ECONFIG, "embed: unknown dtype %d", dtype);
-    return ee_check_launch("embed");
+    if (e != cudaSuccess) return ee_fail(EE_ECUDA, "embed launch: %s", cudaGetErrorString(e));
+    return EE_OK;
 }

@@ -287,6 +287,22 @@ class Engine:
             self.pos_emb = dev("pos_emb").contiguous() if has_embedding else None
             self.kv = KVCache(self.layer_indices, cfg.max_seq_len, cfg.num_heads,
                               h // cfg.num_heads, dtype, self.device)
+            # bf16 with h % 512 == 0: weights go to the tiled HBM layout of the
+            # TMA-fed GEMV (one 16 KB bulk copy per pipeline stage)
+            lib = _lib.load()
+            self.tiled = (self.dcode == _lib.EE_BF16 and lib.ee_tiled_weight_bytes(h, h) > 0)
+            self.wcode = _lib.EE_BF16_TILED if self.tiled else self.dcode
+
+            def mat(t):  # (N, K) row-major -> kernel layout
+                t = t.contiguous()
+                if not self.tiled:
+                    return t
+                out = torch.empty(lib.ee_tiled_weight_bytes(t.shape[0], t.shape[1]) // 2,
+                                  dtype=torch.bfloat16, device=self.device)
+                call("ee_pack_tiled", ptr(t), t.shape[0], t.shape[1], ptr(out),
+                     stream_ptr(self.stream))
+                return out
+
             self.packed = []
             self.layers_c = (_lib.EeLayer * max(1, len(self.layer_indices)))()
             for i, l in enumerate(self.layer_indices):
@@ -294,12 +310,13 @@ class Engine:
                 wqkv = torch.cat([dev(p + "wq").t(), dev(p + "wk").t(), dev(p + "wv").t()], 0)
                 lw = {
                     "attn_norm": dev(p + "attn_norm", torch.float32).contiguous(),
-                    "wqkv": wqkv.contiguous(),
-                    "wo": dev(p + "wo").t().contiguous(),
+                    "wqkv": mat(wqkv),
+                    "wo": mat(dev(p + "wo").t()),
                     "mlp_norm": dev(p + "mlp_norm", torch.float32).contiguous(),
-                    "w1": dev(p + "w1").t().contiguous(),
-                    "w2": dev(p + "w2").t().contiguous(),
+                    "w1": mat(dev(p + "w1").t()),
+                    "w2": mat(dev(p + "w2").t()),
                 }
+                del wqkv
                 self.packed.append(lw)
                 c = self.layers_c[i]
                 for k in ("attn_norm", "wqkv", "wo", "mlp_norm", "w1", "w2"):
@@ -313,8 +330,10 @@ class Engine:
                         f"head kind {hd.kind!r} is not supported for cached inference")
                 e = _Head()
                 e.desc = hd
-                e.W = dev(hd.param_names["out"]).contiguous()
-                e.V = e.W.shape[0]
+                w_out = dev(hd.param_names["out"])
+                e.V = w_out.shape[0]
+                e.W = mat(w_out)
+                del w_out
                 e.norm = (dev(hd.param_names["norm"], torch.float32).contiguous()
                           if "norm" in hd.param_names else None)
                 e.pre_norm = e.w1t = e.w2t = None
@@ -374,7 +393,7 @@ class Engine:
                 old = self._x_old
                 self.x[:old.shape[0]].copy_(old)
             self.dec = _lib.EeDecoder(h=h, nh=cfg.num_heads, s_max=cfg.max_seq_len,
-                                      max_rows=rows, dtype=self.dcode, eps=NORM_EPS,
+                                      max_rows=rows, dtype=self.wcode, eps=NORM_EPS,
                                       xn=self.xn.data_ptr(), q=self.q.data_ptr(),
                                       attn=self.attn.data_ptr(), ws=self.attn_ws.data_ptr(),
                                       ws_bytes=wsb)
@@ -412,7 +431,7 @@ class Engine:
              ptr(self.tok_emb), ptr(self.pos_emb), self.h, self.dcode, dst,
              stream_ptr(_torch().cuda.current_stream(self.device)))
 
-    def eval_head(self, e: _Head, rows_ptr, m, threshold, slot):
+    def eval_head(self, e: _Head, rows_ptr, m, threshold, slot, logits_dbg=None):
         """Fused head on m gathered rows of x; results into result slot."""
         h = self.h
         s = stream_ptr(self.stream)
@@ -429,15 +448,13 @@ class Engine:
                  EE_EPI_RESIDUAL, ptr(self.head_x), h, s)
             xsrc, rows_ptr = self.head_x, None
             self.launches += 4
-        call("ee_rmsnorm_rows", ptr(xsrc), h, rows_ptr, m, h, ptr(e.norm), NORM_EPS,
-             ptr(self.head_xn), self.dcode, s)
-        self.launches += 2
-        call("ee_exit_head_infer", ptr(self.head_xn), m, h, ptr(e.W), e.V, self.dcode,
-             float(threshold),
+        self.launches += 1 if self.dcode == _lib.EE_BF16 else 2
+        call("ee_exit_head_infer", ptr(xsrc), h, rows_ptr, m, h, ptr(e.norm), NORM_EPS,
+             ptr(e.W), e.V, self.wcode, float(threshold),
              ctypes.c_void_p(self.r_tok.data_ptr() + 4 * _HEAD_MAX_ROWS * slot),
              ctypes.c_void_p(self.r_conf.data_ptr() + 4 * _HEAD_MAX_ROWS * slot),
              ctypes.c_void_p(self.r_fire.data_ptr() + _HEAD_MAX_ROWS * slot),
-             ctypes.c_void_p(self.r_bad.data_ptr() + 4 * slot), None,
+             ctypes.c_void_p(self.r_bad.data_ptr() + 4 * slot), ptr(logits_dbg),
              ptr(self.head_ws), self.head_ws.numel(), s)
 
     def fetch_results(self, nslots):
@@ -460,7 +477,7 @@ class Engine:
         arr = (ctypes.c_int32 * n)(*m_active)
         layers = ctypes.c_void_p(ctypes.addressof(self.layers_c) +
                                  la * ctypes.sizeof(_lib.EeLayer))
-        self.launches += 7 * sum(1 for v in m_active if v)
+        self.launches += (5 if self.dcode == _lib.EE_BF16 else 7) * sum(1 for v in m_active if v)
         call("ee_decode_layers", ctypes.byref(self.dec), layers, n, n_rows, arr, ptr(self.x),
              self.ctrl_ptr(pos_off), int(max_pos), stream_ptr(self.stream))
 
@@ -1004,25 +1021,7 @@ def head_logits(model: EarlyExitModel, head_key, rows, threshold=1.0, *, dtype=N
         eng.x[:m].copy_(torch.from_numpy(rows))
         eng.upload_ctrl(list(range(m)))
         dbg = torch.zeros((m, e.V), dtype=torch.float32, device=eng.device)
-        h = eng.h
-        s = stream_ptr(eng.stream)
-        # same sequence as Engine.eval_head, plus the logits dump
-        xsrc, rows_ptr = eng.x, eng.ctrl_ptr(0)
-        if e.desc.kind == "mlp+embed":
-            call("ee_rmsnorm_rows", ptr(eng.x), h, rows_ptr, m, h, None, NORM_EPS,
-                 ptr(eng.head_x), _lib.EE_F32, s)
-            call("ee_rmsnorm_rows", ptr(eng.head_x), h, None, m, h, ptr(e.pre_norm), NORM_EPS,
-                 ptr(eng.head_xn), eng.dcode, s)
-            call("ee_gemv", ptr(eng.head_xn), m, h, ptr(e.w1t), 4 * h, eng.dcode, EE_EPI_GELU,
-                 ptr(eng.head_mid), 4 * h, s)
-            call("ee_gemv", ptr(eng.head_mid), m, 4 * h, ptr(e.w2t), h, eng.dcode,
-                 EE_EPI_RESIDUAL, ptr(eng.head_x), h, s)
-            xsrc, rows_ptr = eng.head_x, None
-        call("ee_rmsnorm_rows", ptr(xsrc), h, rows_ptr, m, h, ptr(e.norm), NORM_EPS,
-             ptr(eng.head_xn), eng.dcode, s)
-        call("ee_exit_head_infer", ptr(eng.head_xn), m, h, ptr(e.W), e.V, eng.dcode,
-             float(threshold), ptr(eng.r_tok), ptr(eng.r_conf), ptr(eng.r_fire), ptr(eng.r_bad),
-             ptr(dbg), ptr(eng.head_ws), eng.head_ws.numel(), s)
+        eng.eval_head(e, eng.ctrl_ptr(0), m, threshold, 0, logits_dbg=dbg)
         eng.fetch_results(1)
         out = dbg.cpu().numpy()
     return (out, eng.h_tok[0, :m].numpy().copy(), eng.h_conf[0, :m].numpy().copy(),
