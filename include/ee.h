@@ -70,9 +70,12 @@ size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, int64_t nh, i
  * re-laid out as [N/16 tiles][K/512 stages][16 rows][512] (zero rows pad N;
  * 16-byte chunk c of row r stored at chunk c ^ (r & 7)), so each pipeline
  * stage is one contiguous 16 KB bulk copy.  ee_tiled_weight_bytes returns 0
- * when the shape is not packable (K % 512 != 0).  One-time, at load. */
+ * when the shape is not packable (K % 512 != 0).  One-time, at load.
+ * col_scale (K float32, nullable) multiplies column k — how an RMSNorm
+ * weight is folded into the matrix that consumes the normed rows. */
 size_t ee_tiled_weight_bytes(int64_t N, int64_t K);
-int ee_pack_tiled(const void* W, int64_t N, int64_t K, void* out, void* stream);
+int ee_pack_tiled(const void* W, int64_t N, int64_t K, const float* col_scale, void* out,
+                  void* stream);
 
 /* Token + position embedding rows: out[r] = tok_emb[tok[r]] + pos_emb[pos[r]]
  * (float32 out).  Replaces `_InferParams.embed` (eepipe/inference.py:187-191)
@@ -146,8 +149,11 @@ typedef struct {
 
 typedef struct {
     int64_t h, nh, s_max, max_rows;
-    int dtype;
+    int dtype;  /* EE_F32, EE_BF16 or EE_BF16_TILED (weights of ee_layer_t) */
     float eps;
+    float* x;   /* (max_rows, h) float32 residual rows (the rows of a pass) */
+    void* xb;   /* tiled mode: (max_rows, h) bf16 copy of x */
+    float* ssq; /* tiled mode: (max_rows, h/16) per-16-column sums of x^2 */
     void* xn;   /* (max_rows, 4h) dtype scratch */
     float* q;   /* (max_rows, h) float32 scratch */
     void* attn; /* (max_rows, h) dtype scratch */
@@ -155,24 +161,33 @@ typedef struct {
     size_t ws_bytes;
 } ee_decoder_t;
 
-/* One transformer layer for the first m rows of x (float32, (m, h), updated
- * in place), KV written at pos[r] before any row attends:
- * RMSNorm -> QKV(+KV write) -> attention -> wo + residual -> RMSNorm ->
- * w1 + GELU -> w2 + residual.  Replaces `_layer_step`
- * (eepipe/inference.py:216-229). */
-int ee_decode_layer(const ee_decoder_t* dec, const ee_layer_t* layer, float* x, int64_t m,
+/* Row statistics for tiled mode: xb = bf16(x), ssq[r][t] = sum_{i<16}
+ * x[r][16t+i]^2.  Must be called for rows whose x was written outside the
+ * decoder (embedding, rows received from another pipeline stage); the
+ * decoder keeps them current for the rows it updates. */
+int ee_row_stats(const float* x, int64_t ldx, int64_t m, int64_t h, void* xb, float* ssq,
+                 void* stream);
+
+/* One transformer layer for rows [row0, row0+m) of dec->x (float32, updated
+ * in place), KV written at pos[i] (the positions of those rows) before any
+ * row attends: RMSNorm -> QKV(+KV write) -> attention -> wo + residual ->
+ * RMSNorm -> w1 + GELU -> w2 + residual.  In tiled mode the norm weights
+ * must have been folded into the Wqkv / W1 columns (ee_pack_tiled with
+ * col_scale).  Replaces `_layer_step` (eepipe/inference.py:216-229). */
+int ee_decode_layer(const ee_decoder_t* dec, const ee_layer_t* layer, int64_t row0, int64_t m,
                     const int32_t* pos, int32_t max_pos, void* stream);
 
-/* Layers [0, n_layers) of `layers` in order over n_rows rows of x that are
- * ordered by entry depth DESCENDING, so the rows a layer must advance (entry
- * < layer) are always a suffix: layer i advances rows [n_rows - m_active[i],
- * n_rows) (m_active[i] == 0 skips the layer).  This is the batched back-fill
+/* Layers [0, n_layers) of `layers` in order over rows [0, n_rows) of dec->x,
+ * which are ordered by entry depth DESCENDING, so the rows a layer must
+ * advance (entry < layer) are always a suffix: layer i advances rows
+ * [n_rows - m_active[i], n_rows) (m_active[i] == 0 skips the layer); pos
+ * holds the positions of rows 0..n_rows-1.  This is the batched back-fill
  * pass of KV recomputation (`run_pass` layer loop,
  * eepipe/inference.py:316-326): one weight read per layer serves every
  * deferred row plus the new one. */
 int ee_decode_layers(const ee_decoder_t* dec, const ee_layer_t* layers, int32_t n_layers,
-                     int64_t n_rows, const int32_t* m_active, float* x, const int32_t* pos,
-                     int32_t max_pos, void* stream);
+                     int64_t n_rows, const int32_t* m_active, const int32_t* pos, int32_t max_pos,
+                     void* stream);
 
 /* ---- training exit head (fused CE) ---------------------------------- */
 

@@ -36,8 +36,9 @@ class EeLayer(ctypes.Structure):
 
 class EeDecoder(ctypes.Structure):
     _fields_ = [("h", c_int64), ("nh", c_int64), ("s_max", c_int64), ("max_rows", c_int64),
-                ("dtype", c_int), ("eps", c_float), ("xn", c_void_p), ("q", c_void_p),
-                ("attn", c_void_p), ("ws", c_void_p), ("ws_bytes", c_size_t)]
+                ("dtype", c_int), ("eps", c_float), ("x", c_void_p), ("xb", c_void_p),
+                ("ssq", c_void_p), ("xn", c_void_p), ("q", c_void_p), ("attn", c_void_p),
+                ("ws", c_void_p), ("ws_bytes", c_size_t)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/ee.h
@@ -47,7 +48,8 @@ SIGNATURES = {
     "ee_device_sms": (c_int, []),
     "ee_workspace_bytes": (c_size_t, [c_int, c_int64, c_int64, c_int64, c_int64, c_int64]),
     "ee_tiled_weight_bytes": (c_size_t, [c_int64, c_int64]),
-    "ee_pack_tiled": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "ee_pack_tiled": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ee_row_stats": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
     "ee_embed": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int, c_void_p,
                          c_void_p]),
     "ee_rmsnorm_rows": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_float,
@@ -62,10 +64,10 @@ SIGNATURES = {
     "ee_exit_head_infer": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p,
                                    c_float, c_void_p, c_int64, c_int, c_float, c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
-    "ee_decode_layer": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int32,
+    "ee_decode_layer": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int32,
                                 c_void_p]),
     "ee_decode_layers": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p,
-                                 c_void_p, c_int32, c_void_p]),
+                                 c_int32, c_void_p]),
     "ee_exit_head_train": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                                    c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                    c_void_p]),

@@ -106,3 +106,17 @@ int ee_sm_count();  // cached per process
 constexpr int kTiledKS = 512;  // k elements per tile stage
 // activation / KV dtype for a weight dtype (tiled bf16 weights -> bf16)
 static inline int act_dtype(int dt) { return dt == EE_F32 ? EE_F32 : (dt == EE_BF16_TILED ? EE_BF16 : dt); }
+int launch_row_stats(const float* x, int64_t ldx, int64_t m, int64_t h, void* xb, float* ssq,
+                     cudaStream_t s);
+// tiled-mode GEMV with folded RMSNorm (ssq != nullptr) and, for residual
+// epilogues, refreshed row statistics (xb_out/ssq_out != nullptr)
+struct GemvNorm {
+    const float* ssq;  // input-row sum-of-squares partials (K/16 per row) or nullptr
+    float eps;
+    bf16* xb_out;      // residual epilogue: bf16 copy of the updated rows
+    float* ssq_out;    // residual epilogue: their sum-of-squares partials
+};
+int launch_gemv_tiled(const bf16* x, int64_t m, int64_t K, const void* W, int64_t N, int epi,
+                      void* out, int64_t ldo, GemvNorm nrm, cudaStream_t s);
+int launch_qkv_tiled(const bf16* x, int64_t m, int64_t h, const void* Wqkv, GemvNorm nrm,
+                     float* q, void* kc, void* vc, const int32_t* pos, cudaStream_t s);

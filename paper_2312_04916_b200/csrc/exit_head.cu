@@ -119,7 +119,8 @@ struct HeadEpi {
     float* dbg;
     bool bad;
 
-    __device__ void tile(const float* red, int n0, int r0, int N, int mm, int cols) {
+    __device__ void tile(const float* red, int n0, int r0, int N, int mm, int cols,
+                         const float* /*inv*/) {
         using namespace tma_gemv;
         const int tid = threadIdx.x;
         const int nr = min(kRows, V - n0);
@@ -175,7 +176,7 @@ template <int NB>
 __global__ void __launch_bounds__(tma_gemv::kThreads)
 k_exit_head_tma(const bf16* __restrict__ W, int V, int K, const bf16* __restrict__ X, int m,
                 HeadEpi epi) {
-    tma_gemv::gemv_body<NB>(W, V, K, X, K, m, epi);
+    tma_gemv::gemv_body<NB>(W, V, K, X, K, m, tma_gemv::RowNorm{nullptr, 0.f}, epi);
 }
 
 // ---- fp32 parity path --------------------------------------------------------

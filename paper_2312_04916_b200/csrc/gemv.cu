@@ -66,13 +66,15 @@ struct EpiQKV {  // q, k, v = dot_rows(h1, wq|wk|wv); KVCache.fill (inference.py
 template <class Fn>
 struct TileApply {
     Fn fn;
-    __device__ void tile(const float* red, int n0, int r0, int N, int m, int cols) {
+    __device__ void tile(const float* red, int n0, int r0, int N, int m, int cols,
+                         const float* inv) {
         using namespace tma_gemv;
         for (int i = threadIdx.x; i < kRows * cols; i += kConsumers * 32) {
             const int row = i & 15, col = i >> 4;
             const int o = row * kMaxCols + col;
-            const float v = ((red[o] + red[kRows * kMaxCols + o]) + red[2 * kRows * kMaxCols + o]) +
-                            red[3 * kRows * kMaxCols + o];
+            float v = ((red[o] + red[kRows * kMaxCols + o]) + red[2 * kRows * kMaxCols + o]) +
+                      red[3 * kRows * kMaxCols + o];
+            if (inv) v *= inv[col];
             const int n = n0 + row, r = r0 + col;
             if (n < N && r < m) fn(n, r, v);
         }
@@ -80,13 +82,51 @@ struct TileApply {
     __device__ void finish() {}
 };
 
+// Residual epilogue that also refreshes the row statistics consumed by the
+// next folded-norm GEMV: x += v, xb = bf16(x), ssq[r][n0/16] = sum of the 16
+// squares in ascending order (same arithmetic as k_row_stats).
+struct TileResidualStats {
+    float* x;
+    int64_t ldx;
+    bf16* xb;
+    float* ssq;
+    __device__ void tile(const float* red, int n0, int r0, int N, int m, int cols,
+                         const float* /*inv*/) {
+        using namespace tma_gemv;
+        __shared__ float vt[kRows][kMaxCols + 1];
+        for (int i = threadIdx.x; i < kRows * cols; i += kConsumers * 32) {
+            const int row = i & 15, col = i >> 4;
+            const int o = row * kMaxCols + col;
+            const float v = ((red[o] + red[kRows * kMaxCols + o]) + red[2 * kRows * kMaxCols + o]) +
+                            red[3 * kRows * kMaxCols + o];
+            const int n = n0 + row, r = r0 + col;
+            float nv = 0.f;
+            if (n < N && r < m) {
+                float* p = x + (int64_t)r * ldx + n;
+                nv = *p + v;
+                *p = nv;
+                xb[(int64_t)r * ldx + n] = __float2bfloat16_rn(nv);
+            }
+            vt[row][col] = nv;
+        }
+        consumers_sync();
+        const int c = threadIdx.x;
+        if (c < cols && r0 + c < m) {
+            float s = 0.f;
+#pragma unroll
+            for (int row = 0; row < kRows; ++row) s = fmaf(vt[row][c], vt[row][c], s);
+            ssq[(int64_t)(r0 + c) * (ldx >> 4) + (n0 >> 4)] = s;
+        }
+    }
+    __device__ void finish() {}
+};
+
 // ---- TMA-fed kernel (tiled weights) ------------------------------------------
-template <int NB, class Fn>
+template <int NB, class Epi>
 __global__ void __launch_bounds__(tma_gemv::kThreads)
 k_gemv_tma(const bf16* __restrict__ W, int N, int K, const bf16* __restrict__ X, int64_t ldx,
-           int m, Fn fn) {
-    TileApply<Fn> epi{fn};
-    tma_gemv::gemv_body<NB>(W, N, K, X, ldx, m, epi);
+           int m, tma_gemv::RowNorm rn, Epi epi) {
+    tma_gemv::gemv_body<NB>(W, N, K, X, ldx, m, rn, epi);
 }
 
 // ---- LDG kernels (row-major bf16, fp32 parity mode) ----------------------------
@@ -148,10 +188,10 @@ k_gemv_f32(const float* __restrict__ W, int N, int64_t K, const float* __restric
 }
 
 // ---- launchers ------------------------------------------------------------
-template <int NB, class Fn>
-int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K, Fn fn,
-               cudaStream_t s) {
-    auto kern = k_gemv_tma<NB, Fn>;
+template <int NB, class Epi>
+int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K,
+               tma_gemv::RowNorm rn, Epi epi, cudaStream_t s) {
+    auto kern = k_gemv_tma<NB, Epi>;
     const size_t smem = tma_gemv::smem_bytes(NB);
     static bool configured[16] = {};
     int dev = 0;
@@ -166,18 +206,24 @@ int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, 
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
     const unsigned grid = (unsigned)std::min<int64_t>(items, (int64_t)ee_sm_count() * per_sm);
     cudaError_t e = launch_ex(kern, dim3(grid), dim3(tma_gemv::kThreads), smem, s,
-                              (const bf16*)W, (int)N, (int)K, X, ldx, (int)m, fn);
+                              (const bf16*)W, (int)N, (int)K, X, ldx, (int)m, rn, epi);
     if (e != cudaSuccess) return ee_fail(EE_ECUDA, "gemv_tma launch: %s", cudaGetErrorString(e));
     return EE_OK;
 }
 
-template <class Fn>
-int run_tma(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K, Fn fn,
-            cudaStream_t s) {
+template <class Epi>
+int run_tma_epi(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K,
+                tma_gemv::RowNorm rn, Epi epi, cudaStream_t s) {
     EE_REQUIRE(K % kTiledKS == 0, EE_ESHAPE, "tiled gemv needs K %% %d == 0 (K=%lld)", kTiledKS,
                (long long)K);
-    if (m <= 8) return run_tma_nb<1>(X, ldx, m, W, N, K, fn, s);
-    return run_tma_nb<2>(X, ldx, m, W, N, K, fn, s);
+    if (m <= 8) return run_tma_nb<1>(X, ldx, m, W, N, K, rn, epi, s);
+    return run_tma_nb<2>(X, ldx, m, W, N, K, rn, epi, s);
+}
+
+template <class Fn>
+int run_tma(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K, Fn fn,
+            cudaStream_t s, tma_gemv::RowNorm rn = {nullptr, 0.f}) {
+    return run_tma_epi(X, ldx, m, W, N, K, rn, TileApply<Fn>{fn}, s);
 }
 
 template <class Epi>
@@ -245,6 +291,31 @@ int launch_qkv(const void* xn, int64_t m, int64_t h, const void* Wqkv, int dtype
     if (dtype == EE_F32)
         return run_f32(xn, m, h, Wqkv, 3 * h, EpiQKV<float>{q, (float*)kc, (float*)vc, pos, (int)h}, s);
     return run_any(dtype, xn, m, h, Wqkv, 3 * h, EpiQKV<bf16>{q, (bf16*)kc, (bf16*)vc, pos, (int)h}, s);
+}
+
+int launch_gemv_tiled(const bf16* x, int64_t m, int64_t K, const void* W, int64_t N, int epi,
+                      void* out, int64_t ldo, GemvNorm nrm, cudaStream_t s) {
+    if (m == 0 || N == 0) return EE_OK;
+    const tma_gemv::RowNorm rn{nrm.ssq, nrm.eps};
+    switch (epi) {
+        case EE_EPI_STORE: return run_tma(x, K, m, W, N, K, EpiStore{(float*)out, ldo}, s, rn);
+        case EE_EPI_GELU: return run_tma(x, K, m, W, N, K, EpiGelu<bf16>{(bf16*)out, ldo}, s, rn);
+        case EE_EPI_RESIDUAL:
+            if (nrm.xb_out && nrm.ssq_out) {
+                EE_REQUIRE(ldo % 16 == 0 && ldo == N, EE_ESHAPE, "residual stats need ldo == N");
+                return run_tma_epi(x, K, m, W, N, K, rn,
+                                   TileResidualStats{(float*)out, ldo, nrm.xb_out, nrm.ssq_out}, s);
+            }
+            return run_tma(x, K, m, W, N, K, EpiResidual{(float*)out, ldo}, s, rn);
+    }
+    return ee_fail(EE_ECONFIG, "gemv_tiled: unknown epilogue %d", epi);
+}
+
+int launch_qkv_tiled(const bf16* x, int64_t m, int64_t h, const void* Wqkv, GemvNorm nrm,
+                     float* q, void* kc, void* vc, const int32_t* pos, cudaStream_t s) {
+    if (m == 0) return EE_OK;
+    return run_tma(x, h, m, Wqkv, 3 * h, h, EpiQKV<bf16>{q, (bf16*)kc, (bf16*)vc, pos, (int)h}, s,
+                   tma_gemv::RowNorm{nrm.ssq, nrm.eps});
 }
 
 extern "C" int ee_gemv(const void* x, int64_t m, int64_t K, const void* W, int64_t N, int dtype,

@@ -40,7 +40,7 @@ constexpr int kMaxCols = 16;                  // activation rows per work item (
 __host__ __device__ constexpr int stage_bytes(int NB) { return kWBytes + 8 * NB * kXPitch; }
 __host__ inline size_t smem_bytes(int NB) {
     return (size_t)kStages * stage_bytes(NB) + 3 * kStages * 8 +
-           (size_t)kConsumers * kRows * kMaxCols * 4 + 64;
+           (size_t)kConsumers * kRows * kMaxCols * 4 + kMaxCols * 4 + 64;
 }
 
 // ---- PTX wrappers -----------------------------------------------------------
@@ -85,14 +85,26 @@ __device__ __forceinline__ uint4 lds16(uint32_t addr) {
     return r;
 }
 
+// Folded RMSNorm: when `ssq` is given, the activation rows are the RAW
+// residual rows (bf16 copy) and the norm weight has been folded into W's
+// columns at pack time; the consumers compute 1/rms per row from the
+// per-16-column sum-of-squares partials ssq[row][0..K/16) (summed in a fixed
+// order) and the epilogue scales each output by it:
+//   sum_k W[n,k] (x[k] w[k] / rms) = (1/rms) sum_k (W[n,k] w[k]) x[k].
+struct RowNorm {
+    const float* ssq;  // (rows, K/16) or nullptr
+    float eps;
+};
+
 // Work item i -> tile = i % tiles, column group = i / tiles; a CTA takes
 // items blockIdx.x, +gridDim.x, ...  Epi provides tile(red, n0, r0, N, m,
-// cols) and finish(), both called by the 128 consumer threads.
-// K must be a multiple of 512, W in the tiled layout.
+// cols, inv) and finish(), both called by the 128 consumer threads (inv is
+// the per-column 1/rms or nullptr).  K must be a multiple of 512, W in the
+// tiled layout.
 template <int NB, class Epi>
 __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int K,
                                           const bf16* __restrict__ X, int64_t ldx, int m,
-                                          Epi& epi) {
+                                          RowNorm rn, Epi& epi) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int cols = 8 * NB;
     constexpr int sbytes = stage_bytes(NB);
@@ -101,6 +113,7 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
     uint64_t* xfull = wfull + kStages;
     uint64_t* empty = xfull + kStages;
     float* red = reinterpret_cast<float*>(empty + kStages);  // [kConsumers][16][kMaxCols]
+    float* inv = red + kConsumers * kRows * kMaxCols;        // [kMaxCols]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles = (N + kRows - 1) / kRows;
@@ -166,12 +179,29 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
     const int g = lane >> 2, t = lane & 3;
     const uint32_t ring_u32 = smem_u32(ring);
     int q = 0;
+    int cur_grp = -1;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int tile = it % tiles;
         const int grp = it / tiles;
         const int n0 = tile * kRows;
         const int r0 = grp * cols;
         const int mr = min(cols, m - r0);
+        if (rn.ssq != nullptr && grp != cur_grp) {
+            // 1/rms of this group's rows: warp w sums rows w, w+4, ... ;
+            // lane-strided partials then a fixed xor butterfly
+            const int nt = K >> 4;
+            for (int c = warp; c < cols; c += kConsumers) {
+                const float* sr = rn.ssq + (int64_t)min(r0 + c, m - 1) * nt;
+                float s = 0.f;
+                for (int i = lane; i < nt; i += 32) s += sr[i];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) inv[c] = 1.0f / sqrtf(s / (float)K + rn.eps);
+            }
+            cur_grp = grp;
+            // visibility of inv[] to all consumers is ensured by the
+            // consumers_sync() preceding the epilogue
+        }
         float acc[NB][4];
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.f;
@@ -214,7 +244,7 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
             rw[(g + 8) * kMaxCols + nb * 8 + 2 * t + 1] = acc[nb][3];
         }
         consumers_sync();
-        epi.tile(red, n0, r0, N, m, cols);
+        epi.tile(red, n0, r0, N, m, cols, rn.ssq != nullptr ? inv : nullptr);
         consumers_sync();
     }
     epi.finish();

@@ -105,3 +105,46 @@ extern "C" int ee_embed(const int32_t* tok, const int32_t* pos, int64_t m, const
     if (e != cudaSuccess) return ee_fail(EE_ECUDA, "embed launch: %s", cudaGetErrorString(e));
     return EE_OK;
 }
+
+// ---- row statistics for the folded-RMSNorm GEMVs ---------------------------
+// xb = bf16(x) and ssq[r][t] = sum_{i<16} x[r][16t+i]^2 (ascending fmaf) —
+// exactly what the residual GEMV epilogue produces for rows it updates, so a
+// row's statistics do not depend on which kernel last wrote it.
+namespace {
+__global__ void __launch_bounds__(256)
+k_row_stats(const float* __restrict__ x, int64_t ldx, int m, int h, bf16* __restrict__ xb,
+            float* __restrict__ ssq) {
+    pdl_trigger_dev();
+    pdl_wait_dev();
+    const int nt = h >> 4;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)m * nt) return;
+    const int r = (int)(i / nt), t = (int)(i % nt);
+    const float* xr = x + (int64_t)r * ldx + t * 16;
+    bf16* br = xb + (int64_t)r * h + t * 16;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const float v = xr[k];
+        s = fmaf(v, v, s);
+        br[k] = __float2bfloat16_rn(v);
+    }
+    ssq[(int64_t)r * nt + t] = s;
+}
+}  // namespace
+
+int launch_row_stats(const float* x, int64_t ldx, int64_t m, int64_t h, void* xb, float* ssq,
+                     cudaStream_t s) {
+    if (m == 0) return EE_OK;
+    EE_REQUIRE(m > 0 && h > 0 && h % 16 == 0, EE_ESHAPE, "row_stats: h must be a multiple of 16");
+    const int64_t n = m * (h / 16);
+    cudaError_t e = launch_ex(k_row_stats, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, x,
+                              ldx, (int)m, (int)h, (bf16*)xb, ssq);
+    if (e != cudaSuccess) return ee_fail(EE_ECUDA, "row_stats launch: %s", cudaGetErrorString(e));
+    return EE_OK;
+}
+
+extern "C" int ee_row_stats(const float* x, int64_t ldx, int64_t m, int64_t h, void* xb,
+                            float* ssq, void* stream) {
+    return launch_row_stats(x, ldx, m, h, xb, ssq, as_stream(stream));
+}

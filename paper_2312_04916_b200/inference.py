@@ -293,13 +293,13 @@ class Engine:
             self.tiled = (self.dcode == _lib.EE_BF16 and lib.ee_tiled_weight_bytes(h, h) > 0)
             self.wcode = _lib.EE_BF16_TILED if self.tiled else self.dcode
 
-            def mat(t):  # (N, K) row-major -> kernel layout
+            def mat(t, col_scale=None):  # (N, K) row-major -> kernel layout
                 t = t.contiguous()
                 if not self.tiled:
                     return t
                 out = torch.empty(lib.ee_tiled_weight_bytes(t.shape[0], t.shape[1]) // 2,
                                   dtype=torch.bfloat16, device=self.device)
-                call("ee_pack_tiled", ptr(t), t.shape[0], t.shape[1], ptr(out),
+                call("ee_pack_tiled", ptr(t), t.shape[0], t.shape[1], ptr(col_scale), ptr(out),
                      stream_ptr(self.stream))
                 return out
 
@@ -308,12 +308,16 @@ class Engine:
             for i, l in enumerate(self.layer_indices):
                 p = f"layer{l}."
                 wqkv = torch.cat([dev(p + "wq").t(), dev(p + "wk").t(), dev(p + "wv").t()], 0)
+                attn_norm = dev(p + "attn_norm", torch.float32).contiguous()
+                mlp_norm = dev(p + "mlp_norm", torch.float32).contiguous()
                 lw = {
-                    "attn_norm": dev(p + "attn_norm", torch.float32).contiguous(),
-                    "wqkv": mat(wqkv),
+                    # tiled mode folds the RMSNorm weights into the consuming
+                    # matrices' columns (decode.cu)
+                    "attn_norm": attn_norm,
+                    "wqkv": mat(wqkv, attn_norm),
                     "wo": mat(dev(p + "wo").t()),
-                    "mlp_norm": dev(p + "mlp_norm", torch.float32).contiguous(),
-                    "w1": mat(dev(p + "w1").t()),
+                    "mlp_norm": mlp_norm,
+                    "w1": mat(dev(p + "w1").t(), mlp_norm),
                     "w2": mat(dev(p + "w2").t()),
                 }
                 del wqkv
@@ -376,8 +380,16 @@ class Engine:
         rows = max(rows, 2 * self.max_rows)
         h, cfg = self.h, self.cfg
         self._x_old = getattr(self, "x", None)
+        old_xb, old_ssq = getattr(self, "xb", None), getattr(self, "ssq", None)
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             self.x = torch.zeros((rows, h), dtype=torch.float32, device=self.device)
+            # tiled mode: bf16 copy + sum-of-squares partials of the residual rows
+            self.xb = torch.zeros((rows, h), dtype=torch.bfloat16, device=self.device)
+            self.ssq = torch.zeros((rows, max(1, h // 16)), dtype=torch.float32,
+                                   device=self.device)
+            if old_xb is not None:
+                self.xb[:old_xb.shape[0]].copy_(old_xb)
+                self.ssq[:old_ssq.shape[0]].copy_(old_ssq)
             self.xn = torch.empty((rows, 4 * h), dtype=self.dtype, device=self.device)
             self.q = torch.empty((rows, h), dtype=torch.float32, device=self.device)
             self.attn = torch.empty((rows, h), dtype=self.dtype, device=self.device)
@@ -394,6 +406,8 @@ class Engine:
                 self.x[:old.shape[0]].copy_(old)
             self.dec = _lib.EeDecoder(h=h, nh=cfg.num_heads, s_max=cfg.max_seq_len,
                                       max_rows=rows, dtype=self.wcode, eps=NORM_EPS,
+                                      x=self.x.data_ptr(), xb=self.xb.data_ptr(),
+                                      ssq=self.ssq.data_ptr(),
                                       xn=self.xn.data_ptr(), q=self.q.data_ptr(),
                                       attn=self.attn.data_ptr(), ws=self.attn_ws.data_ptr(),
                                       ws_bytes=wsb)
@@ -429,6 +443,19 @@ class Engine:
         self.launches += 1
         call("ee_embed", ptr(dbuf), ctypes.c_void_p(dbuf.data_ptr() + 4 * m), m,
              ptr(self.tok_emb), ptr(self.pos_emb), self.h, self.dcode, dst,
+             stream_ptr(_torch().cuda.current_stream(self.device)))
+        if out is None:
+            self.refresh_stats(row0, m)
+
+    def refresh_stats(self, row0, m):
+        """Tiled mode: bf16 copy + sum-of-squares partials of rows written
+        outside the decoder (embedding, rows received from another stage)."""
+        if not self.tiled or m == 0:
+            return
+        self.launches += 1
+        call("ee_row_stats", ctypes.c_void_p(self.x.data_ptr() + 4 * row0 * self.h), self.h, m,
+             self.h, ctypes.c_void_p(self.xb.data_ptr() + 2 * row0 * self.h),
+             ctypes.c_void_p(self.ssq.data_ptr() + 4 * row0 * (self.h // 16)),
              stream_ptr(_torch().cuda.current_stream(self.device)))
 
     def eval_head(self, e: _Head, rows_ptr, m, threshold, slot, logits_dbg=None):
@@ -477,8 +504,8 @@ class Engine:
         arr = (ctypes.c_int32 * n)(*m_active)
         layers = ctypes.c_void_p(ctypes.addressof(self.layers_c) +
                                  la * ctypes.sizeof(_lib.EeLayer))
-        self.launches += (5 if self.dcode == _lib.EE_BF16 else 7) * sum(1 for v in m_active if v)
-        call("ee_decode_layers", ctypes.byref(self.dec), layers, n, n_rows, arr, ptr(self.x),
+        self.launches += (5 if self.tiled else 7) * sum(1 for v in m_active if v)
+        call("ee_decode_layers", ctypes.byref(self.dec), layers, n, n_rows, arr,
              self.ctrl_ptr(pos_off), int(max_pos), stream_ptr(self.stream))
 
 
@@ -571,7 +598,7 @@ class _PassRunner:
             return decision is not None and not forced and decision[1] == tap and tap < L
 
         gates = eval_tap(0)
-        if gates and not forced:
+        if gates and not forced and (self.thr < 1.0 or L == 0):
             decide_from(len(slots))
             if decision is not None and decision[1] == 0:
                 self._log(slots, pos)
@@ -596,7 +623,9 @@ class _PassRunner:
                 l = l2 + 1
             la = tap + 1
             gates = eval_tap(tap)
-            if gates and not forced and decision is None:
+            # an early exit can only fire below threshold 1.0: at 1.0 the
+            # pass never stops early, so do not synchronise before the end
+            if gates and not forced and decision is None and (self.thr < 1.0 or tap == L):
                 decide_from(len(slots))
                 if stop_here(tap):
                     depth = tap
@@ -785,6 +814,7 @@ class _InferStage:
                     e._grow(n)
                     e.x[:n].copy_(msg.rows, non_blocking=True)
                     msg.rows.record_stream(self.stream)
+                    e.refresh_stats(0, n)
                     e.upload_ctrl(list(msg.positions))
                     self._check_heads(msg, 0, n)
                     max_pos = max(msg.positions)
