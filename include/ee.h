@@ -191,18 +191,22 @@ int ee_decode_layers(const ee_decoder_t* dec, const ee_layer_t* layers, int32_t 
 
 /* ---- training exit head (fused CE) ---------------------------------- */
 
-/* Weighted cross-entropy of one exit head and its gradients, without the
- * (n, V) logits in HBM.  x (n, h) bf16 (already normed if the head has a
- * norm), W (V, h) bf16, targets int64 (n).  Writes
+/* Weighted cross-entropy of one exit head and its gradients on tcgen05
+ * tensor cores, without the (n, V) logits in HBM (four TMA-fed tcgen05
+ * GEMMs whose epilogues do the online softmax; see exit_head_train.cu).
+ * x (n, h) bf16 (already normed if the head has a norm), W (V, h) bf16,
+ * Wt = W^T (h, V) bf16 or NULL (then transposed into the workspace),
+ * targets int64 (n), validated by the caller.  Writes
  *   *loss  = weight * mean_i CE_i (float32, device scalar),
  *   dx     = d loss / d x  (n, h) float32,
  *   dw_acc += d loss / d W (V, h) float32 (accumulated across microbatches).
- * Replaces `run_head` matmul + `cross_entropy` fwd/bwd + the matmul backward
- * (eepipe/model.py:219-230, eepipe/autodiff.py:158-179, 301-323,
- * eepipe/_ckernels.pyx:130-167). */
-int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
-                       const int64_t* targets, float weight, float* loss, float* dx, float* dw_acc,
-                       void* ws, size_t ws_bytes, void* stream);
+ * n, h, V multiples of 8.  Workspace: ee_workspace_bytes(EE_OP_EXIT_HEAD_TRAIN,
+ * n, h, V, 0, 0).  Replaces `run_head` matmul + `cross_entropy` fwd/bwd + the
+ * matmul backward (eepipe/model.py:219-230, eepipe/autodiff.py:158-179,
+ * 301-323, eepipe/_ckernels.pyx:130-167). */
+int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, const void* Wt,
+                       int64_t V, const int64_t* targets, float weight, float* loss, float* dx,
+                       float* dw_acc, void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

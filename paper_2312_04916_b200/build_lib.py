@@ -45,8 +45,7 @@ def build(force=False, verbose=False):
         if p.returncode != 0:
             sys.stderr.write(out.decode())
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", OUT + ".tmp",
-           "-lcuda"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", OUT + ".tmp"]
     subprocess.check_call(cmd)
     os.replace(OUT + ".tmp", OUT)
     with open(os.path.join(objdir, "ptxas.log"), "w") as f:

@@ -1,0 +1,280 @@
+// Warp-specialised tcgen05 GEMM for sm_100a:   C[M, N] = A[M, K] · B[N, K]^T
+// (both operands K-major bf16, fp32 accumulation in tensor memory), with
+// pluggable epilogues.  Used by the fused training exit head
+// (exit_head_train.cu).
+//
+//   warp 0 (one lane)  TMA producer: 128x64 A tile + BNx64 B tile per stage
+//                      (cp.async.bulk.tensor.2d, SWIZZLE_128B), 4-stage ring
+//                      of full/empty mbarriers.
+//   warp 1 (one lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16,
+//                      UMMA 128 x BN x 16, accumulator in TMEM; smem stages
+//                      are released with tcgen05.commit -> empty[s].
+//                      Two TMEM accumulators (2 x BN columns) so the
+//                      epilogue of tile i overlaps the MMAs of tile i+1.
+//   warps 2..5         epilogue: tcgen05.ld 32x32b.x16 (row = TMEM lane),
+//                      per-row epilogue functor, then release the TMEM
+//                      buffer (tmem_empty mbarrier).
+// Persistent grid (one CTA per SM), static tile schedule with M fastest so
+// CTAs working at the same time share the B tile in L2.
+#pragma once
+
+#include <cuda.h>
+
+#include "ee_common.cuh"
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr int kABytes = BM * BK * 2;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024 /*align*/ + 256;
+};
+
+// ---- PTX wrappers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TCW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TCW_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// K-major, 128-byte swizzle, canonical UMMA layout: rows of 128 B, 8-row
+// atoms 1024 B apart (SBO), LBO unused (1), descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
+    return (uint64_t)((smem_addr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Kernel.  Epi::chunk(row, col0, v[16], nvalid) is called per 16-column chunk
+// for every row of the tile (called by the owning epilogue thread, in
+// ascending column order); Epi::begin_tile / end_tile bracket a tile for
+// the thread's row.
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M,
+          int N, int K, Epi epi) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+    const int ntiles = tiles_m * tiles_n;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mb_init(&full[s], 1);
+            mb_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mb_init(&tfull[b], 1);
+            mb_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(tmem_slot)),
+                     "n"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&ta) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tb) : "memory");
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int mb = t % tiles_m, nb = t / tiles_m;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mb_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * C::kStageBytes;
+                    mb_expect_tx(&full[s], C::kStageBytes);
+                    tma_load_2d(st, &ta, kb * BK, mb * BM, &full[s]);
+                    tma_load_2d(st + kABytes, &tb, kb * BK, nb * BN, &full[s]);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+            int s = 0;
+            uint32_t ph = 0;
+            int acc = 0;
+            uint32_t aph = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mb_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mb_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = su32(smem + s * C::kStageBytes);
+                    const uint32_t b0 = a0 + kABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc_mma(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                               (kb | k) != 0);
+                    tc_commit(&empty[s]);  // smem stage free once these MMAs completed
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                if (++acc == 2) {
+                    acc = 0;
+                    aph ^= 1;
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue (warps 2..5) ----------------
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int row_in_tile = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int mb = t % tiles_m, nb = t / tiles_m;
+            mb_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = mb * BM + row_in_tile;
+            const int col0 = nb * BN;
+            epi.begin_tile(row, col0, nb, row < M);
+            const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 16) {
+                float v[16];
+                tmem_ld16(base + c, v);
+                const int nvalid = min(16, N - (col0 + c));
+                if (row < M && nvalid > 0) epi.chunk(row, col0 + c, v, nvalid);
+            }
+            epi.end_tile(row, col0, nb, row < M);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(C::kTmemCols));
+    }
+}
+
+// Host: 2-D bf16 tensor map of a row-major (rows x cols) matrix, box
+// (64 cols x box_rows rows), 128-byte swizzle, zero fill out of bounds.
+int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+
+template <int BN, class Epi>
+int launch_tc_gemm(const void* A, const void* B, int M, int N, int K, Epi epi, cudaStream_t s) {
+    CUtensorMap ta, tb;
+    int rc;
+    if ((rc = make_tmap_bf16(&ta, A, M, K, BM))) return rc;
+    if ((rc = make_tmap_bf16(&tb, B, N, K, BN))) return rc;
+    auto kern = k_tc_gemm<BN, Epi>;
+    static bool configured[16] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!configured[dev & 15]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<BN>::kSmem);
+        configured[dev & 15] = true;
+    }
+    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int grid = tiles < ee_sm_count() ? tiles : ee_sm_count();
+    kern<<<grid, kThreads, Cfg<BN>::kSmem, s>>>(ta, tb, M, N, K, epi);
+    return ee_check_launch("tc_gemm");
+}
+
+}  // namespace tc
