@@ -194,8 +194,8 @@ int ee_decode_layers(const ee_decoder_t* dec, const ee_layer_t* layers, int32_t 
 /* Weighted cross-entropy of one exit head and its gradients on tcgen05
  * tensor cores, without the (n, V) logits in HBM (four TMA-fed tcgen05
  * GEMMs whose epilogues do the online softmax; see exit_head_train.cu).
- * x (n, h) bf16 (already normed if the head has a norm), W (V, h) bf16,
- * Wt = W^T (h, V) bf16 or NULL (then transposed into the workspace),
+ * x (n, h) bf16 (already normed if the head has a norm), W (V, h) bf16
+ * (both also read MN-major by the backward GEMMs: no transposed copies),
  * targets int64 (n), validated by the caller.  Writes
  *   *loss  = weight * mean_i CE_i (float32, device scalar),
  *   dx     = d loss / d x  (n, h) float32,
@@ -204,9 +204,9 @@ int ee_decode_layers(const ee_decoder_t* dec, const ee_layer_t* layers, int32_t 
  * n, h, V, 0, 0).  Replaces `run_head` matmul + `cross_entropy` fwd/bwd + the
  * matmul backward (eepipe/model.py:219-230, eepipe/autodiff.py:158-179,
  * 301-323, eepipe/_ckernels.pyx:130-167). */
-int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, const void* Wt,
-                       int64_t V, const int64_t* targets, float weight, float* loss, float* dx,
-                       float* dw_acc, void* ws, size_t ws_bytes, void* stream);
+int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
+                       const int64_t* targets, float weight, float* loss, float* dx, float* dw_acc,
+                       void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

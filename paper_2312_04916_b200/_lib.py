@@ -68,9 +68,9 @@ SIGNATURES = {
                                 c_void_p]),
     "ee_decode_layers": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p,
                                  c_int32, c_void_p]),
-    "ee_exit_head_train": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64,
-                                   c_void_p, c_float, c_void_p, c_void_p, c_void_p, c_void_p,
-                                   c_size_t, c_void_p]),
+    "ee_exit_head_train": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                   c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                   c_void_p]),
 }
 
 _lib = None

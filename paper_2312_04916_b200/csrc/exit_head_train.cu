@@ -12,11 +12,12 @@
 //                          sum-exp + the target logit (logits stay in TMEM)
 //   M   merge partials in fixed order -> lse, loss (deterministic)
 //   K2  S = X W^T (again)  epilogue: G = w/n (exp(S - lse) - [v == t]) in
-//                          bf16, stored row-major (G) and transposed (G^T)
-//   K3  dX  = G  . (W^T)^T  (A = G   [n x V], B = W^T [h x V], K = V)
-//   K4  dW += G^T . (X^T)^T (A = G^T [V x n], B = X^T [h x n], K = n)
-// Only the logit GRADIENT G (bf16) reaches HBM, and only because the two
-// backward GEMMs contract it along different axes; the logits themselves,
+//                          bf16 (row-major n x V)
+//   K3  dX  = G  W    A = G K-major, B = W read MN-major   (K = V)
+//   K4  dW += G^T X   A = G read MN-major, B = X MN-major  (K = n)
+// MN-major operands are consumed in place through the UMMA descriptor (no
+// transposed copies).  Only the logit GRADIENT G (bf16) reaches HBM, because
+// the two backward GEMMs contract it along different axes; the logits,
 // the softmax probabilities and the reference's cached (n, V) float64 probs
 // (_ckernels.pyx:130-151) never exist in memory.  Executed FLOPs are
 // 8 n h V (S is recomputed once); the roofline is quoted on the algorithmic
@@ -28,34 +29,31 @@
 namespace {
 
 constexpr int kBN = 256;
+constexpr int kParts = 2;  // per-row softmax partials per 256-column tile (epilogue halves)
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct TrainWs {
-    bf16 *xt, *wt, *g, *gt;
+    bf16* g;
     float *pmax, *psum, *tgt, *lse, *rowloss;
 };
 
-TrainWs carve(void* ws, int64_t n, int64_t h, int64_t V, bool need_wt) {
+TrainWs carve(void* ws, int64_t n, int64_t V) {
     TrainWs w;
     char* p = (char*)ws;
-    const int64_t ntn = (V + kBN - 1) / kBN;
-    w.xt = (bf16*)p; p += al((size_t)h * n * 2);
-    w.wt = need_wt ? (bf16*)p : nullptr; p += need_wt ? al((size_t)h * V * 2) : 0;
+    const int64_t ntn = kParts * ((V + kBN - 1) / kBN);
     w.pmax = (float*)p; p += al((size_t)n * ntn * 4);
     w.psum = (float*)p; p += al((size_t)n * ntn * 4);
     w.tgt = (float*)p; p += al((size_t)n * 4);
     w.lse = (float*)p; p += al((size_t)n * 4);
     w.rowloss = (float*)p; p += al((size_t)n * 4);
-    w.g = (bf16*)p; p += al((size_t)n * V * 2);
-    w.gt = (bf16*)p; p += al((size_t)n * V * 2);
+    w.g = (bf16*)p;
     return w;
 }
 
-size_t carve_bytes(int64_t n, int64_t h, int64_t V, bool need_wt) {
-    const int64_t ntn = (V + kBN - 1) / kBN;
-    return al((size_t)h * n * 2) + (need_wt ? al((size_t)h * V * 2) : 0) +
-           2 * al((size_t)n * ntn * 4) + 3 * al((size_t)n * 4) + 2 * al((size_t)n * V * 2);
+size_t carve_bytes(int64_t n, int64_t V) {
+    const int64_t ntn = kParts * ((V + kBN - 1) / kBN);
+    return 2 * al((size_t)n * ntn * 4) + 3 * al((size_t)n * 4) + al((size_t)n * V * 2);
 }
 
 // ---- epilogues ----------------------------------------------------------------
@@ -88,12 +86,12 @@ struct EpiLse {  // K1: per (row, tile) online max / sum-exp, target logit
     }
 };
 
-struct EpiGrad {  // K2: G = scale * (exp(S - lse) - onehot), bf16, G and G^T
+struct EpiGrad {  // K2: G = scale * (exp(S - lse) - onehot), bf16
     const int64_t* targets;
     const float* lse;
     float scale;
-    bf16 *g, *gt;
-    int M, N;
+    bf16* g;
+    int N;
     float l;
     int64_t t;
     __device__ void begin_tile(int row, int, int, bool valid) {
@@ -120,7 +118,6 @@ struct EpiGrad {  // K2: G = scale * (exp(S - lse) - onehot), bf16, G and G^T
         } else {
             for (int j = 0; j < nvalid; ++j) gr[j] = __float2bfloat16_rn(gv[j]);
         }
-        for (int j = 0; j < nvalid; ++j) gt[(int64_t)(col + j) * M + row] = __float2bfloat16_rn(gv[j]);
     }
     __device__ void end_tile(int, int, int, bool) {}
 };
@@ -153,36 +150,44 @@ struct EpiF32 {  // K3 store / K4 accumulate
 };
 
 // ---- small kernels ---------------------------------------------------------
-__global__ void k_transpose_bf16(const bf16* __restrict__ in, int64_t rows, int64_t cols,
-                                 bf16* __restrict__ out) {
-    __shared__ bf16 tile[32][33];
-    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
-    for (int i = threadIdx.y; i < 32; i += 8) {
-        const int64_t r = r0 + i, c = c0 + threadIdx.x;
-        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+// per-row merge of the tile partials in ascending (tile, half) order: one
+// warp per row, lane-strided partial merges then a fixed xor butterfly
+__device__ __forceinline__ void lse_combine(float& m1, float& s1, float m2, float s2) {
+    if (s2 == 0.f) return;
+    if (s1 == 0.f) {
+        m1 = m2;
+        s1 = s2;
+        return;
     }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += 8) {
-        const int64_t c = c0 + i, r = r0 + threadIdx.x;
-        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
-    }
+    const float M = fmaxf(m1, m2);
+    s1 = s1 * expf(m1 - M) + s2 * expf(m2 - M);
+    m1 = M;
 }
-
-// per-row merge of the tile partials in ascending tile order
 __global__ void k_lse_merge(const float* __restrict__ pmax, const float* __restrict__ psum,
                             const float* __restrict__ tgt, int n, int ntn, float* __restrict__ lse,
                             float* __restrict__ rowloss) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (i >= n) return;
     const float* pm = pmax + (int64_t)i * ntn;
     const float* ps = psum + (int64_t)i * ntn;
-    float M = -INFINITY;
-    for (int b = 0; b < ntn; ++b) M = fmaxf(M, pm[b]);
-    float S = 0.f;
-    for (int b = 0; b < ntn; ++b) S += ps[b] * expf(pm[b] - M);
-    const float l = M + logf(S);
-    lse[i] = l;
-    rowloss[i] = l - tgt[i];
+    float M = -INFINITY, S = 0.f;
+    for (int b = lane; b < ntn; b += 32) lse_combine(M, S, pm[b], ps[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, M, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, S, o);
+        // symmetric combine so both lanes of a pair hold identical values
+        const float Mx = fmaxf(M, m2);
+        const float a = (S == 0.f) ? 0.f : S * expf(M - Mx);
+        const float c = (s2 == 0.f) ? 0.f : s2 * expf(m2 - Mx);
+        S = (lane & o) ? (c + a) : (a + c);
+        M = Mx;
+    }
+    if (lane == 0) {
+        const float l = M + logf(S);
+        lse[i] = l;
+        rowloss[i] = l - tgt[i];
+    }
 }
 
 // fixed-shape tree sum of the per-row losses -> weight/n * sum (one CTA)
@@ -198,12 +203,6 @@ __global__ void k_loss_sum(const float* __restrict__ rowloss, int n, float scale
         __syncthreads();
     }
     if (threadIdx.x == 0) *loss = sh[0] * scale;
-}
-
-int transpose(const bf16* in, int64_t rows, int64_t cols, bf16* out, cudaStream_t s) {
-    const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
-    k_transpose_bf16<<<grid, dim3(32, 8), 0, s>>>(in, rows, cols, out);
-    return ee_check_launch("transpose");
 }
 
 }  // namespace
@@ -241,51 +240,42 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 }
 }  // namespace tc
 
-size_t exit_head_train_ws_bytes(int64_t n, int64_t h, int64_t V) {
-    return carve_bytes(n, h, V, true);
-}
+size_t exit_head_train_ws_bytes(int64_t n, int64_t /*h*/, int64_t V) { return carve_bytes(n, V); }
 
-extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, const void* Wt,
-                                  int64_t V, const int64_t* targets, float weight, float* loss,
-                                  float* dx, float* dw_acc, void* ws, size_t ws_bytes,
-                                  void* stream) {
+extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
+                                  const int64_t* targets, float weight, float* loss, float* dx,
+                                  float* dw_acc, void* ws, size_t ws_bytes, void* stream) {
     EE_REQUIRE(n > 0 && h > 0 && V > 0 && n % 8 == 0 && h % 8 == 0 && V % 8 == 0, EE_ESHAPE,
                "exit_head_train: n, h, V must be positive multiples of 8 (n=%lld h=%lld V=%lld)",
                (long long)n, (long long)h, (long long)V);
-    EE_REQUIRE(n < (1ll << 31) / 1 && V < (1ll << 31), EE_ESHAPE, "exit_head_train: too large");
-    EE_REQUIRE(ws && ws_bytes >= carve_bytes(n, h, V, Wt == nullptr), EE_ESHAPE,
-               "exit_head_train: workspace too small (%zu < %zu)", ws_bytes,
-               carve_bytes(n, h, V, Wt == nullptr));
+    EE_REQUIRE(n < (1ll << 31) && V < (1ll << 31), EE_ESHAPE, "exit_head_train: too large");
+    EE_REQUIRE(ws && ws_bytes >= carve_bytes(n, V), EE_ESHAPE,
+               "exit_head_train: workspace too small (%zu < %zu)", ws_bytes, carve_bytes(n, V));
     cudaStream_t s = as_stream(stream);
-    TrainWs w = carve(ws, n, h, V, Wt == nullptr);
-    const int ntn = (int)((V + kBN - 1) / kBN);
+    TrainWs w = carve(ws, n, V);
+    const int ntn = (int)(kParts * ((V + kBN - 1) / kBN));
     const float scale = weight / (float)n;
     int rc;
-    // operands for the backward GEMMs (K-major everywhere)
-    if ((rc = transpose((const bf16*)x, n, h, w.xt, s))) return rc;
-    const bf16* wt = (const bf16*)Wt;
-    if (!wt) {
-        if ((rc = transpose((const bf16*)W, V, h, w.wt, s))) return rc;
-        wt = w.wt;
-    }
-    // K1: online log-sum-exp partials + target logits
-    if ((rc = tc::launch_tc_gemm<kBN>(x, W, (int)n, (int)V, (int)h,
-                                      EpiLse{targets, w.pmax, w.psum, w.tgt, ntn, 0.f, 0.f, 0}, s)))
+    // K1: online log-sum-exp partials + target logits (A = X and B = W K-major)
+    if ((rc = tc::launch_tc_gemm<kBN, false, false, false>(
+             x, W, (int)n, (int)V, (int)h, EpiLse{targets, w.pmax, w.psum, w.tgt, ntn, 0.f, 0.f, 0},
+             s)))
         return rc;
-    k_lse_merge<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w.pmax, w.psum, w.tgt, (int)n, ntn,
+    k_lse_merge<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(w.pmax, w.psum, w.tgt, (int)n, ntn,
                                                             w.lse, w.rowloss);
     if ((rc = ee_check_launch("lse_merge"))) return rc;
     k_loss_sum<<<1, 1024, 0, s>>>(w.rowloss, (int)n, scale, loss);
     if ((rc = ee_check_launch("loss_sum"))) return rc;
-    // K2: logit gradient (bf16), both layouts
-    if ((rc = tc::launch_tc_gemm<kBN>(
-             x, W, (int)n, (int)V, (int)h,
-             EpiGrad{targets, w.lse, scale, w.g, w.gt, (int)n, (int)V, 0.f, 0}, s)))
+    // K2: logit gradient G (bf16, n x V)
+    if ((rc = tc::launch_tc_gemm<kBN, false, false, false>(
+             x, W, (int)n, (int)V, (int)h, EpiGrad{targets, w.lse, scale, w.g, (int)V, 0.f, 0}, s)))
         return rc;
-    // K3: dX = G . W
-    if ((rc = tc::launch_tc_gemm<kBN>(w.g, wt, (int)n, (int)h, (int)V, EpiF32<false>{dx, (int)h}, s)))
+    // K3: dX = G W     (W (V x h) is the MN-major B operand, K = V)
+    if ((rc = tc::launch_tc_gemm<kBN, false, true, false>(w.g, W, (int)n, (int)h, (int)V,
+                                                          EpiF32<false>{dx, (int)h}, s)))
         return rc;
-    // K4: dW += G^T . X
-    return tc::launch_tc_gemm<kBN>(w.gt, w.xt, (int)V, (int)h, (int)n, EpiF32<true>{dw_acc, (int)h},
-                                   s);
+    // K4: dW += G^T X  (G and X both MN-major, K = n); N-fastest tile order so
+    // concurrent CTAs share each G column block
+    return tc::launch_tc_gemm<kBN, true, true, true>(w.g, x, (int)V, (int)h, (int)n,
+                                                     EpiF32<true>{dw_acc, (int)h}, s);
 }

@@ -11,9 +11,10 @@
 //                      are released with tcgen05.commit -> empty[s].
 //                      Two TMEM accumulators (2 x BN columns) so the
 //                      epilogue of tile i overlaps the MMAs of tile i+1.
-//   warps 2..5         epilogue: tcgen05.ld 32x32b.x16 (row = TMEM lane),
-//                      per-row epilogue functor, then release the TMEM
-//                      buffer (tmem_empty mbarrier).
+//   warps 2..9         epilogue: two warps per TMEM lane quarter, each owning
+//                      half of the tile's columns; tcgen05.ld 32x32b.x16
+//                      (row = TMEM lane), per-row epilogue functor, then
+//                      release the TMEM buffer (tmem_empty mbarrier).
 // Persistent grid (one CTA per SM), static tile schedule with M fastest so
 // CTAs working at the same time share the B tile in L2.
 #pragma once
@@ -27,7 +28,8 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kStages = 4;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + kEpiWarps * 32;
 constexpr int kABytes = BM * BK * 2;
 
 template <int BN>
@@ -101,23 +103,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// K-major, 128-byte swizzle, canonical UMMA layout: rows of 128 B, 8-row
-// atoms 1024 B apart (SBO), LBO unused (1), descriptor version 1 (sm_100).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
-    return (uint64_t)((smem_addr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+// Canonical UMMA shared-memory descriptors, 128-byte swizzle, version 1.
+// K-major tile (rows x 64 k): rows of 128 B, 8-row atoms 1024 B apart (SBO),
+//   LBO unused (1); the k-th UMMA_K=16 slice starts 32*k bytes in.
+// MN-major tile (64 k rows x MN): 64-element MN chunks of 64 rows x 128 B
+//   (8 KB, one TMA box each) -> LBO = 8 KB between MN chunks, SBO = 1 KB
+//   between 8-row k groups; the k-th UMMA_K=16 slice starts 2 KB*k in.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr, uint32_t lbo16, uint32_t sbo16) {
+    return (uint64_t)((smem_addr & 0x3FFFF) >> 4) | ((uint64_t)lbo16 << 16) |
+           ((uint64_t)sbo16 << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t tile_addr, int k) {
+    return MN ? sw128_desc(tile_addr + k * 2048, 512, 64) : sw128_desc(tile_addr + k * 32, 1, 64);
 }
 
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// kind::f16 instruction descriptor: D f32, A/B bf16, majors, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // Kernel.  Epi::chunk(row, col0, v[16], nvalid) is called per 16-column chunk
-// for every row of the tile (called by the owning epilogue thread, in
-// ascending column order); Epi::begin_tile / end_tile bracket a tile for
-// the thread's row.
-template <int BN, class Epi>
+// for every row of the tile (by the epilogue thread owning that row and
+// column half, in ascending column order); Epi::begin_tile / end_tile
+// bracket one (row, half-tile) with part = 2 * n_tile + half.
+// A_MN / B_MN: operand stored MN-major (row-major (K, MN) in HBM) instead of
+// K-major; N_FASTEST: tile order (pick so the larger operand is shared by
+// the CTAs running at the same time).
+template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M,
           int N, int K, Epi epi) {
@@ -142,7 +156,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
         }
         for (int b = 0; b < 2; ++b) {
             mb_init(&tfull[b], 1);
-            mb_init(&tempty[b], 4);
+            mb_init(&tempty[b], kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -165,13 +179,25 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
             int s = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int mb = t % tiles_m, nb = t / tiles_m;
+                const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
+                const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
                 for (int kb = 0; kb < nk; ++kb) {
                     mb_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * C::kStageBytes;
                     mb_expect_tx(&full[s], C::kStageBytes);
-                    tma_load_2d(st, &ta, kb * BK, mb * BM, &full[s]);
-                    tma_load_2d(st + kABytes, &tb, kb * BK, nb * BN, &full[s]);
+                    if (A_MN) {
+                        for (int c = 0; c < BM / 64; ++c)
+                            tma_load_2d(st + c * 8192, &ta, mb * BM + c * 64, kb * BK, &full[s]);
+                    } else {
+                        tma_load_2d(st, &ta, kb * BK, mb * BM, &full[s]);
+                    }
+                    if (B_MN) {
+                        for (int c = 0; c < BN / 64; ++c)
+                            tma_load_2d(st + kABytes + c * 8192, &tb, nb * BN + c * 64, kb * BK,
+                                        &full[s]);
+                    } else {
+                        tma_load_2d(st + kABytes, &tb, kb * BK, nb * BN, &full[s]);
+                    }
                     if (++s == kStages) {
                         s = 0;
                         ph ^= 1;
@@ -182,7 +208,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     } else if (warp == 1) {
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
-            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+            constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
@@ -198,8 +224,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
                     const uint32_t b0 = a0 + kABytes;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        tc_mma(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
-                               (kb | k) != 0);
+                        tc_mma(d, op_desc<A_MN>(a0, k), op_desc<B_MN>(b0, k), idesc, (kb | k) != 0);
                     tc_commit(&empty[s]);  // smem stage free once these MMAs completed
                     if (++s == kStages) {
                         s = 0;
@@ -214,27 +239,31 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
             }
         }
     } else {
-        // ---------------- epilogue (warps 2..5) ----------------
+        // ---------------- epilogue (warps 2..9) ----------------
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int half = (warp - 2) >> 2;  // which half of the tile's columns
         const int row_in_tile = quarter * 32 + lane;
         int acc = 0;
         uint32_t aph = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int mb = t % tiles_m, nb = t / tiles_m;
+            const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
+            const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
             mb_wait(&tfull[acc], aph);
             tc_fence_after();
             const int row = mb * BM + row_in_tile;
-            const int col0 = nb * BN;
-            epi.begin_tile(row, col0, nb, row < M);
-            const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+            const int col0 = nb * BN + half * (BN / 2);
+            const int part = nb * 2 + half;  // partial index for per-tile reductions
+            epi.begin_tile(row, col0, part, row < M);
+            const uint32_t base =
+                tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * (BN / 2);
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 16) {
+            for (int c = 0; c < BN / 2; c += 16) {
                 float v[16];
                 tmem_ld16(base + c, v);
                 const int nvalid = min(16, N - (col0 + c));
                 if (row < M && nvalid > 0) epi.chunk(row, col0 + c, v, nvalid);
             }
-            epi.end_tile(row, col0, nb, row < M);
+            epi.end_tile(row, col0, part, row < M);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mb_arrive(&tempty[acc]);
@@ -257,13 +286,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
 // (64 cols x box_rows rows), 128-byte swizzle, zero fill out of bounds.
 int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
 
-template <int BN, class Epi>
+// C[M, N] = A . B^T with A given as (M, K) row-major (A_MN = false) or as
+// (K, M) row-major (A_MN = true); B likewise as (N, K) or (K, N).
+template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
 int launch_tc_gemm(const void* A, const void* B, int M, int N, int K, Epi epi, cudaStream_t s) {
     CUtensorMap ta, tb;
     int rc;
-    if ((rc = make_tmap_bf16(&ta, A, M, K, BM))) return rc;
-    if ((rc = make_tmap_bf16(&tb, B, N, K, BN))) return rc;
-    auto kern = k_tc_gemm<BN, Epi>;
+    if ((rc = A_MN ? make_tmap_bf16(&ta, A, K, M, BK) : make_tmap_bf16(&ta, A, M, K, BM))) return rc;
+    if ((rc = B_MN ? make_tmap_bf16(&tb, B, K, N, BK) : make_tmap_bf16(&tb, B, N, K, BN))) return rc;
+    auto kern = k_tc_gemm<BN, A_MN, B_MN, N_FASTEST, Epi>;
     static bool configured[16] = {};
     int dev = 0;
     cudaGetDevice(&dev);

@@ -42,7 +42,7 @@ def _workspace(device, nbytes):
     return buf
 
 
-def exit_head_loss_and_grads(x, W, targets, weight=1.0, Wt=None, dw_acc=None):
+def exit_head_loss_and_grads(x, W, targets, weight=1.0, dw_acc=None):
     """Fused exit head: returns (loss (0-d float32 tensor), dx (n, h) float32,
     dW (V, h) float32).  x (n, h) and W (V, h) bf16 CUDA tensors; targets
     int64 (n,).  dW is accumulated into ``dw_acc`` when given (microbatch
@@ -60,8 +60,6 @@ def exit_head_loss_and_grads(x, W, targets, weight=1.0, Wt=None, dw_acc=None):
         raise TokenError("target id out of vocabulary range")
     x = x.to(torch.bfloat16).contiguous()
     W = W.to(torch.bfloat16).contiguous()
-    if Wt is not None:
-        Wt = Wt.contiguous()
     lib = _lib.load()
     need = lib.ee_workspace_bytes(_lib.EE_OP_EXIT_HEAD_TRAIN, n, h, V, 0, 0)
     ws = _workspace(x.device, need)
@@ -69,7 +67,7 @@ def exit_head_loss_and_grads(x, W, targets, weight=1.0, Wt=None, dw_acc=None):
     dx = torch.empty((n, h), dtype=torch.float32, device=x.device)
     if dw_acc is None:
         dw_acc = torch.zeros((V, h), dtype=torch.float32, device=x.device)
-    call("ee_exit_head_train", ptr(x), n, h, ptr(W), ptr(Wt), V, ptr(targets), float(weight),
+    call("ee_exit_head_train", ptr(x), n, h, ptr(W), V, ptr(targets), float(weight),
          ptr(loss), ptr(dx), ptr(dw_acc), ptr(ws), ws.numel(), stream_ptr())
     return loss, dx, dw_acc
 

@@ -17,17 +17,16 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(n, h, device="cuda", generator=g).bfloat16()
     w = (torch.randn(V, h, device="cuda", generator=g) * 0.02).bfloat16()
-    wt = w.t().contiguous()
     t = torch.randint(0, V, (n,), device="cuda", generator=g)
     acc = torch.zeros(V, h, device="cuda")
     for _ in range(2):
-        exit_head_loss_and_grads(x, w, t, 1.0, Wt=wt, dw_acc=acc)
+        exit_head_loss_and_grads(x, w, t, 1.0, dw_acc=acc)
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
-        loss, dx, _ = exit_head_loss_and_grads(x, w, t, 1.0, Wt=wt, dw_acc=acc)
+        loss, dx, _ = exit_head_loss_and_grads(x, w, t, 1.0, dw_acc=acc)
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
