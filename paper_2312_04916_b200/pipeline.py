@@ -1,0 +1,460 @@
+"""1F1B pipeline-parallel early-exit training.
+
+Mirrors `eepipe/pipeline.py` (the reference simulates stages with threads
+and `queue.Queue`s):
+
+* each stage follows the structural 1F1B action list
+  (`schedule.regular_actions`, eepipe/schedule.py:170-179): warm-up
+  ``min(P-s, M)`` forwards, then (F, B) pairs, then the trailing backwards;
+* activations x_s flow forward and the early-exit loss-backprop signals
+  g_s = dL_aux/dx_s flow backward over ordered point-to-point channels; a
+  stage's backward step builds the surrogate
+  ``aux = sum_e w_e * CE_e + <g, x_sent>`` (eepipe/pipeline.py:195-223) by
+  ``torch.autograd.backward([local_loss, x_out], [1, g])``;
+* early exits are DEFERRED: their loss is formed inside the backward step
+  (eepipe/pipeline.py:175-192), through the fused tcgen05 head, so no
+  stage ever holds exit logits;
+* gradients accumulate as raw sums over microbatches (:422-427) and tied
+  replicas are summed after the iteration (`sync_tied`, :226-241).
+
+Two transports share the same `StageWorker`:
+
+* `run_iteration_1f1b`: one thread per stage in this process, each stage on
+  its own CUDA stream / device, channels are ordered queues carrying device
+  tensors (the reference's topology, on GPUs);
+* `run_stage_1f1b_dist`: one process per GPU (torchrun), channels are
+  `torch.distributed` point-to-point sends over NCCL (NVLink), tied-replica
+  sync is an all-reduce over the holders' subgroup.  The protocol is covered
+  on CPU with the gloo backend (tests/test_pipeline_dist.py).
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass, field
+from queue import Empty, Queue
+
+from . import schedule as sched
+from .errors import ConfigError, QueueProtocolError, ShapeError
+from .model import StagePartition
+
+_RECV_TIMEOUT = 120.0
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class ActivationMessage:
+    mb: int
+    data: object
+
+
+@dataclass
+class GradientMessage:
+    mb: int
+    data: object
+
+
+@dataclass(frozen=True)
+class WeightSchedule:
+    """Per-exit loss weights over training steps (eepipe/pipeline.py:47-84):
+    ``constant`` returns ``early`` forever; ``linear`` interpolates from
+    ``early`` to ``early_end`` over ``span_steps`` and clamps.  The final
+    exit's weight stays fixed."""
+
+    kind: str = "constant"
+    early: tuple = ()
+    early_end: tuple = ()
+    span_steps: int = 0
+    final_weight: float = 1.0
+
+
+def weight_at_step(ws: WeightSchedule, step: int):
+    if ws.kind == "constant":
+        early = list(ws.early)
+    elif ws.kind == "linear":
+        if len(ws.early_end) != len(ws.early):
+            raise ConfigError("linear schedule needs early_end for every early exit")
+        frac = 1.0 if ws.span_steps <= 0 else min(max(step / ws.span_steps, 0.0), 1.0)
+        early = [a + (b - a) * frac for a, b in zip(ws.early, ws.early_end)]
+    else:
+        raise ConfigError(f"unknown weight schedule {ws.kind!r}")
+    return early + [ws.final_weight]
+
+
+@dataclass
+class IterationOptions:
+    microbatch_size: int
+    defer_exit_forward: bool = True
+    weight_schedule: WeightSchedule | None = None
+    step: int = 0
+
+
+@dataclass
+class TrainStepReport:
+    """Per-iteration record (subset of eepipe/pipeline.py:133-161): per-exit
+    mean losses, per-stage executed event order, message counts, wall clock
+    and device time per stage action kind."""
+
+    per_exit_loss: dict = field(default_factory=dict)
+    event_log: dict = field(default_factory=dict)
+    activation_messages: dict = field(default_factory=dict)
+    gradient_messages: dict = field(default_factory=dict)
+    wall_clock: dict = field(default_factory=dict)
+    max_in_flight: dict = field(default_factory=dict)
+    weights_used: tuple = ()
+
+
+class TaggedChannel:
+    """Ordered in-process P2P channel; regular microbatch ids must arrive in
+    strictly increasing order (eepipe/pipeline.py:87-122)."""
+
+    def __init__(self, name):
+        self.name = name
+        self.q = Queue()
+        self.last = 0
+        self.count = 0
+
+    def send(self, msg):
+        self.count += 1
+        self.q.put(msg)
+
+    def recv(self, expect_mb):
+        try:
+            msg = self.q.get(timeout=_RECV_TIMEOUT)
+        except Empty:
+            raise QueueProtocolError(f"{self.name}: timed out waiting for microbatch {expect_mb}")
+        if isinstance(msg, BaseException):
+            raise msg
+        if msg.mb != expect_mb or msg.mb <= self.last:
+            raise QueueProtocolError(
+                f"{self.name}: expected microbatch {expect_mb}, got {msg.mb} (last {self.last})")
+        self.last = msg.mb
+        return msg
+
+
+class DistChannel:
+    """torch.distributed P2P channel carrying (mb id header, tensor) pairs in
+    order between two ranks (NCCL over NVLink on GPUs, gloo on CPU).  Sends
+    are non-blocking (isend), like the reference's queue puts: with blocking
+    sends the 1F1B steady state would deadlock (stage s sending x while
+    stage s+1 sends g back).  `flush` waits for the outstanding sends."""
+
+    def __init__(self, peer, shape, dtype, device, group=None):
+        self.peer, self.shape, self.dtype, self.device = peer, tuple(shape), dtype, device
+        self.group = group
+        self.last = 0
+        self.count = 0
+        self.pending = []
+
+    def send(self, msg):
+        torch = _torch()
+        dist = torch.distributed
+        data = msg.data.contiguous()
+        if tuple(data.shape) != self.shape:
+            raise ShapeError(f"channel expects {self.shape}, got {tuple(data.shape)}")
+        hdr = torch.tensor([msg.mb], dtype=torch.int64, device=self.device)
+        # keep the tensors alive until their sends complete
+        self.pending.append((dist.isend(hdr, self.peer, group=self.group), hdr))
+        self.pending.append((dist.isend(data, self.peer, group=self.group), data))
+        self.count += 1
+
+    def flush(self):
+        for req, _ in self.pending:
+            req.wait()
+        self.pending = []
+
+    def recv(self, expect_mb):
+        torch = _torch()
+        dist = torch.distributed
+        hdr = torch.empty(1, dtype=torch.int64, device=self.device)
+        dist.recv(hdr, self.peer, group=self.group)
+        mb = int(hdr.item())
+        if mb != expect_mb or mb <= self.last:
+            raise QueueProtocolError(f"expected microbatch {expect_mb}, got {mb} (last {self.last})")
+        self.last = mb
+        data = torch.empty(self.shape, dtype=self.dtype, device=self.device)
+        dist.recv(data, self.peer, group=self.group)
+        return type("Msg", (), {"mb": mb, "data": data})
+
+
+class StageCompute:
+    """Product stage compute: the stage's layers with torch autograd on its
+    device and the fused tcgen05 exit heads; exit losses are formed in the
+    backward step (deferred exit forward)."""
+
+    def __init__(self, spec, cfg, model_src, weights, device=None, dtype=None):
+        from .training import TrainModel
+        self.spec = spec
+        self.cfg = cfg
+        self.tm = TrainModel(model_src, dtype=dtype, device=device, names=list(spec.params))
+        self.device = self.tm.device
+        self.weights = weights  # by head key
+        self.head_losses = {hd.key: [] for _, hd in spec.heads}
+
+    def forward(self, tokens_or_x, targets):
+        from .training import embed_tokens, run_layer
+        p = self.tm.params
+        if self.spec.has_embedding:
+            x_in = None
+            x = embed_tokens(p, tokens_or_x, self.cfg.max_seq_len)
+        else:
+            x_in = tokens_or_x.to(self.device).detach().requires_grad_()
+            x = x_in
+        taps = {0: x}
+        for local, layer in enumerate(self.spec.layer_indices, start=1):
+            x = run_layer(p, f"layer{layer}", x, self.cfg.num_heads)
+            taps[local] = x
+        return x, (x_in, x, taps, targets)
+
+    def local_loss(self, state):
+        import numpy as np
+        from .training import head_loss
+        torch = _torch()
+        _, _, taps, targets = state
+        targets = torch.as_tensor(np.asarray(targets)).to(self.device)
+        total = None
+        for local, hd in self.spec.heads:
+            ce = head_loss(self.tm.params, hd, taps[local], targets, self.cfg.num_heads)
+            self.head_losses[hd.key].append(float(ce.detach()))
+            term = ce * self.weights[hd.key]
+            total = term if total is None else total + term
+        return total
+
+    def backward(self, state, g):
+        torch = _torch()
+        x_in, x_out, _, _ = state
+        loss = self.local_loss(state)  # deferred exit forward, eepipe/pipeline.py:393-412
+        if g is None:
+            if loss is None:
+                raise ConfigError("a stage must have a local loss or a received gradient")
+            loss.backward()
+        else:
+            if tuple(g.shape) != tuple(x_out.shape):
+                raise ShapeError(f"gradient shape {tuple(g.shape)} does not match activation "
+                                 f"{tuple(x_out.shape)}")
+            # aux = L_local + <g, x_out>  (eepipe/pipeline.py:195-223)
+            outs, grads = [x_out], [g.to(x_out.dtype)]
+            if loss is not None:
+                outs.insert(0, loss)
+                grads.insert(0, torch.ones_like(loss))
+            torch.autograd.backward(outs, grads)
+        return None if x_in is None else x_in.grad
+
+
+class StageWorker:
+    """Executes one stage's 1F1B action list (eepipe/pipeline.py:301-527)."""
+
+    def __init__(self, index, num_stages, num_mb, compute, data, fwd_in, fwd_out, bwd_in,
+                 bwd_out):
+        self.index, self.P, self.M = index, num_stages, num_mb
+        self.compute = compute
+        self.data = data  # mb -> (tokens, targets)
+        self.fwd_in, self.fwd_out, self.bwd_in, self.bwd_out = fwd_in, fwd_out, bwd_in, bwd_out
+        self.state = {}
+        self.event_log = []
+        self.wall = {"F": 0.0, "B": 0.0}
+        self.in_flight = 0
+        self.max_in_flight = 0
+        self.exception = None
+
+    def run(self):
+        try:
+            for kind, mb in sched.regular_actions(self.P, self.M, self.index):
+                t = time.perf_counter()
+                if kind == sched.FWD:
+                    self._forward(mb)
+                else:
+                    self._backward(mb)
+                self.wall[kind] += time.perf_counter() - t
+                self.event_log.append((kind, mb))
+        except BaseException as exc:  # surfaced by the coordinator
+            self.exception = exc
+            for ch in (self.fwd_out, self.bwd_out):
+                if isinstance(ch, TaggedChannel):
+                    ch.q.put(exc)
+
+    def _forward(self, mb):
+        tokens, targets = self.data[mb]
+        src = tokens if self.fwd_in is None else self.fwd_in.recv(mb).data
+        x_out, st = self.compute.forward(src, targets)
+        self.state[mb] = st
+        self.in_flight += 1
+        self.max_in_flight = max(self.max_in_flight, self.in_flight)
+        if self.fwd_out is not None:
+            self.fwd_out.send(ActivationMessage(mb, x_out.detach()))
+
+    def _backward(self, mb):
+        st = self.state.pop(mb)
+        g = None if self.bwd_in is None else self.bwd_in.recv(mb).data
+        g_in = self.compute.backward(st, g)
+        self.in_flight -= 1
+        if self.bwd_out is not None:
+            if g_in is None:
+                raise ConfigError("stored input activation received no gradient")
+            self.bwd_out.send(GradientMessage(mb, g_in.detach()))
+
+
+def _resolve_weights(heads, options):
+    if options.weight_schedule is not None:
+        w = weight_at_step(options.weight_schedule, options.step)
+        if len(w) != len(heads):
+            raise ConfigError(f"schedule yields {len(w)} weights for {len(heads)} exits")
+        return list(w)
+    return [hd.loss_weight for hd in heads]
+
+
+def _split(batch, mb_size):
+    import numpy as np
+    batch = np.asarray(batch)
+    if batch.ndim != 2 or batch.shape[0] % mb_size:
+        raise ConfigError("batch does not divide into microbatches")
+    M = batch.shape[0] // mb_size
+    return M, {k + 1: (batch[k * mb_size:(k + 1) * mb_size, :-1],
+                       batch[k * mb_size:(k + 1) * mb_size, 1:]) for k in range(M)}
+
+
+def sync_tied(per_stage_grads, tied_replicas=None):
+    """Sum replica gradients by canonical name (eepipe/pipeline.py:226-241);
+    tensors may live on different devices (summed on the first holder's)."""
+    merged = {}
+    for stage_map in per_stage_grads:
+        for name, g in stage_map.items():
+            if name in merged:
+                if merged[name].shape != g.shape:
+                    raise ShapeError(f"replica shape mismatch for {name}")
+                merged[name] = merged[name] + g.to(merged[name].device)
+            else:
+                merged[name] = g
+    return merged
+
+
+def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
+                       devices=None, dtype=None):
+    """One 1F1B iteration over the partition, one thread per stage
+    (eepipe/pipeline.py:537-644).  ``model`` is the EarlyExitModel the stage
+    weights come from (the partition's own copies are used when omitted).
+    Returns (merged gradient map by name, TrainStepReport)."""
+    P = part.num_stages
+    M, data = _split(batch, options.microbatch_size)
+    all_heads = [hd for st in part.stages for _, hd in st.heads]
+    all_heads.sort(key=lambda hd: (hd.layer_index, hd.is_final))
+    weights = _resolve_weights(all_heads, options)
+    wmap = {hd.key: w for hd, w in zip(all_heads, weights)}
+    devices = devices or ["cuda:0"] * P
+    src = model
+    fwd = [TaggedChannel(f"act {s}->{s + 1}") for s in range(1, P)]
+    bwd = [TaggedChannel(f"grad {s + 1}->{s}") for s in range(1, P)]
+    workers = []
+    for s, spec in enumerate(part.stages, start=1):
+        holder = src if src is not None else _SpecModel(part, spec)
+        comp = StageCompute(spec, part.config, holder, wmap, devices[(s - 1) % len(devices)], dtype)
+        workers.append(StageWorker(s, P, M, comp, data,
+                                   fwd[s - 2] if s > 1 else None, fwd[s - 1] if s < P else None,
+                                   bwd[s - 1] if s < P else None, bwd[s - 2] if s > 1 else None))
+    torch = _torch()
+
+    def target(w):
+        dev = w.compute.device
+        with torch.cuda.device(dev), torch.cuda.stream(torch.cuda.Stream(dev)):
+            w.run()
+            torch.cuda.current_stream(dev).synchronize()
+
+    threads = [threading.Thread(target=target, args=(w,), daemon=True, name=f"stage-{w.index}")
+               for w in workers]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=_RECV_TIMEOUT * 2)
+    for w in workers:
+        if w.exception is not None:
+            raise w.exception
+    merged = sync_tied([w.compute.tm.grads() for w in workers], part.tied_replicas)
+    report = TrainStepReport(weights_used=tuple(weights))
+    for w in workers:
+        report.event_log[w.index] = list(w.event_log)
+        report.wall_clock[w.index] = dict(w.wall)
+        report.max_in_flight[w.index] = w.max_in_flight
+        for key, vals in w.compute.head_losses.items():
+            report.per_exit_loss[key] = sum(vals) / len(vals)
+    for s in range(1, P):
+        report.activation_messages[s] = fwd[s - 1].count
+        report.gradient_messages[s + 1] = bwd[s - 1].count
+    return merged, report
+
+
+class _SpecModel:
+    """Adapter exposing a stage's own parameter copies as a model source."""
+
+    def __init__(self, part, spec):
+        self.config = part.config
+        self.params = spec.params
+        self.heads = [hd for _, hd in spec.heads]
+
+
+def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, model=None,
+                        compute_factory=None, dtype=None):
+    """The calling rank's stage of a distributed 1F1B iteration (one process
+    per stage; rank r runs stage r+1).  Activations / gradients travel by
+    `torch.distributed` P2P (NCCL over NVLink on GPUs); tied replicas are
+    summed with an all-reduce over their holders.  ``compute_factory(spec,
+    cfg, wmap)`` overrides the stage compute (tests use a CPU one under
+    gloo).  Returns (this stage's gradient map, partial report)."""
+    torch = _torch()
+    dist = torch.distributed
+    rank, world = dist.get_rank(), dist.get_world_size()
+    P = part.num_stages
+    if world != P:
+        raise ConfigError(f"{world} ranks for {P} stages")
+    s = rank + 1
+    spec = part.stages[rank]
+    M, data = _split(batch, options.microbatch_size)
+    all_heads = sorted([hd for st in part.stages for _, hd in st.heads],
+                       key=lambda hd: (hd.layer_index, hd.is_final))
+    weights = _resolve_weights(all_heads, options)
+    wmap = {hd.key: w for hd, w in zip(all_heads, weights)}
+    if compute_factory is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        comp = StageCompute(spec, part.config, model if model is not None else _SpecModel(part, spec),
+                            wmap, dev, dtype)
+        act_dtype = comp.tm.dtype
+    else:
+        comp = compute_factory(spec, part.config, wmap)
+        dev, act_dtype = comp.device, comp.act_dtype
+    mb_size = options.microbatch_size
+    seq = data[1][0].shape[1]
+    shape = (mb_size, seq, part.config.hidden_dim)
+    fwd_in = DistChannel(rank - 1, shape, act_dtype, dev) if s > 1 else None
+    fwd_out = DistChannel(rank + 1, shape, act_dtype, dev) if s < P else None
+    bwd_in = DistChannel(rank + 1, shape, act_dtype, dev) if s < P else None
+    bwd_out = DistChannel(rank - 1, shape, act_dtype, dev) if s > 1 else None
+    w = StageWorker(s, P, M, comp, data, fwd_in, fwd_out, bwd_in, bwd_out)
+    w.run()
+    for ch in (fwd_out, bwd_out):
+        if ch is not None:
+            ch.flush()
+    if w.exception is not None:
+        raise w.exception
+    grads = comp.tm.grads() if compute_factory is None else comp.grads()
+    # tied replicas: all-reduce(sum) over the holders (every rank joins the
+    # group creation; only holders take part in the reduction)
+    for name, holders in sorted(part.tied_replicas.items()):
+        group = dist.new_group([h - 1 for h in holders])
+        if s in holders:
+            g = grads[name]
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
+    report = TrainStepReport(weights_used=tuple(weights))
+    report.event_log[s] = list(w.event_log)
+    report.wall_clock[s] = dict(w.wall)
+    report.max_in_flight[s] = w.max_in_flight
+    for key, vals in comp.head_losses.items():
+        report.per_exit_loss[key] = sum(vals) / len(vals)
+    if fwd_out is not None:
+        report.activation_messages[s] = fwd_out.count
+    if bwd_out is not None:
+        report.gradient_messages[s] = bwd_out.count
+    return grads, report

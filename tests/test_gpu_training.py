@@ -1,0 +1,81 @@
+"""GPU training path: weighted multi-exit loss with fused tcgen05 heads, the
+single-device gradient oracle and the threaded 1F1B pipeline executor.
+
+Reference anchors: `single_device_gradients` golden (tests/golden wl_*,
+produced by the reference's float64 autodiff) — compared at bf16 tolerance
+(per-exit losses within 2e-2 relative, gradients within 1e-1 relative in
+Frobenius norm: the whole backbone runs in bf16); pipeline vs single-device
+on the GPU — same kernels, so they must agree to 1e-3 relative (the
+reference's own check is < 1e-9 in float64, tests/test_pipeline.py:59-69).
+"""
+import numpy as np
+import pytest
+
+from helpers import arrays, gold
+from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model, partition
+
+pytestmark = pytest.mark.gpu
+
+
+def _wl_model():
+    cfg = ModelConfig(4, 32, 4, 64, 16, exits=(ExitSpec(1, loss_weight=0.25),
+                                               ExitSpec(2, "norm+embed", 0.5)),
+                      tie_embeddings=True)
+    return build_model(cfg, 3)
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def test_weighted_loss_gradients_match_reference():
+    from paper_2312_04916_b200.training import TrainModel, single_device_gradients
+    m = _wl_model()
+    tm = TrainModel(m)
+    batch = arrays()["wl_batch"]
+    grads, per_exit = single_device_gradients(tm, batch, [0.25, 0.5, 1.0], 2)
+    ref_loss = gold()["wl_per_exit"]
+    for k, v in ref_loss.items():
+        assert per_exit[k] == pytest.approx(v, rel=2e-2), k
+    a = arrays()
+    for name, g in grads.items():
+        ref = a[f"wl_grad::{name}"]
+        assert _rel(g.float().cpu().numpy(), ref) < 1e-1, name
+
+
+def test_pipeline_matches_single_device():
+    from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
+    from paper_2312_04916_b200.training import TrainModel, single_device_gradients
+    cfg = ModelConfig(8, 64, 4, 128, 16, exits=(ExitSpec(2, loss_weight=0.3),
+                                                ExitSpec(4, "norm+embed", 0.6)))
+    m = build_model(cfg, 1)
+    batch = np.random.default_rng(2).integers(0, 128, size=(8, 17))
+    ref, ref_loss = single_device_gradients(TrainModel(m), batch, [0.3, 0.6, 1.0], 2)
+    for P in (2, 4):
+        grads, rep = run_iteration_1f1b(partition(m, P), batch, IterationOptions(2), model=m)
+        assert set(grads) == set(ref)
+        for n in ref:
+            assert _rel(grads[n].float().cpu().numpy(), ref[n].float().cpu().numpy()) < 1e-3, n
+        for k, v in ref_loss.items():
+            assert rep.per_exit_loss[k] == pytest.approx(v, rel=1e-3)
+        for s in range(1, P + 1):
+            assert rep.max_in_flight[s] == min(P - s + 1, 4)
+        assert all(c == 4 for c in rep.activation_messages.values())
+
+
+def test_tied_pipeline_sums_replicas():
+    from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
+    from paper_2312_04916_b200.training import TrainModel, single_device_gradients
+    m = _wl_model()
+    batch = arrays()["wl_batch"]
+    ref, _ = single_device_gradients(TrainModel(m), batch, [0.25, 0.5, 1.0], 2)
+    part = partition(m, 2)
+    assert "tok_emb" in part.tied_replicas
+    grads, _ = run_iteration_1f1b(part, batch, IterationOptions(2), model=m)
+    # the replicas' bf16 gradients are summed after the iteration instead of
+    # accumulating inside one autograd graph: bf16 rounding order differs
+    assert _rel(grads["tok_emb"].float().cpu().numpy(), ref["tok_emb"].float().cpu().numpy()) < 1e-2
+    for n in ref:
+        if n != "tok_emb":
+            assert _rel(grads[n].float().cpu().numpy(), ref[n].float().cpu().numpy()) < 1e-3, n
