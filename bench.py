@@ -195,6 +195,45 @@ def run_reference(args):
     return 0
 
 
+def bench_train_head(local, hbm_peak, reps=10):
+    """Fused training exit head (loss + dX + dW, tcgen05) at the C2 shape:
+    n = 2 x 2048 tokens, h = 2048, V = 50304, bf16.  TFLOP/s on the
+    algorithmic 6 n h V, vs the measured bf16 peak."""
+    import torch
+    from paper_2312_04916_b200.training import exit_head_loss_and_grads
+    _, tf_peak, kind = peaks()
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            sustained = float(json.load(f).get("bf16_tflops_sustained", tf_peak))
+    except Exception:
+        sustained = tf_peak
+    n, h, V = 4096, 2048, 50304
+    dev = f"cuda:{local}"
+    g = torch.Generator(device=dev).manual_seed(0)
+    x = torch.randn(n, h, device=dev, generator=g).bfloat16()
+    w = (torch.randn(V, h, device=dev, generator=g) * 0.02).bfloat16()
+    t = torch.randint(0, V, (n,), device=dev, generator=g)
+    acc = torch.zeros(V, h, device=dev)
+    for _ in range(3):
+        exit_head_loss_and_grads(x, w, t, 1.0, dw_acc=acc)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        exit_head_loss_and_grads(x, w, t, 1.0, dw_acc=acc)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    tflops = 6 * n * h * V / (ms * 1e-3) / 1e12
+    return {"workload": "C2 exit head fwd+bwd (n=4096, h=2048, V=50304, bf16)",
+            "ms": ms, "tflops_6nhv": tflops, "executed_tflops_8nhv": tflops * 8 / 6,
+            "roofline": {"bound": "tensor", "achieved": tflops, "peak": tf_peak,
+                         "unit": "TFLOP/s", "frac": tflops / tf_peak,
+                         "frac_of_sustained": tflops / sustained, "peak_kind": kind,
+                         "traffic": None}}
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -208,6 +247,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train-head", action="store_true")
     ap.add_argument("--new-tokens", type=int, default=NEW_TOKENS)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -307,6 +347,11 @@ def main():
                                "early_exits": int(sum(1 for e in tr.exit_layers if e < L)),
                                "modeled_speedup": tr.speedup}
 
+    # ---- fused training exit head at the C2 shape (second half of the metric) --
+    head_train = None
+    if not args.no_train_head:
+        head_train = bench_train_head(local, hbm_peak)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -345,6 +390,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "sweep": sweep,
+        "exit_head_train": head_train,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
