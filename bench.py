@@ -111,6 +111,20 @@ def prompt_tokens():
     return [int(t) for t in np.random.default_rng(1).integers(0, C3["vocab_size"], PROMPT_LEN)]
 
 
+def measured_traffic():
+    """dram bytes (read + write) of one full-depth decode pass from the
+    committed ncu launch list (profiles/r1_decode_pass_traffic.json, ctx 129),
+    next to that pass's algorithmic bytes."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_decode_pass_traffic.json")) as f:
+            t = json.load(f)
+        return {"bytes": t["traffic_bytes"], "algorithmic_bytes": t["algorithmic_bytes_ctx129"],
+                "ratio": t["traffic_bytes"] / t["algorithmic_bytes_ctx129"],
+                "source": "profiles/r1_decode_pass_traffic.json (ncu, ctx 129)"}
+    except Exception:
+        return None
+
+
 def decode_pass_bytes(h, L, ctx):
     """Algorithmic bytes of one full-depth single-row pass:
     weights once + K/V write of the row + K/V read of the prefix (bf16)."""
@@ -143,7 +157,7 @@ def cpu_slice_timing(seconds_budget=20.0):
     for p in range(PROMPT_LEN):
         kv.fill(1, p, rng.normal(size=(nh, h // nh)), rng.normal(size=(nh, h // nh)))
     x = rng.normal(size=(1, h))
-    head = {"kind": "minimalistic", "out": "out"}
+    head = {"kind": "minimalistic", "out": "out", "outT": np.ascontiguousarray(P["out"].T)}
     t_layer, t_head, n = [], [], 0
     t_end = time.perf_counter() + seconds_budget
     while True:
@@ -384,7 +398,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "ee_decode_layers (32 layers, 1 row)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                     "pass_ms": pass_ms, "algorithmic_bytes": pass_bytes, "traffic": None},
+                     "pass_ms": pass_ms, "algorithmic_bytes": pass_bytes,
+                     "traffic": measured_traffic()},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

@@ -81,7 +81,11 @@ def head_logits(P, head, x_row):
         x = x + dot_rows(gelu(dot_rows(h2, P[head["w1"]])), P[head["w2"]])
     if head.get("norm"):
         x = rmsnorm(x, P[head["norm"]])
-    return dot_rows(x, np.ascontiguousarray(P[head["out"]].T))[0]
+    # the reference pre-transposes every head matrix once (inference.py:167)
+    outT = head.get("outT")
+    if outT is None:
+        outT = np.ascontiguousarray(P[head["out"]].T)
+    return dot_rows(x, outT)[0]
 
 
 def embed(P, vocab, tokens, positions):
@@ -149,6 +153,14 @@ def layer_step(P, l, x, positions, kv, nh):
 class Cfg:
     def __init__(self, L, h, nh, V, s_max):
         self.L, self.h, self.nh, self.V, self.s_max = L, h, nh, V, s_max
+
+
+def pretranspose(P, heads):
+    """Cache each head's transposed output matrix, as `_InferParams` does
+    once at construction (inference.py:167)."""
+    for hd in heads:
+        hd["outT"] = np.ascontiguousarray(P[hd["out"]].T)
+    return heads
 
 
 def heads_of(model_heads):
