@@ -7,21 +7,22 @@
 // (eepipe/autodiff.py:170-177):
 //   S = X W^T,  lse_i = log sum_v exp S_iv,  loss = w/n sum_i (lse_i - S_i,t_i)
 //   G = w/n (softmax(S) - onehot(t)),  dX = G W,  dW += G^T X
-// as four tcgen05 GEMMs (tc_gemm.cuh) whose epilogues do the softmax work:
-//   K1  S = X W^T          epilogue: per (row, 256-col tile) online max /
-//                          sum-exp + the target logit (logits stay in TMEM)
-//   M   merge partials in fixed order -> lse, loss (deterministic)
-//   K2  S = X W^T (again)  epilogue: G = w/n (exp(S - lse) - [v == t]) in
-//                          bf16 (row-major n x V)
+// as three tcgen05 GEMMs (tc_gemm.cuh) plus one streaming pass:
+//   K1  S = X W^T          two-pass epilogue per (row, 128-column part):
+//                          part max m_p and target logit, then
+//                          P~ = exp(S - m_p) (bf16, into G's buffer) and
+//                          its sum s_p.  The logits stay in TMEM.
+//   F   per row: merge (m_p, s_p) in fixed part order -> lse, row loss;
+//       G = w/n (P~ exp(m_p - lse) - [v == t])  in place (bf16)
 //   K3  dX  = G  W    A = G K-major, B = W read MN-major   (K = V)
 //   K4  dW += G^T X   A = G read MN-major, B = X MN-major  (K = n)
 // MN-major operands are consumed in place through the UMMA descriptor (no
-// transposed copies).  Only the logit GRADIENT G (bf16) reaches HBM, because
-// the two backward GEMMs contract it along different axes; the logits,
-// the softmax probabilities and the reference's cached (n, V) float64 probs
-// (_ckernels.pyx:130-151) never exist in memory.  Executed FLOPs are
-// 8 n h V (S is recomputed once); the roofline is quoted on the algorithmic
-// 6 n h V.
+// transposed copies).  Only part-normalised probabilities and then the logit
+// GRADIENT G (bf16) reach HBM (the two backward GEMMs contract G along
+// different axes, so it must exist); the logits themselves, the softmax and
+// the reference's cached (n, V) float64 probs (_ckernels.pyx:130-151) never
+// do.  Executed FLOPs = the algorithmic 6 n h V: S is computed
+// once.
 #include <cuda.h>
 
 #include "tc_gemm.cuh"
@@ -57,73 +58,67 @@ size_t carve_bytes(int64_t n, int64_t V) {
 }
 
 // ---- epilogues ----------------------------------------------------------------
-struct EpiLse {  // K1: per (row, tile) online max / sum-exp, target logit
+// K1: pass 1 = part max + target logit, pass 2 = P~ = exp(S - m) in bf16
+// (row-major n x V, G's buffer) and its sum.  A part with no valid column
+// keeps (m, s) = (-inf, 0), which the merge skips.
+struct EpiProb {
+    static constexpr bool kTwoPass = true;
     const int64_t* targets;
     float *pmax, *psum, *tgt;
-    int ntn;
+    bf16* g;
+    int ntn, N;
     float m, s;
-    int64_t t;
+    int t;  // target id of the row (V < 2^31), -1 for padding rows
     __device__ void begin_tile(int row, int, int, bool valid) {
         m = -INFINITY;
         s = 0.f;
-        t = valid ? targets[row] : -1;
+        t = valid ? (int)targets[row] : -1;
     }
-    __device__ void chunk(int row, int col, const float* v, int nvalid) {
-        float cm = -INFINITY;
-        for (int j = 0; j < nvalid; ++j) cm = fmaxf(cm, v[j]);
-        const float nm = fmaxf(m, cm);
-        float acc = s * expf(m - nm);
-        for (int j = 0; j < nvalid; ++j) acc += expf(v[j] - nm);
-        s = acc;
-        m = nm;
-        if (t >= col && t < col + nvalid) tgt[row] = v[t - col];
-    }
-    __device__ void end_tile(int row, int, int nb, bool valid) {
-        if (valid) {
-            pmax[(int64_t)row * ntn + nb] = m;
-            psum[(int64_t)row * ntn + nb] = s;
-        }
-    }
-};
-
-struct EpiGrad {  // K2: G = scale * (exp(S - lse) - onehot), bf16
-    const int64_t* targets;
-    const float* lse;
-    float scale;
-    bf16* g;
-    int N;
-    float l;
-    int64_t t;
-    __device__ void begin_tile(int row, int, int, bool valid) {
-        if (valid) {
-            l = lse[row];
-            t = targets[row];
-        }
-    }
-    __device__ void chunk(int row, int col, const float* v, int nvalid) {
-        float gv[16];
+    __device__ void pre(int row, int col, const float* v, int nvalid) {
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-            gv[j] = scale * expf(v[j] - l) - ((int64_t)(col + j) == t ? scale : 0.f);
+            if (j < nvalid) m = fmaxf(m, v[j]);
+        const int d = t - col;
+        if ((unsigned)d < (unsigned)nvalid) {  // rare: the target is in this chunk
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j == d) tgt[row] = v[j];  // register-indexed (no local copy)
+        }
+    }
+    __device__ void chunk(int row, int col, const float* v, int nvalid) {
+        float e[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            e[j] = j < nvalid ? __expf(v[j] - m) : 0.f;
+            s += e[j];
+        }
         bf16* gr = g + (int64_t)row * N + col;
         if (nvalid == 16) {
             uint32_t w[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                __nv_bfloat162 b = __floats2bfloat162_rn(gv[2 * j], gv[2 * j + 1]);
+                __nv_bfloat162 b = __floats2bfloat162_rn(e[2 * j], e[2 * j + 1]);
                 w[j] = *reinterpret_cast<uint32_t*>(&b);
             }
             reinterpret_cast<uint4*>(gr)[0] = make_uint4(w[0], w[1], w[2], w[3]);
             reinterpret_cast<uint4*>(gr)[1] = make_uint4(w[4], w[5], w[6], w[7]);
         } else {
-            for (int j = 0; j < nvalid; ++j) gr[j] = __float2bfloat16_rn(gv[j]);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < nvalid) gr[j] = __float2bfloat16_rn(e[j]);
         }
     }
-    __device__ void end_tile(int, int, int, bool) {}
+    __device__ void end_tile(int row, int, int part, bool valid) {
+        if (valid) {
+            pmax[(int64_t)row * ntn + part] = m;
+            psum[(int64_t)row * ntn + part] = s;
+        }
+    }
 };
 
 template <bool ACCUM>
 struct EpiF32 {  // K3 store / K4 accumulate
+    static constexpr bool kTwoPass = false;
     float* out;
     int ldo;
     __device__ void begin_tile(int, int, int, bool) {}
@@ -143,7 +138,9 @@ struct EpiF32 {  // K3 store / K4 accumulate
                 *reinterpret_cast<float4*>(o + j) = c;
             }
         } else {
-            for (int j = 0; j < nvalid; ++j) o[j] = ACCUM ? o[j] + v[j] : v[j];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < nvalid) o[j] = ACCUM ? o[j] + v[j] : v[j];
         }
     }
     __device__ void end_tile(int, int, int, bool) {}
@@ -163,30 +160,65 @@ __device__ __forceinline__ void lse_combine(float& m1, float& s1, float m2, floa
     s1 = s1 * expf(m1 - M) + s2 * expf(m2 - M);
     m1 = M;
 }
-__global__ void k_lse_merge(const float* __restrict__ pmax, const float* __restrict__ psum,
-                            const float* __restrict__ tgt, int n, int ntn, float* __restrict__ lse,
-                            float* __restrict__ rowloss) {
-    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (i >= n) return;
+// F: one CTA per row.  Warp 0 merges the row's part partials in ascending
+// part order (lane-strided, then a fixed xor butterfly) -> lse and the row
+// loss; then all threads rescale the row's P~ in place to the bf16 logit
+// gradient G = scale (P~ exp(m_p - lse) - [v == t]), 16 bytes at a time
+// (a 16-byte vector never straddles a 128-column part).
+constexpr int kFixThreads = 256;
+constexpr int kPartCols = kBN / kParts;
+__global__ void __launch_bounds__(kFixThreads)
+k_grad_fixup(const float* __restrict__ pmax, const float* __restrict__ psum,
+             const float* __restrict__ tgt, const int64_t* __restrict__ targets, int ntn, int V,
+             float scale, bf16* __restrict__ g, float* __restrict__ lse_out,
+             float* __restrict__ rowloss) {
+    extern __shared__ float fac[];  // ntn part factors
+    __shared__ float sh_lse;
+    const int i = blockIdx.x, lane = threadIdx.x & 31;
     const float* pm = pmax + (int64_t)i * ntn;
     const float* ps = psum + (int64_t)i * ntn;
-    float M = -INFINITY, S = 0.f;
-    for (int b = lane; b < ntn; b += 32) lse_combine(M, S, pm[b], ps[b]);
+    if (threadIdx.x < 32) {
+        float M = -INFINITY, S = 0.f;
+        for (int b = lane; b < ntn; b += 32) lse_combine(M, S, pm[b], ps[b]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, M, o);
-        const float s2 = __shfl_xor_sync(0xffffffffu, S, o);
-        // symmetric combine so both lanes of a pair hold identical values
-        const float Mx = fmaxf(M, m2);
-        const float a = (S == 0.f) ? 0.f : S * expf(M - Mx);
-        const float c = (s2 == 0.f) ? 0.f : s2 * expf(m2 - Mx);
-        S = (lane & o) ? (c + a) : (a + c);
-        M = Mx;
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, M, o);
+            const float s2 = __shfl_xor_sync(0xffffffffu, S, o);
+            // symmetric combine so both lanes of a pair hold identical values
+            const float Mx = fmaxf(M, m2);
+            const float a = (S == 0.f) ? 0.f : S * expf(M - Mx);
+            const float c = (s2 == 0.f) ? 0.f : s2 * expf(m2 - Mx);
+            S = (lane & o) ? (c + a) : (a + c);
+            M = Mx;
+        }
+        if (lane == 0) {
+            const float l = M + logf(S);
+            sh_lse = l;
+            lse_out[i] = l;
+            rowloss[i] = l - tgt[i];
+        }
     }
-    if (lane == 0) {
-        const float l = M + logf(S);
-        lse[i] = l;
-        rowloss[i] = l - tgt[i];
+    __syncthreads();
+    const float l = sh_lse;
+    for (int b = threadIdx.x; b < ntn; b += kFixThreads)
+        fac[b] = ps[b] == 0.f ? 0.f : scale * __expf(pm[b] - l);
+    __syncthreads();
+    const int64_t t = targets[i];
+    bf16* gr = g + (int64_t)i * V;
+    for (int c = threadIdx.x * 8; c < V; c += kFixThreads * 8) {
+        const float f = fac[c / kPartCols];
+        uint4 u = *reinterpret_cast<const uint4*>(gr + c);
+        uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w[j]);
+            float2 p = __bfloat1622float2(b);
+            p.x = p.x * f - ((int64_t)(c + 2 * j) == t ? scale : 0.f);
+            p.y = p.y * f - ((int64_t)(c + 2 * j + 1) == t ? scale : 0.f);
+            b = __floats2bfloat162_rn(p.x, p.y);
+            w[j] = *reinterpret_cast<uint32_t*>(&b);
+        }
+        *reinterpret_cast<uint4*>(gr + c) = u;
     }
 }
 
@@ -256,26 +288,23 @@ extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const voi
     const int ntn = (int)(kParts * ((V + kBN - 1) / kBN));
     const float scale = weight / (float)n;
     int rc;
-    // K1: online log-sum-exp partials + target logits (A = X and B = W K-major)
-    if ((rc = tc::launch_tc_gemm<kBN, false, false, false>(
-             x, W, (int)n, (int)V, (int)h, EpiLse{targets, w.pmax, w.psum, w.tgt, ntn, 0.f, 0.f, 0},
-             s)))
+    // K1: S = X W^T -> part max / sum, target logits, P~ into G's buffer
+    if ((rc = tc::launch_tc_gemm2<kBN, false, false, false>(
+             x, W, (int)n, (int)V, (int)h,
+             EpiProb{targets, w.pmax, w.psum, w.tgt, w.g, ntn, (int)V, 0.f, 0.f, 0}, s)))
         return rc;
-    k_lse_merge<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(w.pmax, w.psum, w.tgt, (int)n, ntn,
-                                                            w.lse, w.rowloss);
-    if ((rc = ee_check_launch("lse_merge"))) return rc;
+    // F: lse, row losses, P~ -> G in place
+    k_grad_fixup<<<(unsigned)n, kFixThreads, ntn * sizeof(float), s>>>(
+        w.pmax, w.psum, w.tgt, targets, ntn, (int)V, scale, w.g, w.lse, w.rowloss);
+    if ((rc = ee_check_launch("grad_fixup"))) return rc;
     k_loss_sum<<<1, 1024, 0, s>>>(w.rowloss, (int)n, scale, loss);
     if ((rc = ee_check_launch("loss_sum"))) return rc;
-    // K2: logit gradient G (bf16, n x V)
-    if ((rc = tc::launch_tc_gemm<kBN, false, false, false>(
-             x, W, (int)n, (int)V, (int)h, EpiGrad{targets, w.lse, scale, w.g, (int)V, 0.f, 0}, s)))
-        return rc;
     // K3: dX = G W     (W (V x h) is the MN-major B operand, K = V)
-    if ((rc = tc::launch_tc_gemm<kBN, false, true, false>(w.g, W, (int)n, (int)h, (int)V,
+    if ((rc = tc::launch_tc_gemm2<kBN, false, true, false>(w.g, W, (int)n, (int)h, (int)V,
                                                           EpiF32<false>{dx, (int)h}, s)))
         return rc;
     // K4: dW += G^T X  (G and X both MN-major, K = n); N-fastest tile order so
     // concurrent CTAs share each G column block
-    return tc::launch_tc_gemm<kBN, true, true, true>(w.g, x, (int)V, (int)h, (int)n,
+    return tc::launch_tc_gemm2<kBN, true, true, true>(w.g, x, (int)V, (int)h, (int)n,
                                                      EpiF32<true>{dw_acc, (int)h}, s);
 }

@@ -103,6 +103,69 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Epilogue over one (row, half-tile) of the accumulator.  Two-pass
+// epilogues get the whole half-row (BN/2 fp32) in registers with one
+// tcgen05.wait (pre() over every chunk, then chunk() over every chunk);
+// one-pass epilogues stream it 16 columns at a time.
+template <int BN, class Epi>
+__device__ __forceinline__ void epilogue_half_row(Epi& epi, uint32_t base, int row, int M, int N,
+                                                  int col0) {
+    if constexpr (Epi::kTwoPass) {
+        float v[BN / 2];
+#pragma unroll
+        for (int c = 0; c < BN / 2; c += 16) tmem_ld16_nowait(base + c, v + c);
+        tmem_wait_ld();
+        if (row < M) {
+            if (col0 + BN / 2 <= N) {  // interior tile: nvalid folds to 16
+#pragma unroll
+                for (int c = 0; c < BN / 2; c += 16) epi.pre(row, col0 + c, v + c, 16);
+#pragma unroll
+                for (int c = 0; c < BN / 2; c += 16) epi.chunk(row, col0 + c, v + c, 16);
+            } else {
+#pragma unroll
+                for (int c = 0; c < BN / 2; c += 16) {
+                    const int nvalid = min(16, N - (col0 + c));
+                    if (nvalid > 0) epi.pre(row, col0 + c, v + c, nvalid);
+                }
+#pragma unroll
+                for (int c = 0; c < BN / 2; c += 16) {
+                    const int nvalid = min(16, N - (col0 + c));
+                    if (nvalid > 0) epi.chunk(row, col0 + c, v + c, nvalid);
+                }
+            }
+        }
+    } else {
+        const bool interior = col0 + BN / 2 <= N;
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 16) {
+            float v[16];
+            tmem_ld16(base + c, v);
+            if (row < M) {
+                if (interior) {
+                    epi.chunk(row, col0 + c, v, 16);
+                } else {
+                    const int nvalid = min(16, N - (col0 + c));
+                    if (nvalid > 0) epi.chunk(row, col0 + c, v, nvalid);
+                }
+            }
+        }
+    }
+}
+
 // Canonical UMMA shared-memory descriptors, 128-byte swizzle, version 1.
 // K-major tile (rows x 64 k): rows of 128 B, 8-row atoms 1024 B apart (SBO),
 //   LBO unused (1); the k-th UMMA_K=16 slice starts 32*k bytes in.
@@ -127,7 +190,9 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 // Kernel.  Epi::chunk(row, col0, v[16], nvalid) is called per 16-column chunk
 // for every row of the tile (by the epilogue thread owning that row and
 // column half, in ascending column order); Epi::begin_tile / end_tile
-// bracket one (row, half-tile) with part = 2 * n_tile + half.
+// bracket one (row, half-tile) with part = 2 * n_tile + half.  An epilogue
+// with kTwoPass = true first sees every chunk of the (row, half-tile) through
+// Epi::pre (same order), then through Epi::chunk (epilogue_half_row).
 // A_MN / B_MN: operand stored MN-major (row-major (K, MN) in HBM) instead of
 // K-major; N_FASTEST: tile order (pick so the larger operand is shared by
 // the CTAs running at the same time).
@@ -256,13 +321,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
             epi.begin_tile(row, col0, part, row < M);
             const uint32_t base =
                 tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * (BN / 2);
-#pragma unroll 1
-            for (int c = 0; c < BN / 2; c += 16) {
-                float v[16];
-                tmem_ld16(base + c, v);
-                const int nvalid = min(16, N - (col0 + c));
-                if (row < M && nvalid > 0) epi.chunk(row, col0 + c, v, nvalid);
-            }
+            epilogue_half_row<BN>(epi, base, row, M, N, col0);
             epi.end_tile(row, col0, part, row < M);
             tc_fence_before();
             __syncwarp();
@@ -278,6 +337,225 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(C::kTmemCols));
+    }
+}
+
+// ---- CTA-pair (cta_group::2) variant -----------------------------------------
+// A cluster of two CTAs on one TPC computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (UMMA 256 x BN x 16): CTA r stages rows
+// [128 r, 128 r + 128) of A and columns [BN/2 r, BN/2 r + BN/2) of B, so each
+// SM streams half of B through shared memory (the 1-CTA 128 x 256 tile is
+// shared-memory-bandwidth bound at ~75% of the tensor pipe).  The leader
+// (rank 0) issues every MMA; both CTAs' TMA loads complete on the leader's
+// full[s] barrier; commits are multicast to both CTAs' empty / tmem_full
+// barriers; both CTAs' epilogue warps release the accumulator on the
+// leader's tmem_empty.  Each CTA's TMEM holds the accumulator rows of its
+// own 128 A rows, so the epilogue is identical to the 1-CTA kernel.
+constexpr int kStages2 = 6;
+
+template <int BN>
+struct Cfg2 {
+    static constexpr int kBBytes = (BN / 2) * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kTmemCols = 2 * BN;
+    static constexpr size_t kSmem = (size_t)kStages2 * kStageBytes + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(su32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mb_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the barrier at this smem offset in both CTAs of the pair once
+// all previously issued MMAs have completed
+__device__ __forceinline__ void tc_commit2(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], m;\n\t}" ::"r"(su32(bar))
+        : "memory");
+}
+
+template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M,
+           int N, int K, Epi epi) {
+    using C = Cfg2<BN>;
+    constexpr int BM2 = 2 * BM;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * C::kStageBytes);
+    uint64_t* empty = full + kStages2;
+    uint64_t* tfull = empty + kStages2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int tiles_m = (M + BM2 - 1) / BM2, tiles_n = (N + BN - 1) / BN;
+    const int ntiles = tiles_m * tiles_n;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages2; ++s) {
+            mb_init(&full[s], 1);
+            mb_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mb_init(&tfull[b], 1);
+            mb_init(&tempty[b], 2 * kEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(tmem_slot)),
+                     "n"(C::kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer (both CTAs) ----------------
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&ta) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tb) : "memory");
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = cid; t < ntiles; t += ncl) {
+                const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
+                const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
+                const int m0 = mb * BM2 + (int)rank * BM;
+                const int n0 = nb * BN + (int)rank * (BN / 2);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mb_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * C::kStageBytes;
+                    const uint32_t bar = map_rank(&full[s], 0);
+                    if (rank == 0) mb_expect_tx(&full[s], 2 * C::kStageBytes);
+                    if (A_MN) {
+                        for (int c = 0; c < BM / 64; ++c)
+                            tma_load_2d_pair(st + c * 8192, &ta, m0 + c * 64, kb * BK, bar);
+                    } else {
+                        tma_load_2d_pair(st, &ta, kb * BK, m0, bar);
+                    }
+                    if (B_MN) {
+                        for (int c = 0; c < BN / 128; ++c)
+                            tma_load_2d_pair(st + kABytes + c * 8192, &tb, n0 + c * 64, kb * BK, bar);
+                    } else {
+                        tma_load_2d_pair(st + kABytes, &tb, kb * BK, n0, bar);
+                    }
+                    if (++s == kStages2) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            // ---------------- MMA issuer (leader CTA only) ----------------
+            constexpr uint32_t idesc = idesc_bf16(BM2, BN, A_MN, B_MN);
+            int s = 0;
+            uint32_t ph = 0;
+            int acc = 0;
+            uint32_t aph = 0;
+            for (int t = cid; t < ntiles; t += ncl) {
+                mb_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mb_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = su32(smem + s * C::kStageBytes);
+                    const uint32_t b0 = a0 + kABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc_mma2(d, op_desc<A_MN>(a0, k), op_desc<B_MN>(b0, k), idesc,
+                                (kb | k) != 0);
+                    tc_commit2(&empty[s]);  // both CTAs' stage s free once these MMAs completed
+                    if (++s == kStages2) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                tc_commit2(&tfull[acc]);  // both CTAs' accumulators ready
+                if (++acc == 2) {
+                    acc = 0;
+                    aph ^= 1;
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue (warps 2..9 of both CTAs) ----------------
+        const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int row_in_tile = (int)rank * BM + quarter * 32 + lane;
+        const uint32_t leader_tempty0 = map_rank(&tempty[0], 0);
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int t = cid; t < ntiles; t += ncl) {
+            const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
+            const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
+            mb_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const int row = mb * BM2 + row_in_tile;
+            const int col0 = nb * BN + half * (BN / 2);
+            const int part = nb * 2 + half;
+            epi.begin_tile(row, col0, part, row < M);
+            const uint32_t base =
+                tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * (BN / 2);
+            epilogue_half_row<BN>(epi, base, row, M, N, col0);
+            epi.end_tile(row, col0, part, row < M);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive_remote(leader_tempty0 + acc * 8);
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // all MMAs consumed, all remote arrivals landed
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                      "n"(C::kTmemCols));
     }
 }
@@ -306,6 +584,30 @@ int launch_tc_gemm(const void* A, const void* B, int M, int N, int K, Epi epi, c
     const int grid = tiles < ee_sm_count() ? tiles : ee_sm_count();
     kern<<<grid, kThreads, Cfg<BN>::kSmem, s>>>(ta, tb, M, N, K, epi);
     return ee_check_launch("tc_gemm");
+}
+
+
+// CTA-pair launch: M tiles of 256 rows, grid = 2 x min(tiles, SMs / 2).
+template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
+int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, cudaStream_t s) {
+    CUtensorMap ta, tb;
+    int rc;
+    if ((rc = A_MN ? make_tmap_bf16(&ta, A, K, M, BK) : make_tmap_bf16(&ta, A, M, K, BM))) return rc;
+    if ((rc = B_MN ? make_tmap_bf16(&tb, B, K, N, BK) : make_tmap_bf16(&tb, B, N, K, BN / 2)))
+        return rc;
+    auto kern = k_tc_gemm2<BN, A_MN, B_MN, N_FASTEST, Epi>;
+    static bool configured[16] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!configured[dev & 15]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg2<BN>::kSmem);
+        configured[dev & 15] = true;
+    }
+    const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+    const int pairs = ee_sm_count() / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    kern<<<grid, kThreads, Cfg2<BN>::kSmem, s>>>(ta, tb, M, N, K, epi);
+    return ee_check_launch("tc_gemm2");
 }
 
 }  // namespace tc
