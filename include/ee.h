@@ -208,6 +208,34 @@ int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64
                        const int64_t* targets, float weight, float* loss, float* dx, float* dw_acc,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* ---- optimizer step (fused, multi-tensor) ----------------------------- */
+
+#define EE_OPT_SGD 0
+#define EE_OPT_ADAM 1
+
+/* One parameter tensor of a fused optimizer step; the table itself is a
+ * DEVICE array, entries sorted by `start` (prefix element offsets, tensors
+ * laid end to end in one index space of `total` elements). */
+typedef struct {
+    float* param;       /* float32 master weights (n), updated in place      */
+    const void* grad;   /* gradient (n), float32 or bf16 (grad_dtype)         */
+    float* m;           /* Adam first moment (n), float32; unused for SGD     */
+    float* v;           /* Adam second moment (n), float32; unused for SGD    */
+    void* param_lp;     /* nullable: bf16 copy of the updated weights (n)     */
+    int64_t n;          /* element count                                     */
+    int64_t start;      /* offset of element 0 in the virtual index space    */
+} ee_opt_tensor_t;
+
+/* One optimizer step over every tensor of `table` in a single launch:
+ * SGD p -= lr * g, or Adam m += (1-b1)(g-m), v += (1-b2)(g^2-v),
+ * p -= step_size * m / (sqrt(v) + eps), with g = grad * grad_scale and
+ * step_size = lr * sqrt(1 - b2^t) / (1 - b1^t) computed by the caller.
+ * Replaces `SGD.step` / `Adam.step` (eepipe/training.py:24-53); the caller
+ * passes grad_scale = 1 / num_microbatches (eepipe/training.py:108). */
+int ee_optimizer_step(const ee_opt_tensor_t* table, int32_t n_tensors, int64_t total, int kind,
+                      int grad_dtype, float lr, float beta1, float beta2, float eps,
+                      float grad_scale, float step_size, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

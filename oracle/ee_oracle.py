@@ -386,3 +386,27 @@ def exit_head_train(x, w, targets, weight=1.0, norm_w=None):
         gwx = np.sum(dxs * norm_w[None, :] * x, axis=1)
         dx = dxs * norm_w[None, :] * inv[:, None] - x * (inv ** 3 * gwx / h)[:, None]
     return weight * ce, dx, dw, dnorm
+
+
+# --- optimizers (eepipe/training.py:24-53) ------------------------------------
+
+
+def sgd_step(params, grads, scale, lr):
+    """`SGD.step` (`training.py:28-30`), float64, in place."""
+    for name in sorted(grads):
+        params[name] -= lr * scale * grads[name]
+
+
+def adam_step(params, grads, scale, state, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """`Adam.step` (`training.py:44-53`), float64, in place; ``state`` holds
+    t, m, v across calls."""
+    state["t"] = state.get("t", 0) + 1
+    t = state["t"]
+    correction = np.sqrt(1 - beta2 ** t) / (1 - beta1 ** t)
+    for name in sorted(grads):
+        g = grads[name] * scale
+        m = state.setdefault(("m", name), np.zeros_like(g))
+        v = state.setdefault(("v", name), np.zeros_like(g))
+        m += (1 - beta1) * (g - m)
+        v += (1 - beta2) * (g * g - v)
+        params[name] -= lr * correction * m / (np.sqrt(v) + eps)

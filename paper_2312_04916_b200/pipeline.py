@@ -187,18 +187,19 @@ class StageCompute:
     device and the fused tcgen05 exit heads; exit losses are formed in the
     backward step (deferred exit forward)."""
 
-    def __init__(self, spec, cfg, model_src, weights, device=None, dtype=None):
+    def __init__(self, spec, cfg, model_src, weights, device=None, dtype=None, master_dtype=None):
         from .training import TrainModel
         self.spec = spec
         self.cfg = cfg
-        self.tm = TrainModel(model_src, dtype=dtype, device=device, names=list(spec.params))
+        self.tm = TrainModel(model_src, dtype=dtype, device=device, names=list(spec.params),
+                             master_dtype=master_dtype)
         self.device = self.tm.device
         self.weights = weights  # by head key
         self.head_losses = {hd.key: [] for _, hd in spec.heads}
 
     def forward(self, tokens_or_x, targets):
         from .training import embed_tokens, run_layer
-        p = self.tm.params
+        p = self.tm.compute_params()
         if self.spec.has_embedding:
             x_in = None
             x = embed_tokens(p, tokens_or_x, self.cfg.max_seq_len)
@@ -218,8 +219,9 @@ class StageCompute:
         _, _, taps, targets = state
         targets = torch.as_tensor(np.asarray(targets)).to(self.device)
         total = None
+        params = self.tm.compute_params()
         for local, hd in self.spec.heads:
-            ce = head_loss(self.tm.params, hd, taps[local], targets, self.cfg.num_heads)
+            ce = head_loss(params, hd, taps[local], targets, self.cfg.num_heads)
             self.head_losses[hd.key].append(float(ce.detach()))
             term = ce * self.weights[hd.key]
             total = term if total is None else total + term
@@ -334,7 +336,7 @@ def sync_tied(per_stage_grads, tied_replicas=None):
 
 
 def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
-                       devices=None, dtype=None):
+                       devices=None, dtype=None, master_dtype=None):
     """One 1F1B iteration over the partition, one thread per stage
     (eepipe/pipeline.py:537-644).  ``model`` is the EarlyExitModel the stage
     weights come from (the partition's own copies are used when omitted).
@@ -352,7 +354,8 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
     workers = []
     for s, spec in enumerate(part.stages, start=1):
         holder = src if src is not None else _SpecModel(part, spec)
-        comp = StageCompute(spec, part.config, holder, wmap, devices[(s - 1) % len(devices)], dtype)
+        comp = StageCompute(spec, part.config, holder, wmap, devices[(s - 1) % len(devices)], dtype,
+                            master_dtype)
         workers.append(StageWorker(s, P, M, comp, data,
                                    fwd[s - 2] if s > 1 else None, fwd[s - 1] if s < P else None,
                                    bwd[s - 1] if s < P else None, bwd[s - 2] if s > 1 else None))

@@ -108,23 +108,57 @@ class ExitHeadCE:
 # ---------------------------------------------------------------------------
 
 
+class _CastView(dict):
+    """name -> parameter cast to the compute dtype, cast on first use and
+    cached for one forward/backward (the cast is an autograd node, so the
+    gradient lands in the float32 master leaf)."""
+
+    def __init__(self, masters, dtype):
+        super().__init__()
+        self._masters = masters
+        self._dtype = dtype
+
+    def __missing__(self, name):
+        t = self._masters[name].to(self._dtype)
+        self[name] = t
+        return t
+
+    def __contains__(self, name):
+        return name in self._masters
+
+
 class TrainModel:
     """Device-resident trainable copy of an `EarlyExitModel`: parameters as
     torch tensors (requires_grad) keyed by the reference names, compute dtype
-    bf16 (the fused exit head runs on bf16 tensor cores)."""
+    bf16 (the fused exit head runs on bf16 tensor cores).
 
-    def __init__(self, model: EarlyExitModel, dtype=None, device=None, names=None):
+    With ``master_dtype=torch.float32`` the leaves are float32 and every
+    forward uses bf16 casts of them (`compute_params()`), so gradients are
+    accumulated in float32 across microbatches (the optimizer's input);
+    otherwise the leaves are in the compute dtype."""
+
+    def __init__(self, model: EarlyExitModel, dtype=None, device=None, names=None,
+                 master_dtype=None):
         torch = _torch()
         _lib.require_cuda()
         self.config = model.config
         self.heads = model.heads
         self.device = torch.device(device or "cuda:0")
         self.dtype = dtype or torch.bfloat16
+        self.master_dtype = master_dtype or self.dtype
         self.params = {}
         for name in (names if names is not None else model.params):
             a = model.params[name].data
             t = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
-            self.params[name] = t.to(device=self.device, dtype=self.dtype).detach().requires_grad_()
+            self.params[name] = t.to(device=self.device,
+                                     dtype=self.master_dtype).detach().requires_grad_()
+
+    def compute_params(self):
+        """Parameters in the compute dtype (the leaves themselves when the
+        master dtype is the compute dtype)."""
+        if self.master_dtype == self.dtype:
+            return self.params
+        return _CastView(self.params, self.dtype)
 
     def zero_grad(self):
         for p in self.params.values():
@@ -210,13 +244,14 @@ def forward_all_exits(model: TrainModel, tokens):
     """Logits at every head, depth order (`eepipe/model.py:246-261`)."""
     cfg = model.config
     wanted = {hd.layer_index for hd in model.heads}
-    x = embed_tokens(model.params, tokens, cfg.max_seq_len)
+    params = model.compute_params()
+    x = embed_tokens(params, tokens, cfg.max_seq_len)
     taps = {0: x} if 0 in wanted else {}
     for i in range(1, cfg.num_layers + 1):
-        x = run_layer(model.params, f"layer{i}", x, cfg.num_heads)
+        x = run_layer(params, f"layer{i}", x, cfg.num_heads)
         if i in wanted:
             taps[i] = x
-    return [run_head(model.params, hd, taps[hd.layer_index], cfg.num_heads) for hd in model.heads]
+    return [run_head(params, hd, taps[hd.layer_index], cfg.num_heads) for hd in model.heads]
 
 
 def weighted_loss(model: TrainModel, batch, weights):
@@ -231,17 +266,18 @@ def weighted_loss(model: TrainModel, batch, weights):
     batch = torch.as_tensor(np.asarray(batch) if not isinstance(batch, torch.Tensor) else batch)
     batch = batch.to(model.device)
     wanted = {hd.layer_index for hd in model.heads}
-    x = embed_tokens(model.params, batch[:, :-1], cfg.max_seq_len)
+    params = model.compute_params()
+    x = embed_tokens(params, batch[:, :-1], cfg.max_seq_len)
     targets = batch[:, 1:]
     taps = {0: x} if 0 in wanted else {}
     for i in range(1, cfg.num_layers + 1):
-        x = run_layer(model.params, f"layer{i}", x, cfg.num_heads)
+        x = run_layer(params, f"layer{i}", x, cfg.num_heads)
         if i in wanted:
             taps[i] = x
     total = None
     per_exit = []
     for hd, w in zip(model.heads, weights):
-        ce = head_loss(model.params, hd, taps[hd.layer_index], targets, cfg.num_heads)
+        ce = head_loss(params, hd, taps[hd.layer_index], targets, cfg.num_heads)
         per_exit.append(float(ce.detach()))
         term = ce * w
         total = term if total is None else total + term
@@ -266,3 +302,209 @@ def single_device_gradients(model: TrainModel, batch, weights, microbatch_size):
         for i, v in enumerate(per_exit):
             sums[i] += v
     return model.grads(), {hd.key: sums[i] / num_mb for i, hd in enumerate(model.heads)}
+
+
+# ---------------------------------------------------------------------------
+# Optimizers and the training loop (eepipe/training.py)
+# ---------------------------------------------------------------------------
+
+_OPT_ENTRY = np.dtype([("param", "<u8"), ("grad", "<u8"), ("m", "<u8"), ("v", "<u8"),
+                       ("param_lp", "<u8"), ("n", "<i8"), ("start", "<i8")])  # ee_opt_tensor_t
+
+
+def _param_tensor(p):
+    return getattr(p, "data", p)
+
+
+class _FusedOptimizer:
+    """Shared plumbing of `SGD` / `Adam`: one `ee_optimizer_step` launch over
+    every parameter (include/ee.h, csrc/optim.cu).  Parameters are float32
+    CUDA master tensors (``Param.data`` or bare tensors) updated in place;
+    gradients float32 or bf16 of the same shapes."""
+
+    kind = None
+
+    def _launch(self, params, grads, scale, step_size, moments):
+        torch = _torch()
+        names = sorted(grads)  # the reference's update order (eepipe/training.py:29, 46)
+        if not names:
+            return
+        gdt = torch.float32 if any(grads[n].dtype != torch.bfloat16 for n in names) \
+            else torch.bfloat16
+        table = np.zeros(len(names), dtype=_OPT_ENTRY)
+        keep = []
+        start = 0
+        dev = None
+        for i, name in enumerate(names):
+            p = _param_tensor(params[name])
+            if not (isinstance(p, torch.Tensor) and p.is_cuda and p.dtype == torch.float32
+                    and p.is_contiguous()):
+                raise ShapeError(f"optimizer: {name} must be a contiguous float32 CUDA tensor")
+            g = grads[name]
+            if tuple(g.shape) != tuple(p.shape):
+                raise ShapeError(f"optimizer: gradient of {name} has shape {tuple(g.shape)}, "
+                                 f"parameter {tuple(p.shape)}")
+            g = g.to(device=p.device, dtype=gdt).contiguous()
+            dev = p.device
+            keep.append(g)
+            m, v = moments(name, p) if moments else (None, None)
+            table[i] = (p.data_ptr(), g.data_ptr(), m.data_ptr() if m is not None else 0,
+                        v.data_ptr() if v is not None else 0, 0, p.numel(), start)
+            start += p.numel()
+        tab = torch.from_numpy(table.view(np.uint8)).to(dev, non_blocking=False)
+        keep.append(tab)
+        call("ee_optimizer_step", ptr(tab), len(names), start, self.kind, _lib.dtype_code(gdt),
+             float(self.lr), float(getattr(self, "beta1", 0.0)), float(getattr(self, "beta2", 0.0)),
+             float(getattr(self, "eps", 0.0)), float(scale), float(step_size), stream_ptr())
+        return keep
+
+
+class SGD(_FusedOptimizer):
+    """p -= lr * scale * g (`eepipe/training.py:24-30`)."""
+
+    kind = _lib.EE_OPT_SGD
+
+    def __init__(self, lr):
+        self.lr = lr
+
+    def step(self, params, grads, scale):
+        self._launch(params, grads, scale, 0.0, None)
+
+
+class Adam(_FusedOptimizer):
+    """Adam with the reference's update form (`eepipe/training.py:33-53`):
+    m += (1-b1)(g-m); v += (1-b2)(g²-v);
+    p -= lr·sqrt(1-b2^t)/(1-b1^t) · m/(sqrt(v)+eps); moments float32 on the
+    parameter's device."""
+
+    kind = _lib.EE_OPT_ADAM
+
+    def __init__(self, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.lr = lr
+        self.beta1 = beta1
+        self.beta2 = beta2
+        self.eps = eps
+        self.m: dict = {}
+        self.v: dict = {}
+        self.t = 0
+
+    def _moments(self, name, p):
+        torch = _torch()
+        if name not in self.m:
+            self.m[name] = torch.zeros_like(p)
+            self.v[name] = torch.zeros_like(p)
+        return self.m[name], self.v[name]
+
+    def step(self, params, grads, scale):
+        self.t += 1
+        b1, b2 = self.beta1, self.beta2
+        correction = np.sqrt(1 - b2 ** self.t) / (1 - b1 ** self.t)  # float64, as the reference
+        self._launch(params, grads, scale, self.lr * correction, self._moments)
+
+
+def make_optimizer(kind, lr):
+    from .errors import ConfigError
+    if kind == "sgd":
+        return SGD(lr)
+    if kind == "adam":
+        return Adam(lr)
+    raise ConfigError(f"unknown optimizer {kind!r}")
+
+
+def device_master(model: EarlyExitModel, device=None) -> EarlyExitModel:
+    """float32 device copy of a model: the optimizer's master weights (the
+    reference's monolithic float64 model, `eepipe/training.py:1-8`)."""
+    torch = _torch()
+    from .model import Param
+    dev = torch.device(device or "cuda:0")
+    params = {}
+    for name, p in model.params.items():
+        a = p.data
+        t = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
+        params[name] = Param(t.to(device=dev, dtype=torch.float32).contiguous().clone())
+    return EarlyExitModel(model.config, params, model.heads)
+
+
+def train(run_cfg, corpus, metrics_path=None, progress=None, *, devices=None, dtype=None):
+    """Train per the run configuration; returns (model, history)
+    (`eepipe/training.py:64-136`).
+
+    ``run_cfg`` carries the reference `RunConfig` fields this loop reads
+    (model, seed, stages, microbatch_size, global_batch_size, steps,
+    optimizer, learning_rate, data_seq_len, defer_exit_forward,
+    fill_bubbles, weight_schedule()) — the reference's own RunConfig works
+    as is; ``corpus.batch(rows, row_len, step)`` supplies token ids.  Every
+    step partitions the float32 device master model, runs one 1F1B
+    iteration (`pipeline.run_iteration_1f1b`: stage threads, fused tcgen05
+    exit heads, bf16 compute, float32 gradient accumulation), and applies the fused optimizer with
+    scale 1/num_microbatches.  Metrics: a header record then one record per
+    step (losses, time, microbatches, weights) as line-delimited JSON.
+    Bubble filling is out of scope and rejected."""
+    import json
+    import time
+    from .errors import ConfigError, NonFiniteError
+    from .model import build_model, partition
+    from .pipeline import IterationOptions, run_iteration_1f1b
+    torch = _torch()
+    if getattr(run_cfg, "fill_bubbles", False):
+        raise ConfigError("bubble filling is not supported by this build")
+    _lib.require_cuda()
+    master = device_master(build_model(run_cfg.model, run_cfg.seed),
+                           devices[0] if devices else None)
+    optimizer = make_optimizer(run_cfg.optimizer, run_cfg.learning_rate)
+    rows_per_step = run_cfg.global_batch_size
+    if rows_per_step % run_cfg.microbatch_size:
+        raise ConfigError("global batch not divisible by the microbatch size")
+    num_mb = rows_per_step // run_cfg.microbatch_size
+    row_len = run_cfg.data_seq_len + 1
+    schedule = run_cfg.weight_schedule() if hasattr(run_cfg, "weight_schedule") else None
+    head_keys = None
+    history = []
+    fh = open(metrics_path, "w") if metrics_path else None
+
+    def write(rec):
+        if fh:
+            fh.write(json.dumps(rec, sort_keys=True) + "\n")
+
+    try:
+        for step in range(run_cfg.steps):
+            part = partition(master, run_cfg.stages, copy=False)
+            batch = corpus.batch(rows_per_step, row_len, step)
+            opts = IterationOptions(microbatch_size=run_cfg.microbatch_size,
+                                    defer_exit_forward=getattr(run_cfg, "defer_exit_forward", True),
+                                    weight_schedule=schedule, step=step)
+            t0 = time.perf_counter()
+            grads, report = run_iteration_1f1b(part, batch, opts, model=master, devices=devices,
+                                               dtype=dtype, master_dtype=torch.float32)
+            if not all(np.isfinite(v) for v in report.per_exit_loss.values()):
+                raise NonFiniteError(f"non-finite loss at step {step}")
+            optimizer.step(master.params, grads, 1.0 / num_mb)
+            torch.cuda.synchronize()
+            elapsed = time.perf_counter() - t0
+            if head_keys is None:
+                head_keys = [hd.key for hd in master.heads if hd.key in report.per_exit_loss]
+                write({"record": "header", "heads": head_keys, "steps": run_cfg.steps,
+                       "seed": run_cfg.seed})
+            rec = {"record": "step", "step": step,
+                   "losses": {k: report.per_exit_loss[k] for k in head_keys},
+                   "time": elapsed, "microbatches": num_mb,
+                   "weights": list(report.weights_used)}
+            history.append(rec)
+            write(rec)
+            if progress is not None:
+                progress(rec)
+        if head_keys is None:
+            write({"record": "header", "heads": [], "steps": 0, "seed": run_cfg.seed})
+    finally:
+        if fh:
+            fh.close()
+    return master, history
+
+
+def trailing_average(values, window):
+    """Mean of the last `window` entries at each step (`eepipe/training.py:144-150`)."""
+    out = []
+    for i in range(len(values)):
+        lo = max(0, i - window + 1)
+        out.append(float(np.mean(values[lo:i + 1])))
+    return out
