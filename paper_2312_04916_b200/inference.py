@@ -47,6 +47,8 @@ from .schedule import inference_latency
 _UNSUPPORTED_HEADS = ("layer+embed",)
 _EMIT_TIMEOUT = 120.0
 _HEAD_MAX_ROWS = 16
+_RES_DTYPE = np.dtype([("tok", "<i4", (_HEAD_MAX_ROWS,)), ("conf", "<f4", (_HEAD_MAX_ROWS,)),
+                       ("fire", "u1", (_HEAD_MAX_ROWS,)), ("bad", "<i4"), ("pad", "u1", (12,))])
 
 
 def _torch():
@@ -238,6 +240,7 @@ class _PinnedRing:
         torch = _torch()
         self.cap = cap
         self.bufs = [torch.zeros(cap, dtype=torch.int32).pin_memory() for _ in range(n)]
+        self.views = [b.numpy() for b in self.bufs]  # numpy views: no torch op per fill
         self.events = [None] * n
         self.i = 0
 
@@ -252,7 +255,7 @@ class _PinnedRing:
         if self.events[i] is not None:
             self.events[i].synchronize()
         b = self.bufs[i]
-        b[:n] = torch.from_numpy(arr)
+        self.views[i][:n] = arr
         dst[:n].copy_(b[:n], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(stream)
@@ -354,17 +357,14 @@ class Engine:
             self.head_x = torch.empty((_HEAD_MAX_ROWS, h), dtype=torch.float32, device=self.device)
             self.head_mid = torch.empty((_HEAD_MAX_ROWS, 4 * h), dtype=dtype, device=self.device)
             self.max_slots = 256
-            self.r_tok = torch.zeros((self.max_slots, _HEAD_MAX_ROWS), dtype=torch.int32,
-                                     device=self.device)
-            self.r_conf = torch.zeros((self.max_slots, _HEAD_MAX_ROWS), dtype=torch.float32,
-                                      device=self.device)
-            self.r_fire = torch.zeros((self.max_slots, _HEAD_MAX_ROWS), dtype=torch.uint8,
-                                      device=self.device)
-            self.r_bad = torch.zeros((self.max_slots,), dtype=torch.int32, device=self.device)
-            self.h_tok = torch.zeros_like(self.r_tok, device="cpu").pin_memory()
-            self.h_conf = torch.zeros_like(self.r_conf, device="cpu").pin_memory()
-            self.h_fire = torch.zeros_like(self.r_fire, device="cpu").pin_memory()
-            self.h_bad = torch.zeros_like(self.r_bad, device="cpu").pin_memory()
+            # per-evaluation result slots, packed so one D2H copy fetches them
+            # all: tok int32[R] | conf f32[R] | fire u8[R] | bad int32 | pad
+            self.res = torch.zeros(self.max_slots * _RES_DTYPE.itemsize, dtype=torch.uint8,
+                                   device=self.device)
+            self.h_res_t = torch.zeros(self.res.numel(), dtype=torch.uint8).pin_memory()
+            self.h_res = self.h_res_t.numpy().view(_RES_DTYPE)
+            self.h_tok, self.h_conf = self.h_res["tok"], self.h_res["conf"]
+            self.h_fire, self.h_bad = self.h_res["fire"], self.h_res["bad"]
             self.max_rows = 0
             self._grow(max_rows)
         # accounting for bench.py: kernels launched and host<->device bytes
@@ -422,10 +422,12 @@ class Engine:
     def ctrl_ptr(self, off):
         return ctypes.c_void_p(self.ctrl.data_ptr() + 4 * off)
 
-    def embed_rows(self, tokens, positions, row0, out=None, staging=None):
+    def embed_rows(self, tokens, positions, row0, out=None, staging=None, ctrl_off=None):
         """x[row0:row0+m] = tok_emb[tokens] + pos_emb[positions]  (or into
         ``out`` with a separate (ring, device buffer) ``staging`` pair, for an
-        embedder running beside the stage worker that owns ``x``)."""
+        embedder running beside the stage worker that owns ``x``).  With
+        ``ctrl_off`` the ids and positions were already uploaded with the
+        pass's control block (ctrl[off:off+m], ctrl[off+m:off+2m])."""
         tokens = np.asarray(tokens, dtype=np.int64)
         if tokens.size and (tokens.min() < 0 or tokens.max() >= self.cfg.vocab_size):
             raise TokenError("token id out of vocabulary range")
@@ -437,11 +439,15 @@ class Engine:
         else:
             dst = ptr(out)
             ring, dbuf = staging
-        stage = np.concatenate([tokens, np.asarray(positions, dtype=np.int64)])
-        ring.put(stage, dbuf, _torch().cuda.current_stream(self.device))
-        self.h2d_bytes += 4 * len(stage)
+        if ctrl_off is not None:
+            tok_p, pos_p = self.ctrl_ptr(ctrl_off), self.ctrl_ptr(ctrl_off + m)
+        else:
+            stage = np.concatenate([tokens, np.asarray(positions, dtype=np.int64)])
+            ring.put(stage, dbuf, _torch().cuda.current_stream(self.device))
+            self.h2d_bytes += 4 * len(stage)
+            tok_p, pos_p = ptr(dbuf), ctypes.c_void_p(dbuf.data_ptr() + 4 * m)
         self.launches += 1
-        call("ee_embed", ptr(dbuf), ctypes.c_void_p(dbuf.data_ptr() + 4 * m), m,
+        call("ee_embed", tok_p, pos_p, m,
              ptr(self.tok_emb), ptr(self.pos_emb), self.h, self.dcode, dst,
              stream_ptr(_torch().cuda.current_stream(self.device)))
         if out is None:
@@ -478,22 +484,24 @@ class Engine:
         self.launches += 1 if self.dcode == _lib.EE_BF16 else 2
         call("ee_exit_head_infer", ptr(xsrc), h, rows_ptr, m, h, ptr(e.norm), NORM_EPS,
              ptr(e.W), e.V, self.wcode, float(threshold),
-             ctypes.c_void_p(self.r_tok.data_ptr() + 4 * _HEAD_MAX_ROWS * slot),
-             ctypes.c_void_p(self.r_conf.data_ptr() + 4 * _HEAD_MAX_ROWS * slot),
-             ctypes.c_void_p(self.r_fire.data_ptr() + _HEAD_MAX_ROWS * slot),
-             ctypes.c_void_p(self.r_bad.data_ptr() + 4 * slot), ptr(logits_dbg),
+             self._res_ptr(slot, "tok"), self._res_ptr(slot, "conf"),
+             self._res_ptr(slot, "fire"), self._res_ptr(slot, "bad"), ptr(logits_dbg),
              ptr(self.head_ws), self.head_ws.numel(), s)
 
+    def _res_ptr(self, slot, field):
+        return ctypes.c_void_p(self.res.data_ptr() + slot * _RES_DTYPE.itemsize +
+                               _RES_DTYPE.fields[field][1])
+
     def fetch_results(self, nslots):
-        """D2H of the first nslots result slots, then synchronise."""
+        """One D2H copy of the first nslots result slots, then synchronise;
+        results are read through the numpy views h_tok / h_conf / h_fire."""
         if nslots == 0:
             return
-        for d, hst in ((self.r_tok, self.h_tok), (self.r_conf, self.h_conf),
-                       (self.r_fire, self.h_fire), (self.r_bad, self.h_bad)):
-            hst[:nslots].copy_(d[:nslots], non_blocking=True)
-        self.d2h_bytes += nslots * (9 * _HEAD_MAX_ROWS + 4)
+        nb = nslots * _RES_DTYPE.itemsize
+        self.h_res_t[:nb].copy_(self.res[:nb], non_blocking=True)
+        self.d2h_bytes += nb
         self.stream.synchronize()
-        if bool(self.h_bad[:nslots].any()):
+        if self.h_bad[:nslots].any():
             raise NonFiniteError("non-finite exit logits")
 
     def run_layers(self, la, lb, n_rows, m_active, max_pos, pos_off):
@@ -544,11 +552,13 @@ class _PassRunner:
             taps.setdefault(e.desc.layer_index, []).append(hi)
         self.taps = taps  # tap -> head indices in (tap, is_final) order
 
-    def run(self, n, pos, entry, decide_row, forced):
+    def run(self, n, pos, entry, decide_row, forced, embed=None):
         """Rows [0, n) of engine.x with positions/entries ordered by entry
-        descending.  Returns (decision (token, exit_layer) | None, depth)."""
+        descending.  ``embed = (token, position)`` first embeds the new token
+        into row n-1 (its id travels with the control block: one upload per
+        pass).  Returns (decision (token, exit_layer) | None, depth)."""
         e, L = self.e, self.L
-        # control block: positions, then per-tap gather lists
+        # control block: positions, then per-tap gather lists, then the new token
         ctrl = list(pos)
         lists = {}
         for tap in sorted(self.taps):
@@ -558,7 +568,12 @@ class _PassRunner:
             if rows:
                 lists[tap] = (len(ctrl), rows)
                 ctrl.extend(rows)
+        if embed is not None:
+            emb_off = len(ctrl)
+            ctrl.extend(embed)
         e.upload_ctrl(ctrl)
+        if embed is not None:
+            e.embed_rows([embed[0]], [embed[1]], n - 1, ctrl_off=emb_off)
         max_pos = max(pos)
         slots = []  # (slot, head idx, rows) in evaluation order
         decision = None
@@ -699,10 +714,10 @@ def _kv_recompute(eng, model, prompt, threshold, max_new_tokens, max_deferred):
         position += 1
         forced = len(deferred) >= max_deferred
         n = len(deferred) + 1
-        eng.embed_rows([token], [position], n - 1)
+        eng._grow(n)
         pos = [d.position for d in deferred] + [position]
         ent = [d.exit_layer for d in deferred] + [0]
-        decision, depth = runner.run(n, pos, ent, n - 1, forced)
+        decision, depth = runner.run(n, pos, ent, n - 1, forced, embed=(token, position))
         pass_depths.append(depth)
         if depth < L:
             deferred = [DeferredToken(d.position, max(d.exit_layer, depth), r)
@@ -1054,5 +1069,5 @@ def head_logits(model: EarlyExitModel, head_key, rows, threshold=1.0, *, dtype=N
         eng.eval_head(e, eng.ctrl_ptr(0), m, threshold, 0, logits_dbg=dbg)
         eng.fetch_results(1)
         out = dbg.cpu().numpy()
-    return (out, eng.h_tok[0, :m].numpy().copy(), eng.h_conf[0, :m].numpy().copy(),
-            eng.h_fire[0, :m].numpy().astype(bool))
+    return (out, eng.h_tok[0, :m].copy(), eng.h_conf[0, :m].copy(),
+            eng.h_fire[0, :m].astype(bool))
