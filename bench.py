@@ -125,6 +125,19 @@ def measured_traffic():
         return None
 
 
+def head_traffic():
+    """dram bytes (read + write) of one fused train-head call (all its
+    kernels) from the committed ncu launch list, next to the minimum
+    (X, W read once, dW read-modify-write, G written and read twice)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_train_head_traffic.json")) as f:
+            t = json.load(f)
+        return {"bytes": t["traffic_bytes"], "kernels": t["kernels"],
+                "source": "profiles/r1_train_head_traffic.json (ncu)"}
+    except Exception:
+        return None
+
+
 def decode_pass_bytes(h, L, ctx):
     """Algorithmic bytes of one full-depth single-row pass:
     weights once + K/V write of the row + K/V read of the prefix (bf16)."""
@@ -241,11 +254,64 @@ def bench_train_head(local, hbm_peak, reps=10):
     ms = a.elapsed_time(b) / reps
     tflops = 6 * n * h * V / (ms * 1e-3) / 1e12
     return {"workload": "C2 exit head fwd+bwd (n=4096, h=2048, V=50304, bf16)",
-            "ms": ms, "tflops_6nhv": tflops, "executed_tflops_8nhv": tflops * 8 / 6,
+            "ms": ms, "tflops_6nhv": tflops,
+            "note": "executed FLOPs = algorithmic 6nhV (logits computed once: part-normalised "
+                    "probabilities + in-place gradient fixup, no recompute)",
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": tf_peak,
                          "unit": "TFLOP/s", "frac": tflops / tf_peak,
                          "frac_of_sustained": tflops / sustained, "peak_kind": kind,
-                         "traffic": None}}
+                         "traffic": head_traffic()}}
+
+
+def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
+    """One C2 training step (BASELINE configs[1]): EE-GPT 1.3B (L=24, h=2048,
+    16 heads, V=50304, tied exits at 6 (w 0.25) / 12 (w 0.5)), microbatch 2 x
+    M=8 microbatches of seq 2048, 1F1B executor at P=1 on 1 GPU: bf16 compute
+    (torch matmul / SDPA backbone, fused RMSNorm kernels, fused tcgen05 exit
+    heads), float32 gradient accumulation, fused Adam on float32 master
+    weights.  Device-drawn N(0, 0.02) weights, uniform random tokens.  CUDA
+    events around whole steps (optimizer included)."""
+    import numpy as np
+    import torch
+    from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model, partition
+    from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
+    from paper_2312_04916_b200.training import Adam, apply_update
+    dev = f"cuda:{local}"
+    cfg = ModelConfig(24, 2048, 16, 50304, 2048,
+                      exits=(ExitSpec(6, "minimalistic", 0.25), ExitSpec(12, "minimalistic", 0.5)),
+                      tie_embeddings=True)
+    master = build_model(cfg, 0, init="device", dtype=torch.float32, device=dev)
+    opt = Adam(3e-4)
+    rng = np.random.default_rng(0)
+    batches = [rng.integers(0, cfg.vocab_size, size=(M * mb, seq + 1)) for _ in range(steps + warmup)]
+    part = partition(master, 1, copy=False)
+    computes = []
+
+    def step(i):
+        grads, rep = run_iteration_1f1b(part, batches[i], IterationOptions(microbatch_size=mb),
+                                        model=master, devices=[dev], master_dtype=torch.float32,
+                                        stage_computes=computes)
+        apply_update(opt, master, grads, computes, 1.0 / M)
+        return rep
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(steps):
+        rep = step(warmup + i)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    tokens = M * mb * seq
+    out = {"workload": "C2 EE-GPT 1.3B training step (L=24, h=2048, V=50304, seq 2048, "
+                       "microbatch 2 x 8, tied exits 6/12, P=1, Adam, bf16 compute)",
+           "ms_per_step": ms, "tokens_per_s": tokens / (ms / 1e3), "tokens_per_step": tokens,
+           "per_exit_loss": rep.per_exit_loss, "steps": steps, "warmup": warmup}
+    del computes[:], master, opt
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -262,6 +328,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train-head", action="store_true")
+    ap.add_argument("--no-train-step", action="store_true")
     ap.add_argument("--new-tokens", type=int, default=NEW_TOKENS)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -365,6 +432,9 @@ def main():
     head_train = None
     if not args.no_train_head:
         head_train = bench_train_head(local, hbm_peak)
+    train_step = None
+    if not args.no_train_step:
+        train_step = bench_train_step(local)
 
     if rank != 0:
         if world > 1:
@@ -406,6 +476,7 @@ def main():
         "clocks": clocks,
         "sweep": sweep,
         "exit_head_train": head_train,
+        "train_step": train_step,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))

@@ -58,6 +58,7 @@ extern "C" {
 #define EE_OP_EXIT_HEAD 2
 #define EE_OP_DECODER 3
 #define EE_OP_EXIT_HEAD_TRAIN 4
+#define EE_OP_RMSNORM_BWD 5
 
 const char* ee_last_error(void);
 int ee_abi_version(void);
@@ -208,10 +209,29 @@ int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64
                        const int64_t* targets, float weight, float* loss, float* dx, float* dw_acc,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* ---- training RMSNorm (bf16 activations, float32 statistics) ---------- */
+
+/* y = x * (mean(x^2) + eps)^-1/2 * w row-wise; x, y (n, h) bf16, w (h) float32,
+ * inv_rms (n) float32 saved for the backward.  h % 8 == 0.  Replaces
+ * `rmsnorm_fwd` (eepipe/_pykernels.py:36-41, eepipe/_ckernels.pyx:46-65) on the
+ * training backbone. */
+int ee_rmsnorm_fwd(const void* x, int64_t n, int64_t h, const float* w, float eps, void* y,
+                   float* inv_rms, void* stream);
+
+/* gx (n, h) bf16 and gw (h) float32 (overwritten, or accumulated when
+ * accumulate_gw != 0) from x, w, inv_rms and gy (n, h) bf16; gw is reduced in
+ * a fixed order (deterministic).  Workspace: ee_workspace_bytes(
+ * EE_OP_RMSNORM_BWD, n, h, 0, 0, 0).  Replaces `rmsnorm_bwd`
+ * (eepipe/_pykernels.py:44-49, eepipe/_ckernels.pyx:68-89). */
+int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rms, const void* gy, int64_t n,
+                   int64_t h, void* gx, float* gw, int accumulate_gw, void* ws, size_t ws_bytes,
+                   void* stream);
+
 /* ---- optimizer step (fused, multi-tensor) ----------------------------- */
 
 #define EE_OPT_SGD 0
 #define EE_OPT_ADAM 1
+#define EE_OPT_ACCUM 2 /* param += grad * grad_scale: float32 gradient accumulation */
 
 /* One parameter tensor of a fused optimizer step; the table itself is a
  * DEVICE array, entries sorted by `start` (prefix element offsets, tensors

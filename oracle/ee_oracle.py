@@ -410,3 +410,21 @@ def adam_step(params, grads, scale, state, lr, beta1=0.9, beta2=0.999, eps=1e-8)
         m += (1 - beta1) * (g - m)
         v += (1 - beta2) * (g * g - v)
         params[name] -= lr * correction * m / (np.sqrt(v) + eps)
+
+
+# --- training RMSNorm (eepipe/_pykernels.py:36-49) ----------------------------
+
+
+def rmsnorm_fwd(x, w, eps=EPS):
+    """(y, inv_rms) — `rmsnorm_fwd` (`_pykernels.py:36-41`)."""
+    inv = 1.0 / np.sqrt(np.mean(x * x, axis=1) + eps)
+    return x * inv[:, None] * w[None, :], inv
+
+
+def rmsnorm_bwd(x, w, inv_rms, gout):
+    """(gx, gw) — `rmsnorm_bwd` (`_pykernels.py:44-49`)."""
+    h = x.shape[1]
+    gw = np.sum(gout * x * inv_rms[:, None], axis=0)
+    gwx = np.sum(gout * w[None, :] * x, axis=1)
+    gx = gout * w[None, :] * inv_rms[:, None] - x * (inv_rms ** 3 * gwx / h)[:, None]
+    return gx, gw

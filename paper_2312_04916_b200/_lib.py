@@ -20,7 +20,8 @@ EE_OK, EE_ESHAPE, EE_ETOKEN, EE_ENONFINITE, EE_ECONFIG, EE_ECUDA = range(6)
 EE_F32, EE_BF16, EE_BF16_TILED = 0, 1, 2
 EE_EPI_STORE, EE_EPI_RESIDUAL, EE_EPI_GELU = 0, 1, 2
 EE_OP_ATTENTION, EE_OP_EXIT_HEAD, EE_OP_DECODER, EE_OP_EXIT_HEAD_TRAIN = 1, 2, 3, 4
-EE_OPT_SGD, EE_OPT_ADAM = 0, 1
+EE_OP_RMSNORM_BWD = 5
+EE_OPT_SGD, EE_OPT_ADAM, EE_OPT_ACCUM = 0, 1, 2
 
 _ERRORS = {EE_ESHAPE: ShapeError, EE_ETOKEN: TokenError, EE_ENONFINITE: NonFiniteError,
            EE_ECONFIG: ConfigError, EE_ECUDA: RuntimeError}
@@ -72,6 +73,10 @@ SIGNATURES = {
     "ee_exit_head_train": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                                    c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                    c_void_p]),
+    "ee_rmsnorm_fwd": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_float, c_void_p, c_void_p,
+                               c_void_p]),
+    "ee_rmsnorm_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
+                               c_void_p, c_int, c_void_p, c_size_t, c_void_p]),
     "ee_optimizer_step": (c_int, [c_void_p, c_int32, c_int64, c_int, c_int, c_float, c_float,
                                   c_float, c_float, c_float, c_float, c_void_p]),
 }

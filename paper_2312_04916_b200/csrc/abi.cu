@@ -53,6 +53,7 @@ extern "C" int ee_device_sms(void) {
 }
 
 size_t exit_head_train_ws_bytes(int64_t n, int64_t h, int64_t V);
+size_t rmsnorm_train_ws_bytes(int64_t n, int64_t h);
 
 extern "C" size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, int64_t nh,
                                      int64_t s_max) {
@@ -65,6 +66,8 @@ extern "C" size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, in
             return attention_ws_bytes(m, nh, nh > 0 ? h / nh : 0, s_max);
         case EE_OP_EXIT_HEAD_TRAIN:
             return exit_head_train_ws_bytes(m, h, V);
+        case EE_OP_RMSNORM_BWD:
+            return rmsnorm_train_ws_bytes(m, h);
         default:
             return 0;
     }

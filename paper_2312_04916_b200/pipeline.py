@@ -197,6 +197,12 @@ class StageCompute:
         self.weights = weights  # by head key
         self.head_losses = {hd.key: [] for _, hd in spec.heads}
 
+    def reset(self, weights):
+        """Start a new iteration on the same device state."""
+        self.weights = weights
+        self.head_losses = {hd.key: [] for _, hd in self.spec.heads}
+        self.tm.zero_grad()
+
     def forward(self, tokens_or_x, targets):
         from .training import embed_tokens, run_layer
         p = self.tm.compute_params()
@@ -217,12 +223,14 @@ class StageCompute:
         from .training import head_loss
         torch = _torch()
         _, _, taps, targets = state
-        targets = torch.as_tensor(np.asarray(targets)).to(self.device)
+        from .training import _check_ids, to_device_async
+        _check_ids(targets, self.cfg.vocab_size, "target")
+        targets = to_device_async(np.ascontiguousarray(targets), self.device)
         total = None
         params = self.tm.compute_params()
         for local, hd in self.spec.heads:
-            ce = head_loss(params, hd, taps[local], targets, self.cfg.num_heads)
-            self.head_losses[hd.key].append(float(ce.detach()))
+            ce = head_loss(params, hd, taps[local], targets, self.cfg.num_heads, validated=True)
+            self.head_losses[hd.key].append(ce.detach())  # read after the iteration (no sync)
             term = ce * self.weights[hd.key]
             total = term if total is None else total + term
         return total
@@ -245,6 +253,7 @@ class StageCompute:
                 outs.insert(0, loss)
                 grads.insert(0, torch.ones_like(loss))
             torch.autograd.backward(outs, grads)
+        self.tm.accumulate_grads()  # mixed precision: fold into float32 sums (one launch)
         return None if x_in is None else x_in.grad
 
 
@@ -336,10 +345,14 @@ def sync_tied(per_stage_grads, tied_replicas=None):
 
 
 def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
-                       devices=None, dtype=None, master_dtype=None):
+                       devices=None, dtype=None, master_dtype=None, stage_computes=None):
     """One 1F1B iteration over the partition, one thread per stage
     (eepipe/pipeline.py:537-644).  ``model`` is the EarlyExitModel the stage
     weights come from (the partition's own copies are used when omitted).
+    ``master_dtype=torch.float32`` accumulates gradients in float32
+    (`TrainModel` mixed mode).  ``stage_computes``: a list that keeps the
+    per-stage device state across iterations (filled on the first call,
+    reused — gradients zeroed, weights as the optimizer left them — after).
     Returns (merged gradient map by name, TrainStepReport)."""
     P = part.num_stages
     M, data = _split(batch, options.microbatch_size)
@@ -352,10 +365,17 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
     fwd = [TaggedChannel(f"act {s}->{s + 1}") for s in range(1, P)]
     bwd = [TaggedChannel(f"grad {s + 1}->{s}") for s in range(1, P)]
     workers = []
+    reuse = stage_computes is not None and len(stage_computes) == P
     for s, spec in enumerate(part.stages, start=1):
-        holder = src if src is not None else _SpecModel(part, spec)
-        comp = StageCompute(spec, part.config, holder, wmap, devices[(s - 1) % len(devices)], dtype,
-                            master_dtype)
+        if reuse:
+            comp = stage_computes[s - 1]
+            comp.reset(wmap)
+        else:
+            holder = src if src is not None else _SpecModel(part, spec)
+            comp = StageCompute(spec, part.config, holder, wmap, devices[(s - 1) % len(devices)],
+                                dtype, master_dtype)
+            if stage_computes is not None:
+                stage_computes.append(comp)
         workers.append(StageWorker(s, P, M, comp, data,
                                    fwd[s - 2] if s > 1 else None, fwd[s - 1] if s < P else None,
                                    bwd[s - 1] if s < P else None, bwd[s - 2] if s > 1 else None))
@@ -383,7 +403,7 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
         report.wall_clock[w.index] = dict(w.wall)
         report.max_in_flight[w.index] = w.max_in_flight
         for key, vals in w.compute.head_losses.items():
-            report.per_exit_loss[key] = sum(vals) / len(vals)
+            report.per_exit_loss[key] = sum(float(v) for v in vals) / len(vals)
     for s in range(1, P):
         report.activation_messages[s] = fwd[s - 1].count
         report.gradient_messages[s + 1] = bwd[s - 1].count
@@ -455,7 +475,7 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
     report.wall_clock[s] = dict(w.wall)
     report.max_in_flight[s] = w.max_in_flight
     for key, vals in comp.head_losses.items():
-        report.per_exit_loss[key] = sum(vals) / len(vals)
+        report.per_exit_loss[key] = sum(float(v) for v in vals) / len(vals)
     if fwd_out is not None:
         report.activation_messages[s] = fwd_out.count
     if bwd_out is not None:

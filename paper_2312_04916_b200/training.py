@@ -32,9 +32,11 @@ def _torch():
 _WS = {}
 
 
-def _workspace(device, nbytes):
+def _workspace(device, nbytes, tag="head"):
+    """Scratch buffer per (device, current stream, user): stage threads run on
+    their own streams, so a buffer is never shared by concurrent kernels."""
     torch = _torch()
-    key = str(device)
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream, tag)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
@@ -42,22 +44,45 @@ def _workspace(device, nbytes):
     return buf
 
 
-def exit_head_loss_and_grads(x, W, targets, weight=1.0, dw_acc=None):
+def to_device_async(t, device):
+    """Host tensor / array -> device without a stream synchronisation
+    (pinned staging + non_blocking copy; torch's pinned allocator keeps the
+    staging buffer until the copy has executed)."""
+    torch = _torch()
+    t = torch.as_tensor(np.asarray(t) if not isinstance(t, torch.Tensor) else t)
+    if t.is_cuda:
+        return t.to(device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
+def _check_ids(ids, V, what):
+    """Range check on the HOST (a device-side check would synchronise)."""
+    a = np.asarray(ids)
+    if a.size and (int(a.min()) < 0 or int(a.max()) >= V):
+        raise TokenError(f"{what} id out of vocabulary range")
+
+
+def exit_head_loss_and_grads(x, W, targets, weight=1.0, dw_acc=None, validated=False):
     """Fused exit head: returns (loss (0-d float32 tensor), dx (n, h) float32,
     dW (V, h) float32).  x (n, h) and W (V, h) bf16 CUDA tensors; targets
-    int64 (n,).  dW is accumulated into ``dw_acc`` when given (microbatch
-    accumulation, eepipe/pipeline.py:422-427)."""
+    int64 (n,), host or device (``validated=True``: the caller has
+    range-checked device targets on the host, so no synchronising check).
+    dW is accumulated into ``dw_acc`` when given (microbatch accumulation,
+    eepipe/pipeline.py:422-427)."""
     torch = _torch()
     _lib.require_cuda()
     if x.dim() != 2 or W.dim() != 2 or x.shape[1] != W.shape[1]:
         raise ShapeError(f"exit head: x {tuple(x.shape)} vs W {tuple(W.shape)}")
     n, h = x.shape
     V = W.shape[0]
-    targets = targets.reshape(-1).to(device=x.device, dtype=torch.int64)
+    if not isinstance(targets, torch.Tensor) or not targets.is_cuda:
+        _check_ids(targets, V, "target")
+        targets = to_device_async(np.asarray(targets, dtype=np.int64).reshape(-1), x.device)
+    elif not validated and n and (int(targets.min()) < 0 or int(targets.max()) >= V):
+        raise TokenError("target id out of vocabulary range")
+    targets = targets.reshape(-1).to(dtype=torch.int64)
     if targets.numel() != n:
         raise ShapeError(f"{targets.numel()} targets for {n} rows")
-    if n and (int(targets.min()) < 0 or int(targets.max()) >= V):
-        raise TokenError("target id out of vocabulary range")
     x = x.to(torch.bfloat16).contiguous()
     W = W.to(torch.bfloat16).contiguous()
     lib = _lib.load()
@@ -81,15 +106,15 @@ class ExitHeadCE:
     _fn = None
 
     @classmethod
-    def apply(cls, x, W, targets, weight=1.0):
+    def apply(cls, x, W, targets, weight=1.0, validated=False):
         if cls._fn is None:
             torch = _torch()
 
             class _F(torch.autograd.Function):
                 @staticmethod
-                def forward(ctx, x, W, targets, weight):
+                def forward(ctx, x, W, targets, weight, validated):
                     loss, dx, dw = exit_head_loss_and_grads(x.detach(), W.detach(), targets,
-                                                            weight)
+                                                            weight, validated=validated)
                     ctx.save_for_backward(dx, dw)
                     ctx.dtypes = (x.dtype, W.dtype)
                     return loss
@@ -97,10 +122,11 @@ class ExitHeadCE:
                 @staticmethod
                 def backward(ctx, g):
                     dx, dw = ctx.saved_tensors
-                    return ((dx * g).to(ctx.dtypes[0]), (dw * g).to(ctx.dtypes[1]), None, None)
+                    return ((dx * g).to(ctx.dtypes[0]), (dw * g).to(ctx.dtypes[1]), None, None,
+                            None)
 
             cls._fn = _F
-        return cls._fn.apply(x, W, targets, float(weight))
+        return cls._fn.apply(x, W, targets, float(weight), bool(validated))
 
 
 # ---------------------------------------------------------------------------
@@ -108,34 +134,17 @@ class ExitHeadCE:
 # ---------------------------------------------------------------------------
 
 
-class _CastView(dict):
-    """name -> parameter cast to the compute dtype, cast on first use and
-    cached for one forward/backward (the cast is an autograd node, so the
-    gradient lands in the float32 master leaf)."""
-
-    def __init__(self, masters, dtype):
-        super().__init__()
-        self._masters = masters
-        self._dtype = dtype
-
-    def __missing__(self, name):
-        t = self._masters[name].to(self._dtype)
-        self[name] = t
-        return t
-
-    def __contains__(self, name):
-        return name in self._masters
-
-
 class TrainModel:
     """Device-resident trainable copy of an `EarlyExitModel`: parameters as
     torch tensors (requires_grad) keyed by the reference names, compute dtype
     bf16 (the fused exit head runs on bf16 tensor cores).
 
-    With ``master_dtype=torch.float32`` the leaves are float32 and every
-    forward uses bf16 casts of them (`compute_params()`), so gradients are
-    accumulated in float32 across microbatches (the optimizer's input);
-    otherwise the leaves are in the compute dtype."""
+    With ``master_dtype=torch.float32`` (mixed precision, what `train` uses)
+    the bf16 leaves are views of one flat buffer and every microbatch's
+    gradients are folded into float32 accumulators (one flat buffer) by one
+    fused launch (`accumulate_grads`, ee_optimizer_step kind ACCUM); `grads()`
+    then returns the float32 sums, and the optimizer writes the updated
+    weights straight back into the bf16 leaves (`lp_params`)."""
 
     def __init__(self, model: EarlyExitModel, dtype=None, device=None, names=None,
                  master_dtype=None):
@@ -145,32 +154,178 @@ class TrainModel:
         self.heads = model.heads
         self.device = torch.device(device or "cuda:0")
         self.dtype = dtype or torch.bfloat16
-        self.master_dtype = master_dtype or self.dtype
+        self.mixed = master_dtype is not None and master_dtype != self.dtype
         self.params = {}
-        for name in (names if names is not None else model.params):
+        names = list(names if names is not None else model.params)
+        srcs = {}
+        for name in names:
             a = model.params[name].data
-            t = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
-            self.params[name] = t.to(device=self.device,
-                                     dtype=self.master_dtype).detach().requires_grad_()
+            srcs[name] = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
+        if self.mixed:
+            total = sum(srcs[n].numel() for n in names)
+            self._flat = torch.empty(total, dtype=self.dtype, device=self.device)
+            self._flat_grad = torch.zeros(total, dtype=torch.float32, device=self.device)
+            self.main_grads = {}
+            off = 0
+            for name in names:
+                t = srcs[name]
+                k = t.numel()
+                leaf = self._flat[off:off + k].view(t.shape)
+                leaf.copy_(t.to(device=self.device))
+                self.params[name] = leaf.requires_grad_()
+                self.main_grads[name] = self._flat_grad[off:off + k].view(t.shape)
+                off += k
+        else:
+            for name in names:
+                self.params[name] = srcs[name].to(device=self.device,
+                                                  dtype=self.dtype).detach().requires_grad_()
 
     def compute_params(self):
-        """Parameters in the compute dtype (the leaves themselves when the
-        master dtype is the compute dtype)."""
-        if self.master_dtype == self.dtype:
-            return self.params
-        return _CastView(self.params, self.dtype)
+        return self.params
 
     def zero_grad(self):
         for p in self.params.values():
             p.grad = None
+        if self.mixed:
+            self._flat_grad.zero_()
+
+    def accumulate_grads(self):
+        """Mixed precision: float32 accumulators += this microbatch's bf16
+        gradients (one fused launch), then drop the bf16 gradients."""
+        if not self.mixed:
+            return
+        torch = _torch()
+        items = [(n, p) for n, p in self.params.items() if p.grad is not None]
+        if not items:
+            return
+        table = np.zeros(len(items), dtype=_OPT_ENTRY)
+        keep = []
+        start = 0
+        for i, (name, p) in enumerate(items):
+            g = p.grad.to(self.dtype).contiguous()
+            keep.append(g)
+            acc = self.main_grads[name]
+            table[i] = (acc.data_ptr(), g.data_ptr(), 0, 0, 0, acc.numel(), start)
+            start += _pad4(acc.numel())
+        tab = _device_table(table, self.device)
+        call("ee_optimizer_step", ptr(tab), len(items), start, _lib.EE_OPT_ACCUM,
+             _lib.dtype_code(self.dtype), 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, stream_ptr())
+        for _, p in items:
+            p.grad = None
+        keep.append(tab)
+        self._keep = keep  # alive until the next call (stream-ordered reuse)
 
     def grads(self):
+        if self.mixed:
+            return dict(self.main_grads)
         return {n: p.grad for n, p in self.params.items() if p.grad is not None}
+
+    def lp_params(self):
+        """bf16 leaves the optimizer may overwrite in place (mixed mode)."""
+        return {n: p.detach() for n, p in self.params.items()} if self.mixed else {}
+
+
+class _TableRing:
+    """Asynchronous uploads of small host tables (numpy structured arrays)
+    through a ring of pinned buffers: a buffer is refilled only after the
+    copy that last read it has executed (its event), so no upload blocks the
+    host on the stream (a pageable copy would synchronise every call)."""
+
+    def __init__(self, n=4):
+        self.slots = [None] * n  # (pinned uint8 tensor, device uint8 tensor, event)
+        self.i = 0
+
+    def upload(self, table, device):
+        torch = _torch()
+        raw = table.view(np.uint8)
+        i = self.i
+        self.i = (i + 1) % len(self.slots)
+        slot = self.slots[i]
+        if slot is None or slot[0].numel() < raw.size or slot[1].device != torch.device(device):
+            cap = max(raw.size, 4096)
+            slot = [torch.empty(cap, dtype=torch.uint8).pin_memory(),
+                    torch.empty(cap, dtype=torch.uint8, device=device), None]
+            self.slots[i] = slot
+        if slot[2] is not None:
+            slot[2].synchronize()
+        slot[0].numpy()[:raw.size] = raw
+        slot[1][:raw.size].copy_(slot[0][:raw.size], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(device))
+        slot[2] = ev
+        return slot[1]
+
+
+_TABLES = {}
+
+
+def _device_table(table, device):
+    """Upload a small host table to the device without blocking the host
+    (per-(device, stream) ring of pinned staging buffers)."""
+    torch = _torch()
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    ring = _TABLES.get(key)
+    if ring is None:
+        ring = _TABLES[key] = _TableRing()
+    return ring.upload(table, device)
+
+
+def _pad4(n):
+    """Element offsets in a fused table start on 4-element boundaries so the
+    kernel's 16-byte vector path applies to every aligned tensor."""
+    return (n + 3) & ~3
+
+
+class _RMSNormFn:
+    """torch.autograd.Function over `ee_rmsnorm_fwd` / `ee_rmsnorm_bwd`
+    (csrc/rmsnorm_train.cu): bf16 activations, float32 weight and
+    statistics, deterministic weight gradient."""
+
+    _fn = None
+
+    @classmethod
+    def get(cls):
+        if cls._fn is None:
+            torch = _torch()
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, x, w, eps):
+                    h = x.shape[-1]
+                    x2 = x.reshape(-1, h).contiguous()
+                    wf = w.detach().float().contiguous()
+                    y = torch.empty_like(x2)
+                    inv = torch.empty(x2.shape[0], dtype=torch.float32, device=x.device)
+                    call("ee_rmsnorm_fwd", ptr(x2), x2.shape[0], h, ptr(wf), float(eps), ptr(y),
+                         ptr(inv), stream_ptr())
+                    ctx.save_for_backward(x2, wf, inv)
+                    ctx.wdtype = w.dtype
+                    return y.view(x.shape)
+
+                @staticmethod
+                def backward(ctx, gy):
+                    x2, wf, inv = ctx.saved_tensors
+                    n, h = x2.shape
+                    gy2 = gy.reshape(n, h).to(torch.bfloat16).contiguous()
+                    gx = torch.empty_like(x2)
+                    gw = torch.empty(h, dtype=torch.float32, device=x2.device)
+                    ws = _workspace(x2.device, _lib.load().ee_workspace_bytes(
+                        _lib.EE_OP_RMSNORM_BWD, n, h, 0, 0, 0), tag="rmsnorm")
+                    call("ee_rmsnorm_bwd", ptr(x2), ptr(wf), ptr(inv), ptr(gy2), n, h, ptr(gx),
+                         ptr(gw), 0, ptr(ws), ws.numel(), stream_ptr())
+                    return gx.view(gy.shape), gw.to(ctx.wdtype), None
+
+            cls._fn = _F
+        return cls._fn
 
 
 def rmsnorm(x, w, eps=NORM_EPS):
-    """`eepipe/autodiff.py:228-244` (float32 statistics)."""
+    """`eepipe/autodiff.py:228-244`.  bf16 activations go through the fused
+    sm_100a kernels (`ee_rmsnorm_fwd/bwd`); float32 activations (the parity
+    configuration of the tests) use float32 torch ops."""
     torch = _torch()
+    if x.dtype == torch.bfloat16 and x.is_cuda and x.shape[-1] % 8 == 0:
+        return _RMSNormFn.get().apply(x, w, eps)
     xf = x.float()
     inv = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
     return (xf * inv * w.float()).to(x.dtype)
@@ -213,14 +368,15 @@ def run_head(params, head, x, num_heads):
     return head_input(params, head, x, num_heads) @ params[head.param_names["out"]].t()
 
 
-def head_loss(params, head, x, targets, num_heads):
+def head_loss(params, head, x, targets, num_heads, validated=False):
     """Mean next-token CE of one head through the fused tcgen05 kernel
     (replaces run_head + cross_entropy, eepipe/model.py:219-230 +
-    eepipe/autodiff.py:301-323)."""
+    eepipe/autodiff.py:301-323).  ``validated``: device targets already
+    range-checked on the host."""
     xi = head_input(params, head, x, num_heads)
     h = xi.shape[-1]
     W = params[head.param_names["out"]]
-    return ExitHeadCE.apply(xi.reshape(-1, h), W, targets.reshape(-1), 1.0)
+    return ExitHeadCE.apply(xi.reshape(-1, h), W, targets.reshape(-1), 1.0, validated)
 
 
 def embed_tokens(params, tokens, max_seq_len):
@@ -232,10 +388,13 @@ def embed_tokens(params, tokens, max_seq_len):
     if tokens.shape[1] > max_seq_len:
         raise TokenError(f"sequence length {tokens.shape[1]} exceeds max_seq_len {max_seq_len}")
     V = params["tok_emb"].shape[0]
-    if tokens.numel() and (int(tokens.min()) < 0 or int(tokens.max()) >= V):
-        raise TokenError("token id out of vocabulary range")
+    if tokens.is_cuda:
+        if tokens.numel() and (int(tokens.min()) < 0 or int(tokens.max()) >= V):
+            raise TokenError("token id out of vocabulary range")
+    else:
+        _check_ids(tokens.numpy(), V, "token")
     dev = params["tok_emb"].device
-    tokens = tokens.to(dev)
+    tokens = to_device_async(tokens, dev)
     pos = torch.arange(tokens.shape[1], device=dev)
     return params["tok_emb"][tokens] + params["pos_emb"][pos][None]
 
@@ -264,7 +423,10 @@ def weighted_loss(model: TrainModel, batch, weights):
         raise ShapeError(f"{len(weights)} weights for {len(model.heads)} exits (final included)")
     cfg = model.config
     batch = torch.as_tensor(np.asarray(batch) if not isinstance(batch, torch.Tensor) else batch)
-    batch = batch.to(model.device)
+    validated = not batch.is_cuda
+    if validated:
+        _check_ids(batch.numpy(), cfg.vocab_size, "token")
+    batch = to_device_async(batch, model.device)
     wanted = {hd.layer_index for hd in model.heads}
     params = model.compute_params()
     x = embed_tokens(params, batch[:, :-1], cfg.max_seq_len)
@@ -277,7 +439,7 @@ def weighted_loss(model: TrainModel, batch, weights):
     total = None
     per_exit = []
     for hd, w in zip(model.heads, weights):
-        ce = head_loss(params, hd, taps[hd.layer_index], targets, cfg.num_heads)
+        ce = head_loss(params, hd, taps[hd.layer_index], targets, cfg.num_heads, validated)
         per_exit.append(float(ce.detach()))
         term = ce * w
         total = term if total is None else total + term
@@ -324,7 +486,7 @@ class _FusedOptimizer:
 
     kind = None
 
-    def _launch(self, params, grads, scale, step_size, moments):
+    def _launch(self, params, grads, scale, step_size, moments, lp=None):
         torch = _torch()
         names = sorted(grads)  # the reference's update order (eepipe/training.py:29, 46)
         if not names:
@@ -348,10 +510,16 @@ class _FusedOptimizer:
             dev = p.device
             keep.append(g)
             m, v = moments(name, p) if moments else (None, None)
+            q = lp.get(name) if lp else None
+            if q is not None and (q.dtype != torch.bfloat16 or q.numel() != p.numel()
+                                  or not q.is_contiguous() or q.device != p.device):
+                raise ShapeError(f"optimizer: low-precision copy of {name} must be a contiguous "
+                                 "bf16 tensor of the same size on the same device")
             table[i] = (p.data_ptr(), g.data_ptr(), m.data_ptr() if m is not None else 0,
-                        v.data_ptr() if v is not None else 0, 0, p.numel(), start)
-            start += p.numel()
-        tab = torch.from_numpy(table.view(np.uint8)).to(dev, non_blocking=False)
+                        v.data_ptr() if v is not None else 0,
+                        q.data_ptr() if q is not None else 0, p.numel(), start)
+            start += _pad4(p.numel())
+        tab = _device_table(table, dev)
         keep.append(tab)
         call("ee_optimizer_step", ptr(tab), len(names), start, self.kind, _lib.dtype_code(gdt),
              float(self.lr), float(getattr(self, "beta1", 0.0)), float(getattr(self, "beta2", 0.0)),
@@ -367,8 +535,8 @@ class SGD(_FusedOptimizer):
     def __init__(self, lr):
         self.lr = lr
 
-    def step(self, params, grads, scale):
-        self._launch(params, grads, scale, 0.0, None)
+    def step(self, params, grads, scale, lp=None):
+        self._launch(params, grads, scale, 0.0, None, lp)
 
 
 class Adam(_FusedOptimizer):
@@ -395,11 +563,13 @@ class Adam(_FusedOptimizer):
             self.v[name] = torch.zeros_like(p)
         return self.m[name], self.v[name]
 
-    def step(self, params, grads, scale):
+    def step(self, params, grads, scale, lp=None):
+        """``lp``: optional name -> bf16 tensor that receives the updated
+        weights in the same launch (the compute copy of mixed precision)."""
         self.t += 1
         b1, b2 = self.beta1, self.beta2
         correction = np.sqrt(1 - b2 ** self.t) / (1 - b1 ** self.t)  # float64, as the reference
-        self._launch(params, grads, scale, self.lr * correction, self._moments)
+        self._launch(params, grads, scale, self.lr * correction, self._moments, lp)
 
 
 def make_optimizer(kind, lr):
@@ -423,6 +593,22 @@ def device_master(model: EarlyExitModel, device=None) -> EarlyExitModel:
         t = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
         params[name] = Param(t.to(device=dev, dtype=torch.float32).contiguous().clone())
     return EarlyExitModel(model.config, params, model.heads)
+
+
+def apply_update(optimizer, master, grads, computes, scale):
+    """One fused optimizer launch over the float32 master weights; the
+    updated weights are written straight into the first stage replica's bf16
+    leaves, other replicas (tied embeddings on several stages) are copied."""
+    lp, extra = {}, []
+    for comp in computes:
+        for name, t in comp.tm.lp_params().items():
+            if name in lp or t.device != master.params[name].data.device:
+                extra.append((t, name))
+            else:
+                lp[name] = t
+    optimizer.step(master.params, grads, scale, lp=lp)
+    for dst, name in extra:
+        dst.copy_(master.params[name].data)
 
 
 def train(run_cfg, corpus, metrics_path=None, progress=None, *, devices=None, dtype=None):
@@ -466,19 +652,21 @@ def train(run_cfg, corpus, metrics_path=None, progress=None, *, devices=None, dt
         if fh:
             fh.write(json.dumps(rec, sort_keys=True) + "\n")
 
+    part = partition(master, run_cfg.stages, copy=False)
+    computes = []  # per-stage device state (bf16 weights, float32 gradient sums), kept
     try:
         for step in range(run_cfg.steps):
-            part = partition(master, run_cfg.stages, copy=False)
             batch = corpus.batch(rows_per_step, row_len, step)
             opts = IterationOptions(microbatch_size=run_cfg.microbatch_size,
                                     defer_exit_forward=getattr(run_cfg, "defer_exit_forward", True),
                                     weight_schedule=schedule, step=step)
             t0 = time.perf_counter()
             grads, report = run_iteration_1f1b(part, batch, opts, model=master, devices=devices,
-                                               dtype=dtype, master_dtype=torch.float32)
+                                               dtype=dtype, master_dtype=torch.float32,
+                                               stage_computes=computes)
             if not all(np.isfinite(v) for v in report.per_exit_loss.values()):
                 raise NonFiniteError(f"non-finite loss at step {step}")
-            optimizer.step(master.params, grads, 1.0 / num_mb)
+            apply_update(optimizer, master, grads, computes, 1.0 / num_mb)
             torch.cuda.synchronize()
             elapsed = time.perf_counter() - t0
             if head_keys is None:

@@ -1,0 +1,62 @@
+"""Training-backbone kernels against the float64 oracle: the fused RMSNorm
+forward/backward (`ee_rmsnorm_fwd/bwd`, csrc/rmsnorm_train.cu), the
+reference's `rmsnorm_fwd` / `rmsnorm_bwd` boundary kernels
+(eepipe/_pykernels.py:36-49).
+
+Tolerances: bf16 outputs (y, gx) within 1e-2 relative (Frobenius; one bf16
+rounding), float32 statistics inv_rms within 1e-5 and the float32 weight
+gradient within 1e-4 relative; the oracle runs on the bf16-rounded inputs.
+The weight gradient is deterministic (fixed-order reduction): bitwise equal
+across calls.
+"""
+import numpy as np
+import pytest
+
+import ee_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("n,h", [(1, 8), (37, 264), (4096, 2048), (1000, 5120), (16, 7168)])
+def test_rmsnorm_fwd_bwd_match_oracle(n, h):
+    import torch
+    from paper_2312_04916_b200.training import rmsnorm
+    rng = np.random.default_rng(n * 7 + h)
+    x = torch.tensor(rng.normal(size=(n, h)) * 3.0, dtype=torch.bfloat16, device="cuda")
+    w = torch.tensor(rng.normal(1.0, 0.2, size=h), dtype=torch.float32, device="cuda")
+    g = torch.tensor(rng.normal(size=(n, h)), dtype=torch.bfloat16, device="cuda")
+    xr = x.clone().requires_grad_()
+    wr = w.clone().requires_grad_()
+    y = rmsnorm(xr, wr)
+    y.backward(g)
+    x64, w64, g64 = (t.double().cpu().numpy() for t in (x, w, g))
+    ry, rinv = O.rmsnorm_fwd(x64, w64)
+    rgx, rgw = O.rmsnorm_bwd(x64, w64, rinv, g64)
+    assert y.dtype == torch.bfloat16
+    assert _rel(y.double().detach().cpu().numpy(), ry) < 1e-2
+    assert _rel(xr.grad.double().cpu().numpy(), rgx) < 1e-2
+    assert _rel(wr.grad.double().cpu().numpy(), rgw) < 1e-4
+    # determinism of the fixed-order weight-gradient reduction
+    wr2 = w.clone().requires_grad_()
+    rmsnorm(x.clone().requires_grad_(), wr2).backward(g)
+    assert torch.equal(wr.grad, wr2.grad)
+
+
+def test_rmsnorm_inv_rms_statistics():
+    import ctypes
+    import torch
+    from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+    rng = np.random.default_rng(0)
+    n, h = 64, 4096
+    x = torch.tensor(rng.normal(size=(n, h)), dtype=torch.bfloat16, device="cuda")
+    w = torch.ones(h, device="cuda")
+    y = torch.empty_like(x)
+    inv = torch.empty(n, device="cuda")
+    call("ee_rmsnorm_fwd", ptr(x), n, h, ptr(w), ctypes.c_float(1e-6), ptr(y), ptr(inv),
+         stream_ptr())
+    _, rinv = O.rmsnorm_fwd(x.double().cpu().numpy(), np.ones(h))
+    assert np.abs(inv.cpu().numpy() - rinv).max() / rinv.max() < 1e-5
