@@ -276,6 +276,10 @@ def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
     from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model, partition
     from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
     from paper_2312_04916_b200.training import Adam, apply_update
+    import gc
+    gc.collect()
+    gc.freeze()  # the decode run's host objects stay out of every GC pass of the training loop
+    torch.cuda.empty_cache()
     dev = f"cuda:{local}"
     cfg = ModelConfig(24, 2048, 16, 50304, 2048,
                       exits=(ExitSpec(6, "minimalistic", 0.25), ExitSpec(12, "minimalistic", 0.5)),
@@ -311,6 +315,7 @@ def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
            "per_exit_loss": rep.per_exit_loss, "steps": steps, "warmup": warmup}
     del computes[:], master, opt
     torch.cuda.empty_cache()
+    gc.unfreeze()
     return out
 
 

@@ -344,6 +344,20 @@ def sync_tied(per_stage_grads, tied_replicas=None):
     return merged
 
 
+_STAGE_STREAMS = {}
+
+
+def _stage_stream(device, stage):
+    """One persistent CUDA stream per (device, stage): per-stream scratch
+    (workspaces, upload rings) is then allocated once, not per iteration."""
+    torch = _torch()
+    key = (str(device), stage)
+    st = _STAGE_STREAMS.get(key)
+    if st is None:
+        st = _STAGE_STREAMS[key] = torch.cuda.Stream(device)
+    return st
+
+
 def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
                        devices=None, dtype=None, master_dtype=None, stage_computes=None):
     """One 1F1B iteration over the partition, one thread per stage
@@ -383,7 +397,7 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
 
     def target(w):
         dev = w.compute.device
-        with torch.cuda.device(dev), torch.cuda.stream(torch.cuda.Stream(dev)):
+        with torch.cuda.device(dev), torch.cuda.stream(_stage_stream(dev, w.index)):
             w.run()
             torch.cuda.current_stream(dev).synchronize()
 
