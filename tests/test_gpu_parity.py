@@ -225,3 +225,25 @@ def test_bf16_exit_head_7b_width():
         assert conf[i] == pytest.approx(rconf, rel=1e-3)
         if tok[i] != rtok:  # near-tie: report, allowed only within tolerance
             assert abs(ref[i][tok[i]] - ref[i][rtok]) < 1e-3 * abs(ref[i][rtok])
+
+
+def test_fp32_generation_at_7b_width_matches_reference():
+    """SURVEY Appendix B.3 at real width: a 2-layer h=4096 / V=50304 model with
+    the reference's float64 initialisation (`build_model(cfg, 0)`, identical
+    draws) decoded by the GPU path in fp32 parity mode: identical tokens and
+    exit layers to the reference (tests/golden/golden_7b.json, made by
+    tests/golden/make_7b_slice.py), at threshold 1.0 and at 0.05 (early exits
+    and deferred recomputation at real width); confidences within 1e-4
+    relative (fp32 dot products of length 4096 / softmax over 50304 against
+    float64)."""
+    import json
+    import os
+    from helpers import GOLD_DIR
+    with open(os.path.join(GOLD_DIR, "golden_7b.json")) as f:
+        g = json.load(f)
+    cfg = ModelConfig(2, 4096, 32, 50304, 2048, exits=(ExitSpec(1, "minimalistic", 0.1),))
+    m = build_model(cfg, 0)
+    for key, thr in (("thr1", 1.0), ("thr005", 0.05)):
+        tr = I.generate_kv_recompute(m, g["prompt"], thr, 6, dtype="fp32")
+        _same_decisions(tr, g[key])
+        _close_conf(tr.confidences, g[key]["confidences"], rtol=1e-4)
