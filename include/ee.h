@@ -59,6 +59,7 @@ extern "C" {
 #define EE_OP_DECODER 3
 #define EE_OP_EXIT_HEAD_TRAIN 4
 #define EE_OP_RMSNORM_BWD 5
+#define EE_OP_PREFILL 6
 
 const char* ee_last_error(void);
 int ee_abi_version(void);
@@ -160,6 +161,11 @@ typedef struct {
     void* attn; /* (max_rows, h) dtype scratch */
     void* ws;   /* attention workspace (ee_workspace_bytes(EE_OP_ATTENTION, ...)) */
     size_t ws_bytes;
+    /* tiled mode, nullable: split-K partials of the multi-row (prefill)
+     * tcgen05 GEMM, >= ee_workspace_bytes(EE_OP_PREFILL, max_rows, h, ...);
+     * when null (or too small) every pass uses the GEMV */
+    void* pf_ws;
+    size_t pf_ws_bytes;
 } ee_decoder_t;
 
 /* Row statistics for tiled mode: xb = bf16(x), ssq[r][t] = sum_{i<16}

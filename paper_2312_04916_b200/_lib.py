@@ -21,6 +21,7 @@ EE_F32, EE_BF16, EE_BF16_TILED = 0, 1, 2
 EE_EPI_STORE, EE_EPI_RESIDUAL, EE_EPI_GELU = 0, 1, 2
 EE_OP_ATTENTION, EE_OP_EXIT_HEAD, EE_OP_DECODER, EE_OP_EXIT_HEAD_TRAIN = 1, 2, 3, 4
 EE_OP_RMSNORM_BWD = 5
+EE_OP_PREFILL = 6
 EE_OPT_SGD, EE_OPT_ADAM, EE_OPT_ACCUM = 0, 1, 2
 
 _ERRORS = {EE_ESHAPE: ShapeError, EE_ETOKEN: TokenError, EE_ENONFINITE: NonFiniteError,
@@ -40,7 +41,8 @@ class EeDecoder(ctypes.Structure):
     _fields_ = [("h", c_int64), ("nh", c_int64), ("s_max", c_int64), ("max_rows", c_int64),
                 ("dtype", c_int), ("eps", c_float), ("x", c_void_p), ("xb", c_void_p),
                 ("ssq", c_void_p), ("xn", c_void_p), ("q", c_void_p), ("attn", c_void_p),
-                ("ws", c_void_p), ("ws_bytes", c_size_t)]
+                ("ws", c_void_p), ("ws_bytes", c_size_t), ("pf_ws", c_void_p),
+                ("pf_ws_bytes", c_size_t)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/ee.h

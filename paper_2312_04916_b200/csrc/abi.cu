@@ -54,6 +54,7 @@ extern "C" int ee_device_sms(void) {
 
 size_t exit_head_train_ws_bytes(int64_t n, int64_t h, int64_t V);
 size_t rmsnorm_train_ws_bytes(int64_t n, int64_t h);
+size_t prefill_ws_bytes(int64_t m, int64_t N_max);
 
 extern "C" size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, int64_t nh,
                                      int64_t s_max) {
@@ -68,6 +69,8 @@ extern "C" size_t ee_workspace_bytes(int op, int64_t m, int64_t h, int64_t V, in
             return exit_head_train_ws_bytes(m, h, V);
         case EE_OP_RMSNORM_BWD:
             return rmsnorm_train_ws_bytes(m, h);
+        case EE_OP_PREFILL:
+            return prefill_ws_bytes(m, 4 * h);
         default:
             return 0;
     }

@@ -38,6 +38,30 @@ extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, int64
         float* ssq = D->ssq + row0 * (h / 16);
         const GemvNorm folded{ssq, D->eps, nullptr, nullptr};
         const GemvNorm stats{nullptr, 0.f, xb, ssq};
+        if (m >= kPrefillMinRows && D->pf_ws &&
+            D->pf_ws_bytes >= (size_t)4 * m * 4 * h * sizeof(float)) {
+            // many rows (prompt prefill): tcgen05 GEMMs instead of GEMVs
+            void* pw = D->pf_ws;
+            const size_t pb = D->pf_ws_bytes;
+            if ((rc = launch_prefill_tiled(xb, m, h, L->wqkv, 3 * h, 0, ssq, D->eps, D->q,
+                                           L->kcache, L->vcache, pos, h, nullptr, nullptr, nullptr,
+                                           nullptr, pw, pb, s)))
+                return rc;
+            if ((rc = launch_attention(D->q, m, pos, max_pos, L->kcache, L->vcache, D->nh,
+                                       h / D->nh, dt, D->attn, D->ws, D->ws_bytes, s)))
+                return rc;
+            if ((rc = launch_prefill_tiled((const bf16*)D->attn, m, h, L->wo, h, 2, nullptr, 0.f,
+                                           nullptr, nullptr, nullptr, nullptr, h, nullptr, x, xb,
+                                           ssq, pw, pb, s)))
+                return rc;
+            if ((rc = launch_prefill_tiled(xb, m, h, L->w1, 4 * h, 1, ssq, D->eps, nullptr, nullptr,
+                                           nullptr, nullptr, h, D->xn, nullptr, nullptr, nullptr, pw,
+                                           pb, s)))
+                return rc;
+            return launch_prefill_tiled((const bf16*)D->xn, m, 4 * h, L->w2, h, 2, nullptr, 0.f,
+                                        nullptr, nullptr, nullptr, nullptr, h, nullptr, x, xb, ssq,
+                                        pw, pb, s);
+        }
         if ((rc = launch_qkv_tiled(xb, m, h, L->wqkv, folded, D->q, L->kcache, L->vcache, pos, s)))
             return rc;
         if (!(ablate & 2) &&

@@ -118,5 +118,13 @@ struct GemvNorm {
 };
 int launch_gemv_tiled(const bf16* x, int64_t m, int64_t K, const void* W, int64_t N, int epi,
                       void* out, int64_t ldo, GemvNorm nrm, cudaStream_t s);
+// multi-row (prefill) tcgen05 GEMM over tiled weights (prefill_gemm.cu);
+// epi: 0 = q/K/V write (folded norm), 1 = GELU (folded norm), 2 = residual +
+// row statistics
+int launch_prefill_tiled(const bf16* x, int64_t m, int64_t K, const void* W, int64_t N, int epi,
+                         const float* ssq_in, float eps, float* q, void* kc, void* vc,
+                         const int32_t* pos, int64_t h, void* out, float* xres, bf16* xb,
+                         float* ssq_out, void* ws, size_t ws_bytes, cudaStream_t s);
+constexpr int kPrefillMinRows = 17;  // passes with more rows use the GEMM
 int launch_qkv_tiled(const bf16* x, int64_t m, int64_t h, const void* Wqkv, GemvNorm nrm,
                      float* q, void* kc, void* vc, const int32_t* pos, cudaStream_t s);

@@ -96,7 +96,7 @@ struct RowNorm {
     float eps;
 };
 
-// Work item i -> tile = i % tiles, column group = i / tiles; a CTA takes
+// Work item i -> tile = i / groups, column group = i % groups; a CTA takes
 // items blockIdx.x, +gridDim.x, ...  Epi provides tile(red, n0, r0, N, m,
 // cols, inv) and finish(), both called by the 128 consumer threads (inv is
 // the per-column 1/rms or nullptr).  K must be a multiple of 512, W in the
@@ -143,14 +143,14 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
             const int ks = q % nks;
             const int slot = q % kStages;
             mbar_expect_tx(&wfull[slot], kWBytes);
-            bulk_g2s(ring + slot * sbytes, W + ((int64_t)(it % tiles) * nks + ks) * (kRows * KS),
+            bulk_g2s(ring + slot * sbytes, W + ((int64_t)(it / groups) * nks + ks) * (kRows * KS),
                      kWBytes, &wfull[slot]);
         };
         auto issue_x = [&](int q) {
             const int it = (int)blockIdx.x + (q / nks) * (int)gridDim.x;
             const int ks = q % nks;
             const int slot = q % kStages;
-            const int r0 = (it / tiles) * cols;
+            const int r0 = (it % groups) * cols;
             const int mr = min(cols, m - r0);
             uint8_t* dst = ring + slot * sbytes + kWBytes;
             mbar_expect_tx(&xfull[slot], (uint32_t)(mr * KS * 2));
@@ -181,8 +181,11 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
     int q = 0;
     int cur_grp = -1;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int tile = it % tiles;
-        const int grp = it / tiles;
+        // row groups fastest: the CTAs that process one weight tile for the
+        // different row groups run concurrently, so the tile is fetched from
+        // HBM once and served from L2 to the others (multi-row prefill)
+        const int tile = it / groups;
+        const int grp = it % groups;
         const int n0 = tile * kRows;
         const int r0 = grp * cols;
         const int mr = min(cols, m - r0);

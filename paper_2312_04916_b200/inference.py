@@ -404,13 +404,19 @@ class Engine:
             if self.max_rows:
                 old = self._x_old
                 self.x[:old.shape[0]].copy_(old)
+            # split-K partials of the multi-row (prefill) tcgen05 GEMM
+            pfb = (_lib.load().ee_workspace_bytes(_lib.EE_OP_PREFILL, rows, h, 0, 0, 0)
+                   if self.tiled and rows >= 17 else 0)
+            self.pf_ws = torch.empty(max(pfb, 1), dtype=torch.uint8, device=self.device)
             self.dec = _lib.EeDecoder(h=h, nh=cfg.num_heads, s_max=cfg.max_seq_len,
                                       max_rows=rows, dtype=self.wcode, eps=NORM_EPS,
                                       x=self.x.data_ptr(), xb=self.xb.data_ptr(),
                                       ssq=self.ssq.data_ptr(),
                                       xn=self.xn.data_ptr(), q=self.q.data_ptr(),
                                       attn=self.attn.data_ptr(), ws=self.attn_ws.data_ptr(),
-                                      ws_bytes=wsb)
+                                      ws_bytes=wsb,
+                                      pf_ws=self.pf_ws.data_ptr() if pfb else None,
+                                      pf_ws_bytes=pfb)
         self.max_rows = rows
         self._x_old = None
 
