@@ -9,9 +9,10 @@
 //
 // bf16: the TMA-bulk-fed GEMV body (gemv_tma.cuh) with the RMSNorm fused in
 // its prologue and a softmax-partial epilogue; tiles are statically
-// round-robined over a persistent grid, the last CTA to finish merges the
-// per-tile partials in tile order with a fixed-shape tree (deterministic,
-// row-stable).  fp32 (parity mode): RMSNorm launch + SIMT dot products with
+// round-robined over a persistent grid whose size does not depend on the
+// row count; each CTA folds its tiles' partials in tile order into one
+// running partial per row, and the last CTA to finish merges the CTA
+// partials in CTA order with a fixed-shape tree (deterministic, row-stable).  fp32 (parity mode): RMSNorm launch + SIMT dot products with
 // the same partial/merge scheme.
 #include <algorithm>
 
@@ -61,42 +62,36 @@ __device__ __forceinline__ void combine(float& m1, float& s1, int& i1, float m2,
     i1 = i;
 }
 
-// Fixed-order merge of all unit partials for each column (nthreads threads).
+// Fixed-order merge of all unit partials, one WARP per column (columns
+// round-robin over the NT/32 warps): lane l folds units l, l+32, ... in
+// ascending order, then a xor butterfly with a commutative combine (every
+// lane ends with identical bits).  No block-wide barriers inside the merge.
 template <int NT>
 __device__ void merge_and_decide(const HeadWs& w, int64_t units, int m, float thr, int32_t* token,
                                  float* conf, uint8_t* fire, int32_t* nonfinite, int tid,
                                  void (*sync)()) {
-    __shared__ float sm_m[NT], sm_s[NT];
-    __shared__ int sm_i[NT];
-    for (int c = 0; c < m; ++c) {
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int c = wid; c < m; c += NT / 32) {
         float M = -INFINITY, S = 0.f;
         int I = 0x7fffffff;
-        for (int64_t u = tid; u < units; u += NT)
+        for (int64_t u = lane; u < units; u += 32)
             combine(M, S, I, __ldcg(w.pm + u * kMaxCols + c), __ldcg(w.ps + u * kMaxCols + c),
                     __ldcg(w.pi + u * kMaxCols + c));
-        sm_m[tid] = M;
-        sm_s[tid] = S;
-        sm_i[tid] = I;
-        sync();
-        for (int s = NT / 2; s > 0; s >>= 1) {
-            if (tid < s) {
-                float a = sm_m[tid], b = sm_s[tid];
-                int i = sm_i[tid];
-                combine(a, b, i, sm_m[tid + s], sm_s[tid + s], sm_i[tid + s]);
-                sm_m[tid] = a;
-                sm_s[tid] = b;
-                sm_i[tid] = i;
-            }
-            sync();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, M, o);
+            const float s2 = __shfl_xor_sync(0xffffffffu, S, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, I, o);
+            combine(M, S, I, m2, s2, i2);
         }
-        if (tid == 0) {
-            const float cf = 1.0f / sm_s[0];
-            token[c] = sm_i[0];
+        if (lane == 0) {
+            const float cf = 1.0f / S;
+            token[c] = I;
             conf[c] = cf;
             fire[c] = (thr < 1.0f && cf > thr) ? 1 : 0;
         }
-        sync();
     }
+    sync();
     if (tid == 0) {
         *nonfinite = __ldcg(w.flag);
         *w.flag = 0;
@@ -118,6 +113,10 @@ struct HeadEpi {
     uint8_t* fire;
     float* dbg;
     bool bad;
+    // running partials of this CTA, combined over its tiles in increasing
+    // tile order: thread 16 j holds columns j and j + 8 (rounds k = 0, 1)
+    float rm[2] = {-INFINITY, -INFINITY}, rs[2] = {0.f, 0.f};
+    int ri[2] = {0x7fffffff, 0x7fffffff};
 
     __device__ void tile(const float* red, int n0, int r0, int N, int mm, int cols,
                          const float* /*inv*/) {
@@ -129,24 +128,34 @@ struct HeadEpi {
             return ((red[o] + red[kRows * kMaxCols + o]) + red[2 * kRows * kMaxCols + o]) +
                    red[3 * kRows * kMaxCols + o];
         };
-        if (tid < m) {
-            const int c = tid;
-            float mx = -INFINITY;
-            int idx = n0;
-            for (int i = 0; i < nr; ++i) {
-                const float v = val(i, c);
-                bad |= !isfinite(v);
-                if (v > mx) {
-                    mx = v;
-                    idx = n0 + i;
+        // 16 threads per column (one vocabulary row each), fixed xor
+        // butterflies for the tile max / argmax and the sum of exponentials
+        for (int c0 = 0; c0 < m; c0 += kConsumers * 32 / kRows) {
+            const int c = c0 + (tid >> 4);
+            const int i = tid & 15;
+            const bool act = c < m;
+            const float v = (act && i < nr) ? val(i, c) : -INFINITY;
+            if (act && i < nr) bad |= !isfinite(v);
+            float mx = v;
+            int idx = (act && i < nr) ? n0 + i : 0x7fffffff;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {
+                const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+                if (m2 > mx || (m2 == mx && i2 < idx)) {
+                    mx = m2;
+                    idx = i2;
                 }
             }
-            float sum = 0.f;
-            for (int i = 0; i < nr; ++i) sum += expf(val(i, c) - mx);
-            const int64_t u = n0 / kRows;
-            w.pm[u * kMaxCols + c] = mx;
-            w.ps[u * kMaxCols + c] = sum;
-            w.pi[u * kMaxCols + c] = idx;
+            float e = (act && i < nr) ? expf(v - mx) : 0.f;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+            // lane i == 0 of each column group folds the tile into the CTA's
+            // running partial of that column (tiles in increasing order)
+            if (act && i == 0) {
+                const int k = c0 / (kConsumers * 32 / kRows);
+                combine(rm[k], rs[k], ri[k], mx, e, idx);
+            }
         }
         if (dbg) {
             for (int i = tid; i < kRows * m; i += kConsumers * 32) {
@@ -159,6 +168,22 @@ struct HeadEpi {
     __device__ void finish() {
         using namespace tma_gemv;
         __shared__ int s_last;
+        // one partial per CTA (unit = CTA index); the last CTA merges the
+        // CTA partials in CTA order: a fixed two-level order (tiles of a CTA
+        // ascending, then CTAs ascending) for a fixed grid size
+        if ((threadIdx.x & 15) == 0) {
+            const int64_t u = blockIdx.x;
+            constexpr int per_round = kConsumers * 32 / kRows;  // 8 columns
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int c = k * per_round + (threadIdx.x >> 4);
+                if (c < m) {
+                    w.pm[u * kMaxCols + c] = rm[k];
+                    w.ps[u * kMaxCols + c] = rs[k];
+                    w.pi[u * kMaxCols + c] = ri[k];
+                }
+            }
+        }
         if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(w.flag, 1);
         __threadfence();
         consumers_sync();
@@ -166,17 +191,22 @@ struct HeadEpi {
         consumers_sync();
         if (!s_last) return;
         __threadfence();
-        const int64_t units = (V + kRows - 1) / kRows;
-        merge_and_decide<kConsumers * 32>(w, units, m, thr, token, conf, fire, nonfinite,
+        merge_and_decide<kConsumers * 32>(w, gridDim.x, m, thr, token, conf, fire, nonfinite,
                                           threadIdx.x, sync_consumers);
     }
 };
+
+// weight-ring depth per row configuration (2 CTAs per SM for m <= 8:
+// 2 x 4 x 16 KB of weights in flight per SM)
+template <int NB>
+constexpr int kHeadStages = NB == 1 ? 4 : 6;
 
 template <int NB>
 __global__ void __launch_bounds__(tma_gemv::kThreads)
 k_exit_head_tma(const bf16* __restrict__ W, int V, int K, const bf16* __restrict__ X, int m,
                 HeadEpi epi) {
-    tma_gemv::gemv_body<NB>(W, V, K, X, K, m, tma_gemv::RowNorm{nullptr, 0.f}, epi);
+    tma_gemv::gemv_body<NB, HeadEpi, kHeadStages<NB>>(W, V, K, X, K, m,
+                                                      tma_gemv::RowNorm{nullptr, 0.f}, epi);
 }
 
 // ---- fp32 parity path --------------------------------------------------------
@@ -293,9 +323,11 @@ extern "C" int ee_exit_head_infer(const float* x, int64_t ldx, const int32_t* ro
         if (rc) return rc;
         const bf16* xn = (const bf16*)w.xn;
         const int nb = m <= 8 ? 1 : 2;
-        const size_t smem = tma_gemv::smem_bytes(nb);
-        const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / (smem + 1024)));
-        const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sms * per_sm);
+        const size_t smem = tma_gemv::smem_bytes(nb, nb == 1 ? kHeadStages<1> : kHeadStages<2>);
+        // the grid (and with it the two-level merge order) does not depend
+        // on m: 2 CTAs per SM (m > 8 needs more shared memory and runs the
+        // same grid in two waves; decode passes carry <= 1 + max_deferred rows)
+        const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sms * 2);
         static int conf_smem[2][16] = {};
         int dev = 0;
         cudaGetDevice(&dev);

@@ -38,8 +38,8 @@ constexpr int kXPitch = KS * 2 + 16;          // padded activation row
 constexpr int kMaxCols = 16;                  // activation rows per work item (NB = 2)
 
 __host__ __device__ constexpr int stage_bytes(int NB) { return kWBytes + 8 * NB * kXPitch; }
-__host__ inline size_t smem_bytes(int NB) {
-    return (size_t)kStages * stage_bytes(NB) + 3 * kStages * 8 +
+__host__ inline size_t smem_bytes(int NB, int stages = kStages) {
+    return (size_t)stages * stage_bytes(NB) + 3 * stages * 8 +
            (size_t)kConsumers * kRows * kMaxCols * 4 + kMaxCols * 4 + 64;
 }
 
@@ -101,7 +101,7 @@ struct RowNorm {
 // cols, inv) and finish(), both called by the 128 consumer threads (inv is
 // the per-column 1/rms or nullptr).  K must be a multiple of 512, W in the
 // tiled layout.
-template <int NB, class Epi>
+template <int NB, class Epi, int kStages = tma_gemv::kStages>
 __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int K,
                                           const bf16* __restrict__ X, int64_t ldx, int m,
                                           RowNorm rn, Epi& epi) {
