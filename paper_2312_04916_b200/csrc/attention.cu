@@ -5,207 +5,245 @@
 // 1/sqrt(dh) (eepipe/inference.py:203).
 //
 // Decode attention is latency-bound (a few MB of K/V per layer spread over
-// heads), so the kernel is organised to minimise DEPENDENT memory round
-// trips and to overlap with its neighbours under programmatic dependent
-// launch:
-//   * one CTA (128 threads) per (head, row, 32-position block); the block
-//     partition is keyed by POSITION ONLY (block b = [32b, 32b+32) ∩ [0,p]),
-//     so the result does not depend on how many rows share the launch
-//     (row-stable);
-//   * every thread issues all of its K and V loads at once (a quarter of one
-//     K row and of one V row each: 4 + 4 16-byte loads);
-//   * blocks that lie entirely below the smallest position written by this
-//     pass are read BEFORE griddepcontrol.wait — those K/V entries were
-//     written by earlier passes, so the loads overlap the QKV GEMV that is
-//     still running;
-//   * the block partial (max, sum-exp, acc[dh]) goes to a workspace; the
-//     last CTA of a (row, head) merges the partials in ascending block order
-//     (fixed order, deterministic).
+// heads): what matters is the number of DEPENDENT steps between the QKV GEMV
+// finishing and the Wo GEMV starting.  Organisation:
+//   * one CTA (8 warps) per (head, row, 256-position chunk); warp w owns the
+//     32-position block 8 c + w, lane j its position: q.K in registers,
+//     warp max / sum-exp by shuffles, P.V with each lane owning dh/32 output
+//     dimensions (coalesced V rows);
+//   * blocks and chunks are keyed by POSITION ONLY, and every merge runs in a
+//     fixed order (warps of a chunk in block order through shared memory,
+//     chunks in chunk order), so a row's result does not depend on how many
+//     rows share the launch (row-stable) and is deterministic;
+//   * rows up to position 255 need no cross-CTA step at all; longer rows
+//     publish one partial per chunk and the last CTA of the (row, head)
+//     merges them;
+//   * K/V rows that predate this pass (positions below every row of the
+//     launch) are prefetched into L2 BEFORE griddepcontrol.wait, overlapping
+//     the QKV GEMV that is still writing the new rows.
 #include "ee_common.cuh"
 
 namespace {
 
-constexpr int kBlk = 32;
-constexpr int kThreads = 128;
-constexpr int kMaxDh = 128;  // per-thread quarter rows: dh <= 128
+constexpr int kBlk = 32;                      // positions per warp block
+constexpr int kWarpsA = 8;                    // blocks per chunk
+constexpr int kChunk = kBlk * kWarpsA;        // 256 positions per CTA
+constexpr int kThreadsA = kWarpsA * 32;
+constexpr int kMaxDh = 128;
 constexpr int kRowsPerLaunch = 64;
-constexpr int kMaxBlocks = 64;  // s_max <= 2048
+constexpr int kMaxChunks = 8;                 // s_max <= 2048
 
-template <typename T> struct Q;  // 16-byte vector of T
-template <> struct Q<bf16> {
-    static constexpr int N = 8;
-    __device__ static void cvt(const uint4& u, float* v) {
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
-            v[2 * i] = f.x;
-            v[2 * i + 1] = f.y;
-        }
-    }
-};
-template <> struct Q<float> {
-    static constexpr int N = 4;
-    __device__ static void cvt(const uint4& u, float* v) {
-        v[0] = __uint_as_float(u.x);
-        v[1] = __uint_as_float(u.y);
-        v[2] = __uint_as_float(u.z);
-        v[3] = __uint_as_float(u.w);
-    }
-};
+template <typename T> __device__ __forceinline__ void load4(const T* p, float* v);
+template <> __device__ __forceinline__ void load4<bf16>(const bf16* p, float* v) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+template <> __device__ __forceinline__ void load4<float>(const float* p, float* v) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
-// Per (thread) share of a 32 x dh block: row j = tid / 4, quarter qd = tid % 4
-// covering dims [qd*dq, (qd+1)*dq), dq = dh / 4, in 16-byte vectors.
-template <typename T>
-struct BlockLoad {
-    static constexpr int VN = Q<T>::N;
-    static constexpr int kMaxVec = kMaxDh / 4 / VN;  // vectors per quarter row
-    uint4 k[kMaxVec], v[kMaxVec];
-    __device__ void issue(const T* kc, const T* vc, int64_t row_off, int nvec, bool valid) {
-#pragma unroll
-        for (int i = 0; i < kMaxVec; ++i) {
-            if (valid && i < nvec) {
-                k[i] = *reinterpret_cast<const uint4*>(kc + row_off + i * VN);
-                v[i] = *reinterpret_cast<const uint4*>(vc + row_off + i * VN);
-            }
-        }
-    }
-};
-
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+template <typename T, bool DH128>
+__global__ void __launch_bounds__(kThreadsA)
 k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int m,
               const T* __restrict__ kc, const T* __restrict__ vc, int nh, int dh, float scale,
               T* __restrict__ out, float* __restrict__ part, int* __restrict__ ctr) {
     __shared__ float s_q[kMaxDh];
-    __shared__ float s_p[kBlk];
-    __shared__ __align__(16) float s_v[kBlk][kMaxDh + 4];
-    __shared__ float s_stat[2];
+    __shared__ float s_m[kWarpsA], s_l[kWarpsA];
+    __shared__ float s_acc[kWarpsA][kMaxDh];
     __shared__ int s_last;
-    constexpr int VN = Q<T>::N;
 
     pdl_trigger_dev();
-    const int hh = blockIdx.x, r = blockIdx.y, b = blockIdx.z;
+    const int hh = blockIdx.x, r = blockIdx.y, ch = blockIdx.z;
     const int h = nh * dh;
     const int p = pos[r];  // host-written control data: safe before the wait
-    const int nblk = p / kBlk + 1;
-    if (b >= nblk) {
+    const int nch = p / kChunk + 1;
+    if (ch >= nch) {
         pdl_wait_dev();
         return;
     }
-    int pmin = p;
-    for (int i = 0; i < m; ++i) pmin = min(pmin, pos[i]);
-    const int tid = threadIdx.x;
-    const int j = tid >> 2, qd = tid & 3;
-    const int dq = dh >> 2;
-    const int nvec = dq / VN;
-    const int j0 = b * kBlk;
-    const int nj = min(kBlk, p + 1 - j0);
-    const bool valid = j < nj;
-    const int64_t row_off = (int64_t)(j0 + j) * h + hh * dh + qd * dq;
-
-    BlockLoad<T> ld;
-    const bool old = (j0 + kBlk) <= pmin;  // every position of the block predates this pass
-    if (VEC && old) ld.issue(kc, vc, row_off, nvec, valid);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j0 = ch * kChunk + warp * kBlk;          // this warp's block
+    const int jj = j0 + lane;                          // this lane's position
+    const bool valid = jj <= p;
+    const bool wvalid = j0 <= p;
+    const T* krow = kc + (int64_t)jj * h + hh * dh;
+    const T* vrow = vc + (int64_t)jj * h + hh * dh;
+    {
+        int pmin = p;
+        for (int i = 0; i < m; ++i) pmin = min(pmin, pos[i]);
+        if (valid && jj < pmin) {  // written by an earlier pass: fetch while QKV runs
+            const int bytes = dh * (int)sizeof(T);
+            for (int o = 0; o < bytes; o += 128) {
+                prefetch_l2((const char*)krow + o);
+                prefetch_l2((const char*)vrow + o);
+            }
+        }
+    }
     pdl_wait_dev();
-    if (VEC && !old) ld.issue(kc, vc, row_off, nvec, valid);
-
-    for (int d = tid; d < dh; d += kThreads) s_q[d] = q[(int64_t)r * h + hh * dh + d];
+    for (int d = threadIdx.x; d < dh; d += kThreadsA) s_q[d] = q[(int64_t)r * h + hh * dh + d];
     __syncthreads();
 
-    // score of position j0 + j: 4 threads x (dh/4) dims, fixed-order combine
-    float sc = 0.f;
-    if (VEC) {
+    float mx = -INFINITY, l = 0.f;
+    float acc[kMaxDh / 32][4];
+    if (wvalid) {
+        // score of this lane's position: fixed-order dot product.  DH = 128
+        // (the configs' head dim) issues the whole K row and this lane's V
+        // columns of the block before using any of them: one memory round
+        // trip per warp
+        float sc = 0.f;
+        const int nj = min(kBlk, p + 1 - j0);
+        const T* vb = vc + (int64_t)j0 * h + hh * dh;
 #pragma unroll
-        for (int i = 0; i < BlockLoad<T>::kMaxVec; ++i) {
-            if (i < nvec) {
-                float kv[VN];
-                Q<T>::cvt(ld.k[i], kv);
+        for (int g = 0; g < kMaxDh / 128; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+        if constexpr (DH128) {
+            // bf16 only: the raw K row (16 x 16 B) and this lane's 4 V columns
+            // of the block's 32 positions (32 x 8 B) stay packed in registers
+            uint4 kraw[16];
+            uint2 vraw[kBlk];
+            if (valid) {
 #pragma unroll
-                for (int e = 0; e < VN; ++e) sc = fmaf(s_q[qd * dq + i * VN + e], kv[e], sc);
+                for (int i = 0; i < 16; ++i) kraw[i] = reinterpret_cast<const uint4*>(krow)[i];
+            }
+#pragma unroll
+            for (int j = 0; j < kBlk; ++j)
+                if (j < nj) vraw[j] = *reinterpret_cast<const uint2*>(vb + (int64_t)j * h + 4 * lane);
+            if (valid) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t w4[4] = {kraw[i].x, kraw[i].y, kraw[i].z, kraw[i].w};
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const float2 f =
+                            __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e2]));
+                        sc = fmaf(s_q[8 * i + 2 * e2], f.x, sc);
+                        sc = fmaf(s_q[8 * i + 2 * e2 + 1], f.y, sc);
+                    }
+                }
+            }
+            const float sv = valid ? sc * scale : -INFINITY;
+            mx = sv;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float e = valid ? expf(sv - mx) : 0.f;
+            l = e;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+#pragma unroll
+            for (int j = 0; j < kBlk; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, e, j);
+                if (j < nj) {
+                    const float2 a =
+                        __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vraw[j].x));
+                    const float2 b =
+                        __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vraw[j].y));
+                    acc[0][0] = fmaf(pj, a.x, acc[0][0]);
+                    acc[0][1] = fmaf(pj, a.y, acc[0][1]);
+                    acc[0][2] = fmaf(pj, b.x, acc[0][2]);
+                    acc[0][3] = fmaf(pj, b.y, acc[0][3]);
+                }
+            }
+        } else {
+            if (valid) {
+                for (int d = 0; d < dh; d += 4) {
+                    float kv[4];
+                    load4<T>(krow + d, kv);
+                    sc = fmaf(s_q[d], kv[0], sc);
+                    sc = fmaf(s_q[d + 1], kv[1], sc);
+                    sc = fmaf(s_q[d + 2], kv[2], sc);
+                    sc = fmaf(s_q[d + 3], kv[3], sc);
+                }
+            }
+            const float sv = valid ? sc * scale : -INFINITY;
+            mx = sv;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float e = valid ? expf(sv - mx) : 0.f;
+            l = e;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+            // P.V: lane owns output dims [4 lane, 4 lane + 4)
+            for (int j = 0; j < nj; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, e, j);
+                if (4 * lane < dh) {
+                    float v4[4];
+                    load4<T>(vb + (int64_t)j * h + 4 * lane, v4);
+                    acc[0][0] = fmaf(pj, v4[0], acc[0][0]);
+                    acc[0][1] = fmaf(pj, v4[1], acc[0][1]);
+                    acc[0][2] = fmaf(pj, v4[2], acc[0][2]);
+                    acc[0][3] = fmaf(pj, v4[3], acc[0][3]);
+                }
             }
         }
-    } else if (valid) {
-        for (int e = 0; e < dq; ++e) sc = fmaf(s_q[qd * dq + e], to_f32(kc[row_off + e]), sc);
-    }
-    sc += __shfl_xor_sync(0xffffffffu, sc, 1);
-    sc += __shfl_xor_sync(0xffffffffu, sc, 2);
-    // V rows to shared memory for the position-ordered reduction
-    if (VEC) {
 #pragma unroll
-        for (int i = 0; i < BlockLoad<T>::kMaxVec; ++i) {
-            if (i < nvec) {
-                float vv[VN];
-                Q<T>::cvt(ld.v[i], vv);
-#pragma unroll
-                for (int e = 0; e < VN; ++e) s_v[j][qd * dq + i * VN + e] = valid ? vv[e] : 0.f;
+        for (int g = 0; g < kMaxDh / 128; ++g) {
+            const int d0 = 4 * (lane + 32 * g);
+            if (d0 < dh) {
+                s_acc[warp][d0] = acc[g][0];
+                s_acc[warp][d0 + 1] = acc[g][1];
+                s_acc[warp][d0 + 2] = acc[g][2];
+                s_acc[warp][d0 + 3] = acc[g][3];
             }
         }
-    } else {
-        for (int e = 0; e < dq; ++e) s_v[j][qd * dq + e] = valid ? to_f32(vc[row_off + e]) : 0.f;
     }
-    if (qd == 0) s_p[j] = valid ? sc * scale : -INFINITY;
-    __syncthreads();
-    if (tid < 32) {
-        float s = s_p[tid];
-        float mx = s;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const float e = tid < nj ? expf(s - mx) : 0.f;
-        float l = e;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-        s_p[tid] = e;
-        if (tid == 0) {
-            s_stat[0] = mx;
-            s_stat[1] = l;
-        }
+    if (lane == 0) {
+        s_m[warp] = mx;
+        s_l[warp] = l;
     }
     __syncthreads();
-    const int64_t slot = ((int64_t)r * nh + hh) * kMaxBlocks + b;
+    // merge the chunk's blocks in block order
+    const int nb = min(kWarpsA, (p - ch * kChunk) / kBlk + 1);
+    float M = -INFINITY;
+    for (int w = 0; w < nb; ++w) M = fmaxf(M, s_m[w]);
+    float L = 0.f;
+    for (int w = 0; w < nb; ++w) L += s_l[w] * expf(s_m[w] - M);
+    const int64_t slot = ((int64_t)r * nh + hh) * kMaxChunks + ch;
     const int stride = dh + 2;
-    for (int d = tid; d < dh; d += kThreads) {
-        float a = 0.f;
-        for (int jj = 0; jj < nj; ++jj) a = fmaf(s_p[jj], s_v[jj][d], a);
-        if (nblk == 1)
-            out[(int64_t)r * h + hh * dh + d] = from_f32<T>(a / s_stat[1]);
-        else
-            part[slot * stride + 2 + d] = a;
+    for (int d = threadIdx.x; d < dh; d += kThreadsA) {
+        float o = 0.f;
+        for (int w = 0; w < nb; ++w) o += s_acc[w][d] * expf(s_m[w] - M);
+        if (nch == 1) out[(int64_t)r * h + hh * dh + d] = from_f32<T>(o / L);
+        else part[slot * stride + 2 + d] = o;
     }
-    if (nblk == 1) return;
-    if (tid == 0) {
-        part[slot * stride] = s_stat[0];
-        part[slot * stride + 1] = s_stat[1];
+    if (nch == 1) return;
+    if (threadIdx.x == 0) {
+        part[slot * stride] = M;
+        part[slot * stride + 1] = L;
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(&ctr[r * nh + hh], 1) == nblk - 1);
+    if (threadIdx.x == 0) s_last = (atomicAdd(&ctr[r * nh + hh], 1) == nch - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // fixed-order merge over blocks 0..nblk-1
-    const float* base = part + ((int64_t)r * nh + hh) * kMaxBlocks * stride;
-    float M = -INFINITY;
-    for (int bb = 0; bb < nblk; ++bb) M = fmaxf(M, __ldcg(base + bb * stride));
-    float L = 0.f;
-    for (int bb = 0; bb < nblk; ++bb) L += __ldcg(base + bb * stride + 1) * expf(__ldcg(base + bb * stride) - M);
-    for (int d = tid; d < dh; d += kThreads) {
+    // fixed-order merge over chunks 0..nch-1
+    const float* base = part + ((int64_t)r * nh + hh) * kMaxChunks * stride;
+    float MM = -INFINITY;
+    for (int c = 0; c < nch; ++c) MM = fmaxf(MM, __ldcg(base + c * stride));
+    float LL = 0.f;
+    for (int c = 0; c < nch; ++c) LL += __ldcg(base + c * stride + 1) * expf(__ldcg(base + c * stride) - MM);
+    for (int d = threadIdx.x; d < dh; d += kThreadsA) {
         float o = 0.f;
-        for (int bb = 0; bb < nblk; ++bb)
-            o += __ldcg(base + bb * stride + 2 + d) * expf(__ldcg(base + bb * stride) - M);
-        out[(int64_t)r * h + hh * dh + d] = from_f32<T>(o / L);
+        for (int c = 0; c < nch; ++c)
+            o += __ldcg(base + c * stride + 2 + d) * expf(__ldcg(base + c * stride) - MM);
+        out[(int64_t)r * h + hh * dh + d] = from_f32<T>(o / LL);
     }
-    if (tid == 0) ctr[r * nh + hh] = 0;  // leave the workspace re-usable
+    if (threadIdx.x == 0) ctr[r * nh + hh] = 0;  // leave the workspace re-usable
 }
 
 size_t counters_bytes(int64_t nh) { return (((size_t)kRowsPerLaunch * nh * 4) + 255) & ~(size_t)255; }
 
 }  // namespace
 
-// Workspace: [counters: 64*nh int32][partials: 64*nh*64*(dh+2) float32].
+// Workspace: [counters: 64*nh int32][partials: 64*nh*kMaxChunks*(dh+2) float32].
 // Zero once at allocation; every call leaves the counters zeroed.
 size_t attention_ws_bytes(int64_t /*m*/, int64_t nh, int64_t dh, int64_t /*s_max*/) {
-    return counters_bytes(nh) + (size_t)kRowsPerLaunch * nh * kMaxBlocks * (dh + 2) * sizeof(float);
+    return counters_bytes(nh) + (size_t)kRowsPerLaunch * nh * kMaxChunks * (dh + 2) * sizeof(float);
 }
 
 int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_pos,
@@ -213,34 +251,31 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
                      void* ws, size_t ws_bytes, cudaStream_t s) {
     if (m == 0) return EE_OK;
     dtype = act_dtype(dtype);
-    const int vn = dtype == EE_BF16 ? 8 : 4;
     EE_REQUIRE(m > 0 && nh > 0 && dh > 0 && max_pos >= 0, EE_ESHAPE, "attention: bad shape");
     EE_REQUIRE(dh <= kMaxDh && dh % 4 == 0, EE_ESHAPE,
                "attention: head_dim must be <= %d and a multiple of 4, got %lld", kMaxDh,
                (long long)dh);
-    const bool vec = dh % (4 * vn) == 0;
-    EE_REQUIRE(max_pos < kMaxBlocks * kBlk, EE_ESHAPE, "attention: position %d beyond %d",
-               max_pos, kMaxBlocks * kBlk);
+    EE_REQUIRE(max_pos < kMaxChunks * kChunk, EE_ESHAPE, "attention: position %d beyond %d",
+               max_pos, kMaxChunks * kChunk);
     EE_REQUIRE(ws != nullptr && ws_bytes >= attention_ws_bytes(m, nh, dh, 0), EE_ESHAPE,
                "attention: workspace too small");
     int* ctr = (int*)ws;
     float* part = (float*)((char*)ws + counters_bytes(nh));
     const float scale = 1.0f / sqrtf((float)dh);
     const int64_t h = nh * dh;
-    const int nblk = max_pos / kBlk + 1;
+    const int nch = max_pos / kChunk + 1;
     for (int64_t r0 = 0; r0 < m; r0 += kRowsPerLaunch) {
         const int64_t mr = m - r0 < kRowsPerLaunch ? m - r0 : kRowsPerLaunch;
-        const dim3 grid((unsigned)nh, (unsigned)mr, (unsigned)nblk);
+        const dim3 grid((unsigned)nh, (unsigned)mr, (unsigned)nch);
         cudaError_t e;
         if (dtype == EE_BF16)
-            e = launch_ex(vec ? k_attn_decode<bf16, true> : k_attn_decode<bf16, false>, grid,
-                          dim3(kThreads), 0, s, q + r0 * h, pos + r0, (int)mr, (const bf16*)kc,
-                          (const bf16*)vc, (int)nh, (int)dh, scale, (bf16*)out + r0 * h, part, ctr);
+            e = launch_ex(dh == 128 ? k_attn_decode<bf16, true> : k_attn_decode<bf16, false>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
+                          (int)mr, (const bf16*)kc, (const bf16*)vc, (int)nh, (int)dh, scale,
+                          (bf16*)out + r0 * h, part, ctr);
         else if (dtype == EE_F32)
-            e = launch_ex(vec ? k_attn_decode<float, true> : k_attn_decode<float, false>, grid,
-                          dim3(kThreads), 0, s, q + r0 * h, pos + r0, (int)mr, (const float*)kc,
-                          (const float*)vc, (int)nh, (int)dh, scale, (float*)out + r0 * h, part,
-                          ctr);
+            e = launch_ex(k_attn_decode<float, false>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
+                          (int)mr, (const float*)kc, (const float*)vc, (int)nh, (int)dh, scale,
+                          (float*)out + r0 * h, part, ctr);
         else
             return ee_fail(EE_ECONFIG, "attention: unknown dtype %d", dtype);
         if (e != cudaSuccess) return ee_fail(EE_ECUDA, "attention launch: %s", cudaGetErrorString(e));
