@@ -207,7 +207,7 @@ int ee_decode_layers(const ee_decoder_t* dec, const ee_layer_t* layers, int32_t 
  *   *loss  = weight * mean_i CE_i (float32, device scalar),
  *   dx     = d loss / d x  (n, h) float32,
  *   dw_acc += d loss / d W (V, h) float32 (accumulated across microbatches).
- * n, h, V multiples of 8.  Workspace: ee_workspace_bytes(EE_OP_EXIT_HEAD_TRAIN,
+ * h, V multiples of 8 (any n).  Workspace: ee_workspace_bytes(EE_OP_EXIT_HEAD_TRAIN,
  * n, h, V, 0, 0).  Replaces `run_head` matmul + `cross_entropy` fwd/bwd + the
  * matmul backward (eepipe/model.py:219-230, eepipe/autodiff.py:158-179,
  * 301-323, eepipe/_ckernels.pyx:130-167). */

@@ -277,8 +277,10 @@ size_t exit_head_train_ws_bytes(int64_t n, int64_t /*h*/, int64_t V) { return ca
 extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
                                   const int64_t* targets, float weight, float* loss, float* dx,
                                   float* dw_acc, void* ws, size_t ws_bytes, void* stream) {
-    EE_REQUIRE(n > 0 && h > 0 && V > 0 && n % 8 == 0 && h % 8 == 0 && V % 8 == 0, EE_ESHAPE,
-               "exit_head_train: n, h, V must be positive multiples of 8 (n=%lld h=%lld V=%lld)",
+    // h and V set row strides of TMA-read matrices (16-byte multiples);
+    // any n works (out-of-range rows / k-blocks are zero-filled by TMA)
+    EE_REQUIRE(n > 0 && h > 0 && V > 0 && h % 8 == 0 && V % 8 == 0, EE_ESHAPE,
+               "exit_head_train: h and V must be positive multiples of 8 (n=%lld h=%lld V=%lld)",
                (long long)n, (long long)h, (long long)V);
     EE_REQUIRE(n < (1ll << 31) && V < (1ll << 31), EE_ESHAPE, "exit_head_train: too large");
     EE_REQUIRE(ws && ws_bytes >= carve_bytes(n, V), EE_ESHAPE,

@@ -47,7 +47,8 @@ def test_train_head_golden_small():
 
 
 @pytest.mark.parametrize("n,h,V,weight", [(256, 512, 1000, 1.0), (384, 256, 4096, 0.25),
-                                          (136, 1024, 2056, 0.5)])
+                                          (136, 1024, 2056, 0.5), (12, 16, 32, 1.0),
+                                          (301, 64, 520, 0.7)])
 def test_train_head_random(n, h, V, weight):
     rng = np.random.default_rng(n + V)
     x = rng.normal(size=(n, h)).astype(np.float32)
