@@ -312,7 +312,7 @@ def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
     out = {"workload": "C2 EE-GPT 1.3B training step (L=24, h=2048, V=50304, seq 2048, "
                        "microbatch 2 x 8, tied exits 6/12, P=1, Adam, bf16 compute)",
            "ms_per_step": ms, "tokens_per_s": tokens / (ms / 1e3), "tokens_per_step": tokens,
-           "per_exit_loss": rep.per_exit_loss, "steps": steps, "warmup": warmup}
+           "per_exit_loss": rep.per_exit_losses, "steps": steps, "warmup": warmup}
     del computes[:], master, opt
     torch.cuda.empty_cache()
     gc.unfreeze()

@@ -95,18 +95,66 @@ class IterationOptions:
 
 
 @dataclass
-class TrainStepReport:
-    """Per-iteration record (subset of eepipe/pipeline.py:133-161): per-exit
-    mean losses, per-stage executed event order, message counts, wall clock
-    and device time per stage action kind."""
+class StageMemoryCounters:
+    """Per-stage memory counters (eepipe/pipeline.py:125-130).  The fused
+    exit head never materialises logits, so ``peak_logit_copies`` is 0 in
+    both exit-forward variants (the reference holds one (b, s, V) copy per
+    deferred head evaluation, and one per in-flight microbatch when eager)."""
 
-    per_exit_loss: dict = field(default_factory=dict)
-    event_log: dict = field(default_factory=dict)
+    stage: int
+    peak_stored_microbatches: int = 0
+    peak_fill_stored: int = 0
+    peak_logit_copies: int = 0
+
+
+@dataclass
+class TrainStepReport:
+    """Per-iteration record with the reference's fields
+    (eepipe/pipeline.py:133-161): per-exit mean losses, per-stage gradient
+    norms, wall clock, per-stage memory counters, microbatch count, per-stage
+    executed (kind, microbatch) order, message counts, weights used."""
+
+    per_exit_losses: dict = field(default_factory=dict)
+    grad_norms: dict = field(default_factory=dict)
+    wall_clock: dict = field(default_factory=dict)
+    memory: list = field(default_factory=list)
+    microbatches: int = 0
+    event_log: list = field(default_factory=list)
     activation_messages: dict = field(default_factory=dict)
     gradient_messages: dict = field(default_factory=dict)
-    wall_clock: dict = field(default_factory=dict)
-    max_in_flight: dict = field(default_factory=dict)
     weights_used: tuple = ()
+    timeline: object = None
+
+    def semantic_state(self):
+        """Everything that must be reproducible under a fixed seed and
+        schedule, wall clock excluded (eepipe/pipeline.py:146-161)."""
+        return (
+            tuple(sorted(self.per_exit_losses.items())),
+            tuple(sorted(self.grad_norms.items())),
+            tuple((m.stage, m.peak_stored_microbatches, m.peak_fill_stored, m.peak_logit_copies)
+                  for m in self.memory),
+            self.microbatches,
+            tuple(tuple(log) for log in self.event_log),
+            tuple(sorted(self.activation_messages.items())),
+            tuple(sorted(self.gradient_messages.items())),
+            self.weights_used,
+        )
+
+    @property
+    def per_exit_loss(self):  # earlier name, kept for callers of this package
+        return self.per_exit_losses
+
+    @property
+    def max_in_flight(self):
+        return {m.stage: m.peak_stored_microbatches for m in self.memory}
+
+
+def _grad_norm(grads):
+    torch = _torch()
+    tot = 0.0
+    for g in grads.values():
+        tot += float(torch.linalg.vector_norm(g.detach().double()) ** 2)
+    return tot ** 0.5
 
 
 class TaggedChannel:
@@ -403,24 +451,29 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
 
     threads = [threading.Thread(target=target, args=(w,), daemon=True, name=f"stage-{w.index}")
                for w in workers]
+    t_start = time.perf_counter()
     for t in threads:
         t.start()
     for t in threads:
         t.join(timeout=_RECV_TIMEOUT * 2)
+    elapsed = time.perf_counter() - t_start
     for w in workers:
         if w.exception is not None:
             raise w.exception
-    merged = sync_tied([w.compute.tm.grads() for w in workers], part.tied_replicas)
-    report = TrainStepReport(weights_used=tuple(weights))
-    for w in workers:
-        report.event_log[w.index] = list(w.event_log)
-        report.wall_clock[w.index] = dict(w.wall)
-        report.max_in_flight[w.index] = w.max_in_flight
-        for key, vals in w.compute.head_losses.items():
-            report.per_exit_loss[key] = sum(float(v) for v in vals) / len(vals)
-    for s in range(1, P):
-        report.activation_messages[s] = fwd[s - 1].count
-        report.gradient_messages[s + 1] = bwd[s - 1].count
+    per_stage = [w.compute.tm.grads() for w in workers]
+    merged = sync_tied(per_stage, part.tied_replicas)
+    report = TrainStepReport(weights_used=tuple(weights), microbatches=M)
+    for w, g in zip(workers, per_stage):
+        report.event_log.append(list(w.event_log))
+        report.memory.append(StageMemoryCounters(w.index, w.max_in_flight))
+        report.grad_norms[w.index] = _grad_norm(g)
+        report.activation_messages[w.index] = w.fwd_out.count if w.fwd_out is not None else 0
+        report.gradient_messages[w.index] = w.bwd_out.count if w.bwd_out is not None else 0
+    for hd in all_heads:
+        vals = [v for w in workers for v in w.compute.head_losses.get(hd.key, [])]
+        report.per_exit_losses[hd.key] = sum(float(v) for v in vals) / len(vals)
+    report.wall_clock = {"forward": sum(w.wall["F"] for w in workers),
+                         "backward": sum(w.wall["B"] for w in workers), "total": elapsed}
     return merged, report
 
 
@@ -484,14 +537,15 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
         if s in holders:
             g = grads[name]
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
-    report = TrainStepReport(weights_used=tuple(weights))
-    report.event_log[s] = list(w.event_log)
-    report.wall_clock[s] = dict(w.wall)
-    report.max_in_flight[s] = w.max_in_flight
+    # this rank's view: its own stage's entries (event_log[s-1], memory[0])
+    report = TrainStepReport(weights_used=tuple(weights), microbatches=M)
+    report.event_log = [[] for _ in range(P)]
+    report.event_log[s - 1] = list(w.event_log)
+    report.memory = [StageMemoryCounters(s, w.max_in_flight)]
+    report.wall_clock = {"forward": w.wall["F"], "backward": w.wall["B"],
+                         "total": w.wall["F"] + w.wall["B"]}
     for key, vals in comp.head_losses.items():
-        report.per_exit_loss[key] = sum(float(v) for v in vals) / len(vals)
-    if fwd_out is not None:
-        report.activation_messages[s] = fwd_out.count
-    if bwd_out is not None:
-        report.gradient_messages[s] = bwd_out.count
+        report.per_exit_losses[key] = sum(float(v) for v in vals) / len(vals)
+    report.activation_messages[s] = fwd_out.count if fwd_out is not None else 0
+    report.gradient_messages[s] = bwd_out.count if bwd_out is not None else 0
     return grads, report

@@ -664,17 +664,17 @@ def train(run_cfg, corpus, metrics_path=None, progress=None, *, devices=None, dt
             grads, report = run_iteration_1f1b(part, batch, opts, model=master, devices=devices,
                                                dtype=dtype, master_dtype=torch.float32,
                                                stage_computes=computes)
-            if not all(np.isfinite(v) for v in report.per_exit_loss.values()):
+            if not all(np.isfinite(v) for v in report.per_exit_losses.values()):
                 raise NonFiniteError(f"non-finite loss at step {step}")
             apply_update(optimizer, master, grads, computes, 1.0 / num_mb)
             torch.cuda.synchronize()
             elapsed = time.perf_counter() - t0
             if head_keys is None:
-                head_keys = [hd.key for hd in master.heads if hd.key in report.per_exit_loss]
+                head_keys = [hd.key for hd in master.heads if hd.key in report.per_exit_losses]
                 write({"record": "header", "heads": head_keys, "steps": run_cfg.steps,
                        "seed": run_cfg.seed})
             rec = {"record": "step", "step": step,
-                   "losses": {k: report.per_exit_loss[k] for k in head_keys},
+                   "losses": {k: report.per_exit_losses[k] for k in head_keys},
                    "time": elapsed, "microbatches": num_mb,
                    "weights": list(report.weights_used)}
             history.append(rec)

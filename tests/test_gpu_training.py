@@ -58,10 +58,11 @@ def test_pipeline_matches_single_device():
         for n in ref:
             assert _rel(grads[n].float().cpu().numpy(), ref[n].float().cpu().numpy()) < 1e-3, n
         for k, v in ref_loss.items():
-            assert rep.per_exit_loss[k] == pytest.approx(v, rel=1e-3)
+            assert rep.per_exit_losses[k] == pytest.approx(v, rel=1e-3)
         for s in range(1, P + 1):
             assert rep.max_in_flight[s] == min(P - s + 1, 4)
-        assert all(c == 4 for c in rep.activation_messages.values())
+        assert all(rep.activation_messages[s] == 4 for s in range(1, P))
+        assert all(rep.gradient_messages[s] == 4 for s in range(2, P + 1))
 
 
 def test_tied_pipeline_sums_replicas():

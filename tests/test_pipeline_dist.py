@@ -177,7 +177,7 @@ def test_distributed_1f1b_matches_single_process(world, tied):
     merged = {}
     for rank, grads, log, inflight, acts, gms in sorted(results, key=lambda r: r[0]):
         s = rank + 1
-        assert log[s] == sched.regular_actions(world, 4, s)
+        assert log[s - 1] == sched.regular_actions(world, 4, s)
         assert inflight[s] == min(world - s + 1, 4)
         if s < world:
             assert acts[s] == 4

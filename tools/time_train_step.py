@@ -58,7 +58,7 @@ def train_step_bench(M=8, mb=2, seq=2048, steps=3, warmup=2, stages=1):
     return {"workload": f"C2 EE-GPT 1.3B training step (L=24, h=2048, V=50304, seq {seq}, "
                         f"microbatch {mb} x {M}, tied exits 6/12, P={stages}, Adam fp32 master)",
             "ms_per_step": ms, "tokens_per_s": tokens / (ms / 1e3), "tokens_per_step": tokens,
-            "losses": rep.per_exit_loss,
+            "losses": rep.per_exit_losses,
             "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9}
 
 
