@@ -8,6 +8,6 @@ timeout 900 python bench.py > gpurun_out/bench.jsonl 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.jsonl 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_decode.csv python tools/prof_decode.py 2 1 > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_train_head.csv python tools/time_train_head.py 4096 2048 50304 1 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemv_tma -s 300 -c 4 -o gpurun_out/gemv_tma_full python tools/prof_decode.py 1 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemv_tma -s 40 -c 4 -o gpurun_out/gemv_tma_full python tools/prof_decode.py 1 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm2 -s 3 -c 3 -o gpurun_out/tc_gemm2_full python tools/time_train_head.py 4096 2048 50304 1 > /dev/null 2>&1
 ls -la gpurun_out
