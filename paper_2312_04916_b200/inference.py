@@ -895,6 +895,11 @@ def generate_pipeline(part: StagePartition, prompt, threshold, max_new_tokens, s
                                   dtype, devices[i % len(devices)]))
     threads = [threading.Thread(target=s.run, daemon=True, name=f"infer-stage-{s.spec.index}")
                for s in stages]
+    # the stage workers and the coordinator are latency-bound Python threads
+    # that mostly wait in CUDA / queue calls: hand the GIL over quickly
+    import sys
+    old_switch = sys.getswitchinterval()
+    sys.setswitchinterval(5e-5)
     for t in threads:
         t.start()
 
@@ -942,6 +947,7 @@ def generate_pipeline(part: StagePartition, prompt, threshold, max_new_tokens, s
         queues[0].put(_FwdMsg(None, [], -1, True, None, stop=True))
         for t in threads:
             t.join(timeout=_EMIT_TIMEOUT)
+        sys.setswitchinterval(old_switch)
     for s in stages:
         if s.exception is not None:
             raise s.exception
