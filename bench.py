@@ -263,6 +263,40 @@ def bench_train_head(local, hbm_peak, reps=10):
                          "traffic": head_traffic()}}
 
 
+def bench_pipeline_stages(model, prompt, local, new_tokens=64):
+    """`generate_pipeline` on the C3 model at P = 2, 4, 8 stages.  The pool
+    gives ONE GPU, so the stage workers are host threads with their own CUDA
+    streams sharing it (the multi-process NCCL path, pipeline_infer.
+    generate_pipeline_dist, is protocol-tested on gloo): all stages' layers
+    still run for every token (KV fill), so throughput is bounded by the
+    single GPU's full-depth rate; early exits shorten the emit latency
+    (modeled speedup, eepipe/schedule.py:553-590)."""
+    import torch
+    from paper_2312_04916_b200 import inference as I
+    from paper_2312_04916_b200.model import partition
+    out = {"note": "P stage workers = threads + CUDA streams on ONE B200 (1-GPU pool); "
+                   f"{new_tokens} new tokens, prompt {PROMPT_LEN}"}
+    for P in (2, 4, 8):
+        part = partition(model, P, copy=False)
+        I.generate_pipeline(part, prompt, 0.8, 4, devices=[f"cuda:{local}"])  # builds stage engines
+        res = {}
+        for thr in (1.0, 0.8, 0.2):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            tr = I.generate_pipeline(part, prompt, thr, new_tokens, devices=[f"cuda:{local}"])
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t
+            res[str(thr)] = {"tokens_per_s": len(tr.tokens) / dt,
+                             "mean_exit_layer": tr.mean_exit_layer,
+                             "modeled_speedup": tr.speedup}
+        out[f"P{P}"] = res
+        for spec in part.stages:  # free this partition's packed stage weights
+            spec.__dict__.pop("_ee_engines", None)
+        del part
+        torch.cuda.empty_cache()
+    return out
+
+
 def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
     """One C2 training step (BASELINE configs[1]): EE-GPT 1.3B (L=24, h=2048,
     16 heads, V=50304, tied exits at 6 (w 0.25) / 12 (w 0.5)), microbatch 2 x
@@ -334,6 +368,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train-head", action="store_true")
     ap.add_argument("--no-train-step", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true")
     ap.add_argument("--new-tokens", type=int, default=NEW_TOKENS)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -433,6 +468,11 @@ def main():
                                "early_exits": int(sum(1 for e in tr.exit_layers if e < L)),
                                "modeled_speedup": tr.speedup}
 
+    # ---- pipeline-based inference: P stage workers on this one GPU ------------
+    pipe = None
+    if not args.no_pipeline and world == 1:
+        pipe = bench_pipeline_stages(model, prompt, local)
+
     # ---- fused training exit head at the C2 shape (second half of the metric) --
     head_train = None
     if not args.no_train_head:
@@ -482,6 +522,7 @@ def main():
         "sweep": sweep,
         "exit_head_train": head_train,
         "train_step": train_step,
+        "pipeline_stages_1gpu": pipe,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))

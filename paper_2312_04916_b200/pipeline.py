@@ -452,10 +452,17 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
     threads = [threading.Thread(target=target, args=(w,), daemon=True, name=f"stage-{w.index}")
                for w in workers]
     t_start = time.perf_counter()
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join(timeout=_RECV_TIMEOUT * 2)
+    import sys
+    old_switch = sys.getswitchinterval()
+    if P > 1:  # several launch-bound stage threads: hand the GIL over quickly
+        sys.setswitchinterval(5e-5)
+    try:
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=_RECV_TIMEOUT * 2)
+    finally:
+        sys.setswitchinterval(old_switch)
     elapsed = time.perf_counter() - t_start
     for w in workers:
         if w.exception is not None:
