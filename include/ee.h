@@ -168,6 +168,16 @@ typedef struct {
     size_t pf_ws_bytes;
 } ee_decoder_t;
 
+/* ee_embed followed, when xb and ssq are non-null (tiled mode), by
+ * ee_row_stats of the new rows (out has row stride h): one call per pass. */
+int ee_embed_stats(const int32_t* tok, const int32_t* pos, int64_t m, const void* tok_emb,
+                   const void* pos_emb, int64_t h, int dtype, float* out, void* xb, float* ssq,
+                   void* stream);
+
+/* Asynchronous host -> device copy of `bytes` from PINNED host memory on
+ * `stream` (the per-pass control block upload). */
+int ee_copy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+
 /* Row statistics for tiled mode: xb = bf16(x), ssq[r][t] = sum_{i<16}
  * x[r][16t+i]^2.  Must be called for rows whose x was written outside the
  * decoder (embedding, rows received from another pipeline stage); the

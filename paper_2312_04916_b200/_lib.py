@@ -56,6 +56,9 @@ SIGNATURES = {
     "ee_row_stats": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
     "ee_embed": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int, c_void_p,
                          c_void_p]),
+    "ee_embed_stats": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int,
+                               c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ee_copy_h2d": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     "ee_rmsnorm_rows": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_float,
                                 c_void_p, c_int, c_void_p]),
     "ee_gemv": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int, c_int, c_void_p,

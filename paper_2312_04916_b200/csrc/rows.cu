@@ -148,3 +148,20 @@ extern "C" int ee_row_stats(const float* x, int64_t ldx, int64_t m, int64_t h, v
                             float* ssq, void* stream) {
     return launch_row_stats(x, ldx, m, h, xb, ssq, as_stream(stream));
 }
+
+// embedding + (tiled mode) row statistics of the new rows in one call
+extern "C" int ee_embed_stats(const int32_t* tok, const int32_t* pos, int64_t m, const void* tok_emb,
+                              const void* pos_emb, int64_t h, int dtype, float* out, void* xb,
+                              float* ssq, void* stream) {
+    int rc = ee_embed(tok, pos, m, tok_emb, pos_emb, h, dtype, out, stream);
+    if (rc || m == 0 || xb == nullptr || ssq == nullptr) return rc;
+    return launch_row_stats(out, h, m, h, xb, ssq, as_stream(stream));
+}
+
+// asynchronous host -> device copy (pinned source) on `stream`
+extern "C" int ee_copy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+    if (bytes == 0) return EE_OK;
+    const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream));
+    EE_REQUIRE(e == cudaSuccess, EE_ECUDA, "copy_h2d: %s", cudaGetErrorString(e));
+    return EE_OK;
+}

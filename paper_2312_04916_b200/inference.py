@@ -254,10 +254,11 @@ class _PinnedRing:
         self.i = (i + 1) % len(self.bufs)
         if self.events[i] is not None:
             self.events[i].synchronize()
-        b = self.bufs[i]
         self.views[i][:n] = arr
-        dst[:n].copy_(b[:n], non_blocking=True)
-        ev = torch.cuda.Event()
+        # one raw cudaMemcpyAsync (no torch slicing / dispatch on the hot path)
+        call("ee_copy_h2d", ctypes.c_void_p(dst.data_ptr()),
+             ctypes.c_void_p(self.bufs[i].data_ptr()), 4 * n, ctypes.c_void_p(stream.cuda_stream))
+        ev = self.events[i] or torch.cuda.Event()
         ev.record(stream)
         self.events[i] = ev
 
@@ -452,12 +453,14 @@ class Engine:
             ring.put(stage, dbuf, _torch().cuda.current_stream(self.device))
             self.h2d_bytes += 4 * len(stage)
             tok_p, pos_p = ptr(dbuf), ctypes.c_void_p(dbuf.data_ptr() + 4 * m)
-        self.launches += 1
-        call("ee_embed", tok_p, pos_p, m,
-             ptr(self.tok_emb), ptr(self.pos_emb), self.h, self.dcode, dst,
+        stats = out is None and self.tiled and m > 0
+        self.launches += 2 if stats else 1
+        # embedding + (tiled mode) the new rows' statistics in one call
+        call("ee_embed_stats", tok_p, pos_p, m, ptr(self.tok_emb), ptr(self.pos_emb), self.h,
+             self.dcode, dst,
+             ctypes.c_void_p(self.xb.data_ptr() + 2 * row0 * self.h) if stats else None,
+             ctypes.c_void_p(self.ssq.data_ptr() + 4 * row0 * (self.h // 16)) if stats else None,
              stream_ptr(_torch().cuda.current_stream(self.device)))
-        if out is None:
-            self.refresh_stats(row0, m)
 
     def refresh_stats(self, row0, m):
         """Tiled mode: bf16 copy + sum-of-squares partials of rows written
