@@ -448,6 +448,7 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     }
     tc_fence_before();
     cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+    __syncthreads();     // (explicit CTA barrier too: the TMEM address is read from smem)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
