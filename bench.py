@@ -222,10 +222,11 @@ def run_reference(args):
     return 0
 
 
-def bench_train_head(local, hbm_peak, reps=10):
-    """Fused training exit head (loss + dX + dW, tcgen05) at the C2 shape:
-    n = 2 x 2048 tokens, h = 2048, V = 50304, bf16.  TFLOP/s on the
-    algorithmic 6 n h V, vs the measured bf16 peak."""
+def bench_train_head(local, hbm_peak, reps=10, n=4096, h=2048, V=50304, tag="C2"):
+    """Fused training exit head (loss + dX + dW, tcgen05) at a training
+    shape: C2 = n 2 x 2048 tokens, h 2048; C4 = n 1 x 2048, h 5120; V = 50304,
+    bf16.  TFLOP/s on the algorithmic 6 n h V, vs the measured
+    bf16 peak."""
     import torch
     from paper_2312_04916_b200.training import exit_head_loss_and_grads
     _, tf_peak, kind = peaks()
@@ -234,7 +235,6 @@ def bench_train_head(local, hbm_peak, reps=10):
             sustained = float(json.load(f).get("bf16_tflops_sustained", tf_peak))
     except Exception:
         sustained = tf_peak
-    n, h, V = 4096, 2048, 50304
     dev = f"cuda:{local}"
     g = torch.Generator(device=dev).manual_seed(0)
     x = torch.randn(n, h, device=dev, generator=g).bfloat16()
@@ -253,7 +253,7 @@ def bench_train_head(local, hbm_peak, reps=10):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
     tflops = 6 * n * h * V / (ms * 1e-3) / 1e12
-    return {"workload": "C2 exit head fwd+bwd (n=4096, h=2048, V=50304, bf16)",
+    return {"workload": f"{tag} exit head fwd+bwd (n={n}, h={h}, V={V}, bf16)",
             "ms": ms, "tflops_6nhv": tflops,
             "note": "executed FLOPs = algorithmic 6nhV (logits computed once: part-normalised "
                     "probabilities + in-place gradient fixup, no recompute)",
@@ -477,6 +477,7 @@ def main():
     head_train = None
     if not args.no_train_head:
         head_train = bench_train_head(local, hbm_peak)
+        head_train["c4_shape"] = bench_train_head(local, hbm_peak, n=2048, h=5120, tag="C4")
     train_step = None
     if not args.no_train_step:
         train_step = bench_train_step(local)
