@@ -260,7 +260,7 @@ def bench_train_head(local, hbm_peak, reps=10, n=4096, h=2048, V=50304, tag="C2"
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": tf_peak,
                          "unit": "TFLOP/s", "frac": tflops / tf_peak,
                          "frac_of_sustained": tflops / sustained, "peak_kind": kind,
-                         "traffic": head_traffic()}}
+                         "traffic": head_traffic() if tag == "C2" else None}}
 
 
 def bench_pipeline_stages(model, prompt, local, new_tokens=64):
