@@ -37,7 +37,10 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct TrainWs {
     bf16* g;
     float *pmax, *psum, *tgt, *lse, *rowloss;
+    int* flags;  // ordered split-K flags of the dX GEMM
 };
+
+constexpr size_t kFlagBytes = 64 * 1024;  // up to 1024 cluster tiles x 16 regions
 
 TrainWs carve(void* ws, int64_t n, int64_t V) {
     TrainWs w;
@@ -48,13 +51,14 @@ TrainWs carve(void* ws, int64_t n, int64_t V) {
     w.tgt = (float*)p; p += al((size_t)n * 4);
     w.lse = (float*)p; p += al((size_t)n * 4);
     w.rowloss = (float*)p; p += al((size_t)n * 4);
+    w.flags = (int*)p; p += kFlagBytes;
     w.g = (bf16*)p;
     return w;
 }
 
 size_t carve_bytes(int64_t n, int64_t V) {
     const int64_t ntn = kParts * ((V + kBN - 1) / kBN);
-    return 2 * al((size_t)n * ntn * 4) + 3 * al((size_t)n * 4) + al((size_t)n * V * 2);
+    return 2 * al((size_t)n * ntn * 4) + 3 * al((size_t)n * 4) + kFlagBytes + al((size_t)n * V * 2);
 }
 
 // ---- epilogues ----------------------------------------------------------------
@@ -63,6 +67,7 @@ size_t carve_bytes(int64_t n, int64_t V) {
 // keeps (m, s) = (-inf, 0), which the merge skips.
 struct EpiProb {
     static constexpr bool kTwoPass = true;
+    static constexpr bool kSplitK = false;
     const int64_t* targets;
     float *pmax, *psum, *tgt;
     bf16* g;
@@ -119,6 +124,7 @@ struct EpiProb {
 template <bool ACCUM>
 struct EpiF32 {  // K3 store / K4 accumulate
     static constexpr bool kTwoPass = false;
+    static constexpr bool kSplitK = false;
     float* out;
     int ldo;
     __device__ void begin_tile(int, int, int, bool) {}
@@ -145,6 +151,90 @@ struct EpiF32 {  // K3 store / K4 accumulate
     }
     __device__ void end_tile(int, int, int, bool) {}
 };
+
+// K3 with ORDERED split-K: split s of tile t adds its partial into dx after
+// split s-1 of the same (tile, warp region) has written (per-region flags,
+// acquire / release), so dx = ((p0 + p1) + p2) + ... in split order —
+// deterministic, with the read-modify-write traffic inside the tensor-bound
+// GEMM instead of a separate reduction pass.  Items run split-major, and a
+// cluster only ever waits for an item of a lower index, so the persistent
+// grid cannot deadlock.  The flags are zero at rest (the last split resets
+// them; the host also clears them per call).
+struct EpiF32Ordered {
+    static constexpr bool kTwoPass = false;
+    static constexpr bool kSplitK = true;
+    float* out;
+    int ldo;
+    int* flags;  // [tiles][16 regions]
+    int splits;
+    int s = 0;
+    int* flag = nullptr;
+    __device__ void set_split(int sp, int t) {
+        s = sp;
+        const int region = (int)tc::cluster_rank() * tc::kEpiWarps + ((int)(threadIdx.x >> 5) - 2);
+        flag = flags + t * 2 * tc::kEpiWarps + region;
+    }
+    __device__ void begin_tile(int, int, int, bool) {
+        if (s > 0) {
+            if ((threadIdx.x & 31) == 0) {
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                } while (v < s);
+            }
+            __syncwarp();
+        }
+    }
+    __device__ void chunk(int row, int col, const float* v, int nvalid) {
+        float* o = out + (int64_t)row * ldo + col;
+        if (nvalid == 16) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+                float4 c = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (s > 0) {
+                    const float4 p = __ldcg(reinterpret_cast<const float4*>(o + j));
+                    c.x = p.x + c.x;
+                    c.y = p.y + c.y;
+                    c.z = p.z + c.z;
+                    c.w = p.w + c.w;
+                }
+                *reinterpret_cast<float4*>(o + j) = c;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < nvalid) o[j] = s > 0 ? __ldcg(o + j) + v[j] : v[j];
+        }
+    }
+    __device__ void end_tile(int, int, int, bool) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+            __threadfence();
+            const int nv = (s == splits - 1) ? 0 : s + 1;
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(nv) : "memory");
+        }
+    }
+};
+
+// split count for a GEMM of `tiles` cluster tiles and nk k-blocks on
+// `pairs` clusters: the smallest S <= 4 whose last wave is >= 95% full
+// (else the best of 1..4), keeping >= 64 k-blocks per split
+static int pick_splits(int tiles, int nk, int pairs) {
+    int best = 1;
+    double best_eff = 0.0;
+    for (int S = 1; S <= 4; ++S) {
+        if (S > 1 && nk / S < 64) break;
+        const int items = tiles * S;
+        const int waves = (items + pairs - 1) / pairs;
+        const double eff = (double)items / ((double)waves * pairs);
+        if (eff >= 0.95) return S;
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = S;
+        }
+    }
+    return best;
+}
 
 // ---- small kernels ---------------------------------------------------------
 // per-row merge of the tile partials in ascending (tile, half) order: one
@@ -301,10 +391,25 @@ extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const voi
     if ((rc = ee_check_launch("grad_fixup"))) return rc;
     k_loss_sum<<<1, 1024, 0, s>>>(w.rowloss, (int)n, scale, loss);
     if ((rc = ee_check_launch("loss_sum"))) return rc;
-    // K3: dX = G W     (W (V x h) is the MN-major B operand, K = V)
-    if ((rc = tc::launch_tc_gemm2<kBN, false, true, false>(w.g, W, (int)n, (int)h, (int)V,
-                                                          EpiF32<false>{dx, (int)h}, s)))
-        return rc;
+    // K3: dX = G W     (W (V x h) is the MN-major B operand, K = V); long
+    // tiles, few of them: ordered split-K fills the last wave
+    {
+        const int tiles = (int)(((n + 255) / 256) * ((h + kBN - 1) / kBN));
+        const bool fits = (size_t)tiles * 2 * tc::kEpiWarps * sizeof(int) <= kFlagBytes;
+        const int S = fits ? pick_splits(tiles, (int)((V + tc::BK - 1) / tc::BK), ee_sm_count() / 2)
+                           : 1;
+        if (S == 1) {
+            if ((rc = tc::launch_tc_gemm2<kBN, false, true, false>(
+                     w.g, W, (int)n, (int)h, (int)V, EpiF32<false>{dx, (int)h}, s)))
+                return rc;
+        } else {
+            const size_t fbytes = (size_t)tiles * 2 * tc::kEpiWarps * sizeof(int);
+            cudaMemsetAsync(w.flags, 0, fbytes, s);
+            if ((rc = tc::launch_tc_gemm2<kBN, false, true, false>(
+                     w.g, W, (int)n, (int)h, (int)V, EpiF32Ordered{dx, (int)h, w.flags, S}, s, S)))
+                return rc;
+        }
+    }
     // K4: dW += G^T X  (G and X both MN-major, K = n); N-fastest tile order so
     // concurrent CTAs share each G column block
     return tc::launch_tc_gemm2<kBN, true, true, true>(w.g, x, (int)V, (int)h, (int)n,

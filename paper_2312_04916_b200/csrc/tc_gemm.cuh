@@ -408,10 +408,18 @@ __device__ __forceinline__ void tc_commit2(uint64_t* bar) {
         : "memory");
 }
 
+// split-K: item i -> (split s = i / ntiles, tile t = i % ntiles); split s
+// covers k-blocks [nk s / S, nk (s+1) / S); an epilogue with kSplitK = true
+// is told the split (set_split) and writes its own partial output
+template <class Epi>
+__device__ __forceinline__ void epi_set_split(Epi& epi, int s, int t) {
+    if constexpr (Epi::kSplitK) epi.set_split(s, t);
+}
+
 template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M,
-           int N, int K, Epi epi) {
+           int N, int K, Epi epi, int splits) {
     using C = Cfg2<BN>;
     constexpr int BM2 = 2 * BM;
     extern __shared__ uint8_t smem_raw[];
@@ -428,6 +436,12 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int tiles_m = (M + BM2 - 1) / BM2, tiles_n = (N + BN - 1) / BN;
     const int ntiles = tiles_m * tiles_n;
     const int nk = (K + BK - 1) / BK;
+    const int nitems = ntiles * splits;
+    auto kr = [&](int it, int& k0, int& k1) {
+        const int sp = it / ntiles;
+        k0 = (int)((int64_t)nk * sp / splits);
+        k1 = (int)((int64_t)nk * (sp + 1) / splits);
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages2; ++s) {
@@ -459,12 +473,15 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tb) : "memory");
             int s = 0;
             uint32_t ph = 0;
-            for (int t = cid; t < ntiles; t += ncl) {
+            for (int it = cid; it < nitems; it += ncl) {
+                const int t = it % ntiles;
                 const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
                 const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
                 const int m0 = mb * BM2 + (int)rank * BM;
                 const int n0 = nb * BN + (int)rank * (BN / 2);
-                for (int kb = 0; kb < nk; ++kb) {
+                int k0, k1;
+                kr(it, k0, k1);
+                for (int kb = k0; kb < k1; ++kb) {
                     mb_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * C::kStageBytes;
                     const uint32_t bar = map_rank(&full[s], 0);
@@ -496,11 +513,13 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             uint32_t ph = 0;
             int acc = 0;
             uint32_t aph = 0;
-            for (int t = cid; t < ntiles; t += ncl) {
+            for (int it = cid; it < nitems; it += ncl) {
+                int k0, k1;
+                kr(it, k0, k1);
                 mb_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + acc * BN;
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = k0; kb < k1; ++kb) {
                     mb_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t a0 = su32(smem + s * C::kStageBytes);
@@ -508,7 +527,7 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
                         tc_mma2(d, op_desc<A_MN>(a0, k), op_desc<B_MN>(b0, k), idesc,
-                                (kb | k) != 0);
+                                (kb > k0 || k > 0) ? 1u : 0u);
                     tc_commit2(&empty[s]);  // both CTAs' stage s free once these MMAs completed
                     if (++s == kStages2) {
                         s = 0;
@@ -530,9 +549,11 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         const uint32_t leader_tempty0 = map_rank(&tempty[0], 0);
         int acc = 0;
         uint32_t aph = 0;
-        for (int t = cid; t < ntiles; t += ncl) {
+        for (int it = cid; it < nitems; it += ncl) {
+            const int t = it % ntiles;
             const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
             const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
+            epi_set_split(epi, it / ntiles, t);
             mb_wait(&tfull[acc], aph);
             tc_fence_after();
             const int row = mb * BM2 + row_in_tile;
@@ -590,7 +611,8 @@ int launch_tc_gemm(const void* A, const void* B, int M, int N, int K, Epi epi, c
 
 // CTA-pair launch: M tiles of 256 rows, grid = 2 x min(tiles, SMs / 2).
 template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
-int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, cudaStream_t s) {
+int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, cudaStream_t s,
+                    int splits = 1) {
     CUtensorMap ta, tb;
     int rc;
     if ((rc = A_MN ? make_tmap_bf16(&ta, A, K, M, BK) : make_tmap_bf16(&ta, A, M, K, BM))) return rc;
@@ -604,10 +626,10 @@ int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg2<BN>::kSmem);
         configured[dev & 15] = true;
     }
-    const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+    const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * splits;
     const int pairs = ee_sm_count() / 2;
     const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    kern<<<grid, kThreads, Cfg2<BN>::kSmem, s>>>(ta, tb, M, N, K, epi);
+    kern<<<grid, kThreads, Cfg2<BN>::kSmem, s>>>(ta, tb, M, N, K, epi, splits);
     return ee_check_launch("tc_gemm2");
 }
 
