@@ -133,20 +133,34 @@ k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* 
     }
 }
 
-// gw_j (+)= sum over CTA partials in CTA order (deterministic)
-__global__ void k_gw_reduce(const float* __restrict__ part, int nparts, int h, int accumulate,
-                            float* __restrict__ gw) {
+// gw_j (+)= sum over CTA partials in CTA order (deterministic), two levels:
+// k_gw_reduce1 sums consecutive groups of partials (grid.y groups) into
+// level-2 partials, k_gw_reduce2 sums those in group order
+constexpr int kGroups = 32;
+__global__ void k_gw_reduce1(const float* __restrict__ part, int nparts, int h,
+                             float* __restrict__ part2) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= h) return;
+    const int g = blockIdx.y;
+    const int p0 = (int)((int64_t)nparts * g / kGroups), p1 = (int)((int64_t)nparts * (g + 1) / kGroups);
+    float s = 0.f;
+    for (int p = p0; p < p1; ++p) s += part[(int64_t)p * h + j];
+    part2[(int64_t)g * h + j] = s;
+}
+__global__ void k_gw_reduce2(const float* __restrict__ part2, int h, int accumulate,
+                             float* __restrict__ gw) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= h) return;
     float s = 0.f;
-    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * h + j];
+#pragma unroll 8
+    for (int g = 0; g < kGroups; ++g) s += part2[(int64_t)g * h + j];
     gw[j] = accumulate ? gw[j] + s : s;
 }
 
 }  // namespace
 
 size_t rmsnorm_train_ws_bytes(int64_t n, int64_t h) {
-    return (size_t)((n + kWarps - 1) / kWarps) * (size_t)h * sizeof(float);
+    return ((size_t)((n + kWarps - 1) / kWarps) + kGroups) * (size_t)h * sizeof(float);
 }
 
 extern "C" int ee_rmsnorm_fwd(const void* x, int64_t n, int64_t h, const float* w, float eps,
@@ -175,7 +189,11 @@ extern "C" int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rm
         int rc;
         if ((rc = ee_check_launch("rmsnorm_bwd"))) return rc;
     }
-    k_gw_reduce<<<(unsigned)((h + 255) / 256), 256, 0, s>>>((const float*)ws, nparts, (int)h,
-                                                           accumulate_gw, gw);
-    return ee_check_launch("rmsnorm_gw_reduce");
+    float* part2 = (float*)ws + (size_t)nparts * h;
+    k_gw_reduce1<<<dim3((unsigned)((h + 255) / 256), kGroups), 256, 0, s>>>((const float*)ws, nparts,
+                                                                           (int)h, part2);
+    int rc;
+    if ((rc = ee_check_launch("rmsnorm_gw_reduce1"))) return rc;
+    k_gw_reduce2<<<(unsigned)((h + 255) / 256), 256, 0, s>>>(part2, (int)h, accumulate_gw, gw);
+    return ee_check_launch("rmsnorm_gw_reduce2");
 }

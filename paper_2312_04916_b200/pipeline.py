@@ -150,11 +150,14 @@ class TrainStepReport:
 
 
 def _grad_norm(grads):
+    """L2 norm over a stage's gradient tensors: one fused multi-tensor norm
+    launch and a single host read (eepipe/pipeline.py:626-631)."""
     torch = _torch()
-    tot = 0.0
-    for g in grads.values():
-        tot += float(torch.linalg.vector_norm(g.detach().double()) ** 2)
-    return tot ** 0.5
+    ts = [g.detach() for g in grads.values()]
+    if not ts:
+        return 0.0
+    norms = torch._foreach_norm([t.float() if t.dtype != torch.float32 else t for t in ts])
+    return float(torch.linalg.vector_norm(torch.stack(norms).double()))
 
 
 class TaggedChannel:
