@@ -206,6 +206,76 @@ int ee_decode_layers(const ee_decoder_t* dec, const ee_layer_t* layers, int32_t 
                      int64_t n_rows, const int32_t* m_active, const int32_t* pos, int32_t max_pos,
                      void* stream);
 
+/* ---- the KV-recomputation decode loop, natively ------------------------ */
+
+/* One exit head as the decode loop sees it (heads sorted by (tap, is_final)). */
+typedef struct {
+    int32_t tap;            /* layer index 0..L the head reads */
+    int32_t is_final;
+    int32_t kind;           /* 0 minimalistic, 1 norm+embed, 2 mlp+embed */
+    const float* norm;      /* nullable: RMSNorm weight before the projection */
+    const float* pre_norm;  /* mlp+embed: RMSNorm weight of the MLP prelude */
+    const void* w1t;        /* mlp+embed: (4h, h) */
+    const void* w2t;        /* mlp+embed: (h, 4h) */
+    const void* W;          /* (V, h) output matrix in the `wcode` layout */
+    int64_t V;
+} ee_head_t;
+
+/* The HBM-resident state of one KV-recomputation engine. */
+typedef struct {
+    const ee_decoder_t* dec;  /* residual rows + scratch (max_rows >= prompt, max_deferred + 1) */
+    const ee_layer_t* layers; /* n_layers entries, layer l at index l - 1 */
+    int32_t n_layers;
+    const ee_head_t* heads;
+    int32_t n_heads;
+    int dcode;                /* activation dtype (EE_F32 / EE_BF16) */
+    int wcode;                /* head weight layout (EE_F32 / EE_BF16 / EE_BF16_TILED) */
+    float eps;
+    const void* tok_emb;      /* (V, h) dcode */
+    const void* pos_emb;      /* (s_max, h) dcode */
+    int32_t* ctrl;            /* device control block (ctrl_cap int32) */
+    int32_t* ctrl_host;       /* PINNED host staging, 2 * ctrl_cap int32 */
+    int64_t ctrl_cap;
+    void* head_ws;            /* ee_workspace_bytes(EE_OP_EXIT_HEAD, 16, h, V_max, ...) */
+    size_t head_ws_bytes;
+    void* head_x;             /* mlp+embed scratch: (16, h) float32 */
+    void* head_xn;            /* (16, h) dcode */
+    void* head_mid;           /* (16, 4h) dcode */
+    uint8_t* res;             /* device result slots: max_slots x res_stride bytes */
+    uint8_t* res_host;        /* PINNED host copy of the result slots */
+    int32_t res_stride, max_slots;
+    int32_t off_tok, off_conf, off_fire, off_bad;  /* field offsets inside a slot */
+    void* stream;
+} ee_engine_t;
+
+typedef struct {
+    const ee_engine_t* engine;
+    /* in */
+    const int32_t* prompt;    /* host, prompt_len ids (validated by the caller) */
+    int32_t prompt_len, max_new, max_deferred, s_max, head_max_rows;
+    float threshold;
+    int32_t n_heads;          /* == engine->n_heads (conf row width) */
+    /* out (host arrays owned by the caller) */
+    int32_t* tokens;          /* [max_new] */
+    int32_t* exit_layers;     /* [max_new] */
+    int32_t* pass_depths;     /* [max_new] depth of the pass that decided each token */
+    double* latency_s;        /* [max_new] host seconds between decisions */
+    float* conf;              /* [s_max][n_heads] confidences (caller-initialised NaN) */
+    uint8_t* kv_mask;         /* nullable [n_layers][s_max] final KV fill mask */
+    int32_t n_generated, flushed;
+    double total_s;
+    int64_t launches, h2d_bytes, d2h_bytes;
+} ee_generate_args_t;
+
+/* `generate_kv_recompute` (eepipe/inference.py:256-381) for one prompt in a
+ * single call: prefill, the per-token batched back-fill passes with the
+ * early-exit decisions, the final flush pass and the KV completeness check.
+ * Synchronises `stream` at exit taps / pass ends (the greedy decision is
+ * data-dependent) and on return.  Errors: EE_ECONFIG (threshold, prompt,
+ * max_deferred, KV discipline), EE_ETOKEN (context overflow),
+ * EE_ENONFINITE (non-finite exit logits). */
+int ee_generate_kv_recompute(ee_generate_args_t* args);
+
 /* ---- training exit head (fused CE) ---------------------------------- */
 
 /* Weighted cross-entropy of one exit head and its gradients on tcgen05

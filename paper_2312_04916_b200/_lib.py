@@ -45,6 +45,34 @@ class EeDecoder(ctypes.Structure):
                 ("pf_ws_bytes", c_size_t)]
 
 
+class EeHead(ctypes.Structure):
+    _fields_ = [("tap", c_int32), ("is_final", c_int32), ("kind", c_int32), ("norm", c_void_p),
+                ("pre_norm", c_void_p), ("w1t", c_void_p), ("w2t", c_void_p), ("W", c_void_p),
+                ("V", c_int64)]
+
+
+class EeEngine(ctypes.Structure):
+    _fields_ = [("dec", c_void_p), ("layers", c_void_p), ("n_layers", c_int32),
+                ("heads", c_void_p), ("n_heads", c_int32), ("dcode", c_int), ("wcode", c_int),
+                ("eps", c_float), ("tok_emb", c_void_p), ("pos_emb", c_void_p),
+                ("ctrl", c_void_p), ("ctrl_host", c_void_p), ("ctrl_cap", c_int64),
+                ("head_ws", c_void_p), ("head_ws_bytes", c_size_t), ("head_x", c_void_p),
+                ("head_xn", c_void_p), ("head_mid", c_void_p), ("res", c_void_p),
+                ("res_host", c_void_p), ("res_stride", c_int32), ("max_slots", c_int32),
+                ("off_tok", c_int32), ("off_conf", c_int32), ("off_fire", c_int32),
+                ("off_bad", c_int32), ("stream", c_void_p)]
+
+
+class EeGenerateArgs(ctypes.Structure):
+    _fields_ = [("engine", c_void_p), ("prompt", c_void_p), ("prompt_len", c_int32),
+                ("max_new", c_int32), ("max_deferred", c_int32), ("s_max", c_int32),
+                ("head_max_rows", c_int32), ("threshold", c_float), ("n_heads", c_int32),
+                ("tokens", c_void_p), ("exit_layers", c_void_p), ("pass_depths", c_void_p),
+                ("latency_s", c_void_p), ("conf", c_void_p), ("kv_mask", c_void_p),
+                ("n_generated", c_int32), ("flushed", c_int32), ("total_s", ctypes.c_double),
+                ("launches", c_int64), ("h2d_bytes", c_int64), ("d2h_bytes", c_int64)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/ee.h
 SIGNATURES = {
     "ee_last_error": (ctypes.c_char_p, []),
@@ -59,6 +87,7 @@ SIGNATURES = {
     "ee_embed_stats": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int,
                                c_void_p, c_void_p, c_void_p, c_void_p]),
     "ee_copy_h2d": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ee_generate_kv_recompute": (c_int, [c_void_p]),
     "ee_rmsnorm_rows": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_float,
                                 c_void_p, c_int, c_void_p]),
     "ee_gemv": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_int, c_int, c_void_p,

@@ -401,6 +401,7 @@ class Engine:
             self.ctrl_cap = 4 * rows + 64 * _HEAD_MAX_ROWS + 64
             self.ctrl = torch.zeros(self.ctrl_cap, dtype=torch.int32, device=self.device)
             self.ring = _PinnedRing(self.ctrl_cap)
+            self.ctrl_host = torch.zeros(2 * self.ctrl_cap, dtype=torch.int32).pin_memory()
             self.tokbuf = torch.zeros(2 * rows, dtype=torch.int32, device=self.device)
             if self.max_rows:
                 old = self._x_old
@@ -497,6 +498,33 @@ class Engine:
              self._res_ptr(slot, "fire"), self._res_ptr(slot, "bad"), ptr(logits_dbg),
              ptr(self.head_ws), self.head_ws.numel(), s)
 
+    def native_engine(self):
+        """The ee_engine_t view of this engine (rebuilt per call: scratch may
+        have grown)."""
+        lib_heads = getattr(self, "_heads_c", None)
+        if lib_heads is None:
+            kinds = {"minimalistic": 0, "norm+embed": 1, "mlp+embed": 2}
+            arr = (_lib.EeHead * len(self.heads))()
+            for i, e in enumerate(self.heads):
+                hd = e.desc
+                arr[i] = _lib.EeHead(hd.layer_index, int(hd.is_final), kinds[hd.kind],
+                                     e.norm.data_ptr() if e.norm is not None else None,
+                                     e.pre_norm.data_ptr() if e.pre_norm is not None else None,
+                                     e.w1t.data_ptr() if e.w1t is not None else None,
+                                     e.w2t.data_ptr() if e.w2t is not None else None,
+                                     e.W.data_ptr(), e.V)
+            self._heads_c = lib_heads = arr
+        f = _RES_DTYPE.fields
+        return _lib.EeEngine(
+            ctypes.addressof(self.dec), ctypes.addressof(self.layers_c), len(self.layer_indices),
+            ctypes.addressof(lib_heads), len(self.heads), self.dcode, self.wcode, NORM_EPS,
+            self.tok_emb.data_ptr(), self.pos_emb.data_ptr(), self.ctrl.data_ptr(),
+            self.ctrl_host.data_ptr(), self.ctrl_cap, self.head_ws.data_ptr(),
+            self.head_ws.numel(), self.head_x.data_ptr(), self.head_xn.data_ptr(),
+            self.head_mid.data_ptr(), self.res.data_ptr(), self.h_res_t.data_ptr(),
+            _RES_DTYPE.itemsize, self.max_slots, f["tok"][1], f["conf"][1], f["fire"][1],
+            f["bad"][1], self.stream.cuda_stream)
+
     def _res_ptr(self, slot, field):
         return ctypes.c_void_p(self.res.data_ptr() + slot * _RES_DTYPE.itemsize +
                                _RES_DTYPE.fields[field][1])
@@ -548,125 +576,6 @@ def _engine_for(owner, params, heads, cfg, layer_indices, has_embedding, dtype, 
 # ---------------------------------------------------------------------------
 
 
-class _PassRunner:
-    """Executes one `run_pass` of the reference on the engine."""
-
-    def __init__(self, eng: Engine, threshold, conf_log):
-        self.e = eng
-        self.thr = threshold
-        self.conf_log = conf_log
-        self.L = eng.cfg.num_layers
-        taps = {}
-        for hi, e in enumerate(eng.heads):
-            taps.setdefault(e.desc.layer_index, []).append(hi)
-        self.taps = taps  # tap -> head indices in (tap, is_final) order
-
-    def run(self, n, pos, entry, decide_row, forced, embed=None):
-        """Rows [0, n) of engine.x with positions/entries ordered by entry
-        descending.  ``embed = (token, position)`` first embeds the new token
-        into row n-1 (its id travels with the control block: one upload per
-        pass).  Returns (decision (token, exit_layer) | None, depth)."""
-        e, L = self.e, self.L
-        # control block: positions, then per-tap gather lists, then the new token
-        ctrl = list(pos)
-        lists = {}
-        for tap in sorted(self.taps):
-            rows = [r for r in range(n)
-                    if (tap > entry[r] or (tap == 0 and entry[r] == 0))
-                    and (r == decide_row or entry[r] > 0)]
-            if rows:
-                lists[tap] = (len(ctrl), rows)
-                ctrl.extend(rows)
-        if embed is not None:
-            emb_off = len(ctrl)
-            ctrl.extend(embed)
-        e.upload_ctrl(ctrl)
-        if embed is not None:
-            e.embed_rows([embed[0]], [embed[1]], n - 1, ctrl_off=emb_off)
-        max_pos = max(pos)
-        slots = []  # (slot, head idx, rows) in evaluation order
-        decision = None
-        checked = 0  # slots whose results have been fetched
-
-        def eval_tap(tap):
-            if tap not in lists:
-                return False
-            off, rows = lists[tap]
-            gates = False
-            for hi in self.taps[tap]:
-                for c0 in range(0, len(rows), _HEAD_MAX_ROWS):
-                    chunk = rows[c0:c0 + _HEAD_MAX_ROWS]
-                    slot = len(slots)
-                    if slot >= e.max_slots:
-                        raise ConfigError("too many head evaluations in one pass")
-                    e.eval_head(e.heads[hi], e.ctrl_ptr(off + c0), len(chunk), self.thr, slot)
-                    slots.append((slot, hi, chunk))
-                    gates |= decide_row in chunk
-            return gates
-
-        def decide_from(upto):
-            nonlocal decision, checked
-            e.fetch_results(upto)
-            for slot, hi, chunk in slots[checked:upto]:
-                hd = e.heads[hi].desc
-                for j, r in enumerate(chunk):
-                    if r == decide_row and decision is None:
-                        tok = int(e.h_tok[slot, j])
-                        if hd.is_final:
-                            decision = (tok, L)
-                        elif bool(e.h_fire[slot, j]):
-                            decision = (tok, hd.layer_index)
-            checked = upto
-
-        def stop_here(tap):
-            return decision is not None and not forced and decision[1] == tap and tap < L
-
-        gates = eval_tap(0)
-        if gates and not forced and (self.thr < 1.0 or L == 0):
-            decide_from(len(slots))
-            if decision is not None and decision[1] == 0:
-                self._log(slots, pos)
-                return decision, 0
-        stops = sorted(t for t in self.taps if t >= 1) or [L]
-        if stops[-1] != L:
-            stops.append(L)
-        la = 1
-        depth = L
-        for tap in stops:
-            # layers la..tap, grouped into runs with a constant active suffix
-            l = la
-            while l <= tap:
-                m_act = sum(1 for r in range(n) if entry[r] < l)
-                l2 = l
-                while l2 + 1 <= tap and sum(1 for r in range(n) if entry[r] < l2 + 1) == m_act:
-                    l2 += 1
-                if m_act:
-                    e.run_layers(l - 1, l2, n, [m_act] * (l2 - l + 1), max_pos, 0)
-                    act_pos = pos[n - m_act:]
-                    e.kv.mark_written(l - 1, l2, act_pos, max(act_pos))
-                l = l2 + 1
-            la = tap + 1
-            gates = eval_tap(tap)
-            # an early exit can only fire below threshold 1.0: at 1.0 the
-            # pass never stops early, so do not synchronise before the end
-            if gates and not forced and decision is None and (self.thr < 1.0 or tap == L):
-                decide_from(len(slots))
-                if stop_here(tap):
-                    depth = tap
-                    break
-        if checked < len(slots):
-            decide_from(len(slots))
-        self._log(slots, pos)
-        return decision, depth
-
-    def _log(self, slots, pos):
-        e = self.e
-        for slot, hi, chunk in slots:
-            key = e.heads[hi].desc.key
-            for j, r in enumerate(chunk):
-                self.conf_log.setdefault(pos[r], {})[key] = float(e.h_conf[slot, j])
-
-
 def generate_kv_recompute(model: EarlyExitModel, prompt, threshold, max_new_tokens,
                           max_deferred=4, *, dtype=None, device=None) -> GenerationTrace:
     """Incremental decoding that batches deferred early-exit tokens into the
@@ -691,66 +600,52 @@ def generate_kv_recompute(model: EarlyExitModel, prompt, threshold, max_new_toke
 
 
 def _kv_recompute(eng, model, prompt, threshold, max_new_tokens, max_deferred):
+    """One native call runs the whole decode loop (`ee_generate_kv_recompute`,
+    csrc/recompute.cu: prefill, per-token batched back-fill passes with the
+    exit decisions, flush, KV completeness); this wrapper validates, sizes
+    the scratch and turns the outputs into a `GenerationTrace`."""
     cfg = model.config
     L = cfg.num_layers
-    eng.kv.reset()
-    trace = GenerationTrace(prompt, threshold, "recompute")
-    conf_log: dict = {}
-    runner = _PassRunner(eng, threshold, conf_log)
-    units = full_pass_units(cfg, len(model.heads))
-    pass_depths = []
-    t_start = time.perf_counter()
-    t_last = t_start
-
-    # Prefill: every prompt row at full depth; its last row decides token 1.
+    tok = np.asarray(prompt, dtype=np.int64)
+    if tok.min() < 0 or tok.max() >= cfg.vocab_size:
+        raise TokenError("token id out of vocabulary range")
     t0 = len(prompt)
+    eng.kv.reset()
     eng._grow(max(t0, max_deferred + 1))
-    eng.embed_rows(prompt, range(t0), 0)
-    decision, _ = runner.run(t0, list(range(t0)), [0] * t0, t0 - 1, True)
-    pass_depths.append(L)
-
-    deferred: list[DeferredToken] = []  # rows 0..len-1 of eng.x, entry descending
-    position = t0 - 1
-    for i in range(max_new_tokens):
-        token, exit_layer = decision
-        trace.tokens.append(token)
-        trace.exit_layers.append(exit_layer)
-        now = time.perf_counter()
-        trace.measured_latencies.append(now - t_last)
-        t_last = now
-        if i == max_new_tokens - 1:
-            break
-        position += 1
-        forced = len(deferred) >= max_deferred
-        n = len(deferred) + 1
-        eng._grow(n)
-        pos = [d.position for d in deferred] + [position]
-        ent = [d.exit_layer for d in deferred] + [0]
-        decision, depth = runner.run(n, pos, ent, n - 1, forced, embed=(token, position))
-        pass_depths.append(depth)
-        if depth < L:
-            deferred = [DeferredToken(d.position, max(d.exit_layer, depth), r)
-                        for r, d in enumerate(deferred)]
-            deferred.append(DeferredToken(position, depth, n - 1))
-        else:
-            deferred = []
-        if len(deferred) > max_deferred:
-            raise RuntimeError("deferred list overflow")  # internal bug guard
-
-    flush_cost = 0.0
-    if deferred:  # complete the remaining KV entries and deep-exit confidences
-        runner.run(len(deferred), [d.position for d in deferred],
-                   [d.exit_layer for d in deferred], None, True)
-        flush_cost = units
-    eng.stream.synchronize()
-    trace.measured_total = time.perf_counter() - t_start
-
-    gen = len(trace.tokens)
-    if gen and not eng.kv.complete(t0 + gen - 1):
-        raise ConfigError("KV fill mask incomplete after generation")
-    trace.confidences = [conf_log.get(t0 - 1 + i, {}) for i in range(gen)]
-    trace.latencies = [units * d / L for d in pass_depths[:gen]]
-    trace.total_latency = sum(trace.latencies) + flush_cost
+    n_heads = len(eng.heads)
+    prompt32 = np.ascontiguousarray(tok, dtype=np.int32)
+    out_tok = np.zeros(max_new_tokens, dtype=np.int32)
+    out_exit = np.zeros(max_new_tokens, dtype=np.int32)
+    out_depth = np.zeros(max_new_tokens, dtype=np.int32)
+    out_lat = np.zeros(max_new_tokens, dtype=np.float64)
+    conf = np.full((cfg.max_seq_len, n_heads), np.nan, dtype=np.float32)
+    kv_mask = np.zeros((L, cfg.max_seq_len), dtype=np.uint8)
+    engine = eng.native_engine()
+    args = _lib.EeGenerateArgs(
+        ctypes.addressof(engine), prompt32.ctypes.data, t0, max_new_tokens, max_deferred,
+        cfg.max_seq_len, _HEAD_MAX_ROWS, float(threshold), n_heads, out_tok.ctypes.data,
+        out_exit.ctypes.data, out_depth.ctypes.data, out_lat.ctypes.data, conf.ctypes.data,
+        kv_mask.ctypes.data, 0, 0, 0.0, 0, 0, 0)
+    call("ee_generate_kv_recompute", ctypes.byref(args))
+    eng.launches += args.launches
+    eng.h2d_bytes += args.h2d_bytes + 4 * t0
+    eng.d2h_bytes += args.d2h_bytes
+    eng.kv.mask[:] = kv_mask.astype(bool)
+    gen = args.n_generated
+    units = full_pass_units(cfg, len(model.heads))
+    trace = GenerationTrace(prompt, threshold, "recompute")
+    trace.tokens = [int(t) for t in out_tok[:gen]]
+    trace.exit_layers = [int(e) for e in out_exit[:gen]]
+    trace.measured_latencies = [float(v) for v in out_lat[:gen]]
+    trace.measured_total = float(args.total_s)
+    keys = [e.desc.key for e in eng.heads]
+    trace.confidences = []
+    for i in range(gen):
+        row = conf[t0 - 1 + i]
+        trace.confidences.append({keys[k]: float(row[k]) for k in range(n_heads)
+                                  if not np.isnan(row[k])})
+    trace.latencies = [units * int(d) / L for d in out_depth[:gen]]
+    trace.total_latency = sum(trace.latencies) + (units if args.flushed else 0.0)
     trace.baseline_latency = units * gen
     return trace
 
@@ -987,19 +882,16 @@ def greedy_reference(model: EarlyExitModel, prompt, max_new_tokens, *, dtype=Non
     final = [hd for hd in model.heads if hd.is_final]
     L = cfg.num_layers
     eng = _engine_for(model, model.params, final, cfg, range(1, L + 1), True, dtype, device)
-    runner = _PassRunner(eng, 1.0, {})
     toks = list(prompt)
     out = []
     torch = _torch()
     with torch.cuda.device(eng.device), torch.cuda.stream(eng.stream):
         for _ in range(max_new_tokens):
-            eng.kv.reset()
-            n = len(toks)
-            eng._grow(n)
-            eng.embed_rows(toks, range(n), 0)
-            decision, _ = runner.run(n, list(range(n)), [0] * n, n - 1, True)
-            out.append(decision[0])
-            toks.append(decision[0])
+            # a fresh cache and one forced full-prefix pass per token: the
+            # prefill of a one-token generation
+            tr = _kv_recompute(eng, model, toks, 1.0, 1, 1)
+            out.append(tr.tokens[0])
+            toks.append(tr.tokens[0])
     return out
 
 
