@@ -57,3 +57,30 @@ def test_sm100a_cubin_present():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", path],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of the ABI structs (`_lib.Ee*`) have the C layout:
+    every field offset and the total size, checked against offsetof() from a
+    tiny C program compiled against include/ee.h."""
+    import subprocess
+    structs = {"ee_layer_t": _lib.EeLayer, "ee_decoder_t": _lib.EeDecoder,
+               "ee_head_t": _lib.EeHead, "ee_engine_t": _lib.EeEngine,
+               "ee_generate_args_t": _lib.EeGenerateArgs}
+    lines = ['#include <stdio.h>', '#include <stddef.h>',
+             f'#include "{os.path.join(ROOT, "include", "ee.h")}"', 'int main(void) {']
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
