@@ -88,10 +88,15 @@ def weight_at_step(ws: WeightSchedule, step: int):
 
 @dataclass
 class IterationOptions:
+    """eepipe/pipeline.py:164-172, plus ``hoist_exit_heads``: form a stage's
+    exit losses before receiving its backward gradient (the paper's §4.2.2
+    Remark; gradients are identical either way)."""
+
     microbatch_size: int
     defer_exit_forward: bool = True
     weight_schedule: WeightSchedule | None = None
     step: int = 0
+    hoist_exit_heads: bool = True
 
 
 @dataclass
@@ -233,6 +238,9 @@ class DistChannel:
         return type("Msg", (), {"mb": mb, "data": data})
 
 
+_UNSET = object()
+
+
 class StageCompute:
     """Product stage compute: the stage's layers with torch autograd on its
     device and the fused tcgen05 exit heads; exit losses are formed in the
@@ -286,10 +294,14 @@ class StageCompute:
             total = term if total is None else total + term
         return total
 
-    def backward(self, state, g):
+    def backward(self, state, g, loss=_UNSET):
+        """``loss``: the stage's local exit loss when the worker already
+        formed it (hoisted ahead of the gradient receive); otherwise it is
+        formed here (deferred exit forward, eepipe/pipeline.py:393-412)."""
         torch = _torch()
         x_in, x_out, _, _ = state
-        loss = self.local_loss(state)  # deferred exit forward, eepipe/pipeline.py:393-412
+        if loss is _UNSET:
+            loss = self.local_loss(state)
         if g is None:
             if loss is None:
                 raise ConfigError("a stage must have a local loss or a received gradient")
@@ -312,11 +324,12 @@ class StageWorker:
     """Executes one stage's 1F1B action list (eepipe/pipeline.py:301-527)."""
 
     def __init__(self, index, num_stages, num_mb, compute, data, fwd_in, fwd_out, bwd_in,
-                 bwd_out):
+                 bwd_out, hoist_exits=True):
         self.index, self.P, self.M = index, num_stages, num_mb
         self.compute = compute
         self.data = data  # mb -> (tokens, targets)
         self.fwd_in, self.fwd_out, self.bwd_in, self.bwd_out = fwd_in, fwd_out, bwd_in, bwd_out
+        self.hoist_exits = hoist_exits and hasattr(compute, "local_loss")
         self.state = {}
         self.event_log = []
         self.wall = {"F": 0.0, "B": 0.0}
@@ -352,8 +365,18 @@ class StageWorker:
 
     def _backward(self, mb):
         st = self.state.pop(mb)
-        g = None if self.bwd_in is None else self.bwd_in.recv(mb).data
-        g_in = self.compute.backward(st, g)
+        if self.hoist_exits and self.bwd_in is not None:
+            # the paper's §4.2.2 Remark (modelled only by the reference,
+            # eepipe/schedule.py:491-502): form the stage's exit losses — with
+            # the fused head that is the whole exit forward AND backward —
+            # before waiting for the downstream gradient, so the exit work
+            # overlaps the pipeline's communication instead of following it
+            loss = self.compute.local_loss(st)
+            g = self.bwd_in.recv(mb).data
+            g_in = self.compute.backward(st, g, loss)
+        else:
+            g = None if self.bwd_in is None else self.bwd_in.recv(mb).data
+            g_in = self.compute.backward(st, g)
         self.in_flight -= 1
         if self.bwd_out is not None:
             if g_in is None:
@@ -443,7 +466,8 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
                 stage_computes.append(comp)
         workers.append(StageWorker(s, P, M, comp, data,
                                    fwd[s - 2] if s > 1 else None, fwd[s - 1] if s < P else None,
-                                   bwd[s - 1] if s < P else None, bwd[s - 2] if s > 1 else None))
+                                   bwd[s - 1] if s < P else None, bwd[s - 2] if s > 1 else None,
+                                   options.hoist_exit_heads))
     torch = _torch()
 
     def target(w):
@@ -532,7 +556,8 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
     fwd_out = DistChannel(rank + 1, shape, act_dtype, dev) if s < P else None
     bwd_in = DistChannel(rank + 1, shape, act_dtype, dev) if s < P else None
     bwd_out = DistChannel(rank - 1, shape, act_dtype, dev) if s > 1 else None
-    w = StageWorker(s, P, M, comp, data, fwd_in, fwd_out, bwd_in, bwd_out)
+    w = StageWorker(s, P, M, comp, data, fwd_in, fwd_out, bwd_in, bwd_out,
+                    options.hoist_exit_heads)
     w.run()
     for ch in (fwd_out, bwd_out):
         if ch is not None:

@@ -125,3 +125,20 @@ def test_determinism_semantic_state():  # test_pipeline.py:135-141
     _, r1 = run_iteration_1f1b(part, batch, IterationOptions(2), model=model)
     _, r2 = run_iteration_1f1b(part, batch, IterationOptions(2), model=model)
     assert r1.semantic_state() == r2.semantic_state()
+
+
+def test_hoisted_exit_heads_identical_gradients():
+    """The §4.2.2 Remark (exit losses formed before the downstream gradient
+    arrives, IterationOptions.hoist_exit_heads) changes only the timing: the
+    gradients are bitwise those of the plain order."""
+    from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
+    model, batch, _ = make_setup(
+        4, (ExitSpec(1, loss_weight=0.25), ExitSpec(2, loss_weight=0.5)), False, seed=8)
+    part = partition(model, 4)
+    g_h, r_h = run_iteration_1f1b(part, batch, IterationOptions(2, hoist_exit_heads=True),
+                                  model=model)
+    g_p, r_p = run_iteration_1f1b(part, batch, IterationOptions(2, hoist_exit_heads=False),
+                                  model=model)
+    for name in g_h:
+        assert bool((g_h[name] == g_p[name]).all()), name
+    assert r_h.per_exit_losses == r_p.per_exit_losses
