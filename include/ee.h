@@ -295,6 +295,15 @@ int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64
                        const int64_t* targets, float weight, float* loss, float* dx, float* dw_acc,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* dW (in x out, float32) += X^T dY for a bf16 linear layer y = x W, X (T x in)
+ * and dY (T x out) bf16 row-major, on the CTA-pair tcgen05 GEMM (operands read
+ * MN-major in place).  The training backbone's gradient-accumulation fusion:
+ * the weight gradient of every microbatch lands in the float32 accumulator
+ * without a bf16 gradient or an accumulation pass (the matmul backward of
+ * `eepipe/autodiff.py:170-177` for the layer weights). */
+int ee_wgrad_accum(const void* X, const void* dY, int64_t T, int64_t in, int64_t out, float* dW,
+                   void* stream);
+
 /* ---- training RMSNorm (bf16 activations, float32 statistics) ---------- */
 
 /* y = x * (mean(x^2) + eps)^-1/2 * w row-wise; x, y (n, h) bf16, w (h) float32,

@@ -107,6 +107,8 @@ SIGNATURES = {
     "ee_exit_head_train": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                                    c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                    c_void_p]),
+    "ee_wgrad_accum": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
+                               c_void_p]),
     "ee_rmsnorm_fwd": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_float, c_void_p, c_void_p,
                                c_void_p]),
     "ee_rmsnorm_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p,

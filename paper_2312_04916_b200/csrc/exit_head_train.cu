@@ -415,3 +415,19 @@ extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const voi
     return tc::launch_tc_gemm2<kBN, true, true, true>(w.g, x, (int)V, (int)h, (int)n,
                                                      EpiF32<true>{dw_acc, (int)h}, s);
 }
+
+// Weight gradient of a bf16 linear layer accumulated straight into a float32
+// buffer: dW (in x out) += X^T dY with X (T x in) and dY (T x out) bf16
+// row-major (both read MN-major by the UMMA descriptors; no transposes) —
+// the backbone's "gradient-accumulation fusion": no bf16 weight gradient, no
+// separate accumulation pass.  in, out multiples of 8; any T.
+extern "C" int ee_wgrad_accum(const void* X, const void* dY, int64_t T, int64_t in, int64_t out,
+                              float* dW, void* stream) {
+    EE_REQUIRE(T > 0 && in > 0 && out > 0 && in % 8 == 0 && out % 8 == 0, EE_ESHAPE,
+               "wgrad_accum: in and out must be positive multiples of 8 (T=%lld in=%lld out=%lld)",
+               (long long)T, (long long)in, (long long)out);
+    EE_REQUIRE(T < (1ll << 31) && in < (1ll << 31) && out < (1ll << 31), EE_ESHAPE,
+               "wgrad_accum: too large");
+    return tc::launch_tc_gemm2<kBN, true, true, true>(X, dY, (int)in, (int)out, (int)T,
+                                                     EpiF32<true>{dW, (int)out}, as_stream(stream));
+}

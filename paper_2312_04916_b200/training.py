@@ -134,6 +134,59 @@ class ExitHeadCE:
 # ---------------------------------------------------------------------------
 
 
+class _ParamView(dict):
+    """Compute parameters plus their float32 gradient accumulators (mixed
+    mode): the backbone's linear layers send their weight gradients straight
+    into ``main_grads`` (`ee_wgrad_accum`)."""
+
+    def __init__(self, params, main_grads):
+        super().__init__(params)
+        self.main_grads = main_grads
+
+
+class _LinearFn:
+    """y = x @ W (bf16) whose backward computes dX with torch and accumulates
+    dW = X^T dY into the float32 main gradient with the CTA-pair tcgen05 GEMM
+    (no bf16 weight gradient; returns None for W)."""
+
+    _fn = None
+
+    @classmethod
+    def get(cls):
+        if cls._fn is None:
+            torch = _torch()
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, x, w, acc):
+                    ctx.save_for_backward(x, w)
+                    ctx.acc = acc
+                    return x @ w
+
+                @staticmethod
+                def backward(ctx, gy):
+                    x, w = ctx.saved_tensors
+                    gx = gy @ w.t()
+                    x2 = x.reshape(-1, x.shape[-1]).contiguous()
+                    g2 = gy.reshape(-1, gy.shape[-1]).to(x2.dtype).contiguous()
+                    call("ee_wgrad_accum", ptr(x2), ptr(g2), x2.shape[0], x2.shape[1], g2.shape[1],
+                         ptr(ctx.acc), stream_ptr())
+                    return gx, None, None
+
+            cls._fn = _F
+        return cls._fn
+
+
+def _matmul(params, name, x):
+    """x @ params[name]; in mixed mode through the fused-accumulation linear."""
+    acc = getattr(params, "main_grads", None)
+    w = params[name]
+    if acc is not None and name in acc and x.dtype == w.dtype and w.shape[0] % 8 == 0 \
+            and w.shape[1] % 8 == 0:
+        return _LinearFn.get().apply(x, w, acc[name])
+    return x @ w
+
+
 class TrainModel:
     """Device-resident trainable copy of an `EarlyExitModel`: parameters as
     torch tensors (requires_grad) keyed by the reference names, compute dtype
@@ -181,6 +234,8 @@ class TrainModel:
                                                   dtype=self.dtype).detach().requires_grad_()
 
     def compute_params(self):
+        if self.mixed:
+            return _ParamView(self.params, self.main_grads)
         return self.params
 
     def zero_grad(self):
@@ -338,12 +393,12 @@ def run_layer(params, prefix, x, num_heads):
     B, S, h = x.shape
     dh = h // num_heads
     h1 = rmsnorm(x, params[f"{prefix}.attn_norm"])
-    q, k, v = (h1 @ params[f"{prefix}.{w}"] for w in ("wq", "wk", "wv"))
+    q, k, v = (_matmul(params, f"{prefix}.{w}", h1) for w in ("wq", "wk", "wv"))
     split = lambda t: t.view(B, S, num_heads, dh).transpose(1, 2)  # noqa: E731
     a = F.scaled_dot_product_attention(split(q), split(k), split(v), is_causal=True)
-    x = x + a.transpose(1, 2).reshape(B, S, h) @ params[f"{prefix}.wo"]
+    x = x + _matmul(params, f"{prefix}.wo", a.transpose(1, 2).reshape(B, S, h))
     h2 = rmsnorm(x, params[f"{prefix}.mlp_norm"])
-    return x + F.gelu(h2 @ params[f"{prefix}.w1"]) @ params[f"{prefix}.w2"]
+    return x + _matmul(params, f"{prefix}.w2", F.gelu(_matmul(params, f"{prefix}.w1", h2)))
 
 
 def head_input(params, head, x, num_heads):
@@ -461,6 +516,7 @@ def single_device_gradients(model: TrainModel, batch, weights, microbatch_size):
         loss, per_exit = weighted_loss(model, batch[k * microbatch_size:(k + 1) * microbatch_size],
                                        weights)
         loss.backward()
+        model.accumulate_grads()  # mixed precision: fold into the float32 sums
         for i, v in enumerate(per_exit):
             sums[i] += v
     return model.grads(), {hd.key: sums[i] / num_mb for i, hd in enumerate(model.heads)}
