@@ -189,6 +189,27 @@ def cpu_slice_timing(seconds_budget=20.0):
     return per_token, tl, th, n
 
 
+def cpu_head_timing(n=256, h=2048, V=50304):
+    """The reference's training exit head on the host (oracle port of
+    `run_head` + `cross_entropy` + the matmul backward, float64, numpy `@`
+    on OpenBLAS with all host threads) on an n-row slice of the C2 shape;
+    GFLOP/s on the same 6 n h V count as the GPU number."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import ee_oracle as O
+    rng = np.random.default_rng(0)
+    x = rng.normal(size=(n, h))
+    w = rng.normal(0, 0.02, size=(V, h))
+    t = rng.integers(0, V, size=n)
+    O.exit_head_train(x[:8], w, t[:8])
+    t0 = time.perf_counter()
+    O.exit_head_train(x, w, t)
+    dt = time.perf_counter() - t0
+    return {"value": 6 * n * h * V / dt / 1e9, "unit": "GFLOP/s (6nhV)", "cores": os.cpu_count(),
+            "kind": "port", "sample": f"oracle port (float64 numpy/OpenBLAS) of the C2 exit head "
+                                      f"fwd+bwd on {n} of the 4096 rows: {dt:.2f} s"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -478,6 +499,8 @@ def main():
     if not args.no_train_head:
         head_train = bench_train_head(local, hbm_peak)
         head_train["c4_shape"] = bench_train_head(local, hbm_peak, n=2048, h=5120, tag="C4")
+    if head_train is not None and not args.no_cpu_baseline and world == 1:
+        head_train["cpu_baseline"] = cpu_head_timing()
     train_step = None
     if not args.no_train_step:
         train_step = bench_train_step(local)
