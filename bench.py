@@ -296,7 +296,11 @@ def bench_pipeline_stages(model, prompt, local, new_tokens=64):
     from paper_2312_04916_b200 import inference as I
     from paper_2312_04916_b200.model import partition
     out = {"note": "P stage workers = threads + CUDA streams on ONE B200 (1-GPU pool); "
-                   f"{new_tokens} new tokens, prompt {PROMPT_LEN}"}
+                   f"{new_tokens} new tokens, prompt {PROMPT_LEN}; every stage still runs all its "
+                   "layers per token (KV fill), so throughput is bounded by the single GPU's "
+                   "full-depth rate, and at P=8 the eight Python stage threads of one "
+                   "interpreter contend for the GIL (the multi-GPU design runs one process "
+                   "per stage: pipeline_infer.generate_pipeline_dist)"}
     for P in (2, 4, 8):
         part = partition(model, P, copy=False)
         I.generate_pipeline(part, prompt, 0.8, 4, devices=[f"cuda:{local}"])  # builds stage engines
