@@ -161,9 +161,11 @@ typedef struct {
     void* attn; /* (max_rows, h) dtype scratch */
     void* ws;   /* attention workspace (ee_workspace_bytes(EE_OP_ATTENTION, ...)) */
     size_t ws_bytes;
-    /* tiled mode, nullable: split-K partials of the multi-row (prefill)
-     * tcgen05 GEMM, >= ee_workspace_bytes(EE_OP_PREFILL, max_rows, h, ...);
-     * when null (or too small) every pass uses the GEMV */
+    /* tiled mode, nullable: split-K partials of the multi-row tcgen05 GEMM,
+     * >= ee_workspace_bytes(EE_OP_PREFILL, max_rows, h, ...).  Callers set it
+     * ONLY for a prompt-prefill pass (every prompt row, computed once in every
+     * inference mode) with > 16 rows; with it null every pass takes the
+     * row-stable GEMV, so decode rows never depend on the pass width */
     void* pf_ws;
     size_t pf_ws_bytes;
 } ee_decoder_t;
@@ -246,6 +248,8 @@ typedef struct {
     int32_t res_stride, max_slots;
     int32_t off_tok, off_conf, off_fire, off_bad;  /* field offsets inside a slot */
     void* stream;
+    void* pf_ws;              /* nullable: prefill GEMM workspace, used for the prefill pass only */
+    size_t pf_ws_bytes;
 } ee_engine_t;
 
 typedef struct {

@@ -60,7 +60,8 @@ class EeEngine(ctypes.Structure):
                 ("head_xn", c_void_p), ("head_mid", c_void_p), ("res", c_void_p),
                 ("res_host", c_void_p), ("res_stride", c_int32), ("max_slots", c_int32),
                 ("off_tok", c_int32), ("off_conf", c_int32), ("off_fire", c_int32),
-                ("off_bad", c_int32), ("stream", c_void_p)]
+                ("off_bad", c_int32), ("stream", c_void_p), ("pf_ws", c_void_p),
+                ("pf_ws_bytes", c_size_t)]
 
 
 class EeGenerateArgs(ctypes.Structure):

@@ -110,6 +110,8 @@ struct Runner {
     // one run_pass; decide_row < 0: flush pass.  embed_tok >= 0: embed the
     // new token into row n-1 first.  Returns rc; decision in (*tok, *layer),
     // *has = 0 if no decision; *depth.
+    const ee_decoder_t* dec = nullptr;  // decoder used by the current pass
+
     int pass(int n, const int32_t* pos, const int32_t* entry, int decide_row, bool forced,
              int embed_tok, int embed_pos, int* tok, int* layer, int* has, int* depth) {
         int rc;
@@ -138,7 +140,7 @@ struct Runner {
             c[len++] = embed_pos;
         }
         if ((rc = upload(c, len))) return rc;
-        const ee_decoder_t* D = E->dec;
+        const ee_decoder_t* D = dec ? dec : E->dec;
         if (embed_tok >= 0) {
             const bool tiled = D->dtype == EE_BF16_TILED;
             launches += tiled ? 2 : 1;
@@ -333,8 +335,14 @@ extern "C" int ee_generate_kv_recompute(ee_generate_args_t* A) {
     std::vector<int32_t> pos(t0), ent(t0, 0);
     for (int i = 0; i < t0; ++i) pos[i] = i;
     int tok = 0, layer = L, has = 0, depth = L;
-    if ((rc = R.pass(t0, pos.data(), ent.data(), t0 - 1, true, -1, 0, &tok, &layer, &has, &depth)))
-        return rc;
+    // the prefill pass (and only it) may take the multi-row tcgen05 GEMM
+    ee_decoder_t dec_prefill = *E->dec;
+    dec_prefill.pf_ws = E->pf_ws;
+    dec_prefill.pf_ws_bytes = E->pf_ws_bytes;
+    R.dec = &dec_prefill;
+    rc = R.pass(t0, pos.data(), ent.data(), t0 - 1, true, -1, 0, &tok, &layer, &has, &depth);
+    R.dec = nullptr;
+    if (rc) return rc;
     EE_REQUIRE(has, EE_ECUDA, "recompute: prefill produced no decision");
     A->pass_depths[0] = L;
     std::vector<int32_t> dpos, dent;  // deferred tokens: rows 0..k-1, entry descending

@@ -410,6 +410,7 @@ class Engine:
             pfb = (_lib.load().ee_workspace_bytes(_lib.EE_OP_PREFILL, rows, h, 0, 0, 0)
                    if self.tiled and rows >= 17 else 0)
             self.pf_ws = torch.empty(max(pfb, 1), dtype=torch.uint8, device=self.device)
+            self.pf_bytes = pfb  # handed to the decoder for prefill passes only
             self.dec = _lib.EeDecoder(h=h, nh=cfg.num_heads, s_max=cfg.max_seq_len,
                                       max_rows=rows, dtype=self.wcode, eps=NORM_EPS,
                                       x=self.x.data_ptr(), xb=self.xb.data_ptr(),
@@ -417,8 +418,7 @@ class Engine:
                                       xn=self.xn.data_ptr(), q=self.q.data_ptr(),
                                       attn=self.attn.data_ptr(), ws=self.attn_ws.data_ptr(),
                                       ws_bytes=wsb,
-                                      pf_ws=self.pf_ws.data_ptr() if pfb else None,
-                                      pf_ws_bytes=pfb)
+                                      pf_ws=None, pf_ws_bytes=0)
         self.max_rows = rows
         self._x_old = None
 
@@ -523,7 +523,8 @@ class Engine:
             self.head_ws.numel(), self.head_x.data_ptr(), self.head_xn.data_ptr(),
             self.head_mid.data_ptr(), self.res.data_ptr(), self.h_res_t.data_ptr(),
             _RES_DTYPE.itemsize, self.max_slots, f["tok"][1], f["conf"][1], f["fire"][1],
-            f["bad"][1], self.stream.cuda_stream)
+            f["bad"][1], self.stream.cuda_stream,
+            self.pf_ws.data_ptr() if self.pf_bytes else None, self.pf_bytes)
 
     def _res_ptr(self, slot, field):
         return ctypes.c_void_p(self.res.data_ptr() + slot * _RES_DTYPE.itemsize +
@@ -541,8 +542,11 @@ class Engine:
         if self.h_bad[:nslots].any():
             raise NonFiniteError("non-finite exit logits")
 
-    def run_layers(self, la, lb, n_rows, m_active, max_pos, pos_off):
-        """Slots [la, lb) of this engine's layers over rows [0, n_rows)."""
+    def run_layers(self, la, lb, n_rows, m_active, max_pos, pos_off, prefill=False):
+        """Slots [la, lb) of this engine's layers over rows [0, n_rows).
+        ``prefill``: the pass carries the prompt rows (computed once in every
+        mode) and may use the multi-row tcgen05 GEMM; decode passes always
+        take the row-stable GEMV."""
         n = lb - la
         if n <= 0:
             return
@@ -550,8 +554,13 @@ class Engine:
         layers = ctypes.c_void_p(ctypes.addressof(self.layers_c) +
                                  la * ctypes.sizeof(_lib.EeLayer))
         self.launches += (5 if self.tiled else 7) * sum(1 for v in m_active if v)
-        call("ee_decode_layers", ctypes.byref(self.dec), layers, n, n_rows, arr,
-             self.ctrl_ptr(pos_off), int(max_pos), stream_ptr(self.stream))
+        if prefill and self.pf_bytes:
+            self.dec.pf_ws, self.dec.pf_ws_bytes = self.pf_ws.data_ptr(), self.pf_bytes
+        try:
+            call("ee_decode_layers", ctypes.byref(self.dec), layers, n, n_rows, arr,
+                 self.ctrl_ptr(pos_off), int(max_pos), stream_ptr(self.stream))
+        finally:
+            self.dec.pf_ws, self.dec.pf_ws_bytes = None, 0
 
 
 _ENGINE_CACHE_ATTR = "_ee_engines"
@@ -745,7 +754,9 @@ class _InferStage:
                     for stop in stops:
                         if stop >= local:
                             e.upload_ctrl(list(msg.positions))
-                            e.run_layers(local - 1, stop, n, [n] * (stop - local + 1), max_pos, 0)
+                            # the prompt message (positions 0..t0-1) is the prefill
+                            e.run_layers(local - 1, stop, n, [n] * (stop - local + 1), max_pos, 0,
+                                         prefill=msg.positions[0] == 0)
                             e.kv.mark_written(local - 1, stop, list(msg.positions), max_pos)
                             self._check_heads(msg, stop, n)
                             local = stop + 1
@@ -948,7 +959,7 @@ def prefill_taps(model: EarlyExitModel, tokens, *, dtype=None, device=None):
         eng.upload_ctrl(list(range(n)))
         taps.append(eng.x[:n].cpu().numpy().copy())
         for l in range(1, L + 1):
-            eng.run_layers(l - 1, l, n, [n], n - 1, 0)
+            eng.run_layers(l - 1, l, n, [n], n - 1, 0, prefill=True)
             eng.kv.mark_written(l - 1, l, list(range(n)), n - 1)
             taps.append(eng.x[:n].cpu().numpy().copy())
     return taps

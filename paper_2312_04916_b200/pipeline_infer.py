@@ -102,7 +102,9 @@ class GpuStage:
             for stop in stops:
                 if stop >= local:
                     e.upload_ctrl(list(positions))
-                    e.run_layers(local - 1, stop, n, [n] * (stop - local + 1), max_pos, 0)
+                    # the prompt message (positions 0..t0-1) is the prefill
+                    e.run_layers(local - 1, stop, n, [n] * (stop - local + 1), max_pos, 0,
+                                 prefill=positions[0] == 0)
                     e.kv.mark_written(local - 1, stop, list(positions), max_pos)
                     check(stop)
                     local = stop + 1

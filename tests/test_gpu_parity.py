@@ -299,3 +299,24 @@ def test_tiled_bf16_modes_bitwise_equal():
             assert reco.tokens == pipe.tokens, thr
             assert reco.exit_layers == pipe.exit_layers, thr
             assert reco.confidences == pipe.confidences, thr
+
+
+def test_tiled_modes_bitwise_equal_with_many_deferred_rows():
+    """max_deferred = 20 makes recompute passes of up to 21 rows (more than the
+    16-row GEMV tile): decode passes must still take the row-stable GEMV
+    (only the prompt prefill may use the multi-row tcgen05 GEMM), so pipeline
+    (one row per message) and recompute agree bitwise; norm+embed and
+    mlp+embed heads on the tiled bf16 path."""
+    import torch
+    cfg = ModelConfig(4, 512, 4, 256, 64, exits=(ExitSpec(1, "norm+embed", 0.3),
+                                                 ExitSpec(2, "mlp+embed", 0.6)))
+    m = build_model(cfg, 13, init="device", dtype=torch.bfloat16)
+    part = partition(m, 2, copy=False)
+    prompt = [int(t) for t in np.random.default_rng(8).integers(0, 256, size=20)]
+    for thr in (0.99 / 256, 1.5 / 256):
+        reco = I.generate_kv_recompute(m, prompt, thr, 30, 20)
+        pipe = I.generate_pipeline(part, prompt, thr, 30)
+        assert reco.tokens == pipe.tokens, thr
+        assert reco.exit_layers == pipe.exit_layers, thr
+        assert reco.confidences == pipe.confidences, thr
+        assert any(e < 4 for e in reco.exit_layers)
