@@ -116,14 +116,22 @@ class ExitHeadCE:
                     loss, dx, dw = exit_head_loss_and_grads(x.detach(), W.detach(), targets,
                                                             weight, validated=validated)
                     ctx.save_for_backward(dx, dw)
+                    ctx.w_main_grad = getattr(W, "_ee_main_grad", None)
                     ctx.dtypes = (x.dtype, W.dtype)
                     return loss
 
                 @staticmethod
                 def backward(ctx, g):
                     dx, dw = ctx.saved_tensors
-                    return ((dx * g).to(ctx.dtypes[0]), (dw * g).to(ctx.dtypes[1]), None, None,
-                            None)
+                    acc = ctx.w_main_grad
+                    if acc is not None:
+                        # mixed precision: dW * g straight into the float32 sum
+                        # of W (one pass; no bf16 gradient of the 50k x h matrix)
+                        acc.view(dw.shape).addcmul_(dw, g.to(dw.dtype))
+                        gw = None
+                    else:
+                        gw = (dw * g).to(ctx.dtypes[1])
+                    return (dx * g).to(ctx.dtypes[0]), gw, None, None, None
 
             cls._fn = _F
         return cls._fn.apply(x, W, targets, float(weight), bool(validated))
@@ -227,6 +235,7 @@ class TrainModel:
                 leaf.copy_(t.to(device=self.device))
                 self.params[name] = leaf.requires_grad_()
                 self.main_grads[name] = self._flat_grad[off:off + k].view(t.shape)
+                leaf._ee_main_grad = self.main_grads[name]  # fused heads accumulate here
                 off += k
         else:
             for name in names:
