@@ -7,10 +7,12 @@
 // Decode attention is latency-bound (a few MB of K/V per layer spread over
 // heads): what matters is the number of DEPENDENT steps between the QKV GEMV
 // finishing and the Wo GEMV starting.  Organisation:
-//   * one CTA (8 warps) per (head, row, 256-position chunk); warp w owns the
-//     32-position block 8 c + w, lane j its position: q.K in registers,
-//     warp max / sum-exp by shuffles, P.V with each lane owning dh/32 output
-//     dimensions (coalesced V rows);
+//   * one CTA (8 warps) per (head, row, 256-position chunk) -- for bf16 with
+//     head_dim 128 per (head, group of <= 16 rows, chunk), the rows sharing
+//     each K/V load (k_attn_rows128); warp w owns the 32-position block
+//     8 c + w, lane j its position: q.K in registers, warp max / sum-exp by
+//     shuffles, P.V with each lane owning dh/32 output dimensions (coalesced
+//     V rows);
 //   * blocks and chunks are keyed by POSITION ONLY, and every merge runs in a
 //     fixed order (warps of a chunk in block order through shared memory,
 //     chunks in chunk order), so a row's result does not depend on how many
@@ -21,17 +23,17 @@
 //   * K/V rows that predate this pass (positions below every row of the
 //     launch) are prefetched into L2 BEFORE griddepcontrol.wait, overlapping
 //     the QKV GEMV that is still writing the new rows.
-#include "ee_common.cuh"
+#include "attn_core.cuh"
 
 namespace {
 
-constexpr int kBlk = 32;                      // positions per warp block
-constexpr int kWarpsA = 8;                    // blocks per chunk
-constexpr int kChunk = kBlk * kWarpsA;        // 256 positions per CTA
+using attn::kBlk;
+using attn::kChunk;
+using attn::kMaxChunks;
+using attn::kMaxDh;
+using attn::kRowsPerLaunch;
+using attn::kWarpsA;
 constexpr int kThreadsA = kWarpsA * 32;
-constexpr int kMaxDh = 128;
-constexpr int kRowsPerLaunch = 64;
-constexpr int kMaxChunks = 8;                 // s_max <= 2048
 
 template <typename T> __device__ __forceinline__ void load4(const T* p, float* v);
 template <> __device__ __forceinline__ void load4<bf16>(const bf16* p, float* v) {
@@ -95,7 +97,7 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
         // score of this lane's position: fixed-order dot product.  DH = 128
         // (the configs' head dim) issues the whole K row and this lane's V
         // columns of the block before using any of them: one memory round
-        // trip per warp
+        // trip per warp (same arithmetic as the generic loop)
         float sc = 0.f;
         const int nj = min(kBlk, p + 1 - j0);
         const T* vb = vc + (int64_t)j0 * h + hh * dh;
@@ -161,11 +163,11 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
             }
             const float sv = valid ? sc * scale : -INFINITY;
             mx = sv;
-#pragma unroll
+    #pragma unroll
             for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             const float e = valid ? expf(sv - mx) : 0.f;
             l = e;
-#pragma unroll
+    #pragma unroll
             for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
             // P.V: lane owns output dims [4 lane, 4 lane + 4)
             for (int j = 0; j < nj; ++j) {
@@ -201,12 +203,12 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
     float M = -INFINITY;
     for (int w = 0; w < nb; ++w) M = fmaxf(M, s_m[w]);
     float L = 0.f;
-    for (int w = 0; w < nb; ++w) L += s_l[w] * expf(s_m[w] - M);
+    for (int w = 0; w < nb; ++w) L = fmaf(s_l[w], expf(s_m[w] - M), L);
     const int64_t slot = ((int64_t)r * nh + hh) * kMaxChunks + ch;
     const int stride = dh + 2;
     for (int d = threadIdx.x; d < dh; d += kThreadsA) {
         float o = 0.f;
-        for (int w = 0; w < nb; ++w) o += s_acc[w][d] * expf(s_m[w] - M);
+        for (int w = 0; w < nb; ++w) o = fmaf(s_acc[w][d], expf(s_m[w] - M), o);
         if (nch == 1) out[(int64_t)r * h + hh * dh + d] = from_f32<T>(o / L);
         else part[slot * stride + 2 + d] = o;
     }
@@ -226,24 +228,155 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
     float MM = -INFINITY;
     for (int c = 0; c < nch; ++c) MM = fmaxf(MM, __ldcg(base + c * stride));
     float LL = 0.f;
-    for (int c = 0; c < nch; ++c) LL += __ldcg(base + c * stride + 1) * expf(__ldcg(base + c * stride) - MM);
+    for (int c = 0; c < nch; ++c)
+        LL = fmaf(__ldcg(base + c * stride + 1), expf(__ldcg(base + c * stride) - MM), LL);
     for (int d = threadIdx.x; d < dh; d += kThreadsA) {
         float o = 0.f;
         for (int c = 0; c < nch; ++c)
-            o += __ldcg(base + c * stride + 2 + d) * expf(__ldcg(base + c * stride) - MM);
+            o = fmaf(__ldcg(base + c * stride + 2 + d), expf(__ldcg(base + c * stride) - MM), o);
         out[(int64_t)r * h + hh * dh + d] = from_f32<T>(o / LL);
     }
     if (threadIdx.x == 0) ctr[r * nh + hh] = 0;  // leave the workspace re-usable
 }
 
-size_t counters_bytes(int64_t nh) { return (((size_t)kRowsPerLaunch * nh * 4) + 255) & ~(size_t)255; }
+// bf16, head_dim 128 (the configs' head dim): one CTA per (head, group of up
+// to 16 rows, 256-position chunk).  Rows of a pass share the layer's K/V
+// prefix, so each warp loads its 32-position block ONCE (block_load128, up to
+// the group's last position) and scores every row of the group from the
+// same registers (block_eval128); per-row results go through shared memory
+// and are merged exactly as in k_attn_decode, so a row's output does not
+// depend on which rows share its group.
+constexpr int kRowsCta = 16;
+constexpr int kRowsKernelMinChunks = 3;  // measured: m = 5 at ctx 320 -> 1024 crossover
+
+// dynamic shared memory: V tiles [kWarpsA][kBlk][dh] bf16, q [rows][dh] and
+// per-row block results [rows][kWarpsA][dh] float32
+__host__ __device__ constexpr size_t rows128_smem(int rows) {
+    return (size_t)kWarpsA * kBlk * kMaxDh * 2 + (size_t)rows * (kMaxDh + kWarpsA * kMaxDh) * sizeof(float);
+}
+
+__global__ void __launch_bounds__(kThreadsA)
+k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int m,
+               const bf16* __restrict__ kc, const bf16* __restrict__ vc, int nh, float scale,
+               bf16* __restrict__ out, float* __restrict__ part, int* __restrict__ ctr) {
+    extern __shared__ __align__(16) float smem_rows[];
+    __shared__ float s_m[kRowsCta][kWarpsA], s_l[kRowsCta][kWarpsA];
+    __shared__ int s_last[kRowsCta];
+    constexpr int dh = kMaxDh;
+    pdl_trigger_dev();
+    const int hh = blockIdx.x, ch = blockIdx.z;
+    const int r0 = blockIdx.y * kRowsCta;
+    const int mr = min(kRowsCta, m - r0);
+    const int h = nh * dh;
+    bf16* s_v = reinterpret_cast<bf16*>(smem_rows);                        // [kWarpsA][kBlk][dh]
+    float* s_q = smem_rows + kWarpsA * kBlk * dh / 2;                      // [mr][dh]
+    float* s_acc = s_q + mr * dh;                                          // [mr][kWarpsA][dh]
+    // host-written control data: safe before the wait
+    int pmax = -1, pmin = 1 << 30;
+    for (int i = 0; i < mr; ++i) pmax = max(pmax, pos[r0 + i]);
+    for (int i = 0; i < m; ++i) pmin = min(pmin, pos[i]);
+    if (pmax < ch * kChunk) {
+        pdl_wait_dev();
+        return;
+    }
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int j0 = ch * kChunk + warp * kBlk;
+    const int jj = j0 + lane;
+    if (jj <= pmax && jj < pmin) {  // written by an earlier pass: fetch while QKV runs
+        prefetch_l2(kc + (int64_t)jj * h + hh * dh);
+        prefetch_l2(kc + (int64_t)jj * h + hh * dh + 64);
+        prefetch_l2(vc + (int64_t)jj * h + hh * dh);
+        prefetch_l2(vc + (int64_t)jj * h + hh * dh + 64);
+    }
+    pdl_wait_dev();
+    for (int t = tid; t < mr * (dh / 4); t += kThreadsA) {
+        const int i = t / (dh / 4), c = t % (dh / 4);
+        reinterpret_cast<float4*>(s_q + i * dh)[c] =
+            reinterpret_cast<const float4*>(q + (int64_t)(r0 + i) * h + hh * dh)[c];
+    }
+    __syncthreads();
+    if (j0 <= pmax) {
+        attn::BlockRegs R;
+        bf16* sv = s_v + warp * kBlk * dh;
+        attn::block_load128(R, sv, kc, vc, h, hh * dh, j0, pmax);
+        for (int i = 0; i < mr; ++i) {
+            const int p = pos[r0 + i];
+            if (j0 > p) continue;  // warp-uniform
+            float mx, l, acc[4];
+            attn::block_eval128(R, sv, s_q + i * dh, j0, p, scale, mx, l, acc);
+            reinterpret_cast<float4*>(s_acc + (i * kWarpsA + warp) * dh)[lane] =
+                make_float4(acc[0], acc[1], acc[2], acc[3]);
+            if (lane == 0) {
+                s_m[i][warp] = mx;
+                s_l[i][warp] = l;
+            }
+        }
+    }
+    __syncthreads();
+    // per (row, dim): the chunk's blocks in block order (k_attn_decode's
+    // expressions)
+    const int stride = dh + 2;
+    for (int t = tid; t < mr * dh; t += kThreadsA) {
+        const int i = t / dh, d = t % dh;
+        const int p = pos[r0 + i];
+        if (p < ch * kChunk) continue;
+        const int nb = min(kWarpsA, (p - ch * kChunk) / kBlk + 1);
+        float M = -INFINITY;
+        for (int w = 0; w < nb; ++w) M = fmaxf(M, s_m[i][w]);
+        float L = 0.f;
+        for (int w = 0; w < nb; ++w) L = fmaf(s_l[i][w], expf(s_m[i][w] - M), L);
+        float o = 0.f;
+        for (int w = 0; w < nb; ++w) o = fmaf(s_acc[(i * kWarpsA + w) * dh + d], expf(s_m[i][w] - M), o);
+        const int r = r0 + i;
+        if (p / kChunk == 0) {
+            out[(int64_t)r * h + hh * dh + d] = __float2bfloat16_rn(o / L);
+        } else {
+            const int64_t slot = ((int64_t)r * nh + hh) * kMaxChunks + ch;
+            part[slot * stride + 2 + d] = o;
+            if (d == 0) {
+                part[slot * stride] = M;
+                part[slot * stride + 1] = L;
+            }
+        }
+    }
+    if (pmax < kChunk) return;  // every row of the group fits one chunk
+    __threadfence();
+    __syncthreads();
+    if (tid < mr) {
+        const int p = pos[r0 + tid];
+        s_last[tid] = p >= ch * kChunk && p >= kChunk &&
+                      atomicAdd(&ctr[(r0 + tid) * nh + hh], 1) == p / kChunk;
+    }
+    __syncthreads();
+    bool any = false;
+    for (int i = 0; i < mr; ++i) any |= s_last[i] != 0;
+    if (!any) return;
+    __threadfence();
+    // rows this CTA completed: fixed-order merge over chunks 0..nch-1
+    for (int t = tid; t < mr * dh; t += kThreadsA) {
+        const int i = t / dh, d = t % dh;
+        if (!s_last[i]) continue;
+        const int r = r0 + i;
+        const int nch = pos[r] / kChunk + 1;
+        const float* base = part + ((int64_t)r * nh + hh) * kMaxChunks * stride;
+        float MM = -INFINITY;
+        for (int c = 0; c < nch; ++c) MM = fmaxf(MM, __ldcg(base + c * stride));
+        float LL = 0.f;
+        for (int c = 0; c < nch; ++c)
+            LL = fmaf(__ldcg(base + c * stride + 1), expf(__ldcg(base + c * stride) - MM), LL);
+        float o = 0.f;
+        for (int c = 0; c < nch; ++c)
+            o = fmaf(__ldcg(base + c * stride + 2 + d), expf(__ldcg(base + c * stride) - MM), o);
+        out[(int64_t)r * h + hh * dh + d] = __float2bfloat16_rn(o / LL);
+    }
+    if (tid < mr && s_last[tid]) ctr[(r0 + tid) * nh + hh] = 0;  // re-usable workspace
+}
 
 }  // namespace
 
-// Workspace: [counters: 64*nh int32][partials: 64*nh*kMaxChunks*(dh+2) float32].
-// Zero once at allocation; every call leaves the counters zeroed.
+// Workspace layout: attn_core.cuh (counters, then partial slots).
 size_t attention_ws_bytes(int64_t /*m*/, int64_t nh, int64_t dh, int64_t /*s_max*/) {
-    return counters_bytes(nh) + (size_t)kRowsPerLaunch * nh * kMaxChunks * (dh + 2) * sizeof(float);
+    return attn::counters_bytes(nh) + attn::partial_slots(nh) * (dh + 2) * sizeof(float);
 }
 
 int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_pos,
@@ -260,7 +393,7 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
     EE_REQUIRE(ws != nullptr && ws_bytes >= attention_ws_bytes(m, nh, dh, 0), EE_ESHAPE,
                "attention: workspace too small");
     int* ctr = (int*)ws;
-    float* part = (float*)((char*)ws + counters_bytes(nh));
+    float* part = (float*)((char*)ws + attn::counters_bytes(nh));
     const float scale = 1.0f / sqrtf((float)dh);
     const int64_t h = nh * dh;
     const int nch = max_pos / kChunk + 1;
@@ -268,8 +401,25 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
         const int64_t mr = m - r0 < kRowsPerLaunch ? m - r0 : kRowsPerLaunch;
         const dim3 grid((unsigned)nh, (unsigned)mr, (unsigned)nch);
         cudaError_t e;
-        if (dtype == EE_BF16)
-            e = launch_ex(dh == 128 ? k_attn_decode<bf16, true> : k_attn_decode<bf16, false>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
+        // rows sharing K/V loads pay off once rows span several chunks; short
+        // rows are latency-bound and run one CTA per row (same arithmetic)
+        if (dtype == EE_BF16 && dh == kMaxDh && mr >= 2 && nch >= kRowsKernelMinChunks) {
+            const int groups = (int)((mr + kRowsCta - 1) / kRowsCta);
+            const size_t smem = rows128_smem((int)(mr < kRowsCta ? mr : kRowsCta));
+            static bool configured[16] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (!configured[dev & 15]) {
+                cudaFuncSetAttribute(k_attn_rows128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)rows128_smem(kRowsCta));
+                configured[dev & 15] = true;
+            }
+            e = launch_ex(k_attn_rows128, dim3((unsigned)nh, (unsigned)groups, (unsigned)nch),
+                          dim3(kThreadsA), smem, s, q + r0 * h, pos + r0, (int)mr,
+                          (const bf16*)kc, (const bf16*)vc, (int)nh, scale, (bf16*)out + r0 * h,
+                          part, ctr);
+        } else if (dtype == EE_BF16)
+            e = launch_ex(dh == kMaxDh ? k_attn_decode<bf16, true> : k_attn_decode<bf16, false>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
                           (int)mr, (const bf16*)kc, (const bf16*)vc, (int)nh, (int)dh, scale,
                           (bf16*)out + r0 * h, part, ctr);
         else if (dtype == EE_F32)

@@ -320,3 +320,22 @@ def test_tiled_modes_bitwise_equal_with_many_deferred_rows():
         assert reco.exit_layers == pipe.exit_layers, thr
         assert reco.confidences == pipe.confidences, thr
         assert any(e < 4 for e in reco.exit_layers)
+
+
+@pytest.mark.parametrize("prompt_len,max_new,max_deferred", [(250, 40, 15), (1900, 140, 3)])
+def test_tiled_modes_bitwise_equal_long_context(prompt_len, max_new, max_deferred):
+    """Pipeline (one row per pass) and KV recomputation (up to 16 rows per
+    pass) agree bitwise when rows cross the 256-position attention chunk
+    boundary (ordered cross-chunk merge) and near the 2048-position limit
+    (8 chunks)."""
+    import torch
+    cfg = ModelConfig(2, 512, 4, 256, 2048, exits=(ExitSpec(1, "minimalistic", 0.3),))
+    m = build_model(cfg, 17, init="device", dtype=torch.bfloat16)
+    part = partition(m, 2, copy=False)
+    prompt = [int(t) for t in np.random.default_rng(prompt_len).integers(0, 256, size=prompt_len)]
+    for thr in (1.0, 1.3 / 256):
+        reco = I.generate_kv_recompute(m, prompt, thr, max_new, max_deferred)
+        pipe = I.generate_pipeline(part, prompt, thr, max_new)
+        assert reco.tokens == pipe.tokens, thr
+        assert reco.exit_layers == pipe.exit_layers, thr
+        assert reco.confidences == pipe.confidences, thr
