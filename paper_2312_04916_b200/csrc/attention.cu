@@ -225,17 +225,8 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
     __threadfence();
     // fixed-order merge over chunks 0..nch-1
     const float* base = part + ((int64_t)r * nh + hh) * kMaxChunks * stride;
-    float MM = -INFINITY;
-    for (int c = 0; c < nch; ++c) MM = fmaxf(MM, __ldcg(base + c * stride));
-    float LL = 0.f;
-    for (int c = 0; c < nch; ++c)
-        LL = fmaf(__ldcg(base + c * stride + 1), expf(__ldcg(base + c * stride) - MM), LL);
-    for (int d = threadIdx.x; d < dh; d += kThreadsA) {
-        float o = 0.f;
-        for (int c = 0; c < nch; ++c)
-            o = fmaf(__ldcg(base + c * stride + 2 + d), expf(__ldcg(base + c * stride) - MM), o);
-        out[(int64_t)r * h + hh * dh + d] = from_f32<T>(o / LL);
-    }
+    for (int d = threadIdx.x; d < dh; d += kThreadsA)
+        out[(int64_t)r * h + hh * dh + d] = from_f32<T>(attn::chunk_merge(base, stride, nch, d));
     if (threadIdx.x == 0) ctr[r * nh + hh] = 0;  // leave the workspace re-usable
 }
 
@@ -359,15 +350,7 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
         const int r = r0 + i;
         const int nch = pos[r] / kChunk + 1;
         const float* base = part + ((int64_t)r * nh + hh) * kMaxChunks * stride;
-        float MM = -INFINITY;
-        for (int c = 0; c < nch; ++c) MM = fmaxf(MM, __ldcg(base + c * stride));
-        float LL = 0.f;
-        for (int c = 0; c < nch; ++c)
-            LL = fmaf(__ldcg(base + c * stride + 1), expf(__ldcg(base + c * stride) - MM), LL);
-        float o = 0.f;
-        for (int c = 0; c < nch; ++c)
-            o = fmaf(__ldcg(base + c * stride + 2 + d), expf(__ldcg(base + c * stride) - MM), o);
-        out[(int64_t)r * h + hh * dh + d] = __float2bfloat16_rn(o / LL);
+        out[(int64_t)r * h + hh * dh + d] = __float2bfloat16_rn(attn::chunk_merge(base, stride, nch, d));
     }
     if (tid < mr && s_last[tid]) ctr[(r0 + tid) * nh + hh] = 0;  // re-usable workspace
 }

@@ -111,4 +111,32 @@ __device__ __forceinline__ void block_eval128(const BlockRegs& R, const bf16* sv
     }
 }
 
+// Cross-chunk merge of one (row, head, dim): chunk partials (M_c, L_c, o_c)
+// at base + c*stride (+0, +1, +2+d), c < nch, all loaded up front (one L2
+// round trip), then folded in chunk order:
+//   out = (sum_c o_c e^(M_c-MM)) / (sum_c L_c e^(M_c-MM)),  MM = max_c M_c
+__device__ __forceinline__ float chunk_merge(const float* base, int stride, int nch, int d) {
+    float Mc[kMaxChunks], Lc[kMaxChunks], oc[kMaxChunks];
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; ++c) {
+        if (c < nch) {
+            Mc[c] = __ldcg(base + c * stride);
+            Lc[c] = __ldcg(base + c * stride + 1);
+            oc[c] = __ldcg(base + c * stride + 2 + d);
+        }
+    }
+    float MM = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; ++c)
+        if (c < nch) MM = fmaxf(MM, Mc[c]);
+    float LL = 0.f, o = 0.f;
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; ++c)
+        if (c < nch) LL = fmaf(Lc[c], expf(Mc[c] - MM), LL);
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; ++c)
+        if (c < nch) o = fmaf(oc[c], expf(Mc[c] - MM), o);
+    return o / LL;
+}
+
 }  // namespace attn

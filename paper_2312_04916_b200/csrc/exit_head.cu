@@ -74,9 +74,23 @@ __device__ void merge_and_decide(const HeadWs& w, int64_t units, int m, float th
     for (int c = wid; c < m; c += NT / 32) {
         float M = -INFINITY, S = 0.f;
         int I = 0x7fffffff;
-        for (int64_t u = lane; u < units; u += 32)
-            combine(M, S, I, __ldcg(w.pm + u * kMaxCols + c), __ldcg(w.ps + u * kMaxCols + c),
-                    __ldcg(w.pi + u * kMaxCols + c));
+        // 16 partials per lane in flight per batch, folded in ascending unit order
+        for (int64_t u0 = lane; u0 < units; u0 += 32 * 16) {
+            float pm[16], ps[16];
+            int pi[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int64_t u = u0 + 32 * k;
+                if (u < units) {
+                    pm[k] = __ldcg(w.pm + u * kMaxCols + c);
+                    ps[k] = __ldcg(w.ps + u * kMaxCols + c);
+                    pi[k] = __ldcg(w.pi + u * kMaxCols + c);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (u0 + 32 * k < units) combine(M, S, I, pm[k], ps[k], pi[k]);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const float m2 = __shfl_xor_sync(0xffffffffu, M, o);

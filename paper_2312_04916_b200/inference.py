@@ -695,9 +695,15 @@ class _InferStage:
         self.eng = _engine_for(spec, spec.params, heads, cfg, spec.layer_indices,
                                spec.has_embedding, dtype, device)
         self.eng.kv.reset()
-        with torch.cuda.device(self.eng.device):
-            self.stream = torch.cuda.Stream(self.eng.device)
-        self.eng.stream = self.stream
+        # one stream per stage engine for the engine's lifetime (not a new one
+        # per call): buffers the engine (re)allocates on it stay ordered with
+        # this stage's work under the caching allocator's per-stream reuse
+        st = getattr(self.eng, "_stage_stream", None)
+        if st is None:
+            with torch.cuda.device(self.eng.device):
+                st = self.eng._stage_stream = torch.cuda.Stream(self.eng.device)
+        self.stream = st
+        self.eng.stream = st
         self.heads_at = {}
         for local, hd in spec.heads:
             hi = next(i for i, e in enumerate(self.eng.heads) if e.desc.key == hd.key)
@@ -818,9 +824,12 @@ def generate_pipeline(part: StagePartition, prompt, threshold, max_new_tokens, s
     # the coordinator embeds on its own stream with its own staging buffers
     # (stage 1's worker owns first.x and first.ring)
     with torch.cuda.device(first.device):
-        emb_stream = torch.cuda.Stream(first.device)
+        emb_stream = getattr(first, "_emb_stream", None)
+        if emb_stream is None:
+            emb_stream = first._emb_stream = torch.cuda.Stream(first.device)
         cap = 2 * max(t0, 1) + 16
-        staging = (_PinnedRing(cap), torch.zeros(cap, dtype=torch.int32, device=first.device))
+        with torch.cuda.stream(emb_stream):
+            staging = (_PinnedRing(cap), torch.zeros(cap, dtype=torch.int32, device=first.device))
 
     def embedded(tokens, positions):
         with torch.cuda.device(first.device), torch.cuda.stream(emb_stream):

@@ -176,20 +176,37 @@ class TaggedChannel:
         self.count = 0
 
     def send(self, msg):
+        """Device tensors are produced asynchronously on the sender's stream:
+        the message carries an event recorded there, and the receiver's
+        stream waits on it before any kernel reads the tensor."""
         self.count += 1
-        self.q.put(msg)
+        ev = None
+        data = getattr(msg, "data", None)
+        if data is not None and getattr(data, "is_cuda", False):
+            torch = _torch()
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(data.device))
+        self.q.put((msg, ev))
 
     def recv(self, expect_mb):
         try:
-            msg = self.q.get(timeout=_RECV_TIMEOUT)
+            item = self.q.get(timeout=_RECV_TIMEOUT)
         except Empty:
             raise QueueProtocolError(f"{self.name}: timed out waiting for microbatch {expect_mb}")
-        if isinstance(msg, BaseException):
-            raise msg
+        if isinstance(item, BaseException):
+            raise item
+        msg, ev = item
         if msg.mb != expect_mb or msg.mb <= self.last:
             raise QueueProtocolError(
                 f"{self.name}: expected microbatch {expect_mb}, got {msg.mb} (last {self.last})")
         self.last = msg.mb
+        if ev is not None:
+            torch = _torch()
+            stream = torch.cuda.current_stream(msg.data.device)
+            stream.wait_event(ev)
+            # the sender's allocator must not recycle the block while this
+            # stream still uses it
+            msg.data.record_stream(stream)
         return msg
 
 
