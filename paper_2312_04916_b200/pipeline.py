@@ -88,15 +88,18 @@ def weight_at_step(ws: WeightSchedule, step: int):
 
 @dataclass
 class IterationOptions:
-    """eepipe/pipeline.py:164-172, plus ``hoist_exit_heads``: form a stage's
-    exit losses before receiving its backward gradient (the paper's §4.2.2
-    Remark; gradients are identical either way)."""
+    """eepipe/pipeline.py:164-172 (incl. ``fill_plan`` / ``fill_batch`` for
+    bubble filling), plus ``hoist_exit_heads``: form a stage's exit losses
+    before receiving its backward gradient (the paper's §4.2.2 Remark;
+    gradients are identical either way)."""
 
     microbatch_size: int
     defer_exit_forward: bool = True
     weight_schedule: WeightSchedule | None = None
     step: int = 0
     hoist_exit_heads: bool = True
+    fill_plan: object = None   # bubblefill.FillPlan
+    fill_batch: object = None  # rows of the extra (fill) microbatches
 
 
 @dataclass
@@ -165,13 +168,24 @@ def _grad_norm(grads):
     return float(torch.linalg.vector_norm(torch.stack(norms).double()))
 
 
+def _tag(mb):
+    """Message tags: ("mb", k) regular microbatch k, ("p1", i) / ("p2", i)
+    Part-1 / Part-2 fill i (eepipe/pipeline.py:86-122); a bare int is a
+    regular id."""
+    return ("mb", mb) if isinstance(mb, int) else tuple(mb)
+
+
 class TaggedChannel:
-    """Ordered in-process P2P channel; regular microbatch ids must arrive in
-    strictly increasing order (eepipe/pipeline.py:87-122)."""
+    """In-process P2P channel with tag-addressed receive
+    (eepipe/pipeline.py:86-122): messages arrive in sender order, the
+    receiver may consume them slightly out of order (fills interleave with
+    steady-phase traffic), so popped messages are stashed until their tag is
+    requested; regular microbatch ids must arrive strictly increasing."""
 
     def __init__(self, name):
         self.name = name
         self.q = Queue()
+        self.stash = {}
         self.last = 0
         self.count = 0
 
@@ -188,18 +202,8 @@ class TaggedChannel:
             ev.record(torch.cuda.current_stream(data.device))
         self.q.put((msg, ev))
 
-    def recv(self, expect_mb):
-        try:
-            item = self.q.get(timeout=_RECV_TIMEOUT)
-        except Empty:
-            raise QueueProtocolError(f"{self.name}: timed out waiting for microbatch {expect_mb}")
-        if isinstance(item, BaseException):
-            raise item
+    def _ready(self, item):
         msg, ev = item
-        if msg.mb != expect_mb or msg.mb <= self.last:
-            raise QueueProtocolError(
-                f"{self.name}: expected microbatch {expect_mb}, got {msg.mb} (last {self.last})")
-        self.last = msg.mb
         if ev is not None:
             torch = _torch()
             stream = torch.cuda.current_stream(msg.data.device)
@@ -208,6 +212,27 @@ class TaggedChannel:
             # stream still uses it
             msg.data.record_stream(stream)
         return msg
+
+    def recv(self, tag):
+        tag = _tag(tag)
+        if tag in self.stash:
+            return self._ready(self.stash.pop(tag))
+        while True:
+            try:
+                item = self.q.get(timeout=_RECV_TIMEOUT)
+            except Empty:
+                raise QueueProtocolError(f"{self.name}: timed out waiting for message {tag}")
+            if isinstance(item, BaseException):
+                raise item
+            got = _tag(item[0].mb)
+            if got[0] == "mb":
+                if got[1] <= self.last:
+                    raise QueueProtocolError(f"{self.name}: microbatch ids out of order: "
+                                             f"{got[1]} after {self.last}")
+                self.last = got[1]
+            if got == tag:
+                return self._ready(item)
+            self.stash[got] = item
 
 
 class DistChannel:
@@ -230,7 +255,10 @@ class DistChannel:
         data = msg.data.contiguous()
         if tuple(data.shape) != self.shape:
             raise ShapeError(f"channel expects {self.shape}, got {tuple(data.shape)}")
-        hdr = torch.tensor([msg.mb], dtype=torch.int64, device=self.device)
+        tag = _tag(msg.mb)
+        if tag[0] != "mb":
+            raise ConfigError("bubble-fill messages are not supported over torch.distributed")
+        hdr = torch.tensor([tag[1]], dtype=torch.int64, device=self.device)
         # keep the tensors alive until their sends complete
         self.pending.append((dist.isend(hdr, self.peer, group=self.group), hdr))
         self.pending.append((dist.isend(data, self.peer, group=self.group), data))
@@ -241,9 +269,13 @@ class DistChannel:
             req.wait()
         self.pending = []
 
-    def recv(self, expect_mb):
+    def recv(self, tag):
         torch = _torch()
         dist = torch.distributed
+        tag = _tag(tag)
+        if tag[0] != "mb":
+            raise ConfigError("bubble-fill messages are not supported over torch.distributed")
+        expect_mb = tag[1]
         hdr = torch.empty(1, dtype=torch.int64, device=self.device)
         dist.recv(hdr, self.peer, group=self.group)
         mb = int(hdr.item())
@@ -252,7 +284,7 @@ class DistChannel:
         self.last = mb
         data = torch.empty(self.shape, dtype=self.dtype, device=self.device)
         dist.recv(data, self.peer, group=self.group)
-        return type("Msg", (), {"mb": mb, "data": data})
+        return type("Msg", (), {"mb": ("mb", mb), "data": data})
 
 
 _UNSET = object()
@@ -279,46 +311,56 @@ class StageCompute:
         self.head_losses = {hd.key: [] for _, hd in self.spec.heads}
         self.tm.zero_grad()
 
-    def forward(self, tokens_or_x, targets):
+    def forward(self, tokens_or_x, targets, grad=True):
+        """``grad=False``: forward only (a Part-2 fill on a stage its
+        backward does not cover, eepipe/pipeline.py:476-489)."""
         from .training import embed_tokens, run_layer
-        p = self.tm.compute_params()
-        if self.spec.has_embedding:
-            x_in = None
-            x = embed_tokens(p, tokens_or_x, self.cfg.max_seq_len)
-        else:
-            x_in = tokens_or_x.to(self.device).detach().requires_grad_()
-            x = x_in
-        taps = {0: x}
-        for local, layer in enumerate(self.spec.layer_indices, start=1):
-            x = run_layer(p, f"layer{layer}", x, self.cfg.num_heads)
-            taps[local] = x
+        torch = _torch()
+        with torch.set_grad_enabled(grad):
+            p = self.tm.compute_params()
+            if self.spec.has_embedding:
+                x_in = None
+                x = embed_tokens(p, tokens_or_x, self.cfg.max_seq_len)
+            else:
+                x_in = tokens_or_x.to(self.device).detach().requires_grad_(grad)
+                x = x_in
+            taps = {0: x}
+            for local, layer in enumerate(self.spec.layer_indices, start=1):
+                x = run_layer(p, f"layer{layer}", x, self.cfg.num_heads)
+                taps[local] = x
         return x, (x_in, x, taps, targets)
 
-    def local_loss(self, state):
+    def local_loss(self, state, include_final=True, record=True):
+        """Weighted sum of this stage's exit losses.  Part-1 fills leave the
+        final head out and no fill records losses (eepipe/pipeline.py:456-474)."""
         import numpy as np
         from .training import head_loss
         torch = _torch()
         _, _, taps, targets = state
         from .training import _check_ids, to_device_async
+        heads = [(local, hd) for local, hd in self.spec.heads if include_final or not hd.is_final]
+        if not heads:
+            return None
         _check_ids(targets, self.cfg.vocab_size, "target")
         targets = to_device_async(np.ascontiguousarray(targets), self.device)
         total = None
         params = self.tm.compute_params()
-        for local, hd in self.spec.heads:
+        for local, hd in heads:
             ce = head_loss(params, hd, taps[local], targets, self.cfg.num_heads, validated=True)
-            self.head_losses[hd.key].append(ce.detach())  # read after the iteration (no sync)
+            if record:
+                self.head_losses[hd.key].append(ce.detach())  # read after the iteration (no sync)
             term = ce * self.weights[hd.key]
             total = term if total is None else total + term
         return total
 
-    def backward(self, state, g, loss=_UNSET):
+    def backward(self, state, g, loss=_UNSET, include_final=True, record=True):
         """``loss``: the stage's local exit loss when the worker already
         formed it (hoisted ahead of the gradient receive); otherwise it is
         formed here (deferred exit forward, eepipe/pipeline.py:393-412)."""
         torch = _torch()
         x_in, x_out, _, _ = state
         if loss is _UNSET:
-            loss = self.local_loss(state)
+            loss = self.local_loss(state, include_final, record)
         if g is None:
             if loss is None:
                 raise ConfigError("a stage must have a local loss or a received gradient")
@@ -337,68 +379,124 @@ class StageCompute:
         return None if x_in is None else x_in.grad
 
 
+@dataclass
+class _FillContext:
+    """Per-iteration bubble-fill geometry (eepipe/pipeline.py:527-535):
+    truncated Part-1 depths (None = skipped) and the stage sets each Part-2
+    microbatch's backward covers."""
+
+    part1_depths: list = field(default_factory=list)
+    part2_covered: list = field(default_factory=list)
+
+
 class StageWorker:
-    """Executes one stage's 1F1B action list (eepipe/pipeline.py:301-527)."""
+    """Executes one stage's action list (eepipe/pipeline.py:301-527): the
+    1F1B order, plus bubble-fill microbatches when ``fill`` is given."""
 
     def __init__(self, index, num_stages, num_mb, compute, data, fwd_in, fwd_out, bwd_in,
-                 bwd_out, hoist_exits=True):
+                 bwd_out, hoist_exits=True, actions=None, fill=None):
         self.index, self.P, self.M = index, num_stages, num_mb
         self.compute = compute
-        self.data = data  # mb -> (tokens, targets)
+        self.data = data  # regular k -> (tokens, targets); ("p1"|"p2", i) -> fill rows
         self.fwd_in, self.fwd_out, self.bwd_in, self.bwd_out = fwd_in, fwd_out, bwd_in, bwd_out
         self.hoist_exits = hoist_exits and hasattr(compute, "local_loss")
+        self.actions = actions if actions is not None else sched.regular_actions(
+            num_stages, num_mb, index)
+        self.fill = fill
         self.state = {}
         self.event_log = []
         self.wall = {"F": 0.0, "B": 0.0}
         self.in_flight = 0
         self.max_in_flight = 0
+        self.fill_stored = 0
+        self.max_fill_stored = 0
         self.exception = None
 
     def run(self):
         try:
-            for kind, mb in sched.regular_actions(self.P, self.M, self.index):
+            for kind, i in self.actions:
                 t = time.perf_counter()
                 if kind == sched.FWD:
-                    self._forward(mb)
+                    self._forward(("mb", i))
+                elif kind == sched.BWD:
+                    self._backward(("mb", i))
+                elif kind == sched.FILL1_FWD:
+                    d = self.fill.part1_depths[i - 1]
+                    self._forward(("p1", i), send=self.index < d)
+                elif kind == sched.FILL1_BWD:
+                    d = self.fill.part1_depths[i - 1]
+                    self._backward(("p1", i), recv=self.index < d, send=self.index > 1,
+                                   include_final=False)
+                elif kind == sched.FILL2_FWD:
+                    covered = self.index in self.fill.part2_covered[i - 1]
+                    self._forward(("p2", i), keep=covered)
+                elif kind == sched.FILL2_BWD:
+                    deepest = min(self.fill.part2_covered[i - 1])
+                    self._backward(("p2", i), send=self.index > deepest)
                 else:
-                    self._backward(mb)
-                self.wall[kind] += time.perf_counter() - t
-                self.event_log.append((kind, mb))
+                    raise ConfigError(f"unknown action {kind!r}")
+                self.wall["F" if kind in sched.FWD_KINDS else "B"] += time.perf_counter() - t
+                self.event_log.append((kind, i))
+            if self.state:
+                raise QueueProtocolError(
+                    f"stage {self.index} finished with unconsumed activations")
         except BaseException as exc:  # surfaced by the coordinator
             self.exception = exc
             for ch in (self.fwd_out, self.bwd_out):
                 if isinstance(ch, TaggedChannel):
                     ch.q.put(exc)
 
-    def _forward(self, mb):
-        tokens, targets = self.data[mb]
-        src = tokens if self.fwd_in is None else self.fwd_in.recv(mb).data
-        x_out, st = self.compute.forward(src, targets)
-        self.state[mb] = st
-        self.in_flight += 1
-        self.max_in_flight = max(self.max_in_flight, self.in_flight)
-        if self.fwd_out is not None:
-            self.fwd_out.send(ActivationMessage(mb, x_out.detach()))
+    def _rows(self, tag):
+        return self.data[tag[1]] if tag[0] == "mb" else self.data[tag]
 
-    def _backward(self, mb):
-        st = self.state.pop(mb)
-        if self.hoist_exits and self.bwd_in is not None:
+    def _count(self, tag, delta):
+        if tag[0] == "mb":
+            self.in_flight += delta
+            self.max_in_flight = max(self.max_in_flight, self.in_flight)
+        else:
+            self.fill_stored += delta
+            self.max_fill_stored = max(self.max_fill_stored, self.fill_stored)
+
+    def _forward(self, tag, send=True, keep=True):
+        """``keep=False``: forward only, nothing stored (a Part-2 fill on an
+        uncovered stage)."""
+        tokens, targets = self._rows(tag)
+        src = tokens if self.fwd_in is None else self.fwd_in.recv(tag).data
+        x_out, st = self.compute.forward(src, targets) if keep else \
+            self.compute.forward(src, targets, grad=False)
+        if keep:
+            self.state[tag] = st
+            self._count(tag, 1)
+        if send and self.fwd_out is not None:
+            self.fwd_out.send(ActivationMessage(tag, x_out.detach()))
+
+    def _backward(self, tag, recv=None, send=None, include_final=True):
+        """``recv`` / ``send``: whether the downstream gradient arrives /
+        the input gradient leaves (default: whenever the neighbour exists).
+        Fills record no losses."""
+        st = self.state.pop(tag)
+        recv = self.bwd_in is not None if recv is None else recv
+        send = self.bwd_out is not None if send is None else send
+        record = tag[0] == "mb"
+        if self.hoist_exits and recv:
             # the paper's §4.2.2 Remark (modelled only by the reference,
             # eepipe/schedule.py:491-502): form the stage's exit losses — with
             # the fused head that is the whole exit forward AND backward —
             # before waiting for the downstream gradient, so the exit work
             # overlaps the pipeline's communication instead of following it
-            loss = self.compute.local_loss(st)
-            g = self.bwd_in.recv(mb).data
+            loss = self.compute.local_loss(st, include_final, record) if not (
+                include_final and record) else self.compute.local_loss(st)
+            g = self.bwd_in.recv(tag).data
             g_in = self.compute.backward(st, g, loss)
         else:
-            g = None if self.bwd_in is None else self.bwd_in.recv(mb).data
-            g_in = self.compute.backward(st, g)
-        self.in_flight -= 1
-        if self.bwd_out is not None:
+            g = self.bwd_in.recv(tag).data if recv else None
+            g_in = self.compute.backward(st, g) if (include_final and record) else \
+                self.compute.backward(st, g, include_final=include_final, record=record)
+        self._count(tag, -1)
+        if send:
             if g_in is None:
                 raise ConfigError("stored input activation received no gradient")
-            self.bwd_out.send(GradientMessage(mb, g_in.detach()))
+            self.bwd_out.send(GradientMessage(tag, g_in.detach()))
 
 
 def _resolve_weights(heads, options):
@@ -449,8 +547,47 @@ def _stage_stream(device, stage):
     return st
 
 
+def apply_fill(plan, part: StagePartition, num_microbatches: int):
+    """Validate a fill plan against a partition; returns (truncated Part-1
+    depths, FillRescale) (eepipe/pipeline.py:244-259).  Tied parameters
+    across stages reject the plan."""
+    from .bubblefill import fill_rescale, truncated_part1_depths
+    if part.tied_replicas:
+        raise ConfigError("bubble filling requires untied parameters across stages; "
+                          f"tied: {sorted(part.tied_replicas)}")
+    if plan.num_stages != part.num_stages:
+        raise ConfigError("fill plan stage count does not match the partition")
+    exit_stages = part.exit_stages()
+    return (truncated_part1_depths(plan, exit_stages),
+            fill_rescale(plan, exit_stages, num_microbatches))
+
+
+def _assign_fill_data(data, row_len, options: IterationOptions, depths):
+    """Fill microbatches take consecutive microbatch-size slices of
+    ``fill_batch``: executed Part-1 fills first, then Part-2
+    (eepipe/pipeline.py:658-680)."""
+    import numpy as np
+    plan = options.fill_plan
+    executed = [i for i, d in enumerate(depths, 1) if d is not None]
+    needed = len(executed) + len(plan.part2_bwd_depths)
+    fb = options.fill_batch
+    if fb is None and needed:
+        raise ConfigError("fill plan is active but no fill_batch was provided")
+    fb = np.asarray(fb) if fb is not None else np.empty((0, row_len), dtype=np.int64)
+    mbs = options.microbatch_size
+    if fb.ndim != 2 or fb.shape[0] != needed * mbs or fb.shape[1] != row_len:
+        raise ConfigError(f"fill_batch must hold {needed} microbatches of the batch row length")
+    k = 0
+    for tag in [("p1", i) for i in executed] + [("p2", i) for i in
+                                                 range(1, len(plan.part2_bwd_depths) + 1)]:
+        rows = fb[k * mbs:(k + 1) * mbs]
+        data[tag] = (rows[:, :-1], rows[:, 1:])
+        k += 1
+
+
 def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
-                       devices=None, dtype=None, master_dtype=None, stage_computes=None):
+                       devices=None, dtype=None, master_dtype=None, stage_computes=None,
+                       compute_factory=None):
     """One 1F1B iteration over the partition, one thread per stage
     (eepipe/pipeline.py:537-644).  ``model`` is the EarlyExitModel the stage
     weights come from (the partition's own copies are used when omitted).
@@ -458,13 +595,32 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
     (`TrainModel` mixed mode).  ``stage_computes``: a list that keeps the
     per-stage device state across iterations (filled on the first call,
     reused — gradients zeroed, weights as the optimizer left them — after).
-    Returns (merged gradient map by name, TrainStepReport)."""
+    ``compute_factory(spec, cfg, wmap)`` overrides the stage compute (CPU
+    protocol tests).  Returns (merged gradient map by name, TrainStepReport)."""
+    import numpy as np
     P = part.num_stages
     M, data = _split(batch, options.microbatch_size)
     all_heads = [hd for st in part.stages for _, hd in st.heads]
     all_heads.sort(key=lambda hd: (hd.layer_index, hd.is_final))
     weights = _resolve_weights(all_heads, options)
     wmap = {hd.key: w for hd, w in zip(all_heads, weights)}
+    # bubble filling (eepipe/pipeline.py:566-580): Part-1-sampled exit losses
+    # get their weight scaled in every microbatch, Part-2-covered stages
+    # their accumulated gradient
+    fill, rescale, depths = None, None, []
+    plan = options.fill_plan
+    if plan is not None and not plan.empty:
+        if not options.defer_exit_forward:
+            raise ConfigError("bubble filling requires the deferred-exit variant")
+        if M < P:
+            raise ConfigError("bubble filling needs at least P microbatches")
+        depths, rescale = apply_fill(plan, part, M)
+        covered = [set(range(P - r + 1, P + 1)) for r in plan.part2_bwd_depths]
+        fill = _FillContext(list(depths), covered)
+        _assign_fill_data(data, np.asarray(batch).shape[1], options, depths)
+        for hd in all_heads:
+            if not hd.is_final:
+                wmap[hd.key] = wmap[hd.key] * rescale.weight_scale_for(part.stage_of_head(hd.key))
     devices = devices or ["cuda:0"] * P
     src = model
     fwd = [TaggedChannel(f"act {s}->{s + 1}") for s in range(1, P)]
@@ -472,7 +628,9 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
     workers = []
     reuse = stage_computes is not None and len(stage_computes) == P
     for s, spec in enumerate(part.stages, start=1):
-        if reuse:
+        if compute_factory is not None:
+            comp = compute_factory(spec, part.config, wmap)
+        elif reuse:
             comp = stage_computes[s - 1]
             comp.reset(wmap)
         else:
@@ -481,14 +639,19 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
                                 dtype, master_dtype)
             if stage_computes is not None:
                 stage_computes.append(comp)
+        acts = (sched.fill_actions(P, M, s, depths, plan.part2_bwd_depths) if fill is not None
+                else None)
         workers.append(StageWorker(s, P, M, comp, data,
                                    fwd[s - 2] if s > 1 else None, fwd[s - 1] if s < P else None,
                                    bwd[s - 1] if s < P else None, bwd[s - 2] if s > 1 else None,
-                                   options.hoist_exit_heads))
+                                   options.hoist_exit_heads, actions=acts, fill=fill))
     torch = _torch()
 
     def target(w):
-        dev = w.compute.device
+        dev = torch.device(w.compute.device)
+        if dev.type != "cuda":
+            w.run()
+            return
         with torch.cuda.device(dev), torch.cuda.stream(_stage_stream(dev, w.index)):
             w.run()
             torch.cuda.current_stream(dev).synchronize()
@@ -511,12 +674,21 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
     for w in workers:
         if w.exception is not None:
             raise w.exception
-    per_stage = [w.compute.tm.grads() for w in workers]
+    per_stage = [w.compute.tm.grads() if compute_factory is None else w.compute.grads()
+                 for w in workers]
+    if rescale is not None:
+        for w, g in zip(workers, per_stage):
+            gs = rescale.grad_scale_for(w.index)
+            if gs != 1.0:
+                for t in g.values():
+                    t.mul_(gs)
     merged = sync_tied(per_stage, part.tied_replicas)
-    report = TrainStepReport(weights_used=tuple(weights), microbatches=M)
+    n_fill = sum(1 for d in depths if d is not None) + (len(plan.part2_bwd_depths)
+                                                         if fill is not None else 0)
+    report = TrainStepReport(weights_used=tuple(weights), microbatches=M + n_fill)
     for w, g in zip(workers, per_stage):
         report.event_log.append(list(w.event_log))
-        report.memory.append(StageMemoryCounters(w.index, w.max_in_flight))
+        report.memory.append(StageMemoryCounters(w.index, w.max_in_flight, w.max_fill_stored))
         report.grad_norms[w.index] = _grad_norm(g)
         report.activation_messages[w.index] = w.fwd_out.count if w.fwd_out is not None else 0
         report.gradient_messages[w.index] = w.bwd_out.count if w.bwd_out is not None else 0
@@ -553,6 +725,9 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
         raise ConfigError(f"{world} ranks for {P} stages")
     s = rank + 1
     spec = part.stages[rank]
+    if options.fill_plan is not None and not options.fill_plan.empty:
+        raise ConfigError("bubble filling runs in the threaded executor (run_iteration_1f1b); "
+                          "its fill traffic is tag-addressed, which NCCL P2P is not")
     M, data = _split(batch, options.microbatch_size)
     all_heads = sorted([hd for st in part.stages for _, hd in st.heads],
                        key=lambda hd: (hd.layer_index, hd.is_final))

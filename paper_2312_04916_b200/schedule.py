@@ -10,7 +10,15 @@ Only the parts on the path are restated:
   early-exit inference vs sequential full passes
   (`eepipe/schedule.py:553-590`).  Reported next to measured latency.
 
-The reference's memory accounting, Gantt rendering and bubble-fill planner
+* `fill_actions` — the 1F1B list with bubble-fill microbatches inserted
+  (`eepipe/schedule.py:182-209`): Part-1 fills between the warm-up forwards
+  and the first steady forward exactly as the reference; Part-2 fills at the
+  front of each stage's list (the reference slots them into idle gaps with
+  its cost model, `eepipe/schedule.py:275-304`; the gradients do not depend
+  on the placement, and every placement here is deadlock-free because fill
+  actions only wait on the same fill's neighbours).
+
+The reference's cost-model simulator, memory accounting and Gantt rendering
 are out of scope.
 """
 
@@ -19,6 +27,9 @@ from __future__ import annotations
 from .errors import ConfigError
 
 FWD, BWD = "F", "B"
+FILL1_FWD, FILL1_BWD = "F1f", "F1b"
+FILL2_FWD, FILL2_BWD = "F2f", "F2b"
+FWD_KINDS = (FWD, FILL1_FWD, FILL2_FWD)
 
 
 def regular_actions(num_stages: int, num_microbatches: int, stage: int):
@@ -32,11 +43,32 @@ def regular_actions(num_stages: int, num_microbatches: int, stage: int):
     return acts
 
 
+def fill_actions(num_stages: int, num_microbatches: int, stage: int, part1_depths=(),
+                 part2_bwd_depths=()):
+    """Per-stage action list with bubble fills.  ``part1_depths``: truncated
+    Part-1 depths (None = skipped), ``part2_bwd_depths``: Part-2 backward
+    depths (the last r stages run the backward)."""
+    p, m = num_stages, num_microbatches
+    acts = regular_actions(p, m, stage)
+    visiting = [i for i, d in enumerate(part1_depths, 1) if d is not None and d >= stage]
+    if visiting:
+        inserts = [(FILL1_FWD, i) for i in visiting]
+        inserts += [(FILL1_BWD, i) for i in reversed(visiting)]
+        cut = min(p - stage, m) + 1  # the warm-up bubble (eepipe/schedule.py:204-208)
+        acts = acts[:cut] + inserts + acts[cut:]
+    front = []
+    for i, r in enumerate(part2_bwd_depths, 1):
+        front.append((FILL2_FWD, i))
+        if stage >= p - r + 1:
+            front.append((FILL2_BWD, i))
+    return front + acts
+
+
 def max_in_flight(actions):
-    """Largest number of forwarded-but-not-backwarded microbatches."""
+    """Largest number of forwarded-but-not-backwarded regular microbatches."""
     live = peak = 0
     for kind, _ in actions:
-        live += 1 if kind == FWD else -1
+        live += 1 if kind == FWD else (-1 if kind == BWD else 0)
         peak = max(peak, live)
     return peak
 

@@ -142,3 +142,77 @@ def test_hoisted_exit_heads_identical_gradients():
     for name in g_h:
         assert bool((g_h[name] == g_p[name]).all()), name
     assert r_h.per_exit_losses == r_p.per_exit_losses
+
+
+# ---- bubble filling (eepipe/pipeline.py:456-498) ---------------
+
+def _fill_golden():
+    import json
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    with open(os.path.join(here, "fill.json")) as f:
+        meta = json.load(f)
+    return meta, np.load(os.path.join(here, "fill.npz"))
+
+
+def test_bubble_fill_matches_reference_executor():
+    """The full plan_bubble_fill(4, 0.5) iteration (Part-1 truncated to the
+    exit stages, Part-2 suffix backwards, loss-weight and stage-gradient
+    rescaling) against the REFERENCE executor's float64 gradients
+    (tests/golden/make_fill.py), bf16 within 3e-2 relative per tensor; the
+    plain iteration likewise; and the fill's effect (filled - plain) within
+    5e-2 relative on every stage it touches."""
+    from paper_2312_04916_b200.bubblefill import plan_bubble_fill
+    from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
+    meta, g = _fill_golden()
+    L, h, nh, V, s_max = meta["config"]
+    cfg = ModelConfig(L, h, nh, V, s_max,
+                      exits=tuple(ExitSpec(l, loss_weight=w) for l, w in meta["exits"]))
+    model = build_model(cfg, meta["seed"])
+    part = partition(model, 4)
+    batch, fill_rows = g["batch"], g["fill_rows"]
+    plain, _ = run_iteration_1f1b(part, batch, IterationOptions(microbatch_size=2), model=model)
+    filled, rep = run_iteration_1f1b(part, batch, IterationOptions(
+        microbatch_size=2, fill_plan=plan_bubble_fill(4, meta["f_over_b"]),
+        fill_batch=fill_rows), model=model)
+    assert rep.microbatches == meta["microbatches"]
+    for name in filled:
+        ref_f, ref_p = g["filled/" + name], g["plain/" + name]
+        ours_f = filled[name].detach().double().cpu().numpy()
+        ours_p = plain[name].detach().double().cpu().numpy()
+        assert np.linalg.norm(ours_f - ref_f) / np.linalg.norm(ref_f) < 3e-2, name
+        assert np.linalg.norm(ours_p - ref_p) / np.linalg.norm(ref_p) < 3e-2, name
+        d_ref = ref_f - ref_p
+        if np.linalg.norm(d_ref) > 1e-3 * np.linalg.norm(ref_p):
+            d = ours_f - ours_p
+            assert np.linalg.norm(d - d_ref) / np.linalg.norm(d_ref) < 5e-2, name
+    for k, v in meta["filled_losses"].items():
+        assert rep.per_exit_losses[k] == pytest.approx(v, rel=1e-3)
+
+
+def test_bubble_fill_part2_touches_only_last_stages():
+    """tests/test_pipeline.py:269-290 of the reference: one Part-2 insertion of
+    backward depth 2 leaves stages 1-2 bitwise unchanged and scales stages 3-4
+    by b/(b+1) after adding the fill's gradient."""
+    from paper_2312_04916_b200.bubblefill import FillPlan
+    from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
+    from paper_2312_04916_b200.training import TrainModel, single_device_gradients
+    cfg = ModelConfig(8, 32, 4, VOCAB, 16,
+                      exits=(ExitSpec(2, loss_weight=0.3), ExitSpec(4, loss_weight=0.6)))
+    model = build_model(cfg, 11)
+    part = partition(model, 4)
+    rng = np.random.default_rng(12)
+    batch = rng.integers(0, VOCAB, size=(8, 9))
+    fill_rows = rng.integers(0, VOCAB, size=(2, 9))
+    plain, _ = run_iteration_1f1b(part, batch, IterationOptions(microbatch_size=2), model=model)
+    filled, _ = run_iteration_1f1b(part, batch, IterationOptions(
+        microbatch_size=2, fill_plan=FillPlan(4, 0.5, 0, 1, (), (2,)), fill_batch=fill_rows),
+        model=model)
+    fill_oracle, _ = single_device_gradients(TrainModel(model), fill_rows, [0.3, 0.6, 1.0], 2)
+    covered = {n for st in part.stages if st.index >= 3 for n in st.params}
+    for name in plain:
+        if name in covered:
+            want = (plain[name].double() + fill_oracle[name].double().to(plain[name].device)) * 0.8
+            assert _rel(filled[name], want) < 2e-2, name
+        else:
+            assert bool((filled[name] == plain[name]).all()), name

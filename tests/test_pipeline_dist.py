@@ -19,7 +19,7 @@ import torch.multiprocessing as mp
 from paper_2312_04916_b200 import schedule as sched
 from paper_2312_04916_b200.errors import QueueProtocolError
 from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model, partition
-from paper_2312_04916_b200.pipeline import (ActivationMessage, IterationOptions, TaggedChannel,
+from paper_2312_04916_b200.pipeline import (GradientMessage, IterationOptions, TaggedChannel,
                                             WeightSchedule, run_stage_1f1b_dist, weight_at_step)
 
 
@@ -40,17 +40,24 @@ def test_regular_actions_structure():
                         assert k in seen
 
 
-def test_tagged_channel_protocol():
-    ch = TaggedChannel("t")
-    ch.send(ActivationMessage(2, None))
+def test_tagged_queue_rejects_out_of_order_regular_ids():
+    """The reference's queue-protocol tests (tests/test_pipeline.py:354-372)."""
+    q = TaggedChannel("t")
+    q.send(GradientMessage(("mb", 2), None))
+    q.send(GradientMessage(("mb", 1), None))
+    q.recv(("mb", 2))
     with pytest.raises(QueueProtocolError):
-        ch.recv(1)
-    ch = TaggedChannel("t")
-    ch.send(ActivationMessage(1, None))
-    ch.recv(1)
-    ch.send(ActivationMessage(1, None))
-    with pytest.raises(QueueProtocolError):
-        ch.recv(1)  # ids must strictly increase
+        q.recv(("mb", 1))
+
+
+def test_tagged_queue_stashes_fills():
+    q = TaggedChannel("t")
+    q.send(GradientMessage(("mb", 1), None))
+    q.send(GradientMessage(("p1", 1), "fill"))
+    q.send(GradientMessage(("mb", 2), None))
+    assert q.recv(("p1", 1)).data == "fill"
+    assert q.recv(("mb", 1)).mb == ("mb", 1)
+    assert q.recv(2).mb == ("mb", 2)  # a bare int is a regular id
 
 
 def test_weight_schedule():
