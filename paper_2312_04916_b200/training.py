@@ -690,15 +690,16 @@ def train(run_cfg, corpus, metrics_path=None, progress=None, *, devices=None, dt
     exit heads, bf16 compute, float32 gradient accumulation), and applies the fused optimizer with
     scale 1/num_microbatches.  Metrics: a header record then one record per
     step (losses, time, microbatches, weights) as line-delimited JSON.
-    Bubble filling is out of scope and rejected."""
+    ``run_cfg.fill_bubbles``: every iteration also runs the
+    plan_bubble_fill(stages, fill_f_over_b) fill microbatches, drawn from
+    ``corpus.batch(n_fill * microbatch_size, row_len, step + 10**9)`` like the
+    reference (`eepipe/training.py:76-101`)."""
     import json
     import time
     from .errors import ConfigError, NonFiniteError
     from .model import build_model, partition
     from .pipeline import IterationOptions, run_iteration_1f1b
     torch = _torch()
-    if getattr(run_cfg, "fill_bubbles", False):
-        raise ConfigError("bubble filling is not supported by this build")
     _lib.require_cuda()
     master = device_master(build_model(run_cfg.model, run_cfg.seed),
                            devices[0] if devices else None)
@@ -718,13 +719,24 @@ def train(run_cfg, corpus, metrics_path=None, progress=None, *, devices=None, dt
             fh.write(json.dumps(rec, sort_keys=True) + "\n")
 
     part = partition(master, run_cfg.stages, copy=False)
+    plan, n_fill = None, 0
+    if getattr(run_cfg, "fill_bubbles", False):
+        from .bubblefill import plan_bubble_fill, truncated_part1_depths
+        plan = plan_bubble_fill(run_cfg.stages, run_cfg.fill_f_over_b)
+        depths = truncated_part1_depths(plan, part.exit_stages())
+        n_fill = sum(1 for d in depths if d is not None) + plan.k_part2
     computes = []  # per-stage device state (bf16 weights, float32 gradient sums), kept
     try:
         for step in range(run_cfg.steps):
             batch = corpus.batch(rows_per_step, row_len, step)
+            fill_batch = None
+            if plan is not None and not plan.empty and n_fill:
+                fill_batch = corpus.batch(n_fill * run_cfg.microbatch_size, row_len,
+                                          step + 10**9)
             opts = IterationOptions(microbatch_size=run_cfg.microbatch_size,
                                     defer_exit_forward=getattr(run_cfg, "defer_exit_forward", True),
-                                    weight_schedule=schedule, step=step)
+                                    weight_schedule=schedule, step=step, fill_plan=plan,
+                                    fill_batch=fill_batch)
             t0 = time.perf_counter()
             grads, report = run_iteration_1f1b(part, batch, opts, model=master, devices=devices,
                                                dtype=dtype, master_dtype=torch.float32,
@@ -740,7 +752,7 @@ def train(run_cfg, corpus, metrics_path=None, progress=None, *, devices=None, dt
                        "seed": run_cfg.seed})
             rec = {"record": "step", "step": step,
                    "losses": {k: report.per_exit_losses[k] for k in head_keys},
-                   "time": elapsed, "microbatches": num_mb,
+                   "time": elapsed, "microbatches": report.microbatches,
                    "weights": list(report.weights_used)}
             history.append(rec)
             write(rec)

@@ -114,3 +114,43 @@ def test_train_three_adam_steps_match_reference(tmp_path):
         err = np.linalg.norm(ours - ref)
         print(f"{name}: |ours - ref| / |ref - init| = {err / disp:.4f}")
         assert err < 0.1 * disp, (name, err / disp)
+
+
+class _StepBatches:
+    """Replays the batches the reference's corpus served, regular (step) and
+    fill (step + 10**9) draws."""
+
+    def __init__(self, regular, fill):
+        self.regular, self.fill = regular, fill
+
+    def batch(self, rows, row_len, step):
+        src = self.fill[step - 10**9] if step >= 10**9 else self.regular[step]
+        assert src.shape == (rows, row_len)
+        return src
+
+
+def test_train_with_bubble_filling_matches_reference():
+    """`train` with fill_bubbles on a 4-stage model (3 Adam steps): per-step
+    per-exit losses within 2e-2 of the reference's `train` and the same
+    microbatch count (4 regular + 1 Part-1 + 2 Part-2 per step;
+    tests/golden/make_fill.py)."""
+    from paper_2312_04916_b200.model import ExitSpec, ModelConfig
+    from paper_2312_04916_b200.pipeline import WeightSchedule
+    from paper_2312_04916_b200.training import train
+    with open(os.path.join(GOLD_DIR, "fill.json")) as f:
+        g = json.load(f)["train"]
+    arr = np.load(os.path.join(GOLD_DIR, "fill.npz"))
+    L, h, nh, V, s_max = g["config"]
+    cfg = ModelConfig(L, h, nh, V, s_max,
+                      exits=tuple(ExitSpec(l, "minimalistic", w) for l, w in g["exits"]))
+    rc = SimpleNamespace(model=cfg, seed=0, stages=g["stages"], microbatch_size=2,
+                         global_batch_size=8, steps=g["steps"], optimizer="adam",
+                         learning_rate=g["lr"], data_seq_len=32, defer_exit_forward=True,
+                         fill_bubbles=True, fill_f_over_b=g["f_over_b"],
+                         weight_schedule=lambda: WeightSchedule(
+                             "constant", early=tuple(w for _, w in g["exits"])))
+    _, hist = train(rc, _StepBatches(arr["train_batches"], arr["train_fill_batches"]))
+    assert [r["microbatches"] for r in hist] == g["microbatches"]
+    for ours, ref in zip(hist, g["losses"]):
+        for k, v in ref.items():
+            assert ours["losses"][k] == pytest.approx(v, rel=2e-2), (ours["step"], k)
