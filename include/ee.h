@@ -308,6 +308,20 @@ int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64
 int ee_wgrad_accum(const void* X, const void* dY, int64_t T, int64_t in, int64_t out, float* dW,
                    void* stream);
 
+/* The training MLP block's GEMMs with the GELU fused into the epilogue
+ * (CTA-pair tcgen05 GEMM), `gelu_fwd` / `gelu_bwd` of eepipe/_pykernels.py:
+ * 27-33 around the w1 / w2 matmuls of eepipe/model.py:214-216:
+ *   ee_mlp_up_gelu:  pre = X W1, act = GELU_erf(pre)        (bf16 outputs)
+ *   ee_mlp_gelu_bwd: dpre = (dY W2^T) * GELU_erf'(pre)      (bf16 output)
+ * X, dY (T x h), pre / act / dpre (T x N) row-major bf16; W1 (h x N) and
+ * W2 (N x h) row-major bf16 (the layer's own weights, read in place).  The
+ * GEMM result is rounded to bf16 before the element-wise op, as the unfused
+ * bf16 path would read it.  h, N multiples of 8. */
+int ee_mlp_up_gelu(const void* X, const void* W1, int64_t T, int64_t h, int64_t N, void* pre,
+                   void* act, void* stream);
+int ee_mlp_gelu_bwd(const void* dY, const void* W2, int64_t T, int64_t h, int64_t N,
+                    const void* pre, void* dpre, void* stream);
+
 /* ---- training RMSNorm (bf16 activations, float32 statistics) ---------- */
 
 /* y = x * (mean(x^2) + eps)^-1/2 * w row-wise; x, y (n, h) bf16, w (h) float32,

@@ -15,6 +15,7 @@ multi-exit objective.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -183,6 +184,74 @@ class _LinearFn:
 
             cls._fn = _F
         return cls._fn
+
+
+class _MLPFn:
+    """GELU(x @ W1) @ W2 with the GELU fused into tcgen05 GEMM epilogues
+    (csrc/mlp_train.cu): forward ee_mlp_up_gelu writes pre and act in one
+    pass; backward ee_mlp_gelu_bwd forms dpre = (dY W2^T) * GELU'(pre) in the
+    epilogue of the dgrad GEMM, and both weight gradients accumulate into the
+    float32 sums with ee_wgrad_accum (eepipe/model.py:214-216)."""
+
+    _fn = None
+
+    @classmethod
+    def get(cls):
+        if cls._fn is None:
+            torch = _torch()
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, x, w1, w2, acc1, acc2):
+                    x2 = x.reshape(-1, x.shape[-1]).contiguous()
+                    T, h = x2.shape
+                    N = w1.shape[1]
+                    pre = torch.empty((T, N), dtype=x.dtype, device=x.device)
+                    act = torch.empty((T, N), dtype=x.dtype, device=x.device)
+                    call("ee_mlp_up_gelu", ptr(x2), ptr(w1), T, h, N, ptr(pre), ptr(act),
+                         stream_ptr())
+                    ctx.save_for_backward(x2, w1, w2, pre, act)
+                    ctx.acc = (acc1, acc2)
+                    ctx.shape = x.shape
+                    return (act @ w2).view(*x.shape[:-1], w2.shape[1])
+
+                @staticmethod
+                def backward(ctx, gy):
+                    x2, w1, w2, pre, act = ctx.saved_tensors
+                    acc1, acc2 = ctx.acc
+                    T, h = x2.shape
+                    N = w1.shape[1]
+                    g2 = gy.reshape(-1, gy.shape[-1]).to(x2.dtype).contiguous()
+                    dpre = torch.empty((T, N), dtype=x2.dtype, device=x2.device)
+                    call("ee_mlp_gelu_bwd", ptr(g2), ptr(w2), T, h, N, ptr(pre), ptr(dpre),
+                         stream_ptr())
+                    call("ee_wgrad_accum", ptr(act), ptr(g2), T, N, w2.shape[1], ptr(acc2),
+                         stream_ptr())
+                    gx = dpre @ w1.t()
+                    call("ee_wgrad_accum", ptr(x2), ptr(dpre), T, h, N, ptr(acc1), stream_ptr())
+                    return gx.view(ctx.shape), None, None, None, None
+
+            cls._fn = _F
+        return cls._fn
+
+
+_MLP_FUSE = os.environ.get("EE_MLP_FUSE", "1") != "0"  # A/B switch (profiling)
+
+
+def _mlp(params, prefix, h2):
+    """GELU(h2 @ w1) @ w2 of a block; in mixed mode through the fused-GELU
+    tcgen05 GEMMs (_MLPFn), else plain torch."""
+    torch = _torch()
+    acc = getattr(params, "main_grads", None)
+    n1, n2 = f"{prefix}.w1", f"{prefix}.w2"
+    w1, w2 = params[n1], params[n2]
+    if (_MLP_FUSE and acc is not None and n1 in acc and n2 in acc
+            and h2.dtype == w1.dtype == torch.bfloat16
+            and w1.shape[0] % 8 == 0 and w1.shape[1] % 8 == 0 and w2.shape[1] % 8 == 0
+            and h2.is_cuda):
+        return _MLPFn.get().apply(h2, w1, w2, acc[n1], acc[n2])
+    F = torch.nn.functional
+    return _matmul(params, n2, F.gelu(_matmul(params, n1, h2)))
 
 
 def _matmul(params, name, x):
@@ -407,7 +476,7 @@ def run_layer(params, prefix, x, num_heads):
     a = F.scaled_dot_product_attention(split(q), split(k), split(v), is_causal=True)
     x = x + _matmul(params, f"{prefix}.wo", a.transpose(1, 2).reshape(B, S, h))
     h2 = rmsnorm(x, params[f"{prefix}.mlp_norm"])
-    return x + _matmul(params, f"{prefix}.w2", F.gelu(_matmul(params, f"{prefix}.w1", h2)))
+    return x + _mlp(params, prefix, h2)
 
 
 def head_input(params, head, x, num_heads):

@@ -108,3 +108,32 @@ def test_mixed_precision_fused_wgrad_matches_plain():
     single_device_gradients(tm, batch, [0.3, 0.6, 1.0], 2)
     assert tm.params["layer1.w1"].grad is None
     assert float(tm.main_grads["layer1.w1"].abs().sum()) > 0
+
+
+@pytest.mark.parametrize("T,h,N", [(300, 64, 264), (4096, 2048, 8192)])
+def test_mlp_gelu_fused_gemms_match_torch(T, h, N):
+    """ee_mlp_up_gelu / ee_mlp_gelu_bwd (GELU fused into tcgen05 GEMM
+    epilogues, csrc/mlp_train.cu) against a float32 torch restatement on the
+    same bf16 inputs: pre, act and dpre within 1e-2 relative (Frobenius; bf16
+    outputs), ragged T / N included."""
+    import torch
+    from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+    g = torch.Generator(device="cuda").manual_seed(T + N)
+    x = (torch.randn(T, h, device="cuda", generator=g)).bfloat16()
+    w1 = (torch.randn(h, N, device="cuda", generator=g) * h ** -0.5).bfloat16()
+    w2 = (torch.randn(N, h, device="cuda", generator=g) * N ** -0.5).bfloat16()
+    dy = torch.randn(T, h, device="cuda", generator=g).bfloat16()
+    pre = torch.empty(T, N, dtype=torch.bfloat16, device="cuda")
+    act = torch.empty_like(pre)
+    dpre = torch.empty_like(pre)
+    call("ee_mlp_up_gelu", ptr(x), ptr(w1), T, h, N, ptr(pre), ptr(act), stream_ptr())
+    call("ee_mlp_gelu_bwd", ptr(dy), ptr(w2), T, h, N, ptr(pre), ptr(dpre), stream_ptr())
+    torch.cuda.synchronize()
+    ref_pre = x.float() @ w1.float()
+    ref_act = torch.nn.functional.gelu(ref_pre)
+    p = ref_pre.clone().requires_grad_()
+    torch.nn.functional.gelu(p).backward(dy.float() @ w2.float().t())
+    rel = lambda a, b: float((a.float() - b).norm() / b.norm())  # noqa: E731
+    assert rel(pre, ref_pre) < 1e-2
+    assert rel(act, ref_act) < 1e-2
+    assert rel(dpre, p.grad) < 1e-2
