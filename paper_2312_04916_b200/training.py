@@ -464,6 +464,19 @@ def rmsnorm(x, w, eps=NORM_EPS):
     return (xf * inv * w.float()).to(x.dtype)
 
 
+_SDPA = os.environ.get("EE_SDPA_BACKEND", "")  # profiling A/B: "", flash, efficient, cudnn
+
+
+def _sdpa_backend():
+    import contextlib
+    if not _SDPA:
+        return contextlib.nullcontext()
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    return sdpa_kernel({"flash": SDPBackend.FLASH_ATTENTION,
+                        "efficient": SDPBackend.EFFICIENT_ATTENTION,
+                        "cudnn": SDPBackend.CUDNN_ATTENTION}[_SDPA])
+
+
 def run_layer(params, prefix, x, num_heads):
     """One pre-norm block (`eepipe/model.py:207-216`)."""
     torch = _torch()
@@ -473,7 +486,8 @@ def run_layer(params, prefix, x, num_heads):
     h1 = rmsnorm(x, params[f"{prefix}.attn_norm"])
     q, k, v = (_matmul(params, f"{prefix}.{w}", h1) for w in ("wq", "wk", "wv"))
     split = lambda t: t.view(B, S, num_heads, dh).transpose(1, 2)  # noqa: E731
-    a = F.scaled_dot_product_attention(split(q), split(k), split(v), is_causal=True)
+    with _sdpa_backend():
+        a = F.scaled_dot_product_attention(split(q), split(k), split(v), is_causal=True)
     x = x + _matmul(params, f"{prefix}.wo", a.transpose(1, 2).reshape(B, S, h))
     h2 = rmsnorm(x, params[f"{prefix}.mlp_norm"])
     return x + _mlp(params, prefix, h2)

@@ -1,6 +1,7 @@
 """Small end-to-end run of every kernel family for compute-sanitizer:
 tiled bf16 decode (KV recompute + pipeline, prefill GEMM, attention, heads),
-fp32 parity decode, fused train head, RMSNorm, optimizer."""
+fp32 parity decode, fused train head, RMSNorm, optimizer, fused-GELU MLP
+GEMMs, weight-gradient accumulation, multi-row long-context attention."""
 import os
 import sys
 
@@ -29,6 +30,28 @@ def main():
     xr = torch.randn(37, 264, device="cuda").bfloat16().requires_grad_()
     wr = torch.ones(264, device="cuda", requires_grad=True)
     rmsnorm(xr, wr).sum().backward()
+    from paper_2312_04916_b200 import _lib
+    from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+    T, h, N = 300, 64, 264  # ragged: partial row and column tiles
+    xm = torch.randn(T, h, device="cuda").bfloat16()
+    w1 = (torch.randn(h, N, device="cuda") * 0.1).bfloat16()
+    w2 = (torch.randn(N, h, device="cuda") * 0.1).bfloat16()
+    pre = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
+    act, dpre = torch.empty_like(pre), torch.empty_like(pre)
+    call("ee_mlp_up_gelu", ptr(xm), ptr(w1), T, h, N, ptr(pre), ptr(act), stream_ptr())
+    call("ee_mlp_gelu_bwd", ptr(xm), ptr(w2), T, h, N, ptr(pre), ptr(dpre), stream_ptr())
+    acc = torch.zeros(h, N, device="cuda")
+    call("ee_wgrad_accum", ptr(xm), ptr(dpre), T, h, N, ptr(acc), stream_ptr())
+    nh, dh, smax = 4, 128, 2048  # rows spanning several chunks -> k_attn_rows128
+    kc = torch.randn(smax, nh * dh, device="cuda").bfloat16()
+    vc = torch.randn(smax, nh * dh, device="cuda").bfloat16()
+    q = torch.randn(5, nh * dh, device="cuda")
+    pos = torch.tensor([700, 1023, 1500, 2000, 2047], dtype=torch.int32, device="cuda")
+    out = torch.empty(5, nh * dh, dtype=torch.bfloat16, device="cuda")
+    wsb = _lib.load().ee_workspace_bytes(_lib.EE_OP_ATTENTION, 5, nh * dh, 0, nh, smax)
+    ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
+    call("ee_decode_attention", ptr(q), 5, ptr(pos), 2047, ptr(kc), ptr(vc), nh, dh,
+         _lib.EE_BF16, ptr(out), ptr(ws), wsb, stream_ptr())
     p = {"a": torch.zeros(1003, device="cuda")}
     Adam(1e-3).step(p, {"a": torch.ones(1003, device="cuda")}, 0.5)
     torch.cuda.synchronize()
