@@ -585,6 +585,24 @@ def _assign_fill_data(data, row_len, options: IterationOptions, depths):
         k += 1
 
 
+_STAGE_EXECUTORS = {}
+
+
+def _stage_executor(device, stage):
+    """One persistent worker thread per (device, stage): library state that
+    is per host thread (the cuDNN handle and its attention execution-plan
+    cache) survives across iterations — a fresh thread per iteration rebuilt
+    the SDPA plan, a ~50 ms host stall at the first attention of every
+    step."""
+    from concurrent.futures import ThreadPoolExecutor
+    key = (str(device), stage)
+    ex = _STAGE_EXECUTORS.get(key)
+    if ex is None:
+        ex = _STAGE_EXECUTORS[key] = ThreadPoolExecutor(max_workers=1,
+                                                        thread_name_prefix=f"stage-{stage}")
+    return ex
+
+
 def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
                        devices=None, dtype=None, master_dtype=None, stage_computes=None,
                        compute_factory=None):
@@ -656,18 +674,16 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
             w.run()
             torch.cuda.current_stream(dev).synchronize()
 
-    threads = [threading.Thread(target=target, args=(w,), daemon=True, name=f"stage-{w.index}")
-               for w in workers]
     t_start = time.perf_counter()
     import sys
     old_switch = sys.getswitchinterval()
     if P > 1:  # several launch-bound stage threads: hand the GIL over quickly
         sys.setswitchinterval(5e-5)
     try:
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join(timeout=_RECV_TIMEOUT * 2)
+        futures = [_stage_executor(torch.device(w.compute.device), w.index).submit(target, w)
+                   for w in workers]
+        for f in futures:
+            f.result(timeout=_RECV_TIMEOUT * 2)
     finally:
         sys.setswitchinterval(old_switch)
     elapsed = time.perf_counter() - t_start

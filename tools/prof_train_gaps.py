@@ -58,6 +58,14 @@ def main():
         print(f"  gaps ({lo}, {hi}] us: n={len(sel)} sum={sum(sel)/1e3:.1f} ms")
     for (a, b), (c, t) in sorted(pairs.items(), key=lambda x: -x[1][1])[:14]:
         print(f"  {c:5d}x {t/1e3:7.2f} ms  after {a!r} before {b!r}")
+    t0 = ev[0].time_range.start
+    end, prev = ev[0].time_range.end, ev[0]
+    for e in ev[1:]:
+        g = e.time_range.start - end
+        if g > 1000:
+            print(f"  big gap {g/1e3:.2f} ms at {(end - t0)/1e3:.1f} ms: after {prev.name[:50]!r} before {e.name[:50]!r}")
+        if e.time_range.end >= end:
+            end, prev = e.time_range.end, e
 
 
 
@@ -81,9 +89,19 @@ def cpu_table():
 
     for _ in range(2):
         step()
-    with profile(activities=[ProfilerActivity.CPU], with_stack=False) as prof:
+    with profile(activities=[ProfilerActivity.CPU], with_stack=True) as prof:
         step()
     print(prof.key_averages().table(sort_by="self_cpu_time_total", row_limit=25))
+    seen = {}
+    for e in prof.events():
+        if e.name in ("cudaStreamSynchronize", "cudaEventSynchronize"):
+            st = " <- ".join(f for f in (e.stack or [])[:6])
+            key = (e.name, st)
+            seen.setdefault(key, [0, 0.0])
+            seen[key][0] += 1
+            seen[key][1] += e.cpu_time_total
+    for (n, st), (c, t) in sorted(seen.items(), key=lambda x: -x[1][1])[:8]:
+        print(f"{n} x{c} {t/1e3:.1f} ms: {st}")
 
 
 if __name__ == "__main__":
