@@ -100,6 +100,7 @@ class IterationOptions:
     hoist_exit_heads: bool = True
     fill_plan: object = None   # bubblefill.FillPlan
     fill_batch: object = None  # rows of the extra (fill) microbatches
+    cost: object = None        # schedule.CostModel overriding the simulator's preset times
 
 
 @dataclass
@@ -547,6 +548,26 @@ def _stage_stream(device, stage):
     return st
 
 
+def cost_model_from_partition(part: StagePartition, num_microbatches: int,
+                              microbatch_size: int, seq_len: int, base=None):
+    """The schedule cost model of a partition (`eepipe/pipeline.py:262-285`):
+    early exits per stage from the partition, the preset (or ``base``)
+    step times."""
+    cfg = part.config
+    counts = [0] * part.num_stages
+    for st in part.stages:
+        counts[st.index - 1] = sum(1 for _, hd in st.heads if not hd.is_final)
+    kw = dict(num_stages=part.num_stages, num_microbatches=num_microbatches,
+              exit_counts=tuple(counts), seq_len=seq_len, microbatch_size=microbatch_size,
+              vocab_size=cfg.vocab_size, hidden_dim=cfg.hidden_dim,
+              layers_per_stage=cfg.num_layers // part.num_stages)
+    if base is not None:
+        kw.update(fwd_time=base.fwd_time, bwd_time=base.bwd_time,
+                  exit_fwd_time=base.exit_fwd_time, exit_bwd_time=base.exit_bwd_time,
+                  embed_fwd_time=base.embed_fwd_time, p2p_latency=base.p2p_latency)
+    return sched.CostModel(**kw)
+
+
 def apply_fill(plan, part: StagePartition, num_microbatches: int):
     """Validate a fill plan against a partition; returns (truncated Part-1
     depths, FillRescale) (eepipe/pipeline.py:244-259).  Tied parameters
@@ -639,6 +660,14 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
         for hd in all_heads:
             if not hd.is_final:
                 wmap[hd.key] = wmap[hd.key] * rescale.weight_scale_for(part.stage_of_head(hd.key))
+    # the per-stage action order is the simulated timeline's
+    # (eepipe/pipeline.py:553-557, 587): the 1F1B lists, with fills placed
+    # where the cost model finds the bubbles
+    seq_len = int(np.asarray(batch).shape[1]) - 1
+    timeline = sched.simulate(
+        cost_model_from_partition(part, M, options.microbatch_size, seq_len, options.cost),
+        "deferred-exit" if options.defer_exit_forward else "eager-exit",
+        plan if fill is not None else None)
     devices = devices or ["cuda:0"] * P
     src = model
     fwd = [TaggedChannel(f"act {s}->{s + 1}") for s in range(1, P)]
@@ -657,12 +686,11 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
                                 dtype, master_dtype)
             if stage_computes is not None:
                 stage_computes.append(comp)
-        acts = (sched.fill_actions(P, M, s, depths, plan.part2_bwd_depths) if fill is not None
-                else None)
         workers.append(StageWorker(s, P, M, comp, data,
                                    fwd[s - 2] if s > 1 else None, fwd[s - 1] if s < P else None,
                                    bwd[s - 1] if s < P else None, bwd[s - 2] if s > 1 else None,
-                                   options.hoist_exit_heads, actions=acts, fill=fill))
+                                   options.hoist_exit_heads, actions=timeline.order(s),
+                                   fill=fill))
     torch = _torch()
 
     def target(w):
@@ -701,7 +729,8 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
     merged = sync_tied(per_stage, part.tied_replicas)
     n_fill = sum(1 for d in depths if d is not None) + (len(plan.part2_bwd_depths)
                                                          if fill is not None else 0)
-    report = TrainStepReport(weights_used=tuple(weights), microbatches=M + n_fill)
+    report = TrainStepReport(weights_used=tuple(weights), microbatches=M + n_fill,
+                             timeline=timeline)
     for w, g in zip(workers, per_stage):
         report.event_log.append(list(w.event_log))
         report.memory.append(StageMemoryCounters(w.index, w.max_in_flight, w.max_fill_stored))

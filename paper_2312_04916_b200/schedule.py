@@ -10,19 +10,23 @@ Only the parts on the path are restated:
   early-exit inference vs sequential full passes
   (`eepipe/schedule.py:553-590`).  Reported next to measured latency.
 
-* `fill_actions` — the 1F1B list with bubble-fill microbatches inserted
-  (`eepipe/schedule.py:182-209`): Part-1 fills between the warm-up forwards
-  and the first steady forward exactly as the reference; Part-2 fills at the
-  front of each stage's list (the reference slots them into idle gaps with
-  its cost model, `eepipe/schedule.py:275-304`; the gradients do not depend
-  on the placement, and every placement here is deadlock-free because fill
-  actions only wait on the same fill's neighbours).
+* `CostModel`, `simulate` (+ `Timeline`, `Event`, `analytic_span`) — the
+  discrete-event model the executor takes its per-stage order from
+  (`eepipe/schedule.py:41-122`, `124-348`): structural lists with Part-1
+  fills between warm-up and steady phase, earliest-start list scheduling
+  along the forward / backward chains, then Part-2 fill chains packed into
+  the idle gaps (earliest fit), validated.  `Timeline.order(s)` is what a
+  stage executes.
+* `fill_actions` — a purely structural fill placement (Part-2 at the front
+  of each list) kept for callers without a cost model.
 
-The reference's cost-model simulator, memory accounting and Gantt rendering
+Memory accounting (`peak_memory`), replay verification and Gantt rendering
 are out of scope.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
 
 from .errors import ConfigError
 
@@ -107,3 +111,280 @@ def inference_latency(exit_stages, stage_times) -> dict:
         "per_token_speedup": [full / t for t in per_token],
         "total_speedup": seq_total / total if total else 1.0,
     }
+
+
+# ---------------------------------------------------------------------------
+# Discrete-event schedule model (eepipe/schedule.py:41-348)
+# ---------------------------------------------------------------------------
+
+VARIANTS = ("standard", "eager-exit", "deferred-exit")
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """Abstract per-step costs (`eepipe/schedule.py:41-80`): forward /
+    backward time per stage, per-exit forward / backward time, early exits
+    per stage (the final head always sits on the last stage and is computed
+    eagerly), embedding time on stage 1, point-to-point latency; the
+    memory-dimension fields are carried for API compatibility."""
+
+    num_stages: int
+    num_microbatches: int
+    fwd_time: float = 1.0
+    bwd_time: float = 2.0
+    exit_fwd_time: float = 0.5
+    exit_bwd_time: float = 1.0
+    exit_counts: tuple = ()
+    seq_len: int = 64
+    microbatch_size: int = 4
+    vocab_size: int = 256
+    hidden_dim: int = 64
+    layers_per_stage: int = 2
+    embed_fwd_time: float = 0.0
+    p2p_latency: float = 0.0
+
+    def __post_init__(self):
+        if self.num_stages < 1 or self.num_microbatches < 1:
+            raise ConfigError("need at least one stage and one microbatch")
+        if min(self.fwd_time, self.bwd_time, self.exit_fwd_time, self.exit_bwd_time) <= 0:
+            raise ConfigError("all times must be positive")
+        counts = tuple(self.exit_counts) if self.exit_counts else (0,) * self.num_stages
+        if len(counts) != self.num_stages:
+            raise ConfigError("exit_counts length must equal num_stages")
+        object.__setattr__(self, "exit_counts", counts)
+
+    def early_exits_on(self, stage):
+        return self.exit_counts[stage - 1]
+
+    def exit_stages(self):
+        return [s for s in range(1, self.num_stages + 1) if self.exit_counts[s - 1]]
+
+
+@dataclass(frozen=True)
+class Event:
+    kind: str
+    mb: int  # regular microbatch (1-based) or fill index
+    stage: int
+    start: float = 0.0
+    end: float = 0.0
+
+    @property
+    def duration(self):
+        return self.end - self.start
+
+    def tag(self):
+        return (self.kind, self.mb)
+
+
+@dataclass
+class Timeline:
+    """Simulated iteration (`eepipe/schedule.py:106-121`)."""
+
+    cost: CostModel
+    variant: str
+    fill_plan: object
+    events: list  # per stage, execution order
+    span: float
+    busy: list
+    decomposition: dict
+    bubble_assumption_violated: bool
+    part1_depths: list = field(default_factory=list)
+
+    def stage_events(self, stage):
+        return self.events[stage - 1]
+
+    def order(self, stage):
+        return [e.tag() for e in self.events[stage - 1]]
+
+
+def _duration_fn(cost: CostModel, variant: str):
+    """(kind, stage) -> duration (`eepipe/schedule.py:124-167`).  Eager exits
+    add their forward to the forward step and their backward to the
+    backward step; deferred exits run forward + backward inside the backward
+    step; the final head is always forward-eager on the last stage."""
+    last = cost.num_stages
+
+    def forward(stage, exits):
+        t = cost.fwd_time + (cost.embed_fwd_time if stage == 1 else 0.0)
+        if exits and variant == "eager-exit":
+            t += cost.exit_fwd_time * cost.early_exits_on(stage)
+        return t + (cost.exit_fwd_time if stage == last else 0.0)
+
+    def backward(stage, exits):
+        t = cost.bwd_time
+        if exits:
+            k = cost.early_exits_on(stage)
+            if variant == "eager-exit":
+                t += cost.exit_bwd_time * k
+            elif variant == "deferred-exit":
+                t += (cost.exit_fwd_time + cost.exit_bwd_time) * k
+        return t + (cost.exit_bwd_time if stage == last else 0.0)
+
+    def duration(kind, stage):
+        if kind == FWD:
+            return forward(stage, True)
+        if kind == BWD:
+            return backward(stage, True)
+        if kind == FILL1_FWD:  # backbone only: the fill's exits run in its backward
+            return cost.fwd_time + (cost.embed_fwd_time if stage == 1 else 0.0)
+        if kind == FILL1_BWD:
+            return cost.bwd_time + (cost.exit_fwd_time + cost.exit_bwd_time) * \
+                cost.early_exits_on(stage)
+        if kind == FILL2_FWD:
+            return forward(stage, False)
+        if kind == FILL2_BWD:
+            return backward(stage, variant == "deferred-exit")
+        raise ValueError(kind)
+
+    return duration
+
+
+def build_action_lists(cost: CostModel, variant: str, fill_plan=None):
+    """Structural per-stage lists with the Part-1 fills slotted between the
+    warm-up forwards and the first steady forward (`eepipe/schedule.py:
+    182-209`).  Returns (lists, truncated Part-1 depths)."""
+    from .bubblefill import truncated_part1_depths
+    p, m = cost.num_stages, cost.num_microbatches
+    lists = [regular_actions(p, m, s) for s in range(1, p + 1)]
+    depths: list = []
+    if fill_plan is not None and not fill_plan.empty:
+        if variant == "eager-exit":
+            raise ConfigError("bubble filling requires the deferred-exit or standard variant")
+        if fill_plan.num_stages != p:
+            raise ConfigError("fill plan stage count does not match the cost model")
+        if m < p:
+            raise ConfigError("bubble filling needs at least P microbatches")
+        depths = truncated_part1_depths(fill_plan, cost.exit_stages())
+        for s in range(1, p + 1):
+            lists[s - 1] = fill_actions(p, m, s, depths, ())
+    return lists, depths
+
+
+def _waits_on(kind, mb, stage, p, part1_depths):
+    """The cross-stage event an action depends on (`eepipe/schedule.py:
+    212-227`), or None."""
+    if kind in (FWD, FILL1_FWD, FILL2_FWD):
+        return (kind, mb, stage - 1) if stage > 1 else None
+    if kind == BWD:
+        return (BWD, mb, stage + 1) if stage < p else (FWD, mb, stage)
+    if kind == FILL1_BWD:
+        d = part1_depths[mb - 1]
+        return (FILL1_BWD, mb, stage + 1) if stage < d else (FILL1_FWD, mb, stage)
+    if kind == FILL2_BWD:
+        return (FILL2_BWD, mb, stage + 1) if stage < p else (FILL2_FWD, mb, stage)
+    raise ValueError(kind)
+
+
+def _schedule_lists(cost, variant, lists, part1_depths):
+    """Earliest start for every action, in list order per stage, after its
+    cross-stage dependency (+ p2p latency) (`eepipe/schedule.py:230-260`)."""
+    p = cost.num_stages
+    dur = _duration_fn(cost, variant)
+    finished: dict = {}
+    nxt = [0] * p
+    free = [0.0] * p
+    events = [[] for _ in range(p)]
+    remaining = sum(len(lst) for lst in lists)
+    while remaining:
+        moved = False
+        for s in range(1, p + 1):
+            lst = lists[s - 1]
+            while nxt[s - 1] < len(lst):
+                kind, mb = lst[nxt[s - 1]]
+                dep = _waits_on(kind, mb, s, p, part1_depths)
+                if dep is not None and dep not in finished:
+                    break
+                ready = finished[dep] + cost.p2p_latency if dep is not None else 0.0
+                start = max(ready, free[s - 1])
+                end = start + dur(kind, s)
+                events[s - 1].append(Event(kind, mb, s, start, end))
+                finished[(kind, mb, s)] = end
+                free[s - 1] = end
+                nxt[s - 1] += 1
+                remaining -= 1
+                moved = True
+        if not moved:
+            raise ConfigError("action lists deadlock: unsatisfiable dependency")
+    return events
+
+
+def _idle_gaps(stage_events):
+    """[(start, end)] idle intervals of a stage, with the open tail last."""
+    gaps, t = [], 0.0
+    for e in stage_events:
+        if e.start > t:
+            gaps.append((t, e.start))
+        t = max(t, e.end)
+    gaps.append((t, float("inf")))
+    return gaps
+
+
+def _pack_part2(cost, variant, events, plan):
+    """Part-2 chains (forward through every stage, backward through the last
+    r) packed into idle gaps without moving existing events: earliest fit per
+    element, same-kind order per stage kept (`eepipe/schedule.py:275-304`)."""
+    p = cost.num_stages
+    dur = _duration_fn(cost, variant)
+    last_same: dict = {}
+    for i, r in enumerate(plan.part2_bwd_depths, 1):
+        chain = [(FILL2_FWD, s) for s in range(1, p + 1)]
+        chain += [(FILL2_BWD, s) for s in range(p, p - r, -1)]
+        ready = 0.0
+        for kind, s in chain:
+            floor = max(ready, last_same.get((kind, s), 0.0))
+            d = dur(kind, s)
+            start = floor
+            for g0, g1 in _idle_gaps(events[s - 1]):
+                start = max(g0, floor)
+                if start + d <= g1 + 1e-9:
+                    break
+            ev = Event(kind, i, s, start, start + d)
+            events[s - 1].append(ev)
+            events[s - 1].sort(key=lambda e: e.start)
+            last_same[(kind, s)] = ev.end
+            ready = ev.end + cost.p2p_latency
+    return events
+
+
+def _check_timeline(cost, events, part1_depths):
+    p = cost.num_stages
+    end = {(e.kind, e.mb, e.stage): e.end for evs in events for e in evs}
+    start = {(e.kind, e.mb, e.stage): e.start for evs in events for e in evs}
+    for evs in events:
+        for a, b in zip(evs, evs[1:]):
+            if b.start < a.end - 1e-9:
+                raise AssertionError(f"overlapping events on stage {a.stage}")
+    for key, t0 in start.items():
+        dep = _waits_on(key[0], key[1], key[2], p, part1_depths)
+        if dep is not None and t0 < end[dep] + cost.p2p_latency - 1e-9:
+            raise AssertionError(f"event {key} starts before its dependency {dep}")
+
+
+def analytic_span(cost: CostModel, variant: str) -> dict:
+    """First microbatch's forwards + last stage's steady phase + last
+    microbatch's backwards (`eepipe/schedule.py:321-330`)."""
+    p, m = cost.num_stages, cost.num_microbatches
+    dur = _duration_fn(cost, variant)
+    warm = sum(dur(FWD, s) for s in range(1, p + 1))
+    steady = (m - 1) * (dur(FWD, p) + dur(BWD, p)) + dur(BWD, p)
+    cool = sum(dur(BWD, s) for s in range(1, p))
+    return {"warmup": warm, "steady": steady, "cooldown": cool, "total": warm + steady + cool}
+
+
+def simulate(cost: CostModel, variant: str, fill_plan=None) -> Timeline:
+    """The timeline the executor follows (`eepipe/schedule.py:333-348`)."""
+    if variant not in VARIANTS:
+        raise ConfigError(f"unknown variant {variant!r}")
+    if variant == "standard":
+        cost = replace(cost, exit_counts=(0,) * cost.num_stages)
+    lists, depths = build_action_lists(cost, variant, fill_plan)
+    events = _schedule_lists(cost, variant, lists, depths)
+    if fill_plan is not None and fill_plan.part2_bwd_depths:
+        events = _pack_part2(cost, variant, events, fill_plan)
+    _check_timeline(cost, events, depths)
+    span = max(e.end for evs in events for e in evs)
+    busy = [sum(e.duration for e in evs) for evs in events]
+    decomposition = analytic_span(cost, variant)
+    violated = fill_plan is None and span > decomposition["total"] + 1e-9
+    return Timeline(cost, variant, fill_plan, events, span, busy, decomposition, violated,
+                    list(depths))

@@ -326,7 +326,10 @@ def test_full_fill_plan_matches_filled_objective(f_over_b, seed):
     for n in want:
         np.testing.assert_allclose(filled[n], want[n], rtol=1e-10, atol=1e-13)
     assert rep.microbatches == 4 + n_extra
-    assert all(len(v) > 0 for v in rep.event_log)
+    # every stage executed exactly the simulated timeline's order
+    # (the first check of eepipe's verify_against_replay)
+    for s in range(1, 5):
+        assert rep.event_log[s - 1] == rep.timeline.order(s), s
     assert max(m.peak_fill_stored for m in rep.memory) >= 1
 
 
@@ -341,3 +344,27 @@ def test_fill_rejects_tied_parameters_and_bad_inputs():
     batch = rng.integers(0, VOCAB, size=(8, 9))
     with pytest.raises(ConfigError):  # no fill batch
         _run(part, params, batch, plan_bubble_fill(4, 0.5))
+
+
+def test_simulator_matches_reference_timelines():
+    """schedule.simulate (structural lists, earliest-start list scheduling,
+    Part-2 gap packing) reproduces the reference simulator's per-stage event
+    order, span, analytic decomposition and bubble flag over 300+ timelines
+    (P 2-8, M P..2P, four exit placements, three variants, with and without
+    bubble filling; tests/golden/make_schedule.py)."""
+    import json
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    with open(os.path.join(here, "schedule.json")) as f:
+        gold = json.load(f)
+    assert len(gold) > 300
+    for g in gold:
+        c = sched.CostModel(g["P"], g["M"], exit_counts=tuple(g["exit_counts"]),
+                            embed_fwd_time=0.3, p2p_latency=0.05)
+        plan = plan_bubble_fill(g["P"], g["f_over_b"]) if g["f_over_b"] else None
+        t = sched.simulate(c, g["variant"], plan)
+        for s in range(1, g["P"] + 1):
+            assert t.order(s) == [tuple(a) for a in g["orders"][s - 1]], (g["P"], g["M"], s)
+        assert t.span == pytest.approx(g["span"], abs=1e-9)
+        assert t.decomposition == pytest.approx(g["decomposition"])
+        assert t.bubble_assumption_violated == g["violated"]
