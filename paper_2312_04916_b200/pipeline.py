@@ -700,6 +700,8 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
             return
         with torch.cuda.device(dev), torch.cuda.stream(_stage_stream(dev, w.index)):
             w.run()
+            from .training import join_wgrad
+            join_wgrad(dev)
             torch.cuda.current_stream(dev).synchronize()
 
     t_start = time.perf_counter()

@@ -200,6 +200,46 @@ class _ParamView(dict):
         self.main_grads = main_grads
 
 
+_WGRAD_SIDE = {}
+_WGRAD_OVERLAP = os.environ.get("EE_WGRAD_STREAM", "1") != "0"
+
+
+def _wgrad_accum(x2, g2, acc):
+    """acc (float32, in x out) += x2^T g2 (ee_wgrad_accum).  The weight
+    gradient is off the backward's critical path (nothing downstream reads it
+    before the optimizer), so it runs on a side stream of the current stream:
+    its under-filled waves (64 tiles on 74 CTA pairs at 2048 x 2048) and
+    tails overlap the input-gradient GEMMs.  `join_wgrad` orders the current
+    stream after it (iteration end)."""
+    torch = _torch()
+    cur = torch.cuda.current_stream(x2.device)
+    side = None
+    if _WGRAD_OVERLAP:
+        key = cur.cuda_stream
+        side = _WGRAD_SIDE.get(key)
+        if side is None:
+            side = _WGRAD_SIDE[key] = torch.cuda.Stream(x2.device)
+        side.wait_stream(cur)
+    if side is None:
+        call("ee_wgrad_accum", ptr(x2), ptr(g2), x2.shape[0], x2.shape[1], g2.shape[1], ptr(acc),
+             stream_ptr())
+        return
+    call("ee_wgrad_accum", ptr(x2), ptr(g2), x2.shape[0], x2.shape[1], g2.shape[1], ptr(acc),
+         ctypes.c_void_p(side.cuda_stream))
+    x2.record_stream(side)
+    g2.record_stream(side)
+
+
+def join_wgrad(device=None):
+    """Order the current stream after every weight-gradient accumulation
+    issued from it (call before reading the float32 gradient sums)."""
+    torch = _torch()
+    cur = torch.cuda.current_stream(device)
+    side = _WGRAD_SIDE.get(cur.cuda_stream)
+    if side is not None:
+        cur.wait_stream(side)
+
+
 class _LinearFn:
     """y = x @ W (bf16) whose backward computes dX with torch and accumulates
     dW = X^T dY into the float32 main gradient with the CTA-pair tcgen05 GEMM
@@ -225,8 +265,7 @@ class _LinearFn:
                     gx = gy @ w.t()
                     x2 = x.reshape(-1, x.shape[-1]).contiguous()
                     g2 = gy.reshape(-1, gy.shape[-1]).to(x2.dtype).contiguous()
-                    call("ee_wgrad_accum", ptr(x2), ptr(g2), x2.shape[0], x2.shape[1], g2.shape[1],
-                         ptr(ctx.acc), stream_ptr())
+                    _wgrad_accum(x2, g2, ctx.acc)
                     return gx, None, None
 
             cls._fn = _F
@@ -272,10 +311,9 @@ class _MLPFn:
                     dpre = torch.empty((T, N), dtype=x2.dtype, device=x2.device)
                     call("ee_mlp_gelu_bwd", ptr(g2), ptr(w2), T, h, N, ptr(pre), ptr(dpre),
                          stream_ptr())
-                    call("ee_wgrad_accum", ptr(act), ptr(g2), T, N, w2.shape[1], ptr(acc2),
-                         stream_ptr())
+                    _wgrad_accum(act, g2, acc2)
                     gx = dpre @ w1.t()
-                    call("ee_wgrad_accum", ptr(x2), ptr(dpre), T, h, N, ptr(acc1), stream_ptr())
+                    _wgrad_accum(x2, dpre, acc1)
                     return gx.view(ctx.shape), None, None, None, None
 
             cls._fn = _F
@@ -397,6 +435,7 @@ class TrainModel:
 
     def grads(self):
         if self.mixed:
+            join_wgrad(self.device)  # side-stream weight gradients (_wgrad_accum)
             return dict(self.main_grads)
         return {n: p.grad for n, p in self.params.items() if p.grad is not None}
 
