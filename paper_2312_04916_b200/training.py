@@ -254,10 +254,17 @@ class _LinearFn:
 
             class _F(torch.autograd.Function):
                 @staticmethod
-                def forward(ctx, x, w, acc):
+                def forward(ctx, x, w, acc, res):
                     ctx.save_for_backward(x, w)
                     ctx.acc = acc
-                    return x @ w
+                    ctx.has_res = res is not None
+                    if res is None:
+                        return x @ w
+                    # residual added by the GEMM itself (beta = 1): one rounding,
+                    # no separate add pass over the (T, h) rows
+                    out = torch.addmm(res.reshape(-1, res.shape[-1]),
+                                      x.reshape(-1, x.shape[-1]), w)
+                    return out.view(res.shape)
 
                 @staticmethod
                 def backward(ctx, gy):
@@ -266,7 +273,7 @@ class _LinearFn:
                     x2 = x.reshape(-1, x.shape[-1]).contiguous()
                     g2 = gy.reshape(-1, gy.shape[-1]).to(x2.dtype).contiguous()
                     _wgrad_accum(x2, g2, ctx.acc)
-                    return gx, None, None
+                    return gx, None, None, (gy if ctx.has_res else None)
 
             cls._fn = _F
         return cls._fn
@@ -288,7 +295,7 @@ class _MLPFn:
 
             class _F(torch.autograd.Function):
                 @staticmethod
-                def forward(ctx, x, w1, w2, acc1, acc2):
+                def forward(ctx, x, w1, w2, acc1, acc2, res):
                     x2 = x.reshape(-1, x.shape[-1]).contiguous()
                     T, h = x2.shape
                     N = w1.shape[1]
@@ -299,7 +306,10 @@ class _MLPFn:
                     ctx.save_for_backward(x2, w1, w2, pre, act)
                     ctx.acc = (acc1, acc2)
                     ctx.shape = x.shape
-                    return (act @ w2).view(*x.shape[:-1], w2.shape[1])
+                    ctx.has_res = res is not None
+                    if res is None:
+                        return (act @ w2).view(*x.shape[:-1], w2.shape[1])
+                    return torch.addmm(res.reshape(-1, res.shape[-1]), act, w2).view(res.shape)
 
                 @staticmethod
                 def backward(ctx, gy):
@@ -314,7 +324,8 @@ class _MLPFn:
                     _wgrad_accum(act, g2, acc2)
                     gx = dpre @ w1.t()
                     _wgrad_accum(x2, dpre, acc1)
-                    return gx.view(ctx.shape), None, None, None, None
+                    return (gx.view(ctx.shape), None, None, None, None,
+                            gy if ctx.has_res else None)
 
             cls._fn = _F
         return cls._fn
@@ -323,9 +334,10 @@ class _MLPFn:
 _MLP_FUSE = os.environ.get("EE_MLP_FUSE", "1") != "0"  # A/B switch (profiling)
 
 
-def _mlp(params, prefix, h2):
-    """GELU(h2 @ w1) @ w2 of a block; in mixed mode through the fused-GELU
-    tcgen05 GEMMs (_MLPFn), else plain torch."""
+def _mlp(params, prefix, h2, residual=None):
+    """[residual +] GELU(h2 @ w1) @ w2 of a block; in mixed mode through the
+    fused-GELU tcgen05 GEMMs (_MLPFn, residual added by the down GEMM), else
+    plain torch."""
     torch = _torch()
     acc = getattr(params, "main_grads", None)
     n1, n2 = f"{prefix}.w1", f"{prefix}.w2"
@@ -334,19 +346,20 @@ def _mlp(params, prefix, h2):
             and h2.dtype == w1.dtype == torch.bfloat16
             and w1.shape[0] % 8 == 0 and w1.shape[1] % 8 == 0 and w2.shape[1] % 8 == 0
             and h2.is_cuda):
-        return _MLPFn.get().apply(h2, w1, w2, acc[n1], acc[n2])
+        return _MLPFn.get().apply(h2, w1, w2, acc[n1], acc[n2], residual)
     F = torch.nn.functional
-    return _matmul(params, n2, F.gelu(_matmul(params, n1, h2)))
+    return _matmul(params, n2, F.gelu(_matmul(params, n1, h2)), residual)
 
 
-def _matmul(params, name, x):
-    """x @ params[name]; in mixed mode through the fused-accumulation linear."""
+def _matmul(params, name, x, residual=None):
+    """[residual +] x @ params[name]; in mixed mode through the
+    fused-accumulation linear (residual added by the GEMM)."""
     acc = getattr(params, "main_grads", None)
     w = params[name]
     if acc is not None and name in acc and x.dtype == w.dtype and w.shape[0] % 8 == 0 \
             and w.shape[1] % 8 == 0:
-        return _LinearFn.get().apply(x, w, acc[name])
-    return x @ w
+        return _LinearFn.get().apply(x, w, acc[name], residual)
+    return x @ w if residual is None else residual + x @ w
 
 
 class TrainModel:
@@ -574,9 +587,9 @@ def run_layer(params, prefix, x, num_heads):
     split = lambda t: t.view(B, S, num_heads, dh).transpose(1, 2)  # noqa: E731
     with _sdpa_backend():
         a = F.scaled_dot_product_attention(split(q), split(k), split(v), is_causal=True)
-    x = x + _matmul(params, f"{prefix}.wo", a.transpose(1, 2).reshape(B, S, h))
+    x = _matmul(params, f"{prefix}.wo", a.transpose(1, 2).reshape(B, S, h), residual=x)
     h2 = rmsnorm(x, params[f"{prefix}.mlp_norm"])
-    return x + _mlp(params, prefix, h2)
+    return _mlp(params, prefix, h2, residual=x)
 
 
 def head_input(params, head, x, num_heads):
