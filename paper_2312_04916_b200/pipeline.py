@@ -169,6 +169,10 @@ def _grad_norm(grads):
     return float(torch.linalg.vector_norm(torch.stack(norms).double()))
 
 
+_KIND_CODE = {"mb": 0, "p1": 1, "p2": 2}
+_KIND_NAME = {v: k for k, v in _KIND_CODE.items()}
+
+
 def _tag(mb):
     """Message tags: ("mb", k) regular microbatch k, ("p1", i) / ("p2", i)
     Part-1 / Part-2 fill i (eepipe/pipeline.py:86-122); a bare int is a
@@ -249,6 +253,7 @@ class DistChannel:
         self.last = 0
         self.count = 0
         self.pending = []
+        self.stash = {}
 
     def send(self, msg):
         torch = _torch()
@@ -257,9 +262,7 @@ class DistChannel:
         if tuple(data.shape) != self.shape:
             raise ShapeError(f"channel expects {self.shape}, got {tuple(data.shape)}")
         tag = _tag(msg.mb)
-        if tag[0] != "mb":
-            raise ConfigError("bubble-fill messages are not supported over torch.distributed")
-        hdr = torch.tensor([tag[1]], dtype=torch.int64, device=self.device)
+        hdr = torch.tensor([_KIND_CODE[tag[0]], tag[1]], dtype=torch.int64, device=self.device)
         # keep the tensors alive until their sends complete
         self.pending.append((dist.isend(hdr, self.peer, group=self.group), hdr))
         self.pending.append((dist.isend(data, self.peer, group=self.group), data))
@@ -271,21 +274,30 @@ class DistChannel:
         self.pending = []
 
     def recv(self, tag):
+        """Messages arrive in the sender's order (NCCL matches point-to-point
+        operations in order); each carries its tag, so a message requested
+        later than it arrives is stashed, like the reference's tagged queue
+        (eepipe/pipeline.py:86-122).  Regular ids must arrive increasing."""
         torch = _torch()
         dist = torch.distributed
         tag = _tag(tag)
-        if tag[0] != "mb":
-            raise ConfigError("bubble-fill messages are not supported over torch.distributed")
-        expect_mb = tag[1]
-        hdr = torch.empty(1, dtype=torch.int64, device=self.device)
-        dist.recv(hdr, self.peer, group=self.group)
-        mb = int(hdr.item())
-        if mb != expect_mb or mb <= self.last:
-            raise QueueProtocolError(f"expected microbatch {expect_mb}, got {mb} (last {self.last})")
-        self.last = mb
-        data = torch.empty(self.shape, dtype=self.dtype, device=self.device)
-        dist.recv(data, self.peer, group=self.group)
-        return type("Msg", (), {"mb": ("mb", mb), "data": data})
+        if tag in self.stash:
+            return self.stash.pop(tag)
+        while True:
+            hdr = torch.empty(2, dtype=torch.int64, device=self.device)
+            dist.recv(hdr, self.peer, group=self.group)
+            code, idx = (int(v) for v in hdr.tolist())
+            got = (_KIND_NAME[code], idx)
+            if got[0] == "mb":
+                if idx <= self.last:
+                    raise QueueProtocolError(f"microbatch ids out of order: {idx} after {self.last}")
+                self.last = idx
+            data = torch.empty(self.shape, dtype=self.dtype, device=self.device)
+            dist.recv(data, self.peer, group=self.group)
+            msg = type("Msg", (), {"mb": got, "data": data})
+            if got == tag:
+                return msg
+            self.stash[got] = msg
 
 
 _UNSET = object()
@@ -624,18 +636,26 @@ def _stage_executor(device, stage):
     return ex
 
 
-def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
-                       devices=None, dtype=None, master_dtype=None, stage_computes=None,
-                       compute_factory=None):
-    """One 1F1B iteration over the partition, one thread per stage
-    (eepipe/pipeline.py:537-644).  ``model`` is the EarlyExitModel the stage
-    weights come from (the partition's own copies are used when omitted).
-    ``master_dtype=torch.float32`` accumulates gradients in float32
-    (`TrainModel` mixed mode).  ``stage_computes``: a list that keeps the
-    per-stage device state across iterations (filled on the first call,
-    reused — gradients zeroed, weights as the optimizer left them — after).
-    ``compute_factory(spec, cfg, wmap)`` overrides the stage compute (CPU
-    protocol tests).  Returns (merged gradient map by name, TrainStepReport)."""
+@dataclass
+class _IterationPlan:
+    M: int
+    data: dict
+    all_heads: list
+    weights: list
+    wmap: dict
+    fill: object
+    rescale: object
+    depths: list
+    plan: object
+    timeline: object
+    n_fill: int
+
+
+def _plan_iteration(part: StagePartition, batch, options: IterationOptions) -> _IterationPlan:
+    """Everything both executors derive before running: microbatches, head
+    weights (Part-1-rescaled), the fill geometry and data, and the simulated
+    timeline whose per-stage order the workers execute
+    (eepipe/pipeline.py:537-590)."""
     import numpy as np
     P = part.num_stages
     M, data = _split(batch, options.microbatch_size)
@@ -668,6 +688,28 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
         cost_model_from_partition(part, M, options.microbatch_size, seq_len, options.cost),
         "deferred-exit" if options.defer_exit_forward else "eager-exit",
         plan if fill is not None else None)
+    n_fill = (sum(1 for d in depths if d is not None) + len(plan.part2_bwd_depths)
+              if fill is not None else 0)
+    return _IterationPlan(M, data, all_heads, weights, wmap, fill, rescale, depths, plan,
+                          timeline, n_fill)
+
+
+def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, model=None,
+                       devices=None, dtype=None, master_dtype=None, stage_computes=None,
+                       compute_factory=None):
+    """One 1F1B iteration over the partition, one thread per stage
+    (eepipe/pipeline.py:537-644).  ``model`` is the EarlyExitModel the stage
+    weights come from (the partition's own copies are used when omitted).
+    ``master_dtype=torch.float32`` accumulates gradients in float32
+    (`TrainModel` mixed mode).  ``stage_computes``: a list that keeps the
+    per-stage device state across iterations (filled on the first call,
+    reused — gradients zeroed, weights as the optimizer left them — after).
+    ``compute_factory(spec, cfg, wmap)`` overrides the stage compute (CPU
+    protocol tests).  Returns (merged gradient map by name, TrainStepReport)."""
+    P = part.num_stages
+    it = _plan_iteration(part, batch, options)
+    M, data, all_heads, weights, wmap = it.M, it.data, it.all_heads, it.weights, it.wmap
+    fill, rescale, depths, plan, timeline = it.fill, it.rescale, it.depths, it.plan, it.timeline
     devices = devices or ["cuda:0"] * P
     src = model
     fwd = [TaggedChannel(f"act {s}->{s + 1}") for s in range(1, P)]
@@ -729,9 +771,7 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
                 for t in g.values():
                     t.mul_(gs)
     merged = sync_tied(per_stage, part.tied_replicas)
-    n_fill = sum(1 for d in depths if d is not None) + (len(plan.part2_bwd_depths)
-                                                         if fill is not None else 0)
-    report = TrainStepReport(weights_used=tuple(weights), microbatches=M + n_fill,
+    report = TrainStepReport(weights_used=tuple(weights), microbatches=M + it.n_fill,
                              timeline=timeline)
     for w, g in zip(workers, per_stage):
         report.event_log.append(list(w.event_log))
@@ -772,14 +812,8 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
         raise ConfigError(f"{world} ranks for {P} stages")
     s = rank + 1
     spec = part.stages[rank]
-    if options.fill_plan is not None and not options.fill_plan.empty:
-        raise ConfigError("bubble filling runs in the threaded executor (run_iteration_1f1b); "
-                          "its fill traffic is tag-addressed, which NCCL P2P is not")
-    M, data = _split(batch, options.microbatch_size)
-    all_heads = sorted([hd for st in part.stages for _, hd in st.heads],
-                       key=lambda hd: (hd.layer_index, hd.is_final))
-    weights = _resolve_weights(all_heads, options)
-    wmap = {hd.key: w for hd, w in zip(all_heads, weights)}
+    it = _plan_iteration(part, batch, options)
+    M, data, weights, wmap = it.M, it.data, it.weights, it.wmap
     if compute_factory is None:
         dev = torch.device("cuda", torch.cuda.current_device())
         comp = StageCompute(spec, part.config, model if model is not None else _SpecModel(part, spec),
@@ -796,7 +830,7 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
     bwd_in = DistChannel(rank + 1, shape, act_dtype, dev) if s < P else None
     bwd_out = DistChannel(rank - 1, shape, act_dtype, dev) if s > 1 else None
     w = StageWorker(s, P, M, comp, data, fwd_in, fwd_out, bwd_in, bwd_out,
-                    options.hoist_exit_heads)
+                    options.hoist_exit_heads, actions=it.timeline.order(s), fill=it.fill)
     w.run()
     for ch in (fwd_out, bwd_out):
         if ch is not None:
@@ -804,6 +838,9 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
     if w.exception is not None:
         raise w.exception
     grads = comp.tm.grads() if compute_factory is None else comp.grads()
+    if it.rescale is not None and it.rescale.grad_scale_for(s) != 1.0:
+        for t in grads.values():
+            t.mul_(it.rescale.grad_scale_for(s))
     # tied replicas: all-reduce(sum) over the holders (every rank joins the
     # group creation; only holders take part in the reduction)
     for name, holders in sorted(part.tied_replicas.items()):
@@ -812,10 +849,11 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
             g = grads[name]
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
     # this rank's view: its own stage's entries (event_log[s-1], memory[0])
-    report = TrainStepReport(weights_used=tuple(weights), microbatches=M)
+    report = TrainStepReport(weights_used=tuple(weights), microbatches=M + it.n_fill,
+                             timeline=it.timeline)
     report.event_log = [[] for _ in range(P)]
     report.event_log[s - 1] = list(w.event_log)
-    report.memory = [StageMemoryCounters(s, w.max_in_flight)]
+    report.memory = [StageMemoryCounters(s, w.max_in_flight, w.max_fill_stored)]
     report.wall_clock = {"forward": w.wall["F"], "backward": w.wall["B"],
                          "total": w.wall["F"] + w.wall["B"]}
     for key, vals in comp.head_losses.items():

@@ -168,6 +168,7 @@ class FillToyCompute:
     def __init__(self, spec, cfg, wmap, params):
         self.spec, self.cfg, self.weights = spec, cfg, wmap
         self.device = torch.device("cpu")
+        self.act_dtype = torch.float64
         self.p = {n: params[n].clone().requires_grad_() for n in spec.params}
         self.head_losses = {hd.key: [] for _, hd in spec.heads}
 

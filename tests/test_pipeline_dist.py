@@ -9,6 +9,7 @@ Mirrors the reference's pipeline tests: in-flight bound P-s+1
 (:356-372) and gradient equivalence with single-device training (:59-69).
 """
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -197,3 +198,75 @@ def test_distributed_1f1b_matches_single_process(world, tied):
     assert set(merged) == set(ref)
     for n in ref:
         np.testing.assert_allclose(merged[n], ref[n].numpy(), rtol=1e-9, atol=1e-12)
+
+
+def _fill_worker(rank, world, port, q):
+    """One rank of a distributed iteration WITH bubble filling (gloo, CPU
+    float64 compute): fill traffic travels over the tagged point-to-point
+    channel (headers carry (kind, index); early arrivals are stashed)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from test_bubblefill import FillToyCompute, _setup
+        from paper_2312_04916_b200.bubblefill import plan_bubble_fill
+        from paper_2312_04916_b200.pipeline import apply_fill
+        model, part, params, rng = _setup(17)
+        plan = plan_bubble_fill(4, 0.5)
+        depths, _ = apply_fill(plan, part, 4)
+        n_extra = sum(1 for d in depths if d is not None) + plan.k_part2
+        batch = rng.integers(0, 32, size=(8, 9))
+        fill_rows = rng.integers(0, 32, size=(2 * n_extra, 9))
+        factory = lambda spec, c, wmap: FillToyCompute(spec, c, wmap, params)  # noqa: E731
+        grads, rep = run_stage_1f1b_dist(
+            part, batch, IterationOptions(microbatch_size=2, fill_plan=plan,
+                                          fill_batch=fill_rows),
+            compute_factory=factory)
+        q.put((rank, {n: g.detach().numpy() for n, g in grads.items()}, rep.event_log,
+               [list(o) for o in (rep.timeline.order(s) for s in range(1, 5))],
+               rep.microbatches))
+    except BaseException as exc:  # pragma: no cover - reported by the parent
+        q.put((rank, repr(exc), None, None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_bubble_fill_matches_threaded_executor():
+    """Bubble filling over torch.distributed (4 ranks, gloo): every rank runs
+    the simulated timeline's order, the fill microbatches travel as tagged
+    messages, and the merged gradients equal the single-process threaded
+    executor's bitwise (float64, same per-stage accumulation order)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_bubblefill import FillToyCompute, _setup
+    from paper_2312_04916_b200.bubblefill import plan_bubble_fill
+    from paper_2312_04916_b200.pipeline import apply_fill, run_iteration_1f1b
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + np.random.default_rng().integers(2000, 4000)
+    procs = [ctx.Process(target=_fill_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in results:
+        assert not isinstance(r[1], str), r[1]
+    model, part, params, rng = _setup(17)
+    plan = plan_bubble_fill(4, 0.5)
+    depths, _ = apply_fill(plan, part, 4)
+    n_extra = sum(1 for d in depths if d is not None) + plan.k_part2
+    batch = rng.integers(0, 32, size=(8, 9))
+    fill_rows = rng.integers(0, 32, size=(2 * n_extra, 9))
+    factory = lambda spec, c, wmap: FillToyCompute(spec, c, wmap, params)  # noqa: E731
+    ref, rep_ref = run_iteration_1f1b(part, batch, IterationOptions(
+        microbatch_size=2, fill_plan=plan, fill_batch=fill_rows), compute_factory=factory)
+    merged = {}
+    for rank, grads, log, orders, nmb in sorted(results, key=lambda r: r[0]):
+        s = rank + 1
+        assert log[s - 1] == [tuple(a) for a in orders[s - 1]]
+        assert nmb == rep_ref.microbatches
+        merged.update(grads)
+    assert set(merged) == set(ref)
+    for n in ref:
+        assert np.array_equal(merged[n], ref[n].detach().numpy()), n
