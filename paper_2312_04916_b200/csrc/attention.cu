@@ -384,9 +384,11 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
         const int64_t mr = m - r0 < kRowsPerLaunch ? m - r0 : kRowsPerLaunch;
         const dim3 grid((unsigned)nh, (unsigned)mr, (unsigned)nch);
         cudaError_t e;
-        // rows sharing K/V loads pay off once rows span several chunks; short
-        // rows are latency-bound and run one CTA per row (same arithmetic)
-        if (dtype == EE_BF16 && dh == kMaxDh && mr >= 2 && nch >= kRowsKernelMinChunks) {
+        // rows spanning several chunks go through the rows kernel (K/V block
+        // loads shared by the group's rows, V staged in shared memory; also
+        // slightly faster for a single row); short rows are latency-bound and
+        // run one CTA per row (same arithmetic)
+        if (dtype == EE_BF16 && dh == kMaxDh && nch >= kRowsKernelMinChunks) {
             const int groups = (int)((mr + kRowsCta - 1) / kRowsCta);
             const size_t smem = rows128_smem((int)(mr < kRowsCta ? mr : kRowsCta));
             static bool configured[16] = {};
