@@ -9,7 +9,8 @@
 // finishing and the Wo GEMV starting.  Organisation:
 //   * one CTA (8 warps) per (head, row, 256-position chunk) -- for bf16 with
 //     head_dim 128 per (head, group of <= 16 rows, chunk), the rows sharing
-//     each K/V load (k_attn_rows128); warp w owns the 32-position block
+//     each K/V load (k_attn_rows128: K tile cp.async'd into shared memory
+//     with an XOR swizzle, V columns in registers); warp w owns the block
 //     8 c + w, lane j its position: q.K in registers, warp max / sum-exp by
 //     shuffles, P.V with each lane owning dh/32 output dimensions (coalesced
 //     V rows);
@@ -50,7 +51,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-template <typename T, bool DH128>
+template <typename T>
 __global__ void __launch_bounds__(kThreadsA)
 k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int m,
               const T* __restrict__ kc, const T* __restrict__ vc, int nh, int dh, float scale,
@@ -94,92 +95,40 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
     float mx = -INFINITY, l = 0.f;
     float acc[kMaxDh / 32][4];
     if (wvalid) {
-        // score of this lane's position: fixed-order dot product.  DH = 128
-        // (the configs' head dim) issues the whole K row and this lane's V
-        // columns of the block before using any of them: one memory round
-        // trip per warp (same arithmetic as the generic loop)
+        // score of this lane's position: fixed-order dot product
         float sc = 0.f;
         const int nj = min(kBlk, p + 1 - j0);
         const T* vb = vc + (int64_t)j0 * h + hh * dh;
 #pragma unroll
         for (int g = 0; g < kMaxDh / 128; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
-        if constexpr (DH128) {
-            // bf16 only: the raw K row (16 x 16 B) and this lane's 4 V columns
-            // of the block's 32 positions (32 x 8 B) stay packed in registers
-            uint4 kraw[16];
-            uint2 vraw[kBlk];
-            if (valid) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) kraw[i] = reinterpret_cast<const uint4*>(krow)[i];
+        if (valid) {
+            for (int d = 0; d < dh; d += 4) {
+                float kv[4];
+                load4<T>(krow + d, kv);
+                sc = fmaf(s_q[d], kv[0], sc);
+                sc = fmaf(s_q[d + 1], kv[1], sc);
+                sc = fmaf(s_q[d + 2], kv[2], sc);
+                sc = fmaf(s_q[d + 3], kv[3], sc);
             }
+        }
+        const float sv = valid ? sc * scale : -INFINITY;
+        mx = sv;
 #pragma unroll
-            for (int j = 0; j < kBlk; ++j)
-                if (j < nj) vraw[j] = *reinterpret_cast<const uint2*>(vb + (int64_t)j * h + 4 * lane);
-            if (valid) {
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float e = valid ? expf(sv - mx) : 0.f;
+        l = e;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const uint32_t w4[4] = {kraw[i].x, kraw[i].y, kraw[i].z, kraw[i].w};
-#pragma unroll
-                    for (int e2 = 0; e2 < 4; ++e2) {
-                        const float2 f =
-                            __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e2]));
-                        sc = fmaf(s_q[8 * i + 2 * e2], f.x, sc);
-                        sc = fmaf(s_q[8 * i + 2 * e2 + 1], f.y, sc);
-                    }
-                }
-            }
-            const float sv = valid ? sc * scale : -INFINITY;
-            mx = sv;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            const float e = valid ? expf(sv - mx) : 0.f;
-            l = e;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-#pragma unroll
-            for (int j = 0; j < kBlk; ++j) {
-                const float pj = __shfl_sync(0xffffffffu, e, j);
-                if (j < nj) {
-                    const float2 a =
-                        __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vraw[j].x));
-                    const float2 b =
-                        __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vraw[j].y));
-                    acc[0][0] = fmaf(pj, a.x, acc[0][0]);
-                    acc[0][1] = fmaf(pj, a.y, acc[0][1]);
-                    acc[0][2] = fmaf(pj, b.x, acc[0][2]);
-                    acc[0][3] = fmaf(pj, b.y, acc[0][3]);
-                }
-            }
-        } else {
-            if (valid) {
-                for (int d = 0; d < dh; d += 4) {
-                    float kv[4];
-                    load4<T>(krow + d, kv);
-                    sc = fmaf(s_q[d], kv[0], sc);
-                    sc = fmaf(s_q[d + 1], kv[1], sc);
-                    sc = fmaf(s_q[d + 2], kv[2], sc);
-                    sc = fmaf(s_q[d + 3], kv[3], sc);
-                }
-            }
-            const float sv = valid ? sc * scale : -INFINITY;
-            mx = sv;
-    #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            const float e = valid ? expf(sv - mx) : 0.f;
-            l = e;
-    #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-            // P.V: lane owns output dims [4 lane, 4 lane + 4)
-            for (int j = 0; j < nj; ++j) {
-                const float pj = __shfl_sync(0xffffffffu, e, j);
-                if (4 * lane < dh) {
-                    float v4[4];
-                    load4<T>(vb + (int64_t)j * h + 4 * lane, v4);
-                    acc[0][0] = fmaf(pj, v4[0], acc[0][0]);
-                    acc[0][1] = fmaf(pj, v4[1], acc[0][1]);
-                    acc[0][2] = fmaf(pj, v4[2], acc[0][2]);
-                    acc[0][3] = fmaf(pj, v4[3], acc[0][3]);
-                }
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        // P.V: lane owns output dims [4 lane, 4 lane + 4)
+        for (int j = 0; j < nj; ++j) {
+            const float pj = __shfl_sync(0xffffffffu, e, j);
+            if (4 * lane < dh) {
+                float v4[4];
+                load4<T>(vb + (int64_t)j * h + 4 * lane, v4);
+                acc[0][0] = fmaf(pj, v4[0], acc[0][0]);
+                acc[0][1] = fmaf(pj, v4[1], acc[0][1]);
+                acc[0][2] = fmaf(pj, v4[2], acc[0][2]);
+                acc[0][3] = fmaf(pj, v4[3], acc[0][3]);
             }
         }
 #pragma unroll
@@ -232,15 +181,16 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
 
 // bf16, head_dim 128 (the configs' head dim): one CTA per (head, group of up
 // to 16 rows, 256-position chunk).  Rows of a pass share the layer's K/V
-// prefix, so each warp loads its 32-position block ONCE (block_load128, up to
-// the group's last position) and scores every row of the group from the
-// same registers (block_eval128); per-row results go through shared memory
+// prefix, so each warp loads its 32-position block ONCE (block_load128_k, up
+// to the group's last position: K into a swizzled shared-memory tile, V into
+// registers) and scores every row of the group from it (block_eval128_k);
+// per-row results go through shared memory
 // and are merged exactly as in k_attn_decode, so a row's output does not
 // depend on which rows share its group.
 constexpr int kRowsCta = 16;
-constexpr int kRowsKernelMinChunks = 3;  // measured: m = 5 at ctx 320 -> 1024 crossover
+constexpr int kRowsKernelMinChunks = 1;  // K staged in smem: faster at every context (m = 1 too)
 
-// dynamic shared memory: V tiles [kWarpsA][kBlk][dh] bf16, q [rows][dh] and
+// dynamic shared memory: K tiles [kWarpsA][kBlk][dh] bf16 (swizzled), q [rows][dh] and
 // per-row block results [rows][kWarpsA][dh] float32
 __host__ __device__ constexpr size_t rows128_smem(int rows) {
     return (size_t)kWarpsA * kBlk * kMaxDh * 2 + (size_t)rows * (kMaxDh + kWarpsA * kMaxDh) * sizeof(float);
@@ -259,7 +209,7 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     const int r0 = blockIdx.y * kRowsCta;
     const int mr = min(kRowsCta, m - r0);
     const int h = nh * dh;
-    bf16* s_v = reinterpret_cast<bf16*>(smem_rows);                        // [kWarpsA][kBlk][dh]
+    bf16* s_k = reinterpret_cast<bf16*>(smem_rows);                        // [kWarpsA][kBlk][dh]
     float* s_q = smem_rows + kWarpsA * kBlk * dh / 2;                      // [mr][dh]
     float* s_acc = s_q + mr * dh;                                          // [mr][kWarpsA][dh]
     // host-written control data: safe before the wait
@@ -287,14 +237,14 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     }
     __syncthreads();
     if (j0 <= pmax) {
-        attn::BlockRegs R;
-        bf16* sv = s_v + warp * kBlk * dh;
-        attn::block_load128(R, sv, kc, vc, h, hh * dh, j0, pmax);
+        attn::BlockRegsV R;
+        bf16* sk = s_k + warp * kBlk * dh;  // this warp's K tile
+        attn::block_load128_k(R, sk, kc, vc, h, hh * dh, j0, pmax);
         for (int i = 0; i < mr; ++i) {
             const int p = pos[r0 + i];
             if (j0 > p) continue;  // warp-uniform
             float mx, l, acc[4];
-            attn::block_eval128(R, sv, s_q + i * dh, j0, p, scale, mx, l, acc);
+            attn::block_eval128_k(R, sk, s_q + i * dh, j0, p, scale, mx, l, acc);
             reinterpret_cast<float4*>(s_acc + (i * kWarpsA + warp) * dh)[lane] =
                 make_float4(acc[0], acc[1], acc[2], acc[3]);
             if (lane == 0) {
@@ -384,10 +334,9 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
         const int64_t mr = m - r0 < kRowsPerLaunch ? m - r0 : kRowsPerLaunch;
         const dim3 grid((unsigned)nh, (unsigned)mr, (unsigned)nch);
         cudaError_t e;
-        // rows spanning several chunks go through the rows kernel (K/V block
-        // loads shared by the group's rows, V staged in shared memory; also
-        // slightly faster for a single row); short rows are latency-bound and
-        // run one CTA per row (same arithmetic)
+        // bf16, head_dim 128: the rows kernel (K/V block loads shared by the
+        // group's rows, K staged swizzled in shared memory, V in registers);
+        // other shapes / fp32: one CTA per row (same arithmetic)
         if (dtype == EE_BF16 && dh == kMaxDh && nch >= kRowsKernelMinChunks) {
             const int groups = (int)((mr + kRowsCta - 1) / kRowsCta);
             const size_t smem = rows128_smem((int)(mr < kRowsCta ? mr : kRowsCta));
@@ -404,11 +353,11 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
                           (const bf16*)kc, (const bf16*)vc, (int)nh, scale, (bf16*)out + r0 * h,
                           part, ctr);
         } else if (dtype == EE_BF16)
-            e = launch_ex(dh == kMaxDh ? k_attn_decode<bf16, true> : k_attn_decode<bf16, false>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
+            e = launch_ex(k_attn_decode<bf16>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
                           (int)mr, (const bf16*)kc, (const bf16*)vc, (int)nh, (int)dh, scale,
                           (bf16*)out + r0 * h, part, ctr);
         else if (dtype == EE_F32)
-            e = launch_ex(k_attn_decode<float, false>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
+            e = launch_ex(k_attn_decode<float>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
                           (int)mr, (const float*)kc, (const float*)vc, (int)nh, (int)dh, scale,
                           (float*)out + r0 * h, part, ctr);
         else

@@ -37,53 +37,67 @@ __host__ __device__ inline size_t partial_slots(int64_t nh) {
 }
 
 // One 32-position block of one head, bf16 K/V, dh = 128, in two steps so
-// several rows can score it (k_attn_rows128): block_load128 issues the raw K
-// row of this lane's position (16 x 16 B, registers) and copies the block's V
-// rows (32 x 256 B) into the warp's shared-memory tile sv with cp.async, for
-// every position <= plim -- one memory round trip per block -- and
-// block_eval128 evaluates one row (position p <= plim, q in shared memory).
-struct BlockRegs {
-    uint4 k[16];
+// several rows can score it (k_attn_rows128), with the K tile staged in
+// shared memory and the V columns in registers: block_load128_k copies the
+// block's K rows
+// (32 x 256 B, coalesced) with cp.async into the warp's tile sk, 16-byte
+// chunk c of row j at chunk c ^ (j & 7) (conflict-free row reads), and
+// block_eval128_k evaluates one row (position p <= plim, q in shared
+// memory), reading this lane's K row back in two 8-chunk halves.  Same
+// arithmetic, same order as k_attn_decode's generic path.
+struct BlockRegsV {
+    uint2 v[kBlk];
 };
 
-__device__ __forceinline__ void block_load128(BlockRegs& R, bf16* sv, const bf16* __restrict__ kc,
-                                              const bf16* __restrict__ vc, int64_t h, int hoff,
-                                              int j0, int plim) {
+__device__ __forceinline__ void block_load128_k(BlockRegsV& R, bf16* sk, const bf16* __restrict__ kc,
+                                                const bf16* __restrict__ vc, int64_t h, int hoff,
+                                                int j0, int plim) {
     const int lane = threadIdx.x & 31;
-    const int jj = j0 + lane;
     const int nj = min(kBlk, plim + 1 - j0);
-    const bf16* vb = vc + (int64_t)j0 * h + hoff + 4 * lane;
-    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(sv + 4 * lane);
-    for (int j = 0; j < nj; ++j)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sdst + j * kMaxDh * 2),
-                     "l"(vb + (int64_t)j * h)
-                     : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    if (jj <= plim) {
-        const uint4* krow = reinterpret_cast<const uint4*>(kc + (int64_t)jj * h + hoff);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sk);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) R.k[i] = krow[i];
+    for (int t = 0; t < kBlk * 16 / 32; ++t) {
+        const int idx = lane + 32 * t;
+        const int j = idx >> 4, c = idx & 15;
+        if (j < nj)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             sbase + (uint32_t)((j * 16 + (c ^ (j & 7))) * 16)),
+                         "l"(kc + (int64_t)(j0 + j) * h + hoff + c * 8)
+                         : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const bf16* vb = vc + (int64_t)j0 * h + hoff + 4 * lane;
+#pragma unroll
+    for (int j = 0; j < kBlk; ++j)
+        if (j < nj) R.v[j] = *reinterpret_cast<const uint2*>(vb + (int64_t)j * h);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
 }
 
-__device__ __forceinline__ void block_eval128(const BlockRegs& R, const bf16* sv, const float* sq,
-                                              int j0, int p, float scale, float& mx, float& l,
-                                              float acc[4]) {
+__device__ __forceinline__ void block_eval128_k(const BlockRegsV& R, const bf16* sk, const float* sq,
+                                                int j0, int p, float scale, float& mx, float& l,
+                                                float acc[4]) {
     const int lane = threadIdx.x & 31;
     const bool valid = j0 + lane <= p;
     const int nj = min(kBlk, p + 1 - j0);
     float sc = 0.f;
     if (valid) {
+        const uint4* krow = reinterpret_cast<const uint4*>(sk) + lane * 16;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t w4[4] = {R.k[i].x, R.k[i].y, R.k[i].z, R.k[i].w};
+        for (int half = 0; half < 2; ++half) {
+            uint4 kk[8];
 #pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e2]));
-                sc = fmaf(sq[8 * i + 2 * e2], f.x, sc);
-                sc = fmaf(sq[8 * i + 2 * e2 + 1], f.y, sc);
+            for (int q8 = 0; q8 < 8; ++q8) kk[q8] = krow[(half * 8 + q8) ^ (lane & 7)];
+#pragma unroll
+            for (int q8 = 0; q8 < 8; ++q8) {
+                const int i = half * 8 + q8;
+                const uint32_t w4[4] = {kk[q8].x, kk[q8].y, kk[q8].z, kk[q8].w};
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e2]));
+                    sc = fmaf(sq[8 * i + 2 * e2], f.x, sc);
+                    sc = fmaf(sq[8 * i + 2 * e2 + 1], f.y, sc);
+                }
             }
         }
     }
@@ -100,9 +114,8 @@ __device__ __forceinline__ void block_eval128(const BlockRegs& R, const bf16* sv
     for (int j = 0; j < kBlk; ++j) {
         const float pj = __shfl_sync(0xffffffffu, e, j);
         if (j < nj) {
-            const uint2 vv = *reinterpret_cast<const uint2*>(sv + j * kMaxDh + 4 * lane);
-            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv.x));
-            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv.y));
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&R.v[j].x));
+            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&R.v[j].y));
             acc[0] = fmaf(pj, a.x, acc[0]);
             acc[1] = fmaf(pj, a.y, acc[1]);
             acc[2] = fmaf(pj, b.x, acc[2]);

@@ -23,7 +23,7 @@ def main():
         eng.kv.reset()
         eng._grow(8)
         for rows in (1, 5):
-            for ctx in (128, 512, 1024, 2000):
+            for ctx in [int(c) for c in os.environ.get('CTXS', '128,512,1024,2000').split(',')]:
                 eng.upload_ctrl([ctx - rows + 1 + r for r in range(rows)])
                 for _ in range(2):
                     eng.run_layers(0, L, rows, [rows] * L, ctx, 0)
