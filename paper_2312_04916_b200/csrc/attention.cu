@@ -180,7 +180,8 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
 }
 
 // bf16, head_dim 128 (the configs' head dim): one CTA per (head, group of up
-// to 16 rows, 256-position chunk).  Rows of a pass share the layer's K/V
+// to 16 rows, 256-position chunk); the group size is chosen per launch so the
+// grid just fills the GPU.  Rows of a pass share the layer's K/V
 // prefix, so each warp loads its 32-position block ONCE (block_load128_k, up
 // to the group's last position: K into a swizzled shared-memory tile, V into
 // registers) and scores every row of the group from it (block_eval128_k);
@@ -199,15 +200,15 @@ __host__ __device__ constexpr size_t rows128_smem(int rows) {
 __global__ void __launch_bounds__(kThreadsA)
 k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int m,
                const bf16* __restrict__ kc, const bf16* __restrict__ vc, int nh, float scale,
-               bf16* __restrict__ out, float* __restrict__ part, int* __restrict__ ctr) {
+               bf16* __restrict__ out, float* __restrict__ part, int* __restrict__ ctr, int g) {
     extern __shared__ __align__(16) float smem_rows[];
     __shared__ float s_m[kRowsCta][kWarpsA], s_l[kRowsCta][kWarpsA];
     __shared__ int s_last[kRowsCta];
     constexpr int dh = kMaxDh;
     pdl_trigger_dev();
     const int hh = blockIdx.x, ch = blockIdx.z;
-    const int r0 = blockIdx.y * kRowsCta;
-    const int mr = min(kRowsCta, m - r0);
+    const int r0 = blockIdx.y * g;  // this CTA's rows: [r0, r0 + mr), g <= kRowsCta
+    const int mr = min(g, m - r0);
     const int h = nh * dh;
     bf16* s_k = reinterpret_cast<bf16*>(smem_rows);                        // [kWarpsA][kBlk][dh]
     float* s_q = smem_rows + kWarpsA * kBlk * dh / 2;                      // [mr][dh]
@@ -338,8 +339,12 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
         // group's rows, K staged swizzled in shared memory, V in registers);
         // other shapes / fp32: one CTA per row (same arithmetic)
         if (dtype == EE_BF16 && dh == kMaxDh && nch >= kRowsKernelMinChunks) {
-            const int groups = (int)((mr + kRowsCta - 1) / kRowsCta);
-            const size_t smem = rows128_smem((int)(mr < kRowsCta ? mr : kRowsCta));
+            // rows per CTA: just enough to fill the GPU with one CTA per SM
+            // (more rows per CTA share more K/V loads but evaluate serially)
+            const int64_t want = (mr * nh * nch + ee_sm_count() - 1) / ee_sm_count();
+            const int g = (int)(want < 1 ? 1 : (want > kRowsCta ? kRowsCta : want));
+            const int groups = (int)((mr + g - 1) / g);
+            const size_t smem = rows128_smem((int)(mr < g ? mr : g));
             static bool configured[16] = {};
             int dev = 0;
             cudaGetDevice(&dev);
@@ -351,7 +356,7 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
             e = launch_ex(k_attn_rows128, dim3((unsigned)nh, (unsigned)groups, (unsigned)nch),
                           dim3(kThreadsA), smem, s, q + r0 * h, pos + r0, (int)mr,
                           (const bf16*)kc, (const bf16*)vc, (int)nh, scale, (bf16*)out + r0 * h,
-                          part, ctr);
+                          part, ctr, g);
         } else if (dtype == EE_BF16)
             e = launch_ex(k_attn_decode<bf16>, grid, dim3(kThreadsA), 0, s, q + r0 * h, pos + r0,
                           (int)mr, (const bf16*)kc, (const bf16*)vc, (int)nh, (int)dh, scale,
