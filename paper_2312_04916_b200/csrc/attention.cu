@@ -182,7 +182,7 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
 // bf16, head_dim 128 (the configs' head dim): one CTA per (head, group of up
 // to 16 rows, 256-position chunk); the group size is chosen per launch so the
 // grid just fills the GPU.  Rows of a pass share the layer's K/V
-// prefix, so each warp loads its 32-position block ONCE (block_load128_k, up
+// prefix, so each warp loads its 32-position block ONCE (block_issue128_k, up
 // to the group's last position: K into a swizzled shared-memory tile, V into
 // registers) and scores every row of the group from it (block_eval128_k);
 // per-row results go through shared memory
@@ -231,6 +231,10 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
         prefetch_l2(vc + (int64_t)jj * h + hh * dh + 64);
     }
     pdl_wait_dev();
+    // the block's K / V loads go out first, the q rows are staged meanwhile
+    attn::BlockRegsV R;
+    bf16* sk = s_k + warp * kBlk * dh;  // this warp's K tile
+    if (j0 <= pmax) attn::block_issue128_k(R, sk, kc, vc, h, hh * dh, j0, pmax);
     for (int t = tid; t < mr * (dh / 4); t += kThreadsA) {
         const int i = t / (dh / 4), c = t % (dh / 4);
         reinterpret_cast<float4*>(s_q + i * dh)[c] =
@@ -238,9 +242,7 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     }
     __syncthreads();
     if (j0 <= pmax) {
-        attn::BlockRegsV R;
-        bf16* sk = s_k + warp * kBlk * dh;  // this warp's K tile
-        attn::block_load128_k(R, sk, kc, vc, h, hh * dh, j0, pmax);
+        attn::block_wait128_k();
         for (int i = 0; i < mr; ++i) {
             const int p = pos[r0 + i];
             if (j0 > p) continue;  // warp-uniform

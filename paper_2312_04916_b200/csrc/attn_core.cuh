@@ -38,7 +38,7 @@ __host__ __device__ inline size_t partial_slots(int64_t nh) {
 
 // One 32-position block of one head, bf16 K/V, dh = 128, in two steps so
 // several rows can score it (k_attn_rows128), with the K tile staged in
-// shared memory and the V columns in registers: block_load128_k copies the
+// shared memory and the V columns in registers: block_issue128_k copies the
 // block's K rows
 // (32 x 256 B, coalesced) with cp.async into the warp's tile sk, 16-byte
 // chunk c of row j at chunk c ^ (j & 7) (conflict-free row reads), and
@@ -49,9 +49,11 @@ struct BlockRegsV {
     uint2 v[kBlk];
 };
 
-__device__ __forceinline__ void block_load128_k(BlockRegsV& R, bf16* sk, const bf16* __restrict__ kc,
-                                                const bf16* __restrict__ vc, int64_t h, int hoff,
-                                                int j0, int plim) {
+// issue: the K tile copy (cp.async, committed) and the V register loads;
+// block_wait128_k completes the K copy for the whole warp
+__device__ __forceinline__ void block_issue128_k(BlockRegsV& R, bf16* sk, const bf16* __restrict__ kc,
+                                                 const bf16* __restrict__ vc, int64_t h, int hoff,
+                                                 int j0, int plim) {
     const int lane = threadIdx.x & 31;
     const int nj = min(kBlk, plim + 1 - j0);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sk);
@@ -70,6 +72,9 @@ __device__ __forceinline__ void block_load128_k(BlockRegsV& R, bf16* sk, const b
 #pragma unroll
     for (int j = 0; j < kBlk; ++j)
         if (j < nj) R.v[j] = *reinterpret_cast<const uint2*>(vb + (int64_t)j * h);
+}
+
+__device__ __forceinline__ void block_wait128_k() {
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
 }
