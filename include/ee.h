@@ -299,6 +299,21 @@ int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64
                        const int64_t* targets, float weight, float* loss, float* dx, float* dw_acc,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* The same head split at the autograd boundary (forward / backward):
+ *   ee_exit_head_train_fwd: *loss as above; G (n, V) bf16 caller buffer
+ *     receives d loss / d logits (kept for the backward);
+ *   ee_exit_head_train_bwd: dx = grad * G W (n, h) float32,
+ *     dw_acc += grad * G^T x (V, h) float32, where grad points to the
+ *     incoming gradient of the loss (device float32 scalar, read by the
+ *     epilogues: no host synchronisation; nullptr = 1).
+ * Same shapes, workspace and reference boundary as ee_exit_head_train. */
+int ee_exit_head_train_fwd(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
+                           const int64_t* targets, float weight, float* loss, void* G, void* ws,
+                           size_t ws_bytes, void* stream);
+int ee_exit_head_train_bwd(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
+                           const void* G, const float* grad, float* dx, float* dw_acc, void* ws,
+                           size_t ws_bytes, void* stream);
+
 /* dW (in x out, float32) += X^T dY for a bf16 linear layer y = x W, X (T x in)
  * and dY (T x out) bf16 row-major, on the CTA-pair tcgen05 GEMM (operands read
  * MN-major in place).  The training backbone's gradient-accumulation fusion:

@@ -122,14 +122,21 @@ struct EpiProb {
 };
 
 template <bool ACCUM>
-struct EpiF32 {  // K3 store / K4 accumulate
+struct EpiF32 {  // K3 store / K4 accumulate, optionally scaled by *gs (device)
     static constexpr bool kTwoPass = false;
     static constexpr bool kSplitK = false;
     float* out;
     int ldo;
-    __device__ void begin_tile(int, int, int, bool) {}
-    __device__ void chunk(int row, int col, const float* v, int nvalid) {
+    const float* gs = nullptr;
+    float g = 1.f;
+    __device__ void begin_tile(int, int, int, bool) {
+        if (gs) g = __ldg(gs);
+    }
+    __device__ void chunk(int row, int col, const float* v0, int nvalid) {
         float* o = out + (int64_t)row * ldo + col;
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = gs ? v0[j] * g : v0[j];
         if (nvalid == 16) {
 #pragma unroll
             for (int j = 0; j < 16; j += 4) {
@@ -167,6 +174,7 @@ struct EpiF32Ordered {
     int ldo;
     int* flags;  // [tiles][16 regions]
     int splits;
+    const float* gs = nullptr;  // optional device scale of every partial
     int s = 0;
     int* flag = nullptr;
     __device__ void set_split(int sp, int t) {
@@ -174,7 +182,9 @@ struct EpiF32Ordered {
         const int region = (int)tc::cluster_rank() * tc::kEpiWarps + ((int)(threadIdx.x >> 5) - 2);
         flag = flags + t * 2 * tc::kEpiWarps + region;
     }
+    float g = 1.f;
     __device__ void begin_tile(int, int, int, bool) {
+        if (gs) g = __ldg(gs);
         if (s > 0) {
             if ((threadIdx.x & 31) == 0) {
                 int v;
@@ -185,8 +195,11 @@ struct EpiF32Ordered {
             __syncwarp();
         }
     }
-    __device__ void chunk(int row, int col, const float* v, int nvalid) {
+    __device__ void chunk(int row, int col, const float* v0, int nvalid) {
         float* o = out + (int64_t)row * ldo + col;
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = gs ? v0[j] * g : v0[j];
         if (nvalid == 16) {
 #pragma unroll
             for (int j = 0; j < 16; j += 4) {
@@ -364,9 +377,9 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 
 size_t exit_head_train_ws_bytes(int64_t n, int64_t /*h*/, int64_t V) { return carve_bytes(n, V); }
 
-extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
-                                  const int64_t* targets, float weight, float* loss, float* dx,
-                                  float* dw_acc, void* ws, size_t ws_bytes, void* stream) {
+namespace {
+
+int check_head_shape(int64_t n, int64_t h, int64_t V, size_t ws_bytes, const void* ws) {
     // h and V set row strides of TMA-read matrices (16-byte multiples);
     // any n works (out-of-range rows / k-blocks are zero-filled by TMA)
     EE_REQUIRE(n > 0 && h > 0 && V > 0 && h % 8 == 0 && V % 8 == 0, EE_ESHAPE,
@@ -375,22 +388,33 @@ extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const voi
     EE_REQUIRE(n < (1ll << 31) && V < (1ll << 31), EE_ESHAPE, "exit_head_train: too large");
     EE_REQUIRE(ws && ws_bytes >= carve_bytes(n, V), EE_ESHAPE,
                "exit_head_train: workspace too small (%zu < %zu)", ws_bytes, carve_bytes(n, V));
-    cudaStream_t s = as_stream(stream);
-    TrainWs w = carve(ws, n, V);
+    return EE_OK;
+}
+
+// K1 + F + loss: G (n x V bf16) = w/n (softmax - onehot), loss = w/n sum CE
+int head_forward(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
+                 const int64_t* targets, float weight, float* loss, bf16* G, TrainWs& w,
+                 cudaStream_t s) {
     const int ntn = (int)(kParts * ((V + kBN - 1) / kBN));
     const float scale = weight / (float)n;
     int rc;
     // K1: S = X W^T -> part max / sum, target logits, P~ into G's buffer
     if ((rc = tc::launch_tc_gemm2<kBN, false, false, false>(
              x, W, (int)n, (int)V, (int)h,
-             EpiProb{targets, w.pmax, w.psum, w.tgt, w.g, ntn, (int)V, 0.f, 0.f, 0}, s)))
+             EpiProb{targets, w.pmax, w.psum, w.tgt, G, ntn, (int)V, 0.f, 0.f, 0}, s)))
         return rc;
     // F: lse, row losses, P~ -> G in place
     k_grad_fixup<<<(unsigned)n, kFixThreads, ntn * sizeof(float), s>>>(
-        w.pmax, w.psum, w.tgt, targets, ntn, (int)V, scale, w.g, w.lse, w.rowloss);
+        w.pmax, w.psum, w.tgt, targets, ntn, (int)V, scale, G, w.lse, w.rowloss);
     if ((rc = ee_check_launch("grad_fixup"))) return rc;
     k_loss_sum<<<1, 1024, 0, s>>>(w.rowloss, (int)n, scale, loss);
-    if ((rc = ee_check_launch("loss_sum"))) return rc;
+    return ee_check_launch("loss_sum");
+}
+
+// K3 + K4: dx = g G W, dw_acc += g G^T X (g: optional device scalar)
+int head_backward(const void* x, int64_t n, int64_t h, const void* W, int64_t V, const bf16* G,
+                  const float* gs, float* dx, float* dw_acc, TrainWs& w, cudaStream_t s) {
+    int rc;
     // K3: dX = G W     (W (V x h) is the MN-major B operand, K = V); long
     // tiles, few of them: ordered split-K fills the last wave
     {
@@ -400,20 +424,59 @@ extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const voi
                            : 1;
         if (S == 1) {
             if ((rc = tc::launch_tc_gemm2<kBN, false, true, false>(
-                     w.g, W, (int)n, (int)h, (int)V, EpiF32<false>{dx, (int)h}, s)))
+                     G, W, (int)n, (int)h, (int)V, EpiF32<false>{dx, (int)h, gs}, s)))
                 return rc;
         } else {
             const size_t fbytes = (size_t)tiles * 2 * tc::kEpiWarps * sizeof(int);
             cudaMemsetAsync(w.flags, 0, fbytes, s);
             if ((rc = tc::launch_tc_gemm2<kBN, false, true, false>(
-                     w.g, W, (int)n, (int)h, (int)V, EpiF32Ordered{dx, (int)h, w.flags, S}, s, S)))
+                     G, W, (int)n, (int)h, (int)V, EpiF32Ordered{dx, (int)h, w.flags, S, gs}, s,
+                     S)))
                 return rc;
         }
     }
     // K4: dW += G^T X  (G and X both MN-major, K = n); N-fastest tile order so
     // concurrent CTAs share each G column block
-    return tc::launch_tc_gemm2<kBN, true, true, true>(w.g, x, (int)V, (int)h, (int)n,
-                                                     EpiF32<true>{dw_acc, (int)h}, s);
+    return tc::launch_tc_gemm2<kBN, true, true, true>(G, x, (int)V, (int)h, (int)n,
+                                                     EpiF32<true>{dw_acc, (int)h, gs}, s);
+}
+
+}  // namespace
+
+extern "C" int ee_exit_head_train(const void* x, int64_t n, int64_t h, const void* W, int64_t V,
+                                  const int64_t* targets, float weight, float* loss, float* dx,
+                                  float* dw_acc, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if ((rc = check_head_shape(n, h, V, ws_bytes, ws))) return rc;
+    cudaStream_t s = as_stream(stream);
+    TrainWs w = carve(ws, n, V);
+    if ((rc = head_forward(x, n, h, W, V, targets, weight, loss, w.g, w, s))) return rc;
+    return head_backward(x, n, h, W, V, w.g, nullptr, dx, dw_acc, w, s);
+}
+
+// The same head split at the autograd boundary: the forward leaves G in a
+// caller buffer; the backward scales by the incoming gradient read from
+// device memory (no host synchronisation) and accumulates dW straight into
+// the caller's float32 gradient sum.
+extern "C" int ee_exit_head_train_fwd(const void* x, int64_t n, int64_t h, const void* W,
+                                      int64_t V, const int64_t* targets, float weight, float* loss,
+                                      void* G, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if ((rc = check_head_shape(n, h, V, ws_bytes, ws))) return rc;
+    EE_REQUIRE(G != nullptr, EE_ESHAPE, "exit_head_train_fwd: null G");
+    TrainWs w = carve(ws, n, V);
+    return head_forward(x, n, h, W, V, targets, weight, loss, (bf16*)G, w, as_stream(stream));
+}
+
+extern "C" int ee_exit_head_train_bwd(const void* x, int64_t n, int64_t h, const void* W,
+                                      int64_t V, const void* G, const float* grad, float* dx,
+                                      float* dw_acc, void* ws, size_t ws_bytes, void* stream) {
+    int rc;
+    if ((rc = check_head_shape(n, h, V, ws_bytes, ws))) return rc;
+    EE_REQUIRE(G != nullptr && dx != nullptr && dw_acc != nullptr, EE_ESHAPE,
+               "exit_head_train_bwd: null argument");
+    TrainWs w = carve(ws, n, V);
+    return head_backward(x, n, h, W, V, (const bf16*)G, grad, dx, dw_acc, w, as_stream(stream));
 }
 
 // Weight gradient of a bf16 linear layer accumulated straight into a float32

@@ -110,13 +110,9 @@ def _check_ids(ids, V, what):
         raise TokenError(f"{what} id out of vocabulary range")
 
 
-def exit_head_loss_and_grads(x, W, targets, weight=1.0, dw_acc=None, validated=False):
-    """Fused exit head: returns (loss (0-d float32 tensor), dx (n, h) float32,
-    dW (V, h) float32).  x (n, h) and W (V, h) bf16 CUDA tensors; targets
-    int64 (n,), host or device (``validated=True``: the caller has
-    range-checked device targets on the host, so no synchronising check).
-    dW is accumulated into ``dw_acc`` when given (microbatch accumulation,
-    eepipe/pipeline.py:422-427)."""
+def _head_inputs(x, W, targets, validated):
+    """Shape / target checks and bf16 operands of the fused train head, plus
+    its per-stream workspace."""
     torch = _torch()
     _lib.require_cuda()
     if x.dim() != 2 or W.dim() != 2 or x.shape[1] != W.shape[1]:
@@ -133,9 +129,21 @@ def exit_head_loss_and_grads(x, W, targets, weight=1.0, dw_acc=None, validated=F
         raise ShapeError(f"{targets.numel()} targets for {n} rows")
     x = x.to(torch.bfloat16).contiguous()
     W = W.to(torch.bfloat16).contiguous()
-    lib = _lib.load()
-    need = lib.ee_workspace_bytes(_lib.EE_OP_EXIT_HEAD_TRAIN, n, h, V, 0, 0)
-    ws = _workspace(x.device, need)
+    need = _lib.load().ee_workspace_bytes(_lib.EE_OP_EXIT_HEAD_TRAIN, n, h, V, 0, 0)
+    return x, W, targets, _workspace(x.device, need)
+
+
+def exit_head_loss_and_grads(x, W, targets, weight=1.0, dw_acc=None, validated=False):
+    """Fused exit head: returns (loss (0-d float32 tensor), dx (n, h) float32,
+    dW (V, h) float32).  x (n, h) and W (V, h) bf16 CUDA tensors; targets
+    int64 (n,), host or device (``validated=True``: the caller has
+    range-checked device targets on the host, so no synchronising check).
+    dW is accumulated into ``dw_acc`` when given (microbatch accumulation,
+    eepipe/pipeline.py:422-427)."""
+    torch = _torch()
+    x, W, targets, ws = _head_inputs(x, W, targets, validated)
+    n, h = x.shape
+    V = W.shape[0]
     loss = torch.zeros((), dtype=torch.float32, device=x.device)
     dx = torch.empty((n, h), dtype=torch.float32, device=x.device)
     if dw_acc is None:
@@ -146,10 +154,13 @@ def exit_head_loss_and_grads(x, W, targets, weight=1.0, dw_acc=None, validated=F
 
 
 class ExitHeadCE:
-    """torch.autograd.Function: weighted CE of one exit head.  The fused
-    kernel produces loss and gradients in one call (the reference defers exit
-    forwards into the backward step anyway, eepipe/pipeline.py:175-192), so
-    backward only scales the saved gradients by the incoming grad."""
+    """torch.autograd.Function: weighted CE of one exit head.  Without a
+    float32 gradient sum on W the fused kernel produces loss and gradients in
+    one call (the reference defers exit forwards into the backward step
+    anyway, eepipe/pipeline.py:175-192) and backward scales them by the
+    incoming gradient; with one (mixed precision) the head is split at the
+    autograd boundary (ee_exit_head_train_fwd / _bwd) so the weight gradient
+    lands in the sum inside the GEMM."""
 
     _fn = None
 
@@ -161,25 +172,47 @@ class ExitHeadCE:
             class _F(torch.autograd.Function):
                 @staticmethod
                 def forward(ctx, x, W, targets, weight, validated):
+                    acc = getattr(W, "_ee_main_grad", None)
+                    ctx.dtypes = (x.dtype, W.dtype)
+                    ctx.split = acc is not None
+                    if ctx.split:
+                        # mixed precision: forward keeps d loss / d logits (G);
+                        # the backward scales by the incoming gradient on the
+                        # device and adds g * G^T x straight into W's float32
+                        # sum inside the GEMM epilogue (no dW buffer, no pass)
+                        x2, W2, t2, ws = _head_inputs(x.detach(), W.detach(), targets,
+                                                      validated)
+                        n, h = x2.shape
+                        V = W2.shape[0]
+                        G = torch.empty((n, V), dtype=torch.bfloat16, device=x2.device)
+                        loss = torch.zeros((), dtype=torch.float32, device=x2.device)
+                        call("ee_exit_head_train_fwd", ptr(x2), n, h, ptr(W2), V, ptr(t2),
+                             float(weight), ptr(loss), ptr(G), ptr(ws), ws.numel(),
+                             stream_ptr())
+                        ctx.save_for_backward(x2, W2, G)
+                        ctx.acc = acc
+                        return loss
                     loss, dx, dw = exit_head_loss_and_grads(x.detach(), W.detach(), targets,
                                                             weight, validated=validated)
                     ctx.save_for_backward(dx, dw)
-                    ctx.w_main_grad = getattr(W, "_ee_main_grad", None)
-                    ctx.dtypes = (x.dtype, W.dtype)
                     return loss
 
                 @staticmethod
                 def backward(ctx, g):
+                    if ctx.split:
+                        x2, W2, G = ctx.saved_tensors
+                        n, h = x2.shape
+                        V = W2.shape[0]
+                        ws = _workspace(x2.device, _lib.load().ee_workspace_bytes(
+                            _lib.EE_OP_EXIT_HEAD_TRAIN, n, h, V, 0, 0))
+                        gs = g.detach().to(torch.float32).reshape(()).contiguous()
+                        dx = torch.empty((n, h), dtype=torch.float32, device=x2.device)
+                        call("ee_exit_head_train_bwd", ptr(x2), n, h, ptr(W2), V, ptr(G),
+                             ptr(gs), ptr(dx), ptr(ctx.acc.view(V, h)), ptr(ws), ws.numel(),
+                             stream_ptr())
+                        return dx.to(ctx.dtypes[0]), None, None, None, None
                     dx, dw = ctx.saved_tensors
-                    acc = ctx.w_main_grad
-                    if acc is not None:
-                        # mixed precision: dW * g straight into the float32 sum
-                        # of W (one pass; no bf16 gradient of the 50k x h matrix)
-                        acc.view(dw.shape).addcmul_(dw, g.to(dw.dtype))
-                        gw = None
-                    else:
-                        gw = (dw * g).to(ctx.dtypes[1])
-                    return (dx * g).to(ctx.dtypes[0]), gw, None, None, None
+                    return (dx * g).to(ctx.dtypes[0]), (dw * g).to(ctx.dtypes[1]), None, None, None
 
             cls._fn = _F
         return cls._fn.apply(x, W, targets, float(weight), bool(validated))

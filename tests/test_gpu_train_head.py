@@ -106,3 +106,36 @@ def test_train_head_ordered_split_k_matches_oracle_and_is_deterministic():
     assert _rel(dw, rdw) < 2e-2
     _, dx2, _, _, _ = _run(x, w, t, 0.5)
     assert np.array_equal(dx, dx2)
+
+
+def test_split_forward_backward_matches_fused():
+    """ee_exit_head_train_fwd / _bwd (the head split at the autograd
+    boundary, used in mixed precision): the forward's loss equals the fused
+    call's bitwise; the backward with an incoming gradient g read from device
+    memory gives g * dx and adds g * dW into an existing float32 sum."""
+    import torch
+    from paper_2312_04916_b200 import _lib
+    from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+    from paper_2312_04916_b200.training import exit_head_loss_and_grads
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n, h, V = 300, 256, 1000
+    x = torch.randn(n, h, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, h, device="cuda", generator=g) * 0.05).bfloat16()
+    t = torch.randint(0, V, (n,), device="cuda", generator=g)
+    loss, dx, dw = exit_head_loss_and_grads(x, W, t.cpu().numpy(), 0.6)
+    lib = _lib.load()
+    wsb = lib.ee_workspace_bytes(_lib.EE_OP_EXIT_HEAD_TRAIN, n, h, V, 0, 0)
+    ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
+    G = torch.empty(n, V, dtype=torch.bfloat16, device="cuda")
+    loss2 = torch.zeros((), device="cuda")
+    call("ee_exit_head_train_fwd", ptr(x), n, h, ptr(W), V, ptr(t), 0.6, ptr(loss2), ptr(G),
+         ptr(ws), wsb, stream_ptr())
+    gs = torch.tensor(0.7, device="cuda")
+    dx2 = torch.empty(n, h, device="cuda")
+    acc = torch.ones(V, h, device="cuda")
+    call("ee_exit_head_train_bwd", ptr(x), n, h, ptr(W), V, ptr(G), ptr(gs), ptr(dx2), ptr(acc),
+         ptr(ws), wsb, stream_ptr())
+    torch.cuda.synchronize()
+    assert float(loss2) == float(loss)
+    assert torch.allclose(dx2, 0.7 * dx, rtol=1e-5, atol=1e-7)
+    assert torch.allclose(acc - 1.0, 0.7 * dw, rtol=1e-4, atol=1e-6)
