@@ -30,7 +30,6 @@ Two transports share the same `StageWorker`:
 
 from __future__ import annotations
 
-import threading
 import time
 from dataclasses import dataclass, field
 from queue import Empty, Queue
