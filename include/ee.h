@@ -243,7 +243,10 @@ typedef struct {
     void* head_x;             /* mlp+embed scratch: (16, h) float32 */
     void* head_xn;            /* (16, h) dcode */
     void* head_mid;           /* (16, 4h) dcode */
-    uint8_t* res;             /* device result slots: max_slots x res_stride bytes */
+    uint8_t* res;             /* result slots the heads write: max_slots x res_stride bytes,
+                               * device memory, or res_host itself (host-mapped: the loop
+                               * then polls each slot's nonfinite word, armed to -1 at
+                               * launch and written last, instead of copy + sync) */
     uint8_t* res_host;        /* PINNED host copy of the result slots */
     int32_t res_stride, max_slots;
     int32_t off_tok, off_conf, off_fire, off_bad;  /* field offsets inside a slot */

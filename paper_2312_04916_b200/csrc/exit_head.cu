@@ -105,6 +105,9 @@ __device__ void merge_and_decide(const HeadWs& w, int64_t units, int m, float th
             fire[c] = (thr < 1.0f && cf > thr) ? 1 : 0;
         }
     }
+    // the outputs may live in host-mapped memory that the host polls through
+    // *nonfinite (written last): make them visible system-wide first
+    __threadfence_system();
     sync();
     if (tid == 0) {
         *nonfinite = __ldcg(w.flag);

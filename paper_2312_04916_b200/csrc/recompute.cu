@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <vector>
 
 #include "ee_common.cuh"
@@ -45,6 +46,7 @@ struct Runner {
     std::vector<std::vector<int>> at_tap;  // head indices per tap
     std::vector<uint8_t> kv;               // [L][s_max] fill mask
     int stage = 0;                         // alternating host staging half
+    bool mapped = false;                   // result slots in host-mapped memory (res == res_host)
     std::chrono::steady_clock::time_point t_start;
 
     int64_t launches = 0, h2d = 0, d2h = 0;
@@ -82,6 +84,8 @@ struct Runner {
         }
         launches += E->dcode == EE_BF16 ? 1 : 2;
         uint8_t* r = E->res + (int64_t)slot * E->res_stride;
+        if (mapped)  // host-mapped result slot: arm its completion word
+            *(volatile int32_t*)(E->res_host + (int64_t)slot * E->res_stride + E->off_bad) = -1;
         return ee_exit_head_infer(xsrc, h, rows, m, h, hd.norm, E->eps, hd.W, hd.V, E->wcode,
                                   A->threshold, (int32_t*)(r + E->off_tok), (float*)(r + E->off_conf),
                                   r + E->off_fire, (int32_t*)(r + E->off_bad), nullptr, E->head_ws,
@@ -182,11 +186,31 @@ struct Runner {
             const int upto = (int)slots.size();
             if (upto == checked) return EE_OK;
             const size_t nb = (size_t)upto * E->res_stride;
-            cudaError_t e = cudaMemcpyAsync(E->res_host, E->res, nb, cudaMemcpyDeviceToHost, s);
-            EE_REQUIRE(e == cudaSuccess, EE_ECUDA, "result copy: %s", cudaGetErrorString(e));
             d2h += nb;
-            e = cudaStreamSynchronize(s);
-            EE_REQUIRE(e == cudaSuccess, EE_ECUDA, "pass sync: %s", cudaGetErrorString(e));
+            if (mapped) {
+                // the heads write straight into host memory; the word each
+                // writes last (nonfinite flag) was armed to -1 at launch
+                for (int k = checked; k < upto; ++k) {
+                    const volatile int32_t* done =
+                        (const volatile int32_t*)(E->res_host + (int64_t)k * E->res_stride + E->off_bad);
+                    long spins = 0;
+                    while (*done == -1) {
+                        if ((++spins & 0xFFFF) == 0) {  // surface a failed launch
+                            const cudaError_t q = cudaStreamQuery(s);
+                            EE_REQUIRE(q == cudaSuccess || q == cudaErrorNotReady, EE_ECUDA,
+                                       "pass sync: %s", cudaGetErrorString(q));
+                            if (q == cudaSuccess && *done == -1)
+                                return ee_fail(EE_ECUDA, "exit head result never arrived");
+                        }
+                    }
+                }
+                std::atomic_thread_fence(std::memory_order_acquire);
+            } else {
+                cudaError_t e = cudaMemcpyAsync(E->res_host, E->res, nb, cudaMemcpyDeviceToHost, s);
+                EE_REQUIRE(e == cudaSuccess, EE_ECUDA, "result copy: %s", cudaGetErrorString(e));
+                e = cudaStreamSynchronize(s);
+                EE_REQUIRE(e == cudaSuccess, EE_ECUDA, "pass sync: %s", cudaGetErrorString(e));
+            }
             for (int k = 0; k < upto; ++k) {
                 const uint8_t* r = E->res_host + (int64_t)k * E->res_stride;
                 EE_REQUIRE(*(const int32_t*)(r + E->off_bad) == 0, EE_ENONFINITE,
@@ -299,6 +323,7 @@ extern "C" int ee_generate_kv_recompute(ee_generate_args_t* A) {
     R.s = as_stream(E->stream);
     R.L = E->n_layers;
     R.h = (int)E->dec->h;
+    R.mapped = E->res == E->res_host;
     for (int i = 0; i < E->n_heads; ++i) {
         const int t = E->heads[i].tap;
         if (R.taps.empty() || R.taps.back() != t) {

@@ -31,6 +31,7 @@ Design (B200-first):
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -47,6 +48,7 @@ from .schedule import inference_latency
 _UNSUPPORTED_HEADS = ("layer+embed",)
 _EMIT_TIMEOUT = 120.0
 _HEAD_MAX_ROWS = 16
+_MAPPED_RESULTS = os.environ.get("EE_MAPPED_RESULTS", "1") != "0"
 _RES_DTYPE = np.dtype([("tok", "<i4", (_HEAD_MAX_ROWS,)), ("conf", "<f4", (_HEAD_MAX_ROWS,)),
                        ("fire", "u1", (_HEAD_MAX_ROWS,)), ("bad", "<i4"), ("pad", "u1", (12,))])
 
@@ -521,7 +523,12 @@ class Engine:
             self.tok_emb.data_ptr(), self.pos_emb.data_ptr(), self.ctrl.data_ptr(),
             self.ctrl_host.data_ptr(), self.ctrl_cap, self.head_ws.data_ptr(),
             self.head_ws.numel(), self.head_x.data_ptr(), self.head_xn.data_ptr(),
-            self.head_mid.data_ptr(), self.res.data_ptr(), self.h_res_t.data_ptr(),
+            self.head_mid.data_ptr(),
+            # result slots: host-mapped pinned memory (the heads write them
+            # directly; the loop polls each slot's last-written word instead
+            # of a copy + stream synchronisation), or device memory + copy
+            self.h_res_t.data_ptr() if _MAPPED_RESULTS else self.res.data_ptr(),
+            self.h_res_t.data_ptr(),
             _RES_DTYPE.itemsize, self.max_slots, f["tok"][1], f["conf"][1], f["fire"][1],
             f["bad"][1], self.stream.cuda_stream,
             self.pf_ws.data_ptr() if self.pf_bytes else None, self.pf_bytes)
