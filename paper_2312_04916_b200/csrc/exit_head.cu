@@ -213,10 +213,11 @@ struct HeadEpi {
     }
 };
 
-// weight-ring depth per row configuration (2 CTAs per SM for m <= 8:
-// 2 x 4 x 16 KB of weights in flight per SM)
+// weight-ring depth per row configuration: two CTAs per SM either way
+// (4 x 24 KB stages for 8-row groups, 3 x 32 KB for 16-row groups), so the
+// fixed grid of 2 x SMs runs in one wave
 template <int NB>
-constexpr int kHeadStages = NB == 1 ? 4 : 6;
+constexpr int kHeadStages = NB == 1 ? 4 : 3;
 
 template <int NB>
 __global__ void __launch_bounds__(tma_gemv::kThreads)
@@ -342,8 +343,7 @@ extern "C" int ee_exit_head_infer(const float* x, int64_t ldx, const int32_t* ro
         const int nb = m <= 8 ? 1 : 2;
         const size_t smem = tma_gemv::smem_bytes(nb, nb == 1 ? kHeadStages<1> : kHeadStages<2>);
         // the grid (and with it the two-level merge order) does not depend
-        // on m: 2 CTAs per SM (m > 8 needs more shared memory and runs the
-        // same grid in two waves; decode passes carry <= 1 + max_deferred rows)
+        // on m: 2 CTAs per SM
         const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sms * 2);
         static int conf_smem[2][16] = {};
         int dev = 0;

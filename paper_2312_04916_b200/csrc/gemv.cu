@@ -7,6 +7,8 @@
 // EE_BF16 (row-major weights, any K % 8 == 0): LDG + mma.sync kernel.
 // EE_F32 (parity mode): SIMT FFMA kernel.
 // All are row-stable: each output's reduction order depends only on (n, k).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "gemv_core.cuh"
@@ -122,11 +124,16 @@ struct TileResidualStats {
 };
 
 // ---- TMA-fed kernel (tiled weights) ------------------------------------------
+// weight-ring depth: 4 stages for 8-row groups, 3 for 16-row groups, so both
+// run two CTAs per SM (~97 KB of shared memory each)
+template <int NB>
+constexpr int kGemvStages = NB == 1 ? 4 : 3;
+
 template <int NB, class Epi>
 __global__ void __launch_bounds__(tma_gemv::kThreads)
 k_gemv_tma(const bf16* __restrict__ W, int N, int K, const bf16* __restrict__ X, int64_t ldx,
            int m, tma_gemv::RowNorm rn, Epi epi) {
-    tma_gemv::gemv_body<NB>(W, N, K, X, ldx, m, rn, epi);
+    tma_gemv::gemv_body<NB, Epi, kGemvStages<NB>>(W, N, K, X, ldx, m, rn, epi);
 }
 
 // ---- LDG kernels (row-major bf16, fp32 parity mode) ----------------------------
@@ -192,7 +199,7 @@ template <int NB, class Epi>
 int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K,
                tma_gemv::RowNorm rn, Epi epi, cudaStream_t s) {
     auto kern = k_gemv_tma<NB, Epi>;
-    const size_t smem = tma_gemv::smem_bytes(NB);
+    const size_t smem = tma_gemv::smem_bytes(NB, kGemvStages<NB>);
     static bool configured[16] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -211,12 +218,20 @@ int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, 
     return EE_OK;
 }
 
+static bool gemv_nb1_only() {  // EE_GEMV_NB1=1: 8-row groups only (A/B runs)
+    static const bool v = getenv("EE_GEMV_NB1") && atoi(getenv("EE_GEMV_NB1")) != 0;
+    return v;
+}
+
 template <class Epi>
 int run_tma_epi(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K,
                 tma_gemv::RowNorm rn, Epi epi, cudaStream_t s) {
     EE_REQUIRE(K % kTiledKS == 0, EE_ESHAPE, "tiled gemv needs K %% %d == 0 (K=%lld)", kTiledKS,
                (long long)K);
-    if (m <= 8) return run_tma_nb<1>(X, ldx, m, W, N, K, rn, epi, s);
+    // 16-row groups for m > 8 (each weight stage serves 16 rows; a 3-deep
+    // ring keeps it at two CTAs per SM).  A row's result does not depend on
+    // the group width: the reduction order is per (n, k).
+    if (m <= 8 || gemv_nb1_only()) return run_tma_nb<1>(X, ldx, m, W, N, K, rn, epi, s);
     return run_tma_nb<2>(X, ldx, m, W, N, K, rn, epi, s);
 }
 

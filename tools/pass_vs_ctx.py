@@ -21,8 +21,8 @@ def main():
     L, st = cfg.num_layers, eng.stream
     with torch.cuda.stream(st):
         eng.kv.reset()
-        eng._grow(8)
-        for rows in (1, 5):
+        eng._grow(16)
+        for rows in [int(r) for r in os.environ.get('ROWS', '1,5').split(',')]:
             for ctx in [int(c) for c in os.environ.get('CTXS', '128,512,1024,2000').split(',')]:
                 eng.upload_ctrl([ctx - rows + 1 + r for r in range(rows)])
                 for _ in range(2):
