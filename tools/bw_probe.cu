@@ -107,8 +107,8 @@ int main() {
         double gbs = timeit([&](int r) { k_ldg<<<sms * bpsm, 256>>>((const uint4*)(buf + r * bytes), bytes / 16, out); });
         printf("ldg  blocks/sm=%2d                                 %7.0f GB/s\n", bpsm, gbs);
     }
-    for (int piece : {1024, 4096, 16384}) {
-        for (int chunk : {16384, 32768}) {
+    for (int piece : {16384, 32768, 65536}) {
+        for (int chunk : {16384, 32768, 65536}) {
             if (piece > chunk) continue;
             for (int stages : {4, 6}) {
                 for (int cps : {1, 2, 3}) {
