@@ -17,6 +17,16 @@
 
 #include "ee_common.cuh"
 
+// kernels ee_decode_layer launches for a pass of m rows (the launch count a
+// caller reports)
+int decode_layer_launches(const ee_decoder_t* D, int64_t m) {
+    if (m == 0) return 0;
+    if (D->dtype != EE_BF16_TILED) return 7;
+    const bool prefill = m >= kPrefillMinRows && D->pf_ws &&
+                         D->pf_ws_bytes >= (size_t)4 * m * 4 * D->h * sizeof(float);
+    return prefill ? 9 : 5;  // 4 x (GEMM + apply) + attention, or 4 GEMVs + attention
+}
+
 extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, int64_t row0, int64_t m,
                                const int32_t* pos, int32_t max_pos, void* stream) {
     if (m == 0) return EE_OK;

@@ -126,5 +126,6 @@ int launch_prefill_tiled(const bf16* x, int64_t m, int64_t K, const void* W, int
                          const int32_t* pos, int64_t h, void* out, float* xres, bf16* xb,
                          float* ssq_out, void* ws, size_t ws_bytes, cudaStream_t s);
 constexpr int kPrefillMinRows = 17;  // passes with more rows use the GEMM
+int decode_layer_launches(const ee_decoder_t* D, int64_t m);
 int launch_qkv_tiled(const bf16* x, int64_t m, int64_t h, const void* Wqkv, GemvNorm nrm,
                      float* q, void* kc, void* vc, const int32_t* pos, cudaStream_t s);

@@ -82,7 +82,7 @@ struct Runner {
             rows = nullptr;
             launches += 4;
         }
-        launches += E->dcode == EE_BF16 ? 1 : 2;
+        launches += 2;  // row gather + norm, then the head GEMV
         uint8_t* r = E->res + (int64_t)slot * E->res_stride;
         if (mapped)  // host-mapped result slot: arm its completion word
             *(volatile int32_t*)(E->res_host + (int64_t)slot * E->res_stride + E->off_bad) = -1;
@@ -280,7 +280,7 @@ struct Runner {
                 while (l2 + 1 <= tap && active(l2 + 1) == m_act) ++l2;
                 if (m_act) {
                     for (int i = 0; i <= l2 - l; ++i) m_act_arr[i] = m_act;
-                    launches += (int64_t)(D->dtype == EE_BF16_TILED ? 5 : 7) * (l2 - l + 1);
+                    launches += (int64_t)decode_layer_launches(D, m_act) * (l2 - l + 1);
                     if ((rc = ee_decode_layers(D, E->layers + (l - 1), l2 - l + 1, n,
                                                m_act_arr.data(), E->ctrl, max_pos, E->stream)))
                         return rc;

@@ -493,7 +493,7 @@ class Engine:
                  EE_EPI_RESIDUAL, ptr(self.head_x), h, s)
             xsrc, rows_ptr = self.head_x, None
             self.launches += 4
-        self.launches += 1 if self.dcode == _lib.EE_BF16 else 2
+        self.launches += 2  # row gather + norm, then the head GEMV
         call("ee_exit_head_infer", ptr(xsrc), h, rows_ptr, m, h, ptr(e.norm), NORM_EPS,
              ptr(e.W), e.V, self.wcode, float(threshold),
              self._res_ptr(slot, "tok"), self._res_ptr(slot, "conf"),
@@ -560,7 +560,11 @@ class Engine:
         arr = (ctypes.c_int32 * n)(*m_active)
         layers = ctypes.c_void_p(ctypes.addressof(self.layers_c) +
                                  la * ctypes.sizeof(_lib.EeLayer))
-        self.launches += (5 if self.tiled else 7) * sum(1 for v in m_active if v)
+        def per(v):  # kernels per layer (decode.cu decode_layer_launches)
+            if not self.tiled:
+                return 7
+            return 9 if prefill and self.pf_bytes and v >= 17 else 5
+        self.launches += sum(per(v) for v in m_active if v)
         if prefill and self.pf_bytes:
             self.dec.pf_ws, self.dec.pf_ws_bytes = self.pf_ws.data_ptr(), self.pf_bytes
         try:
