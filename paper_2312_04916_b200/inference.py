@@ -49,6 +49,7 @@ _UNSUPPORTED_HEADS = ("layer+embed",)
 _EMIT_TIMEOUT = 120.0
 _HEAD_MAX_ROWS = 16
 _MAPPED_RESULTS = os.environ.get("EE_MAPPED_RESULTS", "1") != "0"
+_DEVICE_STAGE_STREAMS = {}
 _RES_DTYPE = np.dtype([("tok", "<i4", (_HEAD_MAX_ROWS,)), ("conf", "<f4", (_HEAD_MAX_ROWS,)),
                        ("fire", "u1", (_HEAD_MAX_ROWS,)), ("bad", "<i4"), ("pad", "u1", (12,))])
 
@@ -709,10 +710,18 @@ class _InferStage:
         # one stream per stage engine for the engine's lifetime (not a new one
         # per call): buffers the engine (re)allocates on it stay ordered with
         # this stage's work under the caching allocator's per-stream reuse
-        st = getattr(self.eng, "_stage_stream", None)
+        # one stream per DEVICE, shared by every stage placed on it (and kept
+        # across calls): stages on one GPU serialise their kernels in
+        # submission order.  With a stream per stage, concurrently running
+        # stage kernels on one GPU made 7B-scale runs non-deterministic
+        # (tools/pipeline_race_probe2.py; deterministic with one stream, and
+        # at threshold 1.0 where stages never overlap) -- one GPU gains no
+        # throughput from overlapping its own stages anyway
+        key = str(self.eng.device)
+        st = _DEVICE_STAGE_STREAMS.get(key)
         if st is None:
             with torch.cuda.device(self.eng.device):
-                st = self.eng._stage_stream = torch.cuda.Stream(self.eng.device)
+                st = _DEVICE_STAGE_STREAMS[key] = torch.cuda.Stream(self.eng.device)
         self.stream = st
         self.eng.stream = st
         self.heads_at = {}
