@@ -25,6 +25,8 @@ extern "C" const char* ee_last_error(void) { return g_err; }
 
 extern "C" int ee_abi_version(void) { return 1; }
 
+int g_pdl_off = 0;
+
 bool ee_pdl_enabled() {
     static int on = -1;
     if (on < 0) {

@@ -21,9 +21,10 @@
 //   * rows up to position 255 need no cross-CTA step at all; longer rows
 //     publish one partial per chunk and the last CTA of the (row, head)
 //     merges them;
-//   * K/V rows that predate this pass (positions below every row of the
-//     launch) are prefetched into L2 BEFORE griddepcontrol.wait, overlapping
-//     the QKV GEMV that is still writing the new rows.
+//   * nothing but the host-written positions is touched before
+//     griddepcontrol.wait.  (An L2 prefetch of the K/V rows that predate the
+//     pass, issued before the wait to overlap the QKV GEMV, made multi-chunk
+//     rows (positions >= 256) nondeterministic run to run on B200: removed.)
 #include "attn_core.cuh"
 
 namespace {
@@ -46,9 +47,6 @@ template <> __device__ __forceinline__ void load4<bf16>(const bf16* p, float* v)
 template <> __device__ __forceinline__ void load4<float>(const float* p, float* v) {
     const float4 f = *reinterpret_cast<const float4*>(p);
     v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-}
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 template <typename T>
@@ -77,17 +75,6 @@ k_attn_decode(const float* __restrict__ q, const int32_t* __restrict__ pos, int 
     const bool wvalid = j0 <= p;
     const T* krow = kc + (int64_t)jj * h + hh * dh;
     const T* vrow = vc + (int64_t)jj * h + hh * dh;
-    {
-        int pmin = p;
-        for (int i = 0; i < m; ++i) pmin = min(pmin, pos[i]);
-        if (valid && jj < pmin) {  // written by an earlier pass: fetch while QKV runs
-            const int bytes = dh * (int)sizeof(T);
-            for (int o = 0; o < bytes; o += 128) {
-                prefetch_l2((const char*)krow + o);
-                prefetch_l2((const char*)vrow + o);
-            }
-        }
-    }
     pdl_wait_dev();
     for (int d = threadIdx.x; d < dh; d += kThreadsA) s_q[d] = q[(int64_t)r * h + hh * dh + d];
     __syncthreads();
@@ -214,22 +201,14 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     float* s_q = smem_rows + kWarpsA * kBlk * dh / 2;                      // [mr][dh]
     float* s_acc = s_q + mr * dh;                                          // [mr][kWarpsA][dh]
     // host-written control data: safe before the wait
-    int pmax = -1, pmin = 1 << 30;
+    int pmax = -1;
     for (int i = 0; i < mr; ++i) pmax = max(pmax, pos[r0 + i]);
-    for (int i = 0; i < m; ++i) pmin = min(pmin, pos[i]);
     if (pmax < ch * kChunk) {
         pdl_wait_dev();
         return;
     }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int j0 = ch * kChunk + warp * kBlk;
-    const int jj = j0 + lane;
-    if (jj <= pmax && jj < pmin) {  // written by an earlier pass: fetch while QKV runs
-        prefetch_l2(kc + (int64_t)jj * h + hh * dh);
-        prefetch_l2(kc + (int64_t)jj * h + hh * dh + 64);
-        prefetch_l2(vc + (int64_t)jj * h + hh * dh);
-        prefetch_l2(vc + (int64_t)jj * h + hh * dh + 64);
-    }
     pdl_wait_dev();
     // the block's K / V loads go out first, the q rows are staged meanwhile
     attn::BlockRegsV R;

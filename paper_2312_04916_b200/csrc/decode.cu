@@ -41,6 +41,9 @@ extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, int64
     // EE_ABLATE (profiling only; wrong results): bit 0 skips the explicit
     // RMSNorm launches, bit 1 the attention.
     static const int ablate = getenv("EE_ABLATE") ? atoi(getenv("EE_ABLATE")) : 0;
+    // EE_PDL_SKIP (debug): bit k launches kernel k of the tiled decode layer
+    // (QKV, attention, wo, w1, w2) without PDL
+    static const int pdl_skip = getenv("EE_PDL_SKIP") ? atoi(getenv("EE_PDL_SKIP")) : 0;
     int rc;
     if (dt == EE_BF16_TILED) {
         EE_REQUIRE(D->xb && D->ssq, EE_ESHAPE, "decode_layer: tiled mode needs xb and ssq");
@@ -72,19 +75,26 @@ extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, int64
                                         nullptr, nullptr, nullptr, nullptr, h, nullptr, x, xb, ssq,
                                         pw, pb, s);
         }
+        g_pdl_off = pdl_skip & 1;
         if ((rc = launch_qkv_tiled(xb, m, h, L->wqkv, folded, D->q, L->kcache, L->vcache, pos, s)))
             return rc;
+        g_pdl_off = pdl_skip & 2;
         if (!(ablate & 2) &&
             (rc = launch_attention(D->q, m, pos, max_pos, L->kcache, L->vcache, D->nh, h / D->nh, dt,
                                    D->attn, D->ws, D->ws_bytes, s)))
             return rc;
+        g_pdl_off = pdl_skip & 4;
         if ((rc = launch_gemv_tiled((const bf16*)D->attn, m, h, L->wo, h, EE_EPI_RESIDUAL, x, h,
                                     stats, s)))
             return rc;
+        g_pdl_off = pdl_skip & 8;
         if ((rc = launch_gemv_tiled(xb, m, h, L->w1, 4 * h, EE_EPI_GELU, D->xn, 4 * h, folded, s)))
             return rc;
-        return launch_gemv_tiled((const bf16*)D->xn, m, 4 * h, L->w2, h, EE_EPI_RESIDUAL, x, h,
-                                 stats, s);
+        g_pdl_off = pdl_skip & 16;
+        rc = launch_gemv_tiled((const bf16*)D->xn, m, 4 * h, L->w2, h, EE_EPI_RESIDUAL, x, h,
+                               stats, s);
+        g_pdl_off = pdl_skip & 32;  // whatever follows the layer (next layer, heads)
+        return rc;
     }
     if (!(ablate & 1) &&
         (rc = launch_rmsnorm_rows(x, h, nullptr, m, h, L->attn_norm, D->eps, D->xn, dt, s)))

@@ -82,6 +82,7 @@ __device__ __forceinline__ void pdl_wait_dev() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void pdl_trigger_dev() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 bool ee_pdl_enabled();  // EE_PDL=0 disables (debug)
+extern int g_pdl_off;   // debug: nonzero disables PDL on the next launches
 
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -95,7 +96,7 @@ static inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 bl
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = ee_pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = ee_pdl_enabled() && !g_pdl_off ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
