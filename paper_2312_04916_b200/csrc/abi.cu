@@ -25,7 +25,7 @@ extern "C" const char* ee_last_error(void) { return g_err; }
 
 extern "C" int ee_abi_version(void) { return 1; }
 
-int g_pdl_off = 0;
+thread_local int g_pdl_off = 0;
 
 bool ee_pdl_enabled() {
     static int on = -1;

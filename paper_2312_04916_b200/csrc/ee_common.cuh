@@ -82,7 +82,7 @@ __device__ __forceinline__ void pdl_wait_dev() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void pdl_trigger_dev() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 bool ee_pdl_enabled();  // EE_PDL=0 disables (debug)
-extern int g_pdl_off;   // debug: nonzero disables PDL on the next launches
+extern thread_local int g_pdl_off;  // debug (EE_PDL_SKIP): nonzero disables PDL on this thread's next launches
 
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
