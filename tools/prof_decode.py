@@ -20,6 +20,7 @@ from paper_2312_04916_b200.model import build_model  # noqa: E402
 def main():
     passes = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     rows = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    ctx = int(sys.argv[3]) if len(sys.argv) > 3 else 128  # first row's position
     cfg = c3_config()
     model = build_model(cfg, 0, init="device", dtype=torch.bfloat16)
     # builds the engine + one short generation (exercises heads)
@@ -29,9 +30,9 @@ def main():
     with torch.cuda.stream(eng.stream):
         eng.kv.reset()
         eng._grow(rows)
-        eng.upload_ctrl([128 + r for r in range(rows)])
+        eng.upload_ctrl([ctx + r for r in range(rows)])
         for _ in range(passes):
-            eng.run_layers(0, L, rows, [rows] * L, 128 + rows, 0)
+            eng.run_layers(0, L, rows, [rows] * L, ctx + rows, 0)
         eng.upload_ctrl(list(range(rows)))
         for i in range(passes):
             eng.eval_head(eng.heads[-1], eng.ctrl_ptr(0), rows, 1.0, i)
