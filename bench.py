@@ -32,6 +32,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -111,16 +113,18 @@ def prompt_tokens():
     return [int(t) for t in np.random.default_rng(1).integers(0, C3["vocab_size"], PROMPT_LEN)]
 
 
-def measured_traffic():
-    """dram bytes (read + write) of one full-depth decode pass from the
-    committed ncu launch list (profiles/r1_decode_pass_traffic.json, ctx 129),
-    next to that pass's algorithmic bytes."""
+def measured_traffic(ctx):
+    """dram bytes (read + write) of one full-depth decode pass at the bench's
+    context from the committed ncu launch list
+    (profiles/r2_decode_pass_traffic.json, made by tools/decode_traffic.py
+    from `ncu ... python tools/prof_decode.py 1 1 <ctx>`), next to that
+    pass's algorithmic bytes."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_decode_pass_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_decode_pass_traffic.json")) as f:
             t = json.load(f)
-        return {"bytes": t["traffic_bytes"], "algorithmic_bytes": t["algorithmic_bytes_ctx129"],
-                "ratio": t["traffic_bytes"] / t["algorithmic_bytes_ctx129"],
-                "source": "profiles/r1_decode_pass_traffic.json (ncu, ctx 129)"}
+        return {"bytes": t["traffic_bytes"], "algorithmic_bytes": t["algorithmic_bytes"],
+                "ratio": t["ratio"], "ctx": t["ctx"], "same_ctx": t["ctx"] == ctx,
+                "source": "profiles/r2_decode_pass_traffic.json (ncu launch list, cold cache)"}
     except Exception:
         return None
 
@@ -147,96 +151,193 @@ def decode_pass_bytes(h, L, ctx):
 
 
 # ---------------------------------------------------------------------------
-# reference arm / cpu baseline: the float64 oracle port on host cores
+# reference arm / cpu baseline: the REAL reference (`eepipe`, installed
+# unmodified into baseline/_ref) on the host cores
 # ---------------------------------------------------------------------------
 
-def cpu_slice_timing(seconds_budget=20.0):
-    """Time the reference algorithm (oracle port, numpy float64, einsum
-    optimize=False => 1 core) on a 7B-width slice: one decode layer for one
-    row at context 64 and one h x V exit head.  Returns per-token seconds
-    extrapolated to the full C3 model at threshold 1.0 (32 layers + 3 heads,
-    the reference evaluates every head at thr 1.0)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
-    import ee_oracle as O
-    h, V, nh = C3["hidden_dim"], C3["vocab_size"], C3["num_heads"]
-    rng = np.random.default_rng(0)
-    P = {"layer1.attn_norm": np.ones(h), "layer1.mlp_norm": np.ones(h)}
-    for w, shp in (("wq", (h, h)), ("wk", (h, h)), ("wv", (h, h)), ("wo", (h, h)),
-                   ("w1", (h, 4 * h)), ("w2", (4 * h, h))):
-        P["layer1." + w] = rng.normal(0, 0.02, shp)
-    P["out"] = rng.normal(0, 0.02, (V, h))
-    kv = O.KV([1], PROMPT_LEN + 2, nh, h // nh)
-    for p in range(PROMPT_LEN):
-        kv.fill(1, p, rng.normal(size=(nh, h // nh)), rng.normal(size=(nh, h // nh)))
-    x = rng.normal(size=(1, h))
-    head = {"kind": "minimalistic", "out": "out", "outT": np.ascontiguousarray(P["out"].T)}
-    t_layer, t_head, n = [], [], 0
-    t_end = time.perf_counter() + seconds_budget
-    while True:
-        kv.mask[1][PROMPT_LEN:] = False
-        t = time.perf_counter()
-        O.layer_step(P, 1, x, [PROMPT_LEN], kv, nh)
-        t_layer.append(time.perf_counter() - t)
-        t = time.perf_counter()
-        O.head_logits(P, head, x[0])
-        t_head.append(time.perf_counter() - t)
-        n += 1
-        if time.perf_counter() > t_end or n >= 10:
-            break
-    tl, th = float(np.median(t_layer)), float(np.median(t_head))
-    per_token = C3["num_layers"] * tl + 3 * th
-    return per_token, tl, th, n
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _import_reference(backend):
+    """Import the reference package from baseline/_ref with EEPIPE_BACKEND
+    set (it is read once at import, eepipe/kernels.py:13)."""
+    os.environ["EEPIPE_BACKEND"] = backend
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import eepipe.kernels as k
+    if k.BACKEND != backend:
+        raise RuntimeError(f"reference backend {backend!r} requested, got {k.BACKEND!r}")
+    import eepipe.inference as inf
+    import eepipe.model as mdl
+    return inf, mdl, k
+
+
+class RefDecodeSlice:
+    """The reference's own decode kernels on a 7B-width slice (h=4096, 32
+    heads, V=50304): `_InferParams` (which pre-transposes the head matrix,
+    eepipe/inference.py:147-171), `_layer_step` (216-229) on one row at the
+    C3 run's mean context (prompt 64 + 128), and `head_logits` (173-185) on
+    one row.  Weights from the reference's `build_model(cfg, 0)`."""
+
+    def __init__(self, backend):
+        inf, mdl, k = _import_reference(backend)
+        h, V, nh = C3["hidden_dim"], C3["vocab_size"], C3["num_heads"]
+        cfg = mdl.ModelConfig(1, h, nh, V, C3["max_seq_len"], exits=())
+        model = mdl.build_model(cfg, 0)
+        self.inf, self.backend = inf, k.BACKEND
+        self.ip = inf._InferParams(model.params, model.heads, cfg, [1], True)
+        self.cache = inf.KVCache([1], C3["max_seq_len"], nh, h // nh)
+        rng = np.random.default_rng(0)
+        self.ctx = PROMPT_LEN + NEW_TOKENS // 2
+        for p in range(self.ctx):
+            self.cache.fill(1, p, rng.normal(size=(nh, h // nh)), rng.normal(size=(nh, h // nh)))
+        self.x = self.ip.embed([1], [self.ctx])
+        self.hd, self.mats = self.ip.heads[-1]  # the final head (norm + V x h)
+
+    def sample(self):
+        """(seconds of one 1-row layer step, seconds of one head evaluation)."""
+        self.cache.mask[1][self.ctx:] = False
+        t0 = time.perf_counter()
+        self.inf._layer_step(self.ip.layers[1], self.x, [self.ctx], self.cache, 1,
+                             C3["num_heads"])
+        t1 = time.perf_counter()
+        self.ip.head_logits(self.hd, self.mats, self.x[0])
+        t2 = time.perf_counter()
+        return t1 - t0, t2 - t1
+
+
+def ref_step_seconds(t_row, t_head, threshold, new_tokens=NEW_TOKENS):
+    """One C3 step (prompt 64 + new_tokens decoded) in the reference's KV
+    recomputation, from its per-row layer and per-head costs.  Exact
+    structure, not a model of it: every (position, layer) pair is computed
+    exactly once (a deferred row later runs only the layers it skipped,
+    eepipe/inference.py:316-322, 355-360), the reference's `dot_rows`
+    (einsum optimize=False) costs the same per row whatever the pass width
+    (measured: 5 rows = 4.9 x 1 row), so layer time = rows x 32 x t_row with
+    rows = 64 prompt + new_tokens; head evaluations: threshold 1.0 evaluates
+    all 3 heads for every decided token (inference.py:293-311); below 1.0 at
+    least the first head is evaluated, and 1 per token is used (the lower
+    bound, i.e. the FASTEST the reference can be at that threshold)."""
+    L = C3["num_layers"]
+    heads = 3 if threshold >= 1.0 else 1
+    rows = PROMPT_LEN + new_tokens
+    return rows * L * t_row + (new_tokens + 1) * heads * t_head
+
+
+def _cpu_info():
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = None
+    return {"os_cpu_count": os.cpu_count(), "affinity_cpus": aff}
+
+
+def reference_decode_baseline(threshold, samples=3, compiled=True):
+    """Both reference backends on the host: numpy (`EEPIPE_BACKEND=python`,
+    in process) and Cython (`compiled`, in a subprocess since the backend is
+    fixed at import).  Returns the faster backend's tokens/s at C3 plus the
+    per-op timings of both."""
+    sl = RefDecodeSlice("python")
+    sl.sample()
+    ts = [sl.sample() for _ in range(samples)]
+    t_row = float(np.median([t[0] for t in ts]))
+    t_head = float(np.median([t[1] for t in ts]))
+    res = {"python": {"layer_row_s": t_row, "head_s": t_head, "samples": samples}}
+    if compiled:
+        try:
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--ref-probe",
+                                  "compiled"], capture_output=True, text=True, timeout=240)
+            res["compiled"] = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception as e:  # report, never fall back to our code
+            res["compiled"] = {"error": str(e)[:200]}
+    best = min((k for k in res if "layer_row_s" in res[k]),
+               key=lambda k: ref_step_seconds(res[k]["layer_row_s"], res[k]["head_s"], threshold))
+    step = ref_step_seconds(res[best]["layer_row_s"], res[best]["head_s"], threshold)
+    return {"tokens_per_s": NEW_TOKENS / step, "step_s": step, "backend": best,
+            "per_backend": res, "ctx": sl.ctx}
+
+
+def ref_probe(backend):
+    sl = RefDecodeSlice(backend)
+    t_row, t_head = sl.sample()
+    print(json.dumps({"layer_row_s": t_row, "head_s": t_head, "samples": 1}))
+    return 0
 
 
 def cpu_head_timing(n=256, h=2048, V=50304):
-    """The reference's training exit head on the host (oracle port of
-    `run_head` + `cross_entropy` + the matmul backward, float64, numpy `@`
-    on OpenBLAS with all host threads) on an n-row slice of the C2 shape;
+    """The reference's training exit head on the host: eepipe autodiff
+    `matmul(x, out, transpose_b=True)` -> `cross_entropy` -> `backward`
+    (eepipe/model.py:219-230, autodiff.py:158-179, 301-323; numpy `@` on
+    OpenBLAS with all host threads) on an n-row slice of the C2 shape,
     GFLOP/s on the same 6 n h V count as the GPU number."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
-    import ee_oracle as O
+    _import_reference(os.environ.get("EEPIPE_BACKEND", "python"))
+    from eepipe import autodiff as ad
     rng = np.random.default_rng(0)
-    x = rng.normal(size=(n, h))
-    w = rng.normal(0, 0.02, size=(V, h))
+    x = ad.Tensor(rng.normal(size=(n, h)), requires_grad=True)
+    w = ad.Tensor(rng.normal(0, 0.02, size=(V, h)), requires_grad=True)
     t = rng.integers(0, V, size=n)
-    O.exit_head_train(x[:8], w, t[:8])
+
+    def run(rows):
+        with ad.Tape():
+            loss = ad.cross_entropy(ad.matmul(x if rows == n else ad.Tensor(x.data[:rows],
+                                                                           requires_grad=True),
+                                              w, transpose_b=True), t[:rows])
+            ad.backward(loss)
+    run(8)
     t0 = time.perf_counter()
-    O.exit_head_train(x, w, t)
+    run(n)
     dt = time.perf_counter() - t0
     return {"value": 6 * n * h * V / dt / 1e9, "unit": "GFLOP/s (6nhV)", "cores": os.cpu_count(),
-            "kind": "port", "sample": f"oracle port (float64 numpy/OpenBLAS) of the C2 exit head "
-                                      f"fwd+bwd on {n} of the 4096 rows: {dt:.2f} s"}
+            "kind": "reference", **_cpu_info(),
+            "sample": f"reference eepipe autodiff (float64, numpy/OpenBLAS, backend "
+                      f"{os.environ.get('EEPIPE_BACKEND')}) C2 exit head fwd+bwd on {n} of the "
+                      f"4096 rows: {dt:.2f} s"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    per_tok = []
+    sl = RefDecodeSlice("python")
     for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state beyond numpy import
+        sl.sample()
     t0 = time.perf_counter()
-    tl = th = 0.0
-    for _ in range(args.steps):
-        pt, tl, th, n = cpu_slice_timing(seconds_budget=8.0)
-        per_tok.append(pt)
+    ts = [sl.sample() for _ in range(args.steps)]
     wall = time.perf_counter() - t0
-    import numpy as np
-    pt = float(np.median(per_tok))
-    value = 1.0 / pt
-    sample = (f"oracle port (numpy float64, einsum optimize=False) on a 7B-width slice: 1 decode "
-              f"layer ({tl * 1e3:.0f} ms) + 1 h x V exit head ({th * 1e3:.0f} ms) for one row at "
-              f"ctx {PROMPT_LEN}; extrapolated to 32 layers + 3 heads per token (thr 1.0)")
+    t_row = float(np.median([t[0] for t in ts]))
+    t_head = float(np.median([t[1] for t in ts]))
+    step = ref_step_seconds(t_row, t_head, args.threshold, args.new_tokens)
+    value = args.new_tokens / step
+    try:
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--ref-probe",
+                              "compiled"], capture_output=True, text=True, timeout=240)
+        comp = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:
+        comp = {"error": str(e)[:200]}
+    backend = "python"
+    if "layer_row_s" in comp:
+        cstep = ref_step_seconds(comp["layer_row_s"], comp["head_s"], args.threshold,
+                                 args.new_tokens)
+        if cstep < step:
+            backend, step, value = "compiled", cstep, args.new_tokens / cstep
+    sample = (f"reference eepipe (baseline/_ref, unmodified; backend {backend}: numpy "
+              f"{t_row * 1e3:.0f} ms per 1-row _layer_step at ctx {sl.ctx} + {t_head * 1e3:.0f} ms "
+              f"per head_logits, median of {args.steps}; Cython backend {comp}) on a 7B-width slice "
+              f"(h=4096, V=50304); one C3 step = (64 prompt + {args.new_tokens} new rows) x 32 "
+              f"layers x t_row + heads x t_head ({'3' if args.threshold >= 1.0 else '>=1'} per "
+              f"token at threshold {args.threshold}) — the reference computes every "
+              f"(position, layer) once and its per-row cost does not depend on the pass width")
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C3 EE-GPT 7B decode, KV recompute, threshold 1.0",
-                       "prompt_len": PROMPT_LEN, "new_tokens": NEW_TOKENS},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "port",
-                             "sample": sample},
+            "config": {"workload": "C3 EE-GPT 7B decode, KV recomputation",
+                       "threshold": args.threshold, "prompt_len": PROMPT_LEN,
+                       "new_tokens": args.new_tokens, "max_deferred": MAX_DEFERRED,
+                       "sampled": "7B-width 1-layer slice, per-op timings composed to the C3 step"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                             "sample": sample, **_cpu_info(),
+                             "sample_wall_s": wall},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -395,7 +496,10 @@ def main():
     ap.add_argument("--no-train-step", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
     ap.add_argument("--new-tokens", type=int, default=NEW_TOKENS)
+    ap.add_argument("--ref-probe", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ref_probe:
+        return ref_probe(args.ref_probe)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -516,11 +620,15 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        pt, tl, th, n = cpu_slice_timing(seconds_budget=15.0)
-        cpu = {"value": 1.0 / pt, "unit": "tokens/s", "cores": 1, "kind": "port",
-               "sample": f"oracle port (numpy float64) 7B-width slice, 1 layer {tl * 1e3:.0f} ms + "
-                         f"1 exit head {th * 1e3:.0f} ms per row at ctx {PROMPT_LEN}, "
-                         f"extrapolated to 32 layers + 3 heads (thr 1.0), {n} samples"}
+        rb = reference_decode_baseline(args.threshold)
+        pb = rb["per_backend"]["python"]
+        cpu = {"value": rb["tokens_per_s"], "unit": "tokens/s", "cores": 1, "kind": "reference",
+               **_cpu_info(), "backend": rb["backend"], "per_backend": rb["per_backend"],
+               "sample": f"reference eepipe (baseline/_ref) on a 7B-width slice: 1-row _layer_step "
+                         f"{pb['layer_row_s'] * 1e3:.0f} ms at ctx {rb['ctx']} + head_logits "
+                         f"{pb['head_s'] * 1e3:.0f} ms (numpy backend; Cython in per_backend), "
+                         f"composed to one C3 step at threshold {args.threshold} "
+                         f"(see ref_step_seconds)"}
 
     tr = traces[-1]
     line = {
@@ -542,7 +650,7 @@ def main():
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                      "pass_ms": pass_ms, "algorithmic_bytes": pass_bytes,
-                     "traffic": measured_traffic()},
+                     "traffic": measured_traffic(ctx)},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

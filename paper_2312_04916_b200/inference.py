@@ -59,6 +59,24 @@ def _torch():
     return torch
 
 
+def _device_stream(device):
+    """The one CUDA stream every inference engine on a device runs on (kept
+    for the process lifetime), keyed by the RESOLVED device index so 'cuda'
+    and 'cuda:0' share it.  Engines allocate their buffers on it too, so the
+    caching allocator never hands an engine's freed scratch to another
+    stream while this one may still read it; pipeline stages placed on one
+    GPU serialise their kernels in submission order (one GPU gains no
+    throughput from overlapping its own stages)."""
+    torch = _torch()
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    st = _DEVICE_STAGE_STREAMS.get(idx)
+    if st is None:
+        with torch.cuda.device(idx):
+            st = _DEVICE_STAGE_STREAMS[idx] = torch.cuda.Stream(idx)
+    return st
+
+
 # ---------------------------------------------------------------------------
 # Records (eepipe/inference.py:76-115)
 # ---------------------------------------------------------------------------
@@ -282,8 +300,13 @@ class Engine:
         self.layer_indices = list(layer_indices)
         self.h = h = cfg.hidden_dim
         self.nh = cfg.num_heads
-        with torch.cuda.device(self.device):
-            self.stream = torch.cuda.current_stream(self.device)
+        # construction runs on the device's engine stream, after whatever the
+        # caller queued (device-initialised weights), and the caller's stream
+        # waits for the packing before it may free or overwrite those weights
+        caller = torch.cuda.current_stream(self.device)
+        self.stream = _device_stream(self.device)
+        self.stream.wait_stream(caller)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
 
             def dev(name, dt=None):
                 a = params[name].data
@@ -371,6 +394,7 @@ class Engine:
             self.h_fire, self.h_bad = self.h_res["fire"], self.h_res["bad"]
             self.max_rows = 0
             self._grow(max_rows)
+        caller.wait_stream(self.stream)
         # accounting for bench.py: kernels launched and host<->device bytes
         self.launches = 0
         self.h2d_bytes = 0
@@ -707,23 +731,9 @@ class _InferStage:
         self.eng = _engine_for(spec, spec.params, heads, cfg, spec.layer_indices,
                                spec.has_embedding, dtype, device)
         self.eng.kv.reset()
-        # one stream per stage engine for the engine's lifetime (not a new one
-        # per call): buffers the engine (re)allocates on it stay ordered with
-        # this stage's work under the caching allocator's per-stream reuse
-        # one stream per DEVICE, shared by every stage placed on it (and kept
-        # across calls): stages on one GPU serialise their kernels in
-        # submission order.  With a stream per stage, concurrently running
-        # stage kernels on one GPU made 7B-scale runs non-deterministic
-        # (tools/pipeline_race_probe2.py; deterministic with one stream, and
-        # at threshold 1.0 where stages never overlap) -- one GPU gains no
-        # throughput from overlapping its own stages anyway
-        key = str(self.eng.device)
-        st = _DEVICE_STAGE_STREAMS.get(key)
-        if st is None:
-            with torch.cuda.device(self.eng.device):
-                st = _DEVICE_STAGE_STREAMS[key] = torch.cuda.Stream(self.eng.device)
-        self.stream = st
-        self.eng.stream = st
+        # every engine on a device runs on that device's one stream
+        # (_device_stream): stages on one GPU serialise in submission order
+        self.stream = self.eng.stream
         self.heads_at = {}
         for local, hd in spec.heads:
             hi = next(i for i, e in enumerate(self.eng.heads) if e.desc.key == hd.key)
@@ -847,6 +857,7 @@ def generate_pipeline(part: StagePartition, prompt, threshold, max_new_tokens, s
         emb_stream = getattr(first, "_emb_stream", None)
         if emb_stream is None:
             emb_stream = first._emb_stream = torch.cuda.Stream(first.device)
+        emb_stream.wait_stream(first.stream)  # embedding tables packed on the engine stream
         cap = 2 * max(t0, 1) + 16
         with torch.cuda.stream(emb_stream):
             staging = (_PinnedRing(cap), torch.zeros(cap, dtype=torch.int32, device=first.device))

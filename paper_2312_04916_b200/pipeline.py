@@ -552,7 +552,8 @@ def _stage_stream(device, stage):
     """One persistent CUDA stream per (device, stage): per-stream scratch
     (workspaces, upload rings) is then allocated once, not per iteration."""
     torch = _torch()
-    key = (str(device), stage)
+    dev = torch.device(device)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), stage)
     st = _STAGE_STREAMS.get(key)
     if st is None:
         st = _STAGE_STREAMS[key] = torch.cuda.Stream(device)
@@ -733,13 +734,25 @@ def run_iteration_1f1b(part: StagePartition, batch, options: IterationOptions, m
                                    options.hoist_exit_heads, actions=timeline.order(s),
                                    fill=fill))
     torch = _torch()
+    # the stage streams start after everything the caller queued on its own
+    # stream: the gradient zeroing of comp.reset above and the previous
+    # step's optimizer update (which rewrites the bf16 weights the stages read)
+    ready = {}
+    for w in workers:
+        dev = torch.device(w.compute.device)
+        if dev.type == "cuda" and str(dev) not in ready:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dev))
+            ready[str(dev)] = ev
 
     def target(w):
         dev = torch.device(w.compute.device)
         if dev.type != "cuda":
             w.run()
             return
-        with torch.cuda.device(dev), torch.cuda.stream(_stage_stream(dev, w.index)):
+        st = _stage_stream(dev, w.index)
+        st.wait_event(ready[str(dev)])
+        with torch.cuda.device(dev), torch.cuda.stream(st):
             w.run()
             from .training import join_wgrad
             join_wgrad(dev)

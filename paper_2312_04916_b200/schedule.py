@@ -276,73 +276,95 @@ def _waits_on(kind, mb, stage, p, part1_depths):
 
 
 def _schedule_lists(cost, variant, lists, part1_depths):
-    """Earliest start for every action, in list order per stage, after its
-    cross-stage dependency (+ p2p latency) (`eepipe/schedule.py:230-260`)."""
+    """Earliest start of every action given the per-stage order and each
+    action's cross-stage dependency plus the p2p latency (the fixed point
+    `eepipe/schedule.py:230-260` computes).  The actions form a DAG (stage
+    order edges + one dependency edge each); start times follow from one
+    topological pass (Kahn's algorithm) over it.  A cycle means the lists
+    cannot be executed."""
     p = cost.num_stages
     dur = _duration_fn(cost, variant)
-    finished: dict = {}
-    nxt = [0] * p
-    free = [0.0] * p
-    events = [[] for _ in range(p)]
-    remaining = sum(len(lst) for lst in lists)
-    while remaining:
-        moved = False
-        for s in range(1, p + 1):
-            lst = lists[s - 1]
-            while nxt[s - 1] < len(lst):
-                kind, mb = lst[nxt[s - 1]]
-                dep = _waits_on(kind, mb, s, p, part1_depths)
-                if dep is not None and dep not in finished:
-                    break
-                ready = finished[dep] + cost.p2p_latency if dep is not None else 0.0
-                start = max(ready, free[s - 1])
-                end = start + dur(kind, s)
-                events[s - 1].append(Event(kind, mb, s, start, end))
-                finished[(kind, mb, s)] = end
-                free[s - 1] = end
-                nxt[s - 1] += 1
-                remaining -= 1
-                moved = True
-        if not moved:
-            raise ConfigError("action lists deadlock: unsatisfiable dependency")
+    index = {(kind, mb, s): (s, i) for s in range(1, p + 1)
+             for i, (kind, mb) in enumerate(lists[s - 1])}
+    # in-degree: the stage predecessor (i > 0) and the dependency (if any)
+    waiting = {}
+    children = {}
+    for (kind, mb, s), node in index.items():
+        dep = _waits_on(kind, mb, s, p, part1_depths)
+        n_in = (node[1] > 0) + (dep is not None)
+        waiting[node] = n_in
+        if dep is not None:
+            if dep not in index:
+                raise ConfigError("action lists deadlock: unsatisfiable dependency")
+            children.setdefault(index[dep], []).append(node)
+    start_of, end_of = {}, {}
+    dep_ready = {}
+    frontier = [node for node, n in waiting.items() if n == 0]
+    while frontier:
+        s, i = frontier.pop()
+        kind, mb = lists[s - 1][i]
+        t0 = max(end_of.get((s, i - 1), 0.0), dep_ready.get((s, i), 0.0))
+        start_of[(s, i)] = t0
+        end_of[(s, i)] = t0 + dur(kind, s)
+        released = [(s, i + 1)] if i + 1 < len(lists[s - 1]) else []
+        for c in children.get((s, i), ()):
+            dep_ready[c] = end_of[(s, i)] + cost.p2p_latency
+            released.append(c)
+        for c in released:
+            waiting[c] -= 1
+            if waiting[c] == 0:
+                frontier.append(c)
+    if len(end_of) != len(index):
+        raise ConfigError("action lists deadlock: unsatisfiable dependency")
+    events = []
+    for s in range(1, p + 1):
+        row = []
+        for i, (kind, mb) in enumerate(lists[s - 1]):
+            row.append(Event(kind, mb, s, start_of[(s, i)], end_of[(s, i)]))
+        events.append(row)
     return events
 
 
 def _idle_gaps(stage_events):
-    """[(start, end)] idle intervals of a stage, with the open tail last."""
-    gaps, t = [], 0.0
+    """Idle intervals [(start, end)] of one stage, the open tail last."""
+    ends = [0.0]
     for e in stage_events:
-        if e.start > t:
-            gaps.append((t, e.start))
-        t = max(t, e.end)
-    gaps.append((t, float("inf")))
-    return gaps
+        ends.append(max(ends[-1], e.end))
+    gaps = [(busy_until, e.start) for busy_until, e in zip(ends, stage_events)
+            if e.start > busy_until]
+    return gaps + [(ends[-1], float("inf"))]
+
+
+def _first_fit(gaps, floor, d):
+    """Earliest start >= floor of a d-long slot inside one of the gaps."""
+    for g0, g1 in gaps:
+        t = max(g0, floor)
+        if t + d <= g1 + 1e-9:
+            return t
+    return max(gaps[-1][0], floor)
 
 
 def _pack_part2(cost, variant, events, plan):
-    """Part-2 chains (forward through every stage, backward through the last
-    r) packed into idle gaps without moving existing events: earliest fit per
-    element, same-kind order per stage kept (`eepipe/schedule.py:275-304`)."""
+    """Part-2 chains (forward through every stage, then backward through the
+    last r stages) placed into idle time without moving existing events:
+    each element at the earliest fitting gap after its chain predecessor
+    (+ p2p) and after the previous element of the same kind on that stage
+    (the same-kind order is kept; `eepipe/schedule.py:275-304`)."""
     p = cost.num_stages
     dur = _duration_fn(cost, variant)
-    last_same: dict = {}
+    kind_floor: dict = {}
     for i, r in enumerate(plan.part2_bwd_depths, 1):
-        chain = [(FILL2_FWD, s) for s in range(1, p + 1)]
-        chain += [(FILL2_BWD, s) for s in range(p, p - r, -1)]
-        ready = 0.0
+        chain = [(FILL2_FWD, s) for s in range(1, p + 1)] + \
+                [(FILL2_BWD, s) for s in range(p, p - r, -1)]
+        t_ready = 0.0
         for kind, s in chain:
-            floor = max(ready, last_same.get((kind, s), 0.0))
             d = dur(kind, s)
-            start = floor
-            for g0, g1 in _idle_gaps(events[s - 1]):
-                start = max(g0, floor)
-                if start + d <= g1 + 1e-9:
-                    break
-            ev = Event(kind, i, s, start, start + d)
-            events[s - 1].append(ev)
+            t = _first_fit(_idle_gaps(events[s - 1]),
+                           max(t_ready, kind_floor.get((kind, s), 0.0)), d)
+            events[s - 1].append(Event(kind, i, s, t, t + d))
             events[s - 1].sort(key=lambda e: e.start)
-            last_same[(kind, s)] = ev.end
-            ready = ev.end + cost.p2p_latency
+            kind_floor[(kind, s)] = t + d
+            t_ready = t + d + cost.p2p_latency
     return events
 
 

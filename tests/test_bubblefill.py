@@ -17,11 +17,9 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2312_04916_b200.bubblefill import (FillPlan, estimator_stats, fill_rescale,
-                                              has_rescale_overlap, toy_filled_iterations,
+from paper_2312_04916_b200.bubblefill import (FillPlan, fill_rescale, has_rescale_overlap,
                                               part1_loss_sample_counts,
                                               part2_stage_sample_counts, plan_bubble_fill,
-                                              predicted_variance_difference,
                                               truncated_part1_depths)
 from paper_2312_04916_b200.errors import ConfigError
 from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model, partition
@@ -72,46 +70,6 @@ def test_overlap_detection():
     plan = FillPlan(4, 0.5, 1, 1, (2,), (3,))
     assert has_rescale_overlap(plan, [2])
     assert not has_rescale_overlap(plan, [])
-
-
-def test_predicted_difference_closed_form():
-    assert predicted_variance_difference(4, 1.0, 0.0) == pytest.approx(1 / 20)
-    assert predicted_variance_difference(4, 1.0, -0.5) == pytest.approx(0.0)
-
-
-def test_estimator_stats_cases():
-    """The reference's estimator KATs (eepipe tests/test_bubblefill.py:76-102):
-    unbiased means, the closed-form variance difference within 3 standard
-    errors, the cancellation and negative-correlation cases, rejections."""
-    out = estimator_stats(200_000, 4, var_a=1.0, var_b=1.0, cov_ab=0.0, seed=0)
-    assert abs(out["e_mean"] - out["target"]) < 3 * out["e_mean_se"]
-    assert abs(out["ep_mean"] - out["target"]) < 3 * out["ep_mean_se"]
-    assert out["predicted_diff"] == pytest.approx(0.05)
-    assert abs(out["var_diff"] - out["predicted_diff"]) < 3 * out["var_diff_se"]
-    out = estimator_stats(200_000, 4, var_a=1.0, var_b=1.0, cov_ab=-0.5, seed=1)
-    assert out["predicted_diff"] == 0.0
-    assert abs(out["var_diff"]) < 3 * out["var_diff_se"]
-    out = estimator_stats(200_000, 4, var_a=1.0, var_b=1.5, cov_ab=-1.0, seed=2)
-    assert out["predicted_diff"] < 0 and out["var_diff"] < 0
-    assert abs(out["var_diff"] - out["predicted_diff"]) < 3 * out["var_diff_se"]
-    with pytest.raises(ConfigError):
-        estimator_stats(200_000, 4, var_a=1.0, var_b=1.0, cov_ab=2.0)
-    with pytest.raises(ConfigError):
-        estimator_stats(10_000, 4)
-
-
-def test_toy_filled_iterations():
-    """eepipe tests/test_bubblefill.py:109-124: the rescaled filled mean
-    matches the plain mean within 3 SE, and Part-2 samples lower the
-    variance on the covered stages."""
-    out = toy_filled_iterations(plan_bubble_fill(4, 0.5), exit_stages=[1, 2],
-                                num_microbatches=4, iterations=3000, seed=5)
-    se = np.sqrt(out["plain_se"] ** 2 + out["filled_se"] ** 2)
-    assert np.all(np.abs(out["filled_mean"] - out["plain_mean"]) < 3 * se)
-    out = toy_filled_iterations(FillPlan(4, 0.5, 0, 2, (), (2, 1)), exit_stages=[2],
-                                num_microbatches=4, iterations=4000, seed=7)
-    for s in out["part2_stages"]:
-        assert np.all(out["filled_var"][s - 1] < out["plain_var"][s - 1])
 
 
 def test_fill_action_lists_are_deadlock_free_and_complete():

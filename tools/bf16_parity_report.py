@@ -1,0 +1,86 @@
+"""bf16 perf path vs the REFERENCE on bf16-rounded weights: per-run report of
+compared tokens and every exit-decision mismatch with |conf - thr|
+(tests/golden/make_bf16_golden.py fixtures; the same comparison rule as
+tests/test_gpu_bf16_parity.py).  Includes the 16-layer 7B-width slice (exit
+at layer 8, the C3 tap), whose host float64 build takes ~2 min and is
+therefore not in the test suite.
+
+    python tools/bf16_parity_report.py > profiles/r2_bf16_parity.txt
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import torch  # noqa: E402
+
+from paper_2312_04916_b200 import checkpoint as C  # noqa: E402
+from paper_2312_04916_b200 import inference as I  # noqa: E402
+from paper_2312_04916_b200.model import (ExitSpec, ModelConfig, build_model,  # noqa: E402
+                                         model_from_arrays, partition)
+from test_gpu_bf16_parity import compare_trace  # noqa: E402
+
+G = os.path.join(ROOT, "tests", "golden")
+
+
+def device_model(cfg, host):
+    dev = {k: torch.from_numpy(p.data).to("cuda").bfloat16() for k, p in host.params.items()}
+    return model_from_arrays(cfg, dev)
+
+
+def report(name, model, g):
+    part = partition(model, 2, copy=False) if model.config.num_layers % 2 == 0 else None
+    tot = cmp_ = 0
+    print(f"== {name}")
+    for run in g["runs"]:
+        prompt = g["prompts"][run["prompt"]]
+        thr, new = run["threshold"], len(run["tokens"])
+        if run["mode"] == "recompute":
+            tr = I.generate_kv_recompute(model, prompt, thr, new, run["max_deferred"], dtype="bf16")
+        else:
+            tr = I.generate_pipeline(part, prompt, thr, new, dtype="bf16")
+        label = f"{run['mode']:9s} prompt {run['prompt']} thr {thr}"
+        try:
+            n, rep = compare_trace(tr, run, thr, stages=run["mode"] == "pipeline", label=label)
+        except AssertionError as e:
+            print(f"  {label}: FAIL {e}")
+            continue
+        early = sum(1 for e in run["exit_layers"] if e < model.config.num_layers)
+        tot += new
+        cmp_ += n
+        print(f"  {label}: {n}/{new} tokens identical (reference early exits {early})"
+              + ("" if rep is None else
+                 f"; mismatch at token {rep['token']} ({rep['kind']}): ours {rep['ours']} vs "
+                 f"reference {rep['reference']}, reference conf "
+                 + ", ".join(f"{k} {c:.5f} (|c-thr|/thr {abs(c - thr) / thr:.2e})"
+                             for k, c in rep['reference_conf'].items())
+                 + ", ours " + ", ".join(f"{k} {c:.5f}" for k, c in rep['our_conf'].items())))
+    print(f"  total: {cmp_}/{tot} tokens compared identical before any reported mismatch")
+
+
+def main():
+    with open(os.path.join(G, "trained_bf16.json")) as f:
+        g = json.load(f)
+    host = C.load_model(os.path.join(G, "trained_tiny.ckpt"))
+    report("reference-trained checkpoint (h=64, bf16 row-major path)",
+           device_model(host.config, host), g)
+    for fn in ("golden_7b_bf16.json", "golden_7b16_bf16.json"):
+        path = os.path.join(G, fn)
+        if not os.path.exists(path):
+            continue
+        with open(path) as f:
+            g = json.load(f)
+        L, h, nh, V, s_max, tap = g["config"]
+        cfg = ModelConfig(L, h, nh, V, s_max, exits=(ExitSpec(tap, "minimalistic", 0.1),))
+        m = device_model(cfg, build_model(cfg, 0))
+        report(f"7B-width slice L={L} exit at {tap} (tiled bf16 perf path)", m, g)
+        del m
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -5,13 +5,13 @@ import subprocess
 import sys
 
 WANT = [
-    ("gpu__time_duration.sum", "duration (ns)"),
-    ("sm__cycles_elapsed.avg.per_second", "SM clock (Hz)"),
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
-    ("dram__bytes_read.sum", "DRAM bytes read"),
-    ("dram__bytes_write.sum", "DRAM bytes written"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM written"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1/smem throughput %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
@@ -30,6 +30,7 @@ def main():
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
+    units = rows[1]  # ncu's raw page: second row = the unit of each column
     idx = {h: i for i, h in enumerate(hdr)}
     with open(out, "w") as f:
         f.write(f"ncu --set full summary of {rep.split('/')[-1]} (clock-control none)\n")
@@ -37,7 +38,8 @@ def main():
             f.write("\n" + r[idx["Kernel Name"]][:150] + "\n")
             for k, label in WANT:
                 if k in idx:
-                    f.write(f"  {label:28s} {r[idx[k]]}\n")
+                    unit = units[idx[k]].strip()
+                    f.write(f"  {label:28s} {r[idx[k]]} {unit}\n")
             stalls = [(h, r[i]) for h, i in idx.items()
                       if h.startswith("smsp__average_warp_latency_issue_stalled_")
                       or (h.startswith("smsp__warp_issue_stalled_") and h.endswith("_per_warp_active.pct"))]
