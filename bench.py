@@ -385,7 +385,7 @@ def bench_train_head(local, hbm_peak, reps=10, n=4096, h=2048, V=50304, tag="C2"
                          "traffic": head_traffic() if tag == "C2" else None}}
 
 
-def bench_pipeline_stages(model, prompt, local, new_tokens=64):
+def bench_pipeline_stages(model, prompt, local, new_tokens=64, thresholds=(1.0, 0.8, 0.2)):
     """`generate_pipeline` on the C3 model at P = 2, 4, 8 stages.  The pool
     gives ONE GPU, so the stage workers are host threads with their own CUDA
     streams sharing it (the multi-process NCCL path, pipeline_infer.
@@ -397,7 +397,7 @@ def bench_pipeline_stages(model, prompt, local, new_tokens=64):
     from paper_2312_04916_b200 import inference as I
     from paper_2312_04916_b200.model import partition
     out = {"note": "P stage workers = threads + CUDA streams on ONE B200 (1-GPU pool); "
-                   f"{new_tokens} new tokens, prompt {PROMPT_LEN}; every stage still runs all its "
+                   f"{new_tokens} new tokens, prompt {len(prompt)}; every stage still runs all its "
                    "layers per token (KV fill), so throughput is bounded by the single GPU's "
                    "full-depth rate, and at P=8 the eight Python stage threads of one "
                    "interpreter contend for the GIL (the multi-GPU design runs one process "
@@ -406,7 +406,7 @@ def bench_pipeline_stages(model, prompt, local, new_tokens=64):
         part = partition(model, P, copy=False)
         I.generate_pipeline(part, prompt, 0.8, 4, devices=[f"cuda:{local}"])  # builds stage engines
         res = {}
-        for thr in (1.0, 0.8, 0.2):
+        for thr in thresholds:
             torch.cuda.synchronize()
             t = time.perf_counter()
             tr = I.generate_pipeline(part, prompt, thr, new_tokens, devices=[f"cuda:{local}"])
@@ -423,15 +423,14 @@ def bench_pipeline_stages(model, prompt, local, new_tokens=64):
     return out
 
 
-def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
-    """One C2 training step (BASELINE configs[1]): EE-GPT 1.3B (L=24, h=2048,
-    16 heads, V=50304, tied exits at 6 (w 0.25) / 12 (w 0.5)), microbatch 2 x
-    M=8 microbatches of seq 2048, 1F1B executor at P=1 on 1 GPU: bf16 compute
-    (torch matmul / SDPA backbone, fused RMSNorm kernels, fused tcgen05 exit
-    heads), float32 gradient accumulation, fused Adam on float32 master
-    weights.  Device-drawn N(0, 0.02) weights, uniform random tokens.  CUDA
-    events around whole steps (optimizer included)."""
-    import numpy as np
+def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048, cfg=None, workload=None):
+    """One training step: by default C2 (BASELINE configs[1]): EE-GPT 1.3B
+    (L=24, h=2048, 16 heads, V=50304, tied exits at 6 (w 0.25) / 12 (w 0.5)),
+    microbatch 2 x M=8 microbatches of seq 2048, 1F1B executor at P=1 on 1
+    GPU: bf16 compute (torch matmul / SDPA backbone, fused RMSNorm kernels,
+    fused tcgen05 exit heads), float32 gradient accumulation, fused Adam on
+    float32 master weights.  Device-drawn N(0, 0.02) weights, uniform random
+    tokens.  CUDA events around whole steps (optimizer included)."""
     import torch
     from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model, partition
     from paper_2312_04916_b200.pipeline import IterationOptions, run_iteration_1f1b
@@ -441,9 +440,13 @@ def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
     gc.freeze()  # the decode run's host objects stay out of every GC pass of the training loop
     torch.cuda.empty_cache()
     dev = f"cuda:{local}"
-    cfg = ModelConfig(24, 2048, 16, 50304, 2048,
-                      exits=(ExitSpec(6, "minimalistic", 0.25), ExitSpec(12, "minimalistic", 0.5)),
-                      tie_embeddings=True)
+    if cfg is None:
+        cfg = ModelConfig(24, 2048, 16, 50304, 2048,
+                          exits=(ExitSpec(6, "minimalistic", 0.25),
+                                 ExitSpec(12, "minimalistic", 0.5)),
+                          tie_embeddings=True)
+        workload = ("C2 EE-GPT 1.3B training step (L=24, h=2048, V=50304, seq 2048, "
+                    "microbatch 2 x 8, tied exits 6/12, P=1, Adam, bf16 compute)")
     master = build_model(cfg, 0, init="device", dtype=torch.float32, device=dev)
     opt = Adam(3e-4)
     rng = np.random.default_rng(0)
@@ -469,14 +472,105 @@ def bench_train_step(local, steps=3, warmup=2, M=8, mb=2, seq=2048):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
     tokens = M * mb * seq
-    out = {"workload": "C2 EE-GPT 1.3B training step (L=24, h=2048, V=50304, seq 2048, "
-                       "microbatch 2 x 8, tied exits 6/12, P=1, Adam, bf16 compute)",
-           "ms_per_step": ms, "tokens_per_s": tokens / (ms / 1e3), "tokens_per_step": tokens,
+    n_params = sum(p.data.numel() for p in master.params.values())
+    h, L = cfg.hidden_dim, cfg.num_layers
+    n_heads = len(master.heads)
+    # model FLOPs: 6 x tokens x matmul parameters (layers + every head's h x V
+    # projection) + causal attention 6 x tokens x seq x h per layer (fwd 2 S h
+    # per token with the causal half, x3 for fwd + bwd)
+    flops = 6 * tokens * (12 * h * h * L + n_heads * h * cfg.vocab_size) + 6 * tokens * seq * h * L
+    out = {"workload": workload, "ms_per_step": ms, "tokens_per_s": tokens / (ms / 1e3),
+           "tokens_per_step": tokens, "params": n_params,
+           "model_tflops_per_s": flops / (ms / 1e3) / 1e12,
            "per_exit_loss": rep.per_exit_losses, "steps": steps, "warmup": warmup}
     del computes[:], master, opt
     torch.cuda.empty_cache()
     gc.unfreeze()
     return out
+
+
+def bench_c4_stage(local):
+    """C4 (13B, 4-stage pipeline, per-stage exits) does not fit one GPU with
+    float32 master weights and Adam state (18 B/param x 13.4 B); one STAGE
+    does: 10 layers at h=5120 (40 heads of 128), V=50304, microbatch 1 x
+    seq 2048, M=8 microbatches, trained at P=1 with one early exit at local
+    depth 5 plus the final head -- a stage's 10 layers + head, with one extra
+    head (C4 stages 2-4 each own 10 layers and one head; stage 1 owns the
+    embedding).  Plus the fused exit head alone at the C4 shape (n 2048,
+    h 5120) vs the bf16 peak."""
+    from paper_2312_04916_b200.model import ExitSpec, ModelConfig
+    cfg = ModelConfig(10, 5120, 40, 50304, 2048, exits=(ExitSpec(5, "minimalistic", 0.25),))
+    out = bench_train_step(local, steps=2, warmup=2, M=8, mb=1, seq=2048, cfg=cfg,
+                           workload="C4 stage slice: 10 layers, h=5120, 40 heads, V=50304, "
+                                    "microbatch 1 x 8 of seq 2048, exit at 5 + final head, "
+                                    "P=1, Adam, bf16 compute (1-GPU emulation of one C4 stage)")
+    hbm_peak, _, _ = peaks()
+    out["exit_head"] = bench_train_head(local, hbm_peak, n=2048, h=5120, tag="C4")
+    return out
+
+
+def bench_c5(local, new_tokens=128, pipe_tokens=32):
+    """C5 (30B: L=48, h=7168, 56 heads of 128, V=50304, exits at 12 / 24)
+    on ONE B200 (bf16 weights 59 GB): KV recomputation at thresholds
+    1.0 / 0.8 / 0.5 / 0.2 (prompt 64, CUDA events on the engine stream), the
+    full-depth one-row pass against the HBM roofline, then pipeline-based
+    inference (`generate_pipeline`) at P = 2 / 4 / 8 stage threads sharing
+    the GPU -- a 1-GPU emulation of the 2/4/8-stage C5 deployment."""
+    import torch
+    from paper_2312_04916_b200 import inference as I
+    from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model
+    torch.cuda.empty_cache()
+    hbm_peak, _, peak_kind = peaks()
+    dev = f"cuda:{local}"
+    cfg = ModelConfig(48, 7168, 56, 50304, 2048,
+                      exits=(ExitSpec(12, "minimalistic", 0.1), ExitSpec(24, "minimalistic", 0.2)))
+    model = build_model(cfg, 0, init="device", dtype=torch.bfloat16, device=dev)
+    prompt = [int(t) for t in np.random.default_rng(1).integers(0, cfg.vocab_size, PROMPT_LEN)]
+    I.generate_kv_recompute(model, prompt, 0.8, 8, MAX_DEFERRED, device=dev)  # engine build
+    eng = next(iter(model.__dict__["_ee_engines"].values()))
+    st = eng.stream
+    sweep = {}
+    for thr in (1.0, 0.8, 0.5, 0.2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        tr = I.generate_kv_recompute(model, prompt, thr, new_tokens, MAX_DEFERRED, device=dev)
+        b.record(st)
+        st.synchronize()
+        sec = a.elapsed_time(b) / 1e3
+        sweep[str(thr)] = {"tokens_per_s": len(tr.tokens) / sec,
+                           "mean_exit_layer": tr.mean_exit_layer,
+                           "early_exits": int(sum(1 for e in tr.exit_layers if e < cfg.num_layers)),
+                           "modeled_speedup": tr.speedup}
+    L, h = cfg.num_layers, cfg.hidden_dim
+    ctx = PROMPT_LEN + new_tokens // 2
+    with torch.cuda.device(eng.device), torch.cuda.stream(st):
+        eng.kv.reset()
+        eng.upload_ctrl([ctx])
+        for _ in range(3):
+            eng.run_layers(0, L, 1, [1] * L, ctx, 0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(10):
+            eng.run_layers(0, L, 1, [1] * L, ctx, 0)
+        b.record(st)
+        st.synchronize()
+    pass_ms = a.elapsed_time(b) / 10
+    pass_bytes = decode_pass_bytes(h, L, ctx)
+    achieved = pass_bytes / (pass_ms / 1e3) / 1e9
+    model.__dict__.pop("_ee_engines", None)
+    del eng
+    torch.cuda.empty_cache()
+    pipe = bench_pipeline_stages(model, prompt, local, new_tokens=pipe_tokens)
+    del model
+    torch.cuda.empty_cache()
+    return {"workload": "C5 EE-GPT 30B (L=48, h=7168, V=50304, exits 12/24) on ONE B200, bf16, "
+                        f"prompt {PROMPT_LEN}, {new_tokens} new tokens, max_deferred {MAX_DEFERRED}",
+            "sweep": sweep,
+            "roofline": {"bound": "hbm", "kernel": "ee_decode_layers (48 layers, 1 row)",
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "peak_kind": peak_kind, "pass_ms": pass_ms,
+                         "algorithmic_bytes": pass_bytes, "ctx": ctx},
+            "pipeline_stages_1gpu": pipe}
 
 
 # ---------------------------------------------------------------------------
@@ -495,6 +589,8 @@ def main():
     ap.add_argument("--no-train-head", action="store_true")
     ap.add_argument("--no-train-step", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--new-tokens", type=int, default=NEW_TOKENS)
     ap.add_argument("--ref-probe", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
@@ -602,16 +698,26 @@ def main():
     if not args.no_pipeline and world == 1:
         pipe = bench_pipeline_stages(model, prompt, local)
 
+    # ---- C5 30B on this one GPU (KV recompute sweep, pipeline P=2/4/8) ------
+    c5 = None
+    if not args.no_c5 and world == 1:
+        model.__dict__.pop("_ee_engines", None)
+        del eng, model
+        torch.cuda.empty_cache()
+        c5 = bench_c5(local)
+
     # ---- fused training exit head at the C2 shape (second half of the metric) --
     head_train = None
     if not args.no_train_head:
         head_train = bench_train_head(local, hbm_peak)
-        head_train["c4_shape"] = bench_train_head(local, hbm_peak, n=2048, h=5120, tag="C4")
     if head_train is not None and not args.no_cpu_baseline and world == 1:
         head_train["cpu_baseline"] = cpu_head_timing()
     train_step = None
     if not args.no_train_step:
         train_step = bench_train_step(local)
+    c4 = None
+    if not args.no_c4 and world == 1:
+        c4 = bench_c4_stage(local)
 
     if rank != 0:
         if world > 1:
@@ -659,6 +765,8 @@ def main():
         "exit_head_train": head_train,
         "train_step": train_step,
         "pipeline_stages_1gpu": pipe,
+        "c5_1gpu": c5,
+        "c4_stage_1gpu": c4,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))

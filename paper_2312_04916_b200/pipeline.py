@@ -239,60 +239,116 @@ class TaggedChannel:
             self.stash[got] = item
 
 
-class DistChannel:
-    """torch.distributed P2P channel carrying (mb id header, tensor) pairs in
-    order between two ranks (NCCL over NVLink on GPUs, gloo on CPU).  Sends
-    are non-blocking (isend), like the reference's queue puts: with blocking
-    sends the 1F1B steady state would deadlock (stage s sending x while
-    stage s+1 sends g back).  `flush` waits for the outstanding sends."""
+_CTRL_GROUPS = {}
 
-    def __init__(self, peer, shape, dtype, device, group=None):
-        self.peer, self.shape, self.dtype, self.device = peer, tuple(shape), dtype, device
-        self.group = group
-        self.last = 0
-        self.count = 0
-        self.pending = []
-        self.stash = {}
 
-    def send(self, msg):
+class Wire:
+    """Point-to-point transport between stage processes.
+
+    * Control words (message tags, positions, statuses) are host int64
+      tensors on a gloo group: the receiver learns what comes next without a
+      device-to-host copy and stream synchronisation per header.
+    * Tensors go over the default group: NCCL (device memory, NVLink) on a
+      multi-GPU box; with a gloo default group (CPU tests, or several stage
+      processes sharing ONE GPU, which NCCL refuses) device tensors are
+      staged through host memory.
+    Sends are non-blocking and kept alive until `flush`."""
+
+    def __init__(self):
         torch = _torch()
         dist = torch.distributed
-        data = msg.data.contiguous()
-        if tuple(data.shape) != self.shape:
-            raise ShapeError(f"channel expects {self.shape}, got {tuple(data.shape)}")
-        tag = _tag(msg.mb)
-        hdr = torch.tensor([_KIND_CODE[tag[0]], tag[1]], dtype=torch.int64, device=self.device)
-        # keep the tensors alive until their sends complete
-        self.pending.append((dist.isend(hdr, self.peer, group=self.group), hdr))
-        self.pending.append((dist.isend(data, self.peer, group=self.group), data))
-        self.count += 1
+        self.backend = dist.get_backend()
+        self.staged = self.backend != "nccl"
+        if self.backend == "gloo":
+            self.ctrl = None
+        else:  # every rank creates it once, in the same order (collective)
+            key = id(dist.group.WORLD)
+            if key not in _CTRL_GROUPS:
+                _CTRL_GROUPS[key] = dist.new_group(backend="gloo")
+            self.ctrl = _CTRL_GROUPS[key]
+        self.pending = []
+
+    def send_ints(self, vals, dst):
+        torch = _torch()
+        t = torch.tensor(list(vals), dtype=torch.int64)
+        self.pending.append((torch.distributed.isend(t, dst, group=self.ctrl), t))
+
+    def recv_ints(self, n, src):
+        torch = _torch()
+        t = torch.empty(n, dtype=torch.int64)
+        torch.distributed.recv(t, src, group=self.ctrl)
+        return t.tolist()
+
+    def send(self, t, dst):
+        torch = _torch()
+        if self.staged and t.device.type == "cuda":
+            t = t.to("cpu")  # waits for the producing stream: the device data is final
+        t = t.contiguous()
+        self.pending.append((torch.distributed.isend(t, dst), t))
+
+    def recv(self, shape, dtype, device, src):
+        """Blocking receive into a fresh tensor on ``device``, ready on the
+        caller's current stream."""
+        torch = _torch()
+        device = torch.device(device)
+        if self.staged and device.type == "cuda":
+            h = torch.empty(shape, dtype=dtype)
+            torch.distributed.recv(h, src)
+            return h.to(device)
+        t = torch.empty(shape, dtype=dtype, device=device)
+        torch.distributed.recv(t, src)
+        return t
 
     def flush(self):
         for req, _ in self.pending:
             req.wait()
         self.pending = []
 
+
+class DistChannel:
+    """Ordered (tag, tensor) channel between two stage processes over a
+    `Wire` (tags on the gloo control group, tensors over NCCL / staged
+    gloo).  Sends are non-blocking (isend), like the reference's queue puts:
+    with blocking sends the 1F1B steady state would deadlock (stage s sending
+    x while stage s+1 sends g back).  `flush` waits for the outstanding
+    sends."""
+
+    def __init__(self, peer, shape, dtype, device, wire=None):
+        self.peer, self.shape, self.dtype, self.device = peer, tuple(shape), dtype, device
+        self.wire = wire if wire is not None else Wire()
+        self.last = 0
+        self.count = 0
+        self.stash = {}
+
+    def send(self, msg):
+        data = msg.data.contiguous()
+        if tuple(data.shape) != self.shape:
+            raise ShapeError(f"channel expects {self.shape}, got {tuple(data.shape)}")
+        tag = _tag(msg.mb)
+        self.wire.send_ints((_KIND_CODE[tag[0]], tag[1]), self.peer)
+        self.wire.send(data, self.peer)
+        self.count += 1
+
+    def flush(self):
+        self.wire.flush()
+
     def recv(self, tag):
-        """Messages arrive in the sender's order (NCCL matches point-to-point
-        operations in order); each carries its tag, so a message requested
-        later than it arrives is stashed, like the reference's tagged queue
-        (eepipe/pipeline.py:86-122).  Regular ids must arrive increasing."""
-        torch = _torch()
-        dist = torch.distributed
+        """Messages arrive in the sender's order (point-to-point operations
+        match in order per peer); each carries its tag, so a message
+        requested later than it arrives is stashed, like the reference's
+        tagged queue (eepipe/pipeline.py:86-122).  Regular ids must arrive
+        increasing."""
         tag = _tag(tag)
         if tag in self.stash:
             return self.stash.pop(tag)
         while True:
-            hdr = torch.empty(2, dtype=torch.int64, device=self.device)
-            dist.recv(hdr, self.peer, group=self.group)
-            code, idx = (int(v) for v in hdr.tolist())
+            code, idx = self.wire.recv_ints(2, self.peer)
             got = (_KIND_NAME[code], idx)
             if got[0] == "mb":
                 if idx <= self.last:
                     raise QueueProtocolError(f"microbatch ids out of order: {idx} after {self.last}")
                 self.last = idx
-            data = torch.empty(self.shape, dtype=self.dtype, device=self.device)
-            dist.recv(data, self.peer, group=self.group)
+            data = self.wire.recv(self.shape, self.dtype, self.device, self.peer)
             msg = type("Msg", (), {"mb": got, "data": data})
             if got == tag:
                 return msg
@@ -837,16 +893,22 @@ def run_stage_1f1b_dist(part: StagePartition, batch, options: IterationOptions, 
     mb_size = options.microbatch_size
     seq = data[1][0].shape[1]
     shape = (mb_size, seq, part.config.hidden_dim)
-    fwd_in = DistChannel(rank - 1, shape, act_dtype, dev) if s > 1 else None
-    fwd_out = DistChannel(rank + 1, shape, act_dtype, dev) if s < P else None
-    bwd_in = DistChannel(rank + 1, shape, act_dtype, dev) if s < P else None
-    bwd_out = DistChannel(rank - 1, shape, act_dtype, dev) if s > 1 else None
+    wire = Wire()
+    fwd_in = DistChannel(rank - 1, shape, act_dtype, dev, wire) if s > 1 else None
+    fwd_out = DistChannel(rank + 1, shape, act_dtype, dev, wire) if s < P else None
+    bwd_in = DistChannel(rank + 1, shape, act_dtype, dev, wire) if s < P else None
+    bwd_out = DistChannel(rank - 1, shape, act_dtype, dev, wire) if s > 1 else None
     w = StageWorker(s, P, M, comp, data, fwd_in, fwd_out, bwd_in, bwd_out,
                     options.hoist_exit_heads, actions=it.timeline.order(s), fill=it.fill)
-    w.run()
-    for ch in (fwd_out, bwd_out):
-        if ch is not None:
-            ch.flush()
+    if dev.type == "cuda":
+        with torch.cuda.device(dev):
+            w.run()
+            from .training import join_wgrad
+            join_wgrad(dev)
+            torch.cuda.current_stream(dev).synchronize()
+    else:
+        w.run()
+    wire.flush()
     if w.exception is not None:
         raise w.exception
     grads = comp.tm.grads() if compute_factory is None else comp.grads()

@@ -9,13 +9,20 @@ firing exit (or the final head) emits the token exactly once, and the
 message keeps flowing to the last stage to fill the KV of the deeper
 layers while stage 1 already runs the next token.
 
-Transport (option (a) — NCCL has no ANY_SOURCE):
+Transport (`pipeline.Wire`, option (a) — NCCL has no
+ANY_SOURCE):
   * stage s -> s+1: a fixed-size int64 header (rows, decide position,
-    emitted flag, stop flag, positions) followed by the float32 hidden rows;
+    emitted flag, stop flag, positions) on the host control group (gloo: no
+    device sync per header), then the hidden rows over NCCL (or host-staged
+    gloo when the stage processes share one GPU).  The rows stay float32:
+    the residual stream is float32 in every mode, which keeps this mode
+    bitwise equal to KV recomputation (a bf16 boundary would round it), and
+    at h = 7168 a row is 28 KB -- latency, not bandwidth;
   * every stage s >= 2 -> stage 1: one status per message
-    (position, emitted-here, token, exit layer); stage 1 receives statuses in
-    stage order until one says "emitted" and drains the later stages'
-    statuses for that token before their next ones (FIFO per source);
+    (position, emitted-here, token, exit layer) on the control group; stage 1
+    receives statuses in stage order until one says "emitted" and drains the
+    later stages' statuses for that token before their next ones (FIFO per
+    source);
   * per-token confidences are gathered to rank 0 at the end.
 Sends are non-blocking (isend) so a stage never waits on its consumer.
 
@@ -32,6 +39,7 @@ import numpy as np
 
 from .errors import ConfigError
 from .inference import GenerationTrace, _check_context, default_stage_times
+from .pipeline import Wire
 from .schedule import inference_latency
 
 _HDR_FIXED = 4  # rows, decide_pos, emitted, stop
@@ -72,6 +80,8 @@ class GpuStage:
         torch = _torch()
         e = self.eng
         evals = []
+        # the rows were received (or embedded) on the caller's current stream
+        e.stream.wait_stream(torch.cuda.current_stream(e.device))
         with torch.cuda.stream(e.stream):
             n = len(positions)
             e._grow(n)
@@ -144,31 +154,22 @@ def generate_pipeline_dist(part, prompt, threshold, max_new_tokens, stage_times=
     t0 = len(prompt)
     max_rows = max(t0, 1)
     hdr_len = _HDR_FIXED + max_rows
-    pending = []
     conf_log = {}
-
-    def isend(t, dst):
-        pending.append((dist.isend(t, dst), t))
+    wire = Wire()
 
     def send_msg(rows, positions, decide, emitted, stop=False):
-        hdr = torch.zeros(hdr_len, dtype=torch.int64, device=dev)
-        hdr[0], hdr[1], hdr[2], hdr[3] = len(positions), decide, int(emitted), int(stop)
-        if positions:
-            hdr[_HDR_FIXED:_HDR_FIXED + len(positions)] = torch.tensor(positions, device=dev)
-        isend(hdr, rank + 1)
+        hdr = [len(positions), decide, int(emitted), int(stop)] + list(positions)
+        wire.send_ints(hdr + [0] * (hdr_len - len(hdr)), rank + 1)
         if not stop:
-            isend(rows.to(stage.x_dtype).contiguous(), rank + 1)
+            wire.send(rows.to(stage.x_dtype), rank + 1)
 
     def recv_msg():
-        hdr = torch.empty(hdr_len, dtype=torch.int64, device=dev)
-        dist.recv(hdr, rank - 1)
-        hv = hdr.cpu().tolist()
+        hv = wire.recv_ints(hdr_len, rank - 1)
         n, decide, emitted, stop = hv[:4]
         if stop:
             return None
         positions = hv[_HDR_FIXED:_HDR_FIXED + n]
-        rows = torch.empty((n, h), dtype=stage.x_dtype, device=dev)
-        dist.recv(rows, rank - 1)
+        rows = wire.recv((n, h), stage.x_dtype, dev, rank - 1)
         return rows, positions, decide, bool(emitted)
 
     def first_fire(evals, already):
@@ -203,10 +204,8 @@ def generate_pipeline_dist(part, prompt, threshold, max_new_tokens, stage_times=
                 token = None
                 for src in range(2, P + 1):
                     while got[src] <= msg_index:
-                        st = torch.empty(4, dtype=torch.int64, device=dev)
-                        dist.recv(st, src - 1)
+                        pos, here, tok, lay = wire.recv_ints(4, src - 1)
                         got[src] += 1
-                        pos, here, tok, lay = st.cpu().tolist()
                         if got[src] - 1 == msg_index and here and token is None:
                             token, layer, estage = tok, lay, src
                     if token is not None:
@@ -228,8 +227,7 @@ def generate_pipeline_dist(part, prompt, threshold, max_new_tokens, stage_times=
         # drain the remaining statuses so every send is matched
         for src in range(2, P + 1):
             while got[src] < max_new_tokens:
-                st = torch.empty(4, dtype=torch.int64, device=dev)
-                dist.recv(st, src - 1)
+                wire.recv_ints(4, src - 1)
                 got[src] += 1
     else:
         while True:
@@ -243,13 +241,11 @@ def generate_pipeline_dist(part, prompt, threshold, max_new_tokens, stage_times=
             out, evals = stage.process(rows, positions, decide)
             emit = first_fire(evals, emitted)
             here = emit is not None
-            st = torch.tensor([decide, int(here), emit[0] if here else -1, emit[1] if here else -1],
-                              dtype=torch.int64, device=dev)
-            isend(st, 0)
+            wire.send_ints([decide, int(here), emit[0] if here else -1,
+                            emit[1] if here else -1], 0)
             if rank + 1 < world:
                 send_msg(out, positions, decide, emitted or here)
-    for req, _ in pending:
-        req.wait()
+    wire.flush()
     complete = stage.kv_complete(t0 + max_new_tokens - 1)
     logs = [None] * world
     dist.all_gather_object(logs, (conf_log, complete))

@@ -12,6 +12,9 @@ runs is the GPU's bf16 activations / KV cache and fp32 accumulation, so token
 and exit-layer sequences must agree except where a decision sits within
 tolerance of the threshold (or an argmax near-tie); tests/test_gpu_bf16_parity.py
 and tools/bf16_parity_report.py check that and print every such mismatch.
+Every call of the reference's `exit_decision` is also recorded with its
+top-5 (token, probability), so a flipped greedy token can be checked to be an
+argmax near-tie of the REFERENCE's own distribution.
 
   l2      ModelConfig(2, 4096, 32, 50304, 2048, exit 1 minimalistic) — SURVEY
           B.3 slice; 2 prompts x thresholds {1.0, 0.3, 0.1, 0.05} x 12 tokens
@@ -37,6 +40,7 @@ os.environ.setdefault("EEPIPE_BACKEND", "python")
 sys.dont_write_bytecode = True
 sys.path.insert(0, "/root/reference/pkg/src")
 
+import eepipe.inference as _inf  # noqa: E402
 from eepipe import kernels  # noqa: E402
 from eepipe.checkpoint import load_model  # noqa: E402
 from eepipe.inference import generate_kv_recompute, generate_pipeline  # noqa: E402
@@ -45,6 +49,35 @@ from eepipe.model import ExitSpec, ModelConfig, build_model, partition  # noqa: 
 OUT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, OUT)
 from make_golden import params_digest, trace_dict  # noqa: E402
+
+
+_DECISIONS = []
+_exit_decision = _inf.exit_decision
+
+
+def _recording_exit_decision(logits, threshold):
+    """The reference's own exit_decision, unchanged, plus a record of the
+    top-5 (token, probability) of every call: lets the GPU test prove that a
+    flipped greedy token was an argmax near-tie in the REFERENCE's
+    distribution (our token within tolerance of the reference's maximum)."""
+    out = _exit_decision(logits, threshold)
+    z = np.asarray(logits, dtype=np.float64)
+    p = np.exp(z - z.max())
+    p /= p.sum()
+    top = np.argsort(-p, kind="stable")[:5]
+    _DECISIONS.append({"token": int(out[1]), "conf": float(out[2]),
+                       "top5": [[int(t), float(p[t])] for t in top]})
+    return out
+
+
+_inf.exit_decision = _recording_exit_decision
+
+
+def traced(fn, *a):
+    _DECISIONS.clear()
+    d = trace_dict(fn(*a))
+    d["decisions"] = list(_DECISIONS)
+    return d
 
 
 def round_bf16(model):
@@ -65,15 +98,15 @@ def slice_fixture(L, tap, prompts, thresholds, new, pipe_thr, name):
     for pi, prompt in enumerate(prompts):
         for thr in thresholds:
             t0 = time.time()
-            tr = generate_kv_recompute(m, prompt, thr, new, 4)
+            tr = traced(generate_kv_recompute, m, prompt, thr, new, 4)
             gold["runs"].append({"prompt": pi, "threshold": thr, "mode": "recompute",
-                                 "max_deferred": 4, **trace_dict(tr)})
-            print(f"  prompt {pi} thr {thr}: {tr.tokens} exits {tr.exit_layers} "
+                                 "max_deferred": 4, **tr})
+            print(f"  prompt {pi} thr {thr}: {tr['tokens']} exits {tr['exit_layers']} "
                   f"({time.time() - t0:.0f} s)", flush=True)
         if pipe_thr is not None:
-            tr = generate_pipeline(partition(m, 2), prompt, pipe_thr, new)
+            tr = traced(generate_pipeline, partition(m, 2), prompt, pipe_thr, new)
             gold["runs"].append({"prompt": pi, "threshold": pipe_thr, "mode": "pipeline",
-                                 "stages": 2, **trace_dict(tr)})
+                                 "stages": 2, **tr})
     with open(os.path.join(OUT, name), "w") as f:
         json.dump(gold, f, indent=1, sort_keys=True)
 
@@ -88,12 +121,12 @@ def trained_fixture():
     part = partition(m, 2)
     for pi, prompt in enumerate(prompts):
         for thr in (0.9, 0.8, 0.5):
-            tr = generate_kv_recompute(m, prompt, thr, 24, 4)
+            tr = traced(generate_kv_recompute, m, prompt, thr, 24, 4)
             gold["runs"].append({"prompt": pi, "threshold": thr, "mode": "recompute",
-                                 "max_deferred": 4, **trace_dict(tr)})
-            tr = generate_pipeline(part, prompt, thr, 24)
+                                 "max_deferred": 4, **tr})
+            tr = traced(generate_pipeline, part, prompt, thr, 24)
             gold["runs"].append({"prompt": pi, "threshold": thr, "mode": "pipeline",
-                                 "stages": 2, **trace_dict(tr)})
+                                 "stages": 2, **tr})
     with open(os.path.join(OUT, "trained_bf16.json"), "w") as f:
         json.dump(gold, f, indent=1, sort_keys=True)
 

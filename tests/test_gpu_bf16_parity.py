@@ -18,8 +18,10 @@ the REFERENCE run on the same bf16-rounded weights.
    2-layer slice of SURVEY B.3 (2 prompts x thresholds 1.0/0.3/0.1/0.05,
    KV recompute + pipeline) and the reference-trained checkpoint (3 prompts x
    0.9/0.8/0.5, both modes).  Tokens and exit layers must be identical until
-   a decision whose confidence lies within CONF_TOL of the threshold (or an
-   argmax whose top-2 reference probabilities are within CONF_TOL) flips; a
+   a decision whose confidence lies within CONF_TOL of the threshold (or a
+   greedy token whose reference probability is within CONF_TOL of the
+   reference's maximum -- an argmax near-tie, checked against the top-5 the
+   fixture records at every reference decision) flips; a
    run is compared up to that point, every such mismatch is printed, and any
    other divergence fails.  Confidences of compared tokens: 5e-2 relative
    (the end-to-end bf16 band derived at CONF_RTOL; the head kernel alone is
@@ -105,11 +107,12 @@ def test_tiled_decode_layer_chain_7b_width(wide, positions):
             x_in = x_gpu  # the next layer is checked on the GPU's own input
 
 
-def _near(ref_conf, thr):
-    return any(abs(c - thr) <= CONF_TOL * thr for c in ref_conf.values())
+def _near(ref_conf, thr, tol):
+    return any(abs(c - thr) <= tol * thr for c in ref_conf.values())
 
 
-def compare_trace(tr, ref, thr, *, stages=False, label=""):
+def compare_trace(tr, ref, thr, *, stages=False, label="", conf_tol=CONF_TOL,
+                  conf_rtol=CONF_RTOL):
     """Tokens / exit layers identical up to the first near-threshold (or
     near-tie) flip.  Returns (compared tokens, mismatch report or None)."""
     n = len(ref["tokens"])
@@ -118,13 +121,15 @@ def compare_trace(tr, ref, thr, *, stages=False, label=""):
                 and (not stages or tr.exit_stages[i] == ref["exit_stages"][i]))
         rc = ref["confidences"][i]
         if not same:
-            near_thr = _near(rc, thr)
-            # greedy argmax near-tie at the deciding head: the reference's top
-            # confidence is tiny (e.g. 2e-3 at random init) so a tie on the
-            # token with the same exit layer is allowed when the confidences
-            # of both runs agree to CONF_TOL (the top-2 are indistinguishable)
-            tie = (tr.exit_layers[i] == ref["exit_layers"][i] and all(
-                abs(tr.confidences[i].get(k, np.inf) - c) <= CONF_TOL * c for k, c in rc.items()))
+            near_thr = _near(rc, thr, conf_tol)
+            # argmax near-tie: same exit layer, and our token is within
+            # CONF_TOL of the maximum of the REFERENCE's own distribution at
+            # the deciding head (its top-5 is recorded with every reference
+            # exit_decision call, tests/golden/make_bf16_golden.py)
+            tie = tr.exit_layers[i] == ref["exit_layers"][i] and any(
+                d["token"] == ref["tokens"][i] and any(
+                    t == tr.tokens[i] and pr >= (1.0 - conf_tol) * d["top5"][0][1]
+                    for t, pr in d["top5"]) for d in ref.get("decisions", ()))
             rep = {"run": label, "token": i, "threshold": thr,
                    "ours": [tr.tokens[i], tr.exit_layers[i]],
                    "reference": [ref["tokens"][i], ref["exit_layers"][i]],
@@ -135,7 +140,7 @@ def compare_trace(tr, ref, thr, *, stages=False, label=""):
         for k, c in rc.items():
             dev = abs(tr.confidences[i][k] - c) / c
             compare_trace.max_dev = max(getattr(compare_trace, "max_dev", 0.0), dev)
-            assert dev <= CONF_RTOL, (label, i, k, tr.confidences[i][k], c)
+            assert dev <= conf_rtol, (label, i, k, tr.confidences[i][k], c)
     return n, None
 
 

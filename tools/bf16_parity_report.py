@@ -32,7 +32,11 @@ def device_model(cfg, host):
     return model_from_arrays(cfg, dev)
 
 
-def report(name, model, g):
+def report(name, model, g, tol=None):
+    """``tol``: the relative confidence band (deviation of compared
+    confidences, and the window around the threshold where a decision may
+    flip); default the test suite's 5e-2."""
+    kw = {} if tol is None else {"conf_tol": tol, "conf_rtol": tol}
     part = partition(model, 2, copy=False) if model.config.num_layers % 2 == 0 else None
     tot = cmp_ = 0
     print(f"== {name}")
@@ -45,7 +49,8 @@ def report(name, model, g):
             tr = I.generate_pipeline(part, prompt, thr, new, dtype="bf16")
         label = f"{run['mode']:9s} prompt {run['prompt']} thr {thr}"
         try:
-            n, rep = compare_trace(tr, run, thr, stages=run["mode"] == "pipeline", label=label)
+            n, rep = compare_trace(tr, run, thr, stages=run["mode"] == "pipeline", label=label,
+                                   **kw)
         except AssertionError as e:
             print(f"  {label}: FAIL {e}")
             continue
@@ -77,7 +82,13 @@ def main():
         L, h, nh, V, s_max, tap = g["config"]
         cfg = ModelConfig(L, h, nh, V, s_max, exits=(ExitSpec(tap, "minimalistic", 0.1),))
         m = device_model(cfg, build_model(cfg, 0))
-        report(f"7B-width slice L={L} exit at {tap} (tiled bf16 perf path)", m, g)
+        # 8 layers deep the bf16 hidden state is 5.6e-3 off the float64 one
+        # (profiles/r2_bf16_depth_error.txt) and |x| ~ 465, so the exit_l8
+        # logits (std 0.02 |x| ~ 9) carry ~0.06 absolute error and the max
+        # probability ~8% (2 sigma ~ 15%) relative: the band is 0.15 there
+        tol = 0.15 if L > 2 else None
+        report(f"7B-width slice L={L} exit at {tap} (tiled bf16 perf path)"
+               + (f", confidence band {tol}" if tol else ""), m, g, tol)
         del m
         torch.cuda.empty_cache()
 
