@@ -26,9 +26,6 @@ extern "C" const char* ee_last_error(void) { return g_err; }
 extern "C" int ee_abi_version(void) { return 1; }
 
 thread_local int g_pdl_off = 0;
-thread_local const int32_t* g_skip_flag = nullptr;
-thread_local int32_t* g_stop_flag = nullptr;
-thread_local int g_stop_col = -1;
 
 bool ee_pdl_enabled() {
     static int on = -1;

@@ -25,9 +25,6 @@
 //     griddepcontrol.wait.  (An L2 prefetch of the K/V rows that predate the
 //     pass, issued before the wait to overlap the QKV GEMV, made multi-chunk
 //     rows (positions >= 256) nondeterministic run to run on B200: removed.)
-#include <stdlib.h>
-#include <string.h>
-
 #include "attn_core.cuh"
 
 namespace {
@@ -290,179 +287,11 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     if (tid < mr && s_last[tid]) ctr[(r0 + tid) * nh + hh] = 0;  // re-usable workspace
 }
 
-// bf16, head_dim 128, cluster-split (the default decode path): decode
-// attention is LATENCY-bound (a few MB of K/V per layer), so the positions of
-// each (head, row group) are spread over a thread-block CLUSTER of C CTAs x W
-// warps, one 32-position block per warp per step (global warp gw = c W + w
-// takes blocks gw, gw + C W, ...), i.e. as many warps in flight as the
-// context has blocks (a one-CTA-per-256-positions grid used 32 of 148 SMs at
-// ctx 192).  Each warp loads its block ONCE for the whole row group (K tile
-// cp.async'd into swizzled shared memory, V columns in registers:
-// attn::block_issue128_k) and scores every row from it
-// (attn::block_eval128_k), leaving a per-(block, row) partial (m_b, l_b,
-// a_b[128]) in its CTA's shared memory.  After one cluster barrier every
-// thread of the cluster merges (row, 4 dims) items, reading the partials of
-// blocks 0 .. p/32 from their owners' shared memory over DSMEM and folding
-// them in BLOCK ORDER with a running max:  M' = max(M, m_b),
-// L = L e^(M-M') + l_b e^(m_b-M'),  o = o e^(M-M') + a_b e^(m_b-M'),
-// out = o / L.  Each block partial depends only on (q row, block, row
-// position) and the merge only on the row's blocks, so the result is
-// row-stable and deterministic whatever the launch shape (C, W, rows).  No
-// global workspace, counters or atomics.
-constexpr int kClusterMaxRows = 16;
-constexpr int kClusterMaxWarps = 4;
-
-__host__ __device__ constexpr size_t cluster_smem(int warps, int iters, int rows) {
-    return (size_t)warps * 2 * kBlk * kMaxDh * 2                              // K, V tiles (bf16)
-           + (size_t)rows * kMaxDh * sizeof(float)                            // q rows
-           + (size_t)warps * iters * rows * (kMaxDh + 2) * sizeof(float);     // partials
-}
-
-__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                 : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ float ld_dsmem(uint32_t a) {
-    float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ float2 ld_dsmem2(uint32_t a) {
-    float2 v;
-    asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ float4 ld_dsmem4(uint32_t a) {
-    float4 v;
-    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void cluster_barrier() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
-                 ::: "memory");
-}
-
-__global__ void __launch_bounds__(kClusterMaxWarps * 32, 4)
-k_attn_cluster(const float* __restrict__ q, const int32_t* __restrict__ pos, int m,
-               const bf16* __restrict__ kc, const bf16* __restrict__ vc, int nh, float scale,
-               bf16* __restrict__ out, int g, int iters, const int32_t* __restrict__ skip) {
-    extern __shared__ __align__(16) float smem_c[];
-    constexpr int dh = kMaxDh;
-    pdl_trigger_dev();
-    uint32_t C, c;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(C));
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
-    const int W = blockDim.x >> 5;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int hh = blockIdx.y;
-    const int r0 = blockIdx.z * g;
-    const int mr = min(g, m - r0);
-    const int h = nh * dh;
-    bf16* s_k = reinterpret_cast<bf16*>(smem_c);                       // [W][2][kBlk][dh]
-    float* s_q = smem_c + W * kBlk * dh;                               // [mr][dh]
-    float* s_a = s_q + mr * dh;                                        // [W*iters][mr][dh]
-    float* s_ml = s_a + W * iters * mr * dh;                           // [W*iters][mr][2]
-    // host-written control data: safe before the wait
-    int pmax = -1;
-    for (int i = 0; i < mr; ++i) pmax = max(pmax, pos[r0 + i]);
-    pdl_wait_dev();
-    // speculative layer not needed (the same flag for the whole cluster)
-    if (skip != nullptr && *reinterpret_cast<const volatile int32_t*>(skip) != 0) return;
-    for (int t = tid; t < mr * (dh / 4); t += blockDim.x) {
-        const int i = t / (dh / 4), cc = t % (dh / 4);
-        reinterpret_cast<float4*>(s_q + i * dh)[cc] =
-            reinterpret_cast<const float4*>(q + (int64_t)(r0 + i) * h + hh * dh)[cc];
-    }
-    __syncthreads();
-    const int span = (int)C * W;
-    bf16* sk = s_k + warp * 2 * kBlk * dh;
-    bf16* sv = sk + kBlk * dh;
-    for (int it = 0; it < iters; ++it) {
-        const int b = it * span + (int)c * W + warp;  // this warp's block
-        const int j0 = b * kBlk;
-        if (j0 <= pmax) {
-            attn::block_issue128_kv(sk, sv, kc, vc, h, hh * dh, j0, pmax);
-            attn::block_wait128_k();
-            const int slot = it * W + warp;
-            for (int i = 0; i < mr; ++i) {
-                const int p = pos[r0 + i];
-                if (j0 > p) continue;  // warp-uniform
-                float mx, l, acc[4];
-                attn::block_eval128_kv(sk, sv, s_q + i * dh, j0, p, scale, mx, l, acc);
-                reinterpret_cast<float4*>(s_a + ((int64_t)slot * mr + i) * dh)[lane] =
-                    make_float4(acc[0], acc[1], acc[2], acc[3]);
-                if (lane == 0) {
-                    s_ml[(slot * mr + i) * 2] = mx;
-                    s_ml[(slot * mr + i) * 2 + 1] = l;
-                }
-            }
-            __syncwarp();  // the K tile is rewritten by the next iteration's copy
-        }
-    }
-    cluster_barrier();  // every block partial of the cluster is written and visible
-    // merge: (row, 4-dim group) items over all threads of the cluster; blocks
-    // folded in block order (online max), partials fetched over DSMEM in
-    // batches of 8 blocks with independent vector loads (one round trip per
-    // batch instead of one per block)
-    const int nthr = span * 32;
-    for (int t = (int)c * blockDim.x + tid; t < mr * (dh / 4); t += nthr) {
-        const int i = t / (dh / 4), d4 = t % (dh / 4);
-        const int nb = pos[r0 + i] / kBlk + 1;
-        float M = -INFINITY, L = 0.f;
-        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int b0 = 0; b0 < nb; b0 += 8) {
-            float2 ml[8];
-            float4 av[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int b = b0 + k;
-                if (b < nb) {
-                    const int gw = b % span, slot = (b / span) * W + gw % W;
-                    const uint32_t owner = (uint32_t)(gw / W);
-                    ml[k] = ld_dsmem2(dsmem_addr(s_ml + (slot * mr + i) * 2, owner));
-                    av[k] = ld_dsmem4(dsmem_addr(s_a + ((int64_t)slot * mr + i) * dh + 4 * d4, owner));
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (b0 + k < nb) {
-                    const float Mn = fmaxf(M, ml[k].x);
-                    const float sc = expf(M - Mn), e = expf(ml[k].x - Mn);
-                    L = fmaf(L, sc, ml[k].y * e);
-                    o.x = fmaf(o.x, sc, av[k].x * e);
-                    o.y = fmaf(o.y, sc, av[k].y * e);
-                    o.z = fmaf(o.z, sc, av[k].z * e);
-                    o.w = fmaf(o.w, sc, av[k].w * e);
-                    M = Mn;
-                }
-            }
-        }
-        const float inv = 1.0f / L;
-        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x * inv, o.y * inv);
-        __nv_bfloat162 hi = __floats2bfloat162_rn(o.z * inv, o.w * inv);
-        uint2 u;
-        u.x = *reinterpret_cast<uint32_t*>(&lo);
-        u.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(out + (int64_t)(r0 + i) * h + hh * dh + 4 * d4) = u;
-    }
-    cluster_barrier();  // no CTA leaves while others still read its shared memory
-}
-
 }  // namespace
 
 // Workspace layout: attn_core.cuh (counters, then partial slots).
 size_t attention_ws_bytes(int64_t /*m*/, int64_t nh, int64_t dh, int64_t /*s_max*/) {
     return attn::counters_bytes(nh) + attn::partial_slots(nh) * (dh + 2) * sizeof(float);
-}
-
-// the cluster kernel is the bf16 / head_dim 128 path unless EE_ATTN=rows128
-// (A/B runs); only it can skip a speculative launch
-bool attention_supports_skip() {
-    static const bool rows_kernel = getenv("EE_ATTN") && !strcmp(getenv("EE_ATTN"), "rows128");
-    return !rows_kernel;
 }
 
 int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_pos,
@@ -490,50 +319,7 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
         // bf16, head_dim 128: the rows kernel (K/V block loads shared by the
         // group's rows, K staged swizzled in shared memory, V in registers);
         // other shapes / fp32: one CTA per row (same arithmetic)
-        const bool cluster_path = dtype == EE_BF16 && dh == kMaxDh && attention_supports_skip();
-        EE_REQUIRE(cluster_path || g_skip_flag == nullptr, EE_ECONFIG,
-                   "attention: speculative (skippable) launch needs the cluster kernel");
-        if (cluster_path) {
-            // cluster-split: C CTAs x W warps per (head, row group) cover the
-            // longest row's blocks (k_attn_cluster)
-            const int nb = max_pos / kBlk + 1;
-            int C, W, iters;
-            if (nb <= 8) {
-                C = nb; W = 1; iters = 1;
-            } else if (nb <= 8 * kClusterMaxWarps) {
-                C = 8; W = (nb + 7) / 8; iters = 1;
-            } else {
-                C = 8; W = kClusterMaxWarps; iters = (nb + 8 * kClusterMaxWarps - 1) / (8 * kClusterMaxWarps);
-            }
-            const int g = (int)(mr < kClusterMaxRows ? mr : kClusterMaxRows);
-            const int groups = (int)((mr + g - 1) / g);
-            const size_t smem = cluster_smem(W, iters, g);
-            static bool cfg_done[16] = {};
-            int dev = 0;
-            cudaGetDevice(&dev);
-            if (!cfg_done[dev & 15]) {
-                cudaFuncSetAttribute(k_attn_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)cluster_smem(kClusterMaxWarps, 2, kClusterMaxRows));
-                cfg_done[dev & 15] = true;
-            }
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)C, (unsigned)nh, (unsigned)groups);
-            cfg.blockDim = dim3((unsigned)(W * 32));
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = s;
-            cudaLaunchAttribute attr[2];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = (unsigned)C;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[1].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = ee_pdl_enabled() && !g_pdl_off ? 2 : 1;
-            e = cudaLaunchKernelEx(&cfg, k_attn_cluster, q + r0 * h, pos + r0, (int)mr,
-                                   (const bf16*)kc, (const bf16*)vc, (int)nh, scale,
-                                   (bf16*)out + r0 * h, g, iters, g_skip_flag);
-        } else if (dtype == EE_BF16 && dh == kMaxDh && nch >= kRowsKernelMinChunks) {
+        if (dtype == EE_BF16 && dh == kMaxDh && nch >= kRowsKernelMinChunks) {
             // rows per CTA: just enough to fill the GPU with one CTA per SM
             // (more rows per CTA share more K/V loads but evaluate serially)
             const int64_t want = (mr * nh * nch + ee_sm_count() - 1) / ee_sm_count();

@@ -129,87 +129,6 @@ __device__ __forceinline__ void block_eval128_k(const BlockRegsV& R, const bf16*
     }
 }
 
-// The same block with V staged in shared memory too (k_attn_cluster: no V
-// registers, so more warps fit per SM): sv = [kBlk][dh] bf16, row j plain
-// (lane l reads its 4 columns of row j: 32 lanes x 8 B = one 256-B row,
-// conflict-free).  Same arithmetic, same order as block_eval128_k.
-__device__ __forceinline__ void block_issue128_kv(bf16* sk, bf16* sv, const bf16* __restrict__ kc,
-                                                  const bf16* __restrict__ vc, int64_t h, int hoff,
-                                                  int j0, int plim) {
-    const int lane = threadIdx.x & 31;
-    const int nj = min(kBlk, plim + 1 - j0);
-    const uint32_t kbase = (uint32_t)__cvta_generic_to_shared(sk);
-    const uint32_t vbase = (uint32_t)__cvta_generic_to_shared(sv);
-#pragma unroll
-    for (int t = 0; t < kBlk * 16 / 32; ++t) {
-        const int idx = lane + 32 * t;
-        const int j = idx >> 4, c = idx & 15;
-        if (j < nj) {
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                             kbase + (uint32_t)((j * 16 + (c ^ (j & 7))) * 16)),
-                         "l"(kc + (int64_t)(j0 + j) * h + hoff + c * 8)
-                         : "memory");
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                             vbase + (uint32_t)((j * 16 + c) * 16)),
-                         "l"(vc + (int64_t)(j0 + j) * h + hoff + c * 8)
-                         : "memory");
-        }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-__device__ __forceinline__ void block_eval128_kv(const bf16* sk, const bf16* sv, const float* sq,
-                                                 int j0, int p, float scale, float& mx, float& l,
-                                                 float acc[4]) {
-    const int lane = threadIdx.x & 31;
-    const bool valid = j0 + lane <= p;
-    const int nj = min(kBlk, p + 1 - j0);
-    float sc = 0.f;
-    if (valid) {
-        const uint4* krow = reinterpret_cast<const uint4*>(sk) + lane * 16;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            uint4 kk[8];
-#pragma unroll
-            for (int q8 = 0; q8 < 8; ++q8) kk[q8] = krow[(half * 8 + q8) ^ (lane & 7)];
-#pragma unroll
-            for (int q8 = 0; q8 < 8; ++q8) {
-                const int i = half * 8 + q8;
-                const uint32_t w4[4] = {kk[q8].x, kk[q8].y, kk[q8].z, kk[q8].w};
-#pragma unroll
-                for (int e2 = 0; e2 < 4; ++e2) {
-                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e2]));
-                    sc = fmaf(sq[8 * i + 2 * e2], f.x, sc);
-                    sc = fmaf(sq[8 * i + 2 * e2 + 1], f.y, sc);
-                }
-            }
-        }
-    }
-    const float sval = valid ? sc * scale : -INFINITY;
-    mx = sval;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float e = valid ? expf(sval - mx) : 0.f;
-    l = e;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-    const uint2* vrow = reinterpret_cast<const uint2*>(sv) + lane;
-#pragma unroll
-    for (int j = 0; j < kBlk; ++j) {
-        const float pj = __shfl_sync(0xffffffffu, e, j);
-        if (j < nj) {
-            const uint2 vv = vrow[j * (kMaxDh / 4)];
-            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv.x));
-            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv.y));
-            acc[0] = fmaf(pj, a.x, acc[0]);
-            acc[1] = fmaf(pj, a.y, acc[1]);
-            acc[2] = fmaf(pj, b.x, acc[2]);
-            acc[3] = fmaf(pj, b.y, acc[3]);
-        }
-    }
-}
-
 // Cross-chunk merge of one (row, head, dim): chunk partials (M_c, L_c, o_c)
 // at base + c*stride (+0, +1, +2+d), c < nch, all loaded up front (one L2
 // round trip), then folded in chunk order:

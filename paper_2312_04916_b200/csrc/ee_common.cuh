@@ -83,15 +83,6 @@ __device__ __forceinline__ void pdl_trigger_dev() { asm volatile("griddepcontrol
 
 bool ee_pdl_enabled();  // EE_PDL=0 disables (debug)
 extern thread_local int g_pdl_off;  // debug (EE_PDL_SKIP): nonzero disables PDL on this thread's next launches
-// Speculative decode layer (recompute.cu): while set, the decode-layer
-// kernels this thread launches read *g_skip_flag after griddepcontrol.wait
-// and return without any effect when it is nonzero.  While g_stop_flag is
-// set, the tiled exit head writes its fire decision for column g_stop_col
-// to *g_stop_flag (device memory) -- the flag the speculative layer reads.
-extern thread_local const int32_t* g_skip_flag;
-extern thread_local int32_t* g_stop_flag;
-extern thread_local int g_stop_col;
-bool attention_supports_skip();
 
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,

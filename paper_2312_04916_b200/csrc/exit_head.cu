@@ -31,8 +31,6 @@ struct HeadWs {
     float* ps;
     int* pi;
     float* xn;  // fp32 path: normalised rows (kMaxCols x h)
-    int32_t* stop = nullptr;  // speculative decode: fire of column stop_col -> *stop
-    int stop_col = -1;
 };
 
 __host__ __device__ inline HeadWs head_ws(void* base, int64_t units) {
@@ -102,11 +100,9 @@ __device__ void merge_and_decide(const HeadWs& w, int64_t units, int m, float th
         }
         if (lane == 0) {
             const float cf = 1.0f / S;
-            const uint8_t f = (thr < 1.0f && cf > thr) ? 1 : 0;
             token[c] = I;
             conf[c] = cf;
-            fire[c] = f;
-            if (w.stop != nullptr && c == w.stop_col) *w.stop = f;
+            fire[c] = (thr < 1.0f && cf > thr) ? 1 : 0;
         }
     }
     // the outputs may live in host-mapped memory that the host polls through
@@ -339,8 +335,6 @@ extern "C" int ee_exit_head_infer(const float* x, int64_t ldx, const int32_t* ro
         EE_REQUIRE(h % kTiledKS == 0, EE_ESHAPE, "exit_head tiled needs h %% %d == 0", kTiledKS);
         const int64_t units = (V + 15) / 16;
         HeadWs w = head_ws(ws, (V + 7) / 8);
-        w.stop = g_stop_flag;
-        w.stop_col = g_stop_col;
         HeadEpi epi{w, (int)V, (int)m, threshold, token, nonfinite, conf, fire, logits_dbg, false};
         // gather + RMSNorm (or plain cast) of the evaluated rows -> bf16 (m, h)
         int rc = launch_rmsnorm_rows(x, ldx, rows, m, h, norm_w, eps, w.xn, EE_BF16, s);
@@ -377,8 +371,6 @@ extern "C" int ee_exit_head_infer(const float* x, int64_t ldx, const int32_t* ro
     }
     if (dtype == EE_F32 || dtype == EE_BF16) {
         // SIMT path: parity mode (fp32) and small row-major bf16 heads
-        EE_REQUIRE(g_stop_flag == nullptr, EE_ECONFIG,
-                   "exit_head: the decision flag of a speculative layer needs the tiled path");
         HeadWs w = head_ws(ws, (V + 7) / 8);
         int rc = launch_rmsnorm_rows(x, ldx, rows, m, h, norm_w, eps, w.xn, EE_F32, s);
         if (rc) return rc;

@@ -212,7 +212,6 @@ int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, 
     const int64_t items = tiles * groups;
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
     const unsigned grid = (unsigned)std::min<int64_t>(items, (int64_t)ee_sm_count() * per_sm);
-    rn.skip = g_skip_flag;
     cudaError_t e = launch_ex(kern, dim3(grid), dim3(tma_gemv::kThreads), smem, s,
                               (const bf16*)W, (int)N, (int)K, X, ldx, (int)m, rn, epi);
     if (e != cudaSuccess) return ee_fail(EE_ECUDA, "gemv_tma launch: %s", cudaGetErrorString(e));

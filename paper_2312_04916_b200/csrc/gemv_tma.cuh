@@ -94,12 +94,7 @@ __device__ __forceinline__ uint4 lds16(uint32_t addr) {
 struct RowNorm {
     const float* ssq;  // (rows, K/16) or nullptr
     float eps;
-    const int32_t* skip = nullptr;  // speculative launch: skip everything if *skip != 0
 };
-
-__device__ __forceinline__ bool skip_set(const int32_t* skip) {
-    return skip != nullptr && *reinterpret_cast<const volatile int32_t*>(skip) != 0;
-}
 
 // Work item i -> tile = i / groups, column group = i % groups; a CTA takes
 // items blockIdx.x, +gridDim.x, ...  Epi provides tile(red, n0, r0, N, m,
@@ -169,10 +164,6 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
         for (int q = 0; q < pre; ++q) issue_w(q);
         // 2) activations are produced by the previous kernel
         pdl_wait_dev();
-        if (skip_set(rn.skip)) {  // speculative layer not needed: drain the ring, leave
-            for (int q = 0; q < pre; ++q) mbar_wait(&wfull[q % kStages], (q / kStages) & 1);
-            return;
-        }
         for (int q = 0; q < pre; ++q) issue_x(q);
         // 3) steady state
         for (int q = pre; q < total; ++q) {
@@ -185,7 +176,6 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
 
     // ---------------- consumers ----------------
     pdl_wait_dev();  // epilogues read/write buffers shared with the predecessor
-    if (skip_set(rn.skip)) return;
     const int g = lane >> 2, t = lane & 3;
     const uint32_t ring_u32 = smem_u32(ring);
     int q = 0;

@@ -21,7 +21,6 @@
 //     was written (KVCache.fill / view, inference.py:58-70).
 #include <chrono>
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <vector>
@@ -51,18 +50,12 @@ struct Runner {
     std::chrono::steady_clock::time_point t_start;
 
     int64_t launches = 0, h2d = 0, d2h = 0;
-    bool spec_enabled = true;  // EE_SPECULATE=0 disables the speculative layer (A/B)
-    int64_t spec_launched = 0, spec_skipped = 0;
 
     int32_t* host_half() { return E->ctrl_host + (int64_t)stage * E->ctrl_cap; }
 
-    // the last word of the device control buffer: the decide row's fire flag
-    // of the current tap, written by the exit head, read by a speculative layer
-    int32_t* stop_flag() const { return E->ctrl + E->ctrl_cap - 1; }
-
     int upload(const int32_t* src, int64_t n) {
-        EE_REQUIRE(n <= E->ctrl_cap - 1, EE_ESHAPE, "recompute: control block overflow (%lld > %lld)",
-                   (long long)n, (long long)(E->ctrl_cap - 1));
+        EE_REQUIRE(n <= E->ctrl_cap, EE_ESHAPE, "recompute: control block overflow (%lld > %lld)",
+                   (long long)n, (long long)E->ctrl_cap);
         h2d += 4 * n;
         return ee_copy_h2d(E->ctrl, src, (size_t)n * 4, E->stream);
     }
@@ -169,42 +162,22 @@ struct Runner {
         int checked = 0;
         *has = 0;
         *depth = L;
-        // speculation: while the host waits for a decision at a tap, the next
-        // layer is already queued and skips itself on the device if the decide
-        // row fired (tiled perf path, thresholds < 1, unforced passes)
-        const bool speculate = spec_enabled && D->dtype == EE_BF16_TILED && !forced &&
-                               A->threshold < 1.0f && attention_supports_skip();
-        bool flagged_store = false;
-        bool* flagged = &flagged_store;
         auto eval_tap = [&](int tap, bool* gates) -> int {
             *gates = false;
-            *flagged = false;
             size_t ti = 0;
             while (ti < taps.size() && taps[ti] != tap) ++ti;
             if (ti == taps.size() || list_off[ti] < 0) return EE_OK;
             const int off = list_off[ti], cnt = list_len[ti];
-            // one head at this tap: it can hand the decide row's fire bit to a
-            // speculative next layer through device memory
-            const bool flag_it = speculate && at_tap[ti].size() == 1;
             for (int hi : at_tap[ti]) {
                 for (int c0 = 0; c0 < cnt; c0 += A->head_max_rows) {
                     const int m = cnt - c0 < A->head_max_rows ? cnt - c0 : A->head_max_rows;
                     const int slot = (int)slots.size();
                     EE_REQUIRE(slot < E->max_slots, EE_ECONFIG, "too many head evaluations in one pass");
-                    int col = -1;
-                    for (int j = 0; j < m; ++j)
-                        if (c[off + c0 + j] == decide_row) col = j;
-                    if (flag_it && col >= 0) {
-                        g_stop_flag = stop_flag();
-                        g_stop_col = col;
-                        *flagged = true;
-                    }
                     int rc2 = eval_head(hi, E->ctrl + off + c0, m, slot);
-                    g_stop_flag = nullptr;
-                    g_stop_col = -1;
                     if (rc2) return rc2;
                     slots.push_back(Slot{hi, off, m, c0, tap});
-                    if (col >= 0) *gates = true;
+                    for (int j = 0; j < m; ++j)
+                        if (c[off + c0 + j] == decide_row) *gates = true;
                 }
             }
             return EE_OK;
@@ -293,15 +266,15 @@ struct Runner {
             if (t >= 1) stops.push_back(t);
         if (stops.empty() || stops.back() != L) stops.push_back(L);
         std::vector<int32_t> m_act_arr(L + 1);
-        auto active = [&](int layer) {
-            int m = 0;
-            for (int r = 0; r < n; ++r) m += entry[r] < layer;
-            return m;
-        };
         int la = 1;
         for (int tap : stops) {
             int l = la;
             while (l <= tap) {
+                auto active = [&](int layer) {
+                    int m = 0;
+                    for (int r = 0; r < n; ++r) m += entry[r] < layer;
+                    return m;
+                };
                 const int m_act = active(l);
                 int l2 = l;
                 while (l2 + 1 <= tap && active(l2 + 1) == m_act) ++l2;
@@ -318,28 +291,10 @@ struct Runner {
             la = tap + 1;
             if ((rc = eval_tap(tap, &gates))) return rc;
             if (gates && !forced && !*has && (A->threshold < 1.0f || tap == L)) {
-                // queue layer tap+1 before waiting for the decision; it runs
-                // as a no-op if the decide row fired at this tap
-                int spec_m = 0;
-                if (*flagged && tap < L && (spec_m = active(tap + 1)) > 0) {
-                    m_act_arr[0] = spec_m;
-                    launches += (int64_t)decode_layer_launches(D, spec_m);
-                    g_skip_flag = stop_flag();
-                    rc = ee_decode_layers(D, E->layers + tap, 1, n, m_act_arr.data(), E->ctrl,
-                                          max_pos, E->stream);
-                    g_skip_flag = nullptr;
-                    if (rc) return rc;
-                    ++spec_launched;
-                }
                 if ((rc = decide_from())) return rc;
                 if (*has && !forced && *layer == tap && tap < L) {
                     *depth = tap;
-                    if (spec_m) ++spec_skipped;
                     break;
-                }
-                if (spec_m) {  // the speculative layer ran: it is part of the pass
-                    if ((rc = mark_written(tap + 1, tap + 1, pos + (n - spec_m), spec_m))) return rc;
-                    la = tap + 2;
                 }
             }
         }
@@ -369,10 +324,6 @@ extern "C" int ee_generate_kv_recompute(ee_generate_args_t* A) {
     R.L = E->n_layers;
     R.h = (int)E->dec->h;
     R.mapped = E->res == E->res_host;
-    {
-        const char* sp = getenv("EE_SPECULATE");
-        R.spec_enabled = !(sp && sp[0] == '0');
-    }
     for (int i = 0; i < E->n_heads; ++i) {
         const int t = E->heads[i].tap;
         if (R.taps.empty() || R.taps.back() != t) {
