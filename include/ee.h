@@ -340,6 +340,18 @@ int ee_mlp_up_gelu(const void* X, const void* W1, int64_t T, int64_t h, int64_t 
 int ee_mlp_gelu_bwd(const void* dY, const void* W2, int64_t T, int64_t h, int64_t N,
                     const void* pre, void* dpre, void* stream);
 
+/* ---- training backbone linears (CTA-pair tcgen05 GEMM) ------------------
+ * The forward and input-gradient matmuls of `run_layer` (eepipe/model.py:
+ * 207-216; `matmul` fwd / bwd, eepipe/autodiff.py:158-179):
+ *   ee_linear_fwd:   Y  = X W   [+ R]   X (T x K), W (K x N), Y / R (T x N)
+ *   ee_linear_dgrad: dX = dY W^T [+ R]  dY (T x N), W (K x N), dX / R (T x K)
+ * bf16 row-major, float32 accumulation, the optional residual R (nullable)
+ * added before the single rounding.  K, N multiples of 8. */
+int ee_linear_fwd(const void* X, const void* W, int64_t T, int64_t K, int64_t N, const void* R,
+                  void* Y, void* stream);
+int ee_linear_dgrad(const void* dY, const void* W, int64_t T, int64_t K, int64_t N, const void* R,
+                    void* dX, void* stream);
+
 /* ---- training RMSNorm (bf16 activations, float32 statistics) ---------- */
 
 /* y = x * (mean(x^2) + eps)^-1/2 * w row-wise; x, y (n, h) bf16, w (h) float32,

@@ -1,0 +1,96 @@
+// Training backbone linears on the CTA-pair tcgen05 GEMM of tc_gemm.cuh
+// (TMA SW128 operands, TMEM accumulators, 8 epilogue warps), replacing the
+// library (cuBLAS) forward and input-gradient matmuls of `run_layer`
+// (eepipe/model.py:207-216; matmul fwd / bwd eepipe/autodiff.py:158-179):
+//
+//   forward:  Y  = X W  [+ R]        X (T, K) bf16, W (K, N) bf16 (read MN-major)
+//   dgrad:    dX = dY W^T [+ R]      dY (T, N) bf16, W (K, N) (read K-major)
+//
+// Outputs bf16 row-major; the optional residual R (bf16, same shape as the
+// output) is added to the float32 accumulator before the single rounding
+// (the `addmm(beta = 1)` the unfused path used: one rounding, no separate
+// add pass over the (T, N) rows).  The weight gradient of the same linears
+// is ee_wgrad_accum (exit_head_train.cu): float32 accumulation in place.
+#include <cuda.h>
+
+#include "tc_gemm.cuh"
+
+namespace {
+
+constexpr int kBN = 256;
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&t);
+}
+
+struct EpiBf16 {
+    static constexpr bool kTwoPass = false;
+    static constexpr bool kSplitK = false;
+    bf16* out;
+    const bf16* res;  // nullable
+    int ld;
+    __device__ void begin_tile(int, int, int, bool) {}
+    __device__ void end_tile(int, int, int, bool) {}
+    __device__ void chunk(int row, int col, const float* v0, int nvalid) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = v0[j];
+        const int64_t off = (int64_t)row * ld + col;
+        if (nvalid == 16) {
+            if (res) {
+                const uint4 r0 = reinterpret_cast<const uint4*>(res + off)[0];
+                const uint4 r1 = reinterpret_cast<const uint4*>(res + off)[1];
+                const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                    v[2 * q] += f.x;
+                    v[2 * q + 1] += f.y;
+                }
+            }
+            uint4 u[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                u[q] = make_uint4(pack2(v[8 * q], v[8 * q + 1]), pack2(v[8 * q + 2], v[8 * q + 3]),
+                                  pack2(v[8 * q + 4], v[8 * q + 5]), pack2(v[8 * q + 6], v[8 * q + 7]));
+            reinterpret_cast<uint4*>(out + off)[0] = u[0];
+            reinterpret_cast<uint4*>(out + off)[1] = u[1];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < nvalid) {
+                    const float r = res ? __bfloat162float(res[off + j]) : 0.f;
+                    out[off + j] = __float2bfloat16_rn(v[j] + r);
+                }
+        }
+    }
+};
+
+int check(const char* what, int64_t T, int64_t K, int64_t N) {
+    EE_REQUIRE(T > 0 && K > 0 && N > 0 && K % 8 == 0 && N % 8 == 0, EE_ESHAPE,
+               "%s: K and N must be positive multiples of 8 (T=%lld K=%lld N=%lld)", what,
+               (long long)T, (long long)K, (long long)N);
+    EE_REQUIRE(T < (1ll << 31) && K < (1ll << 31) && N < (1ll << 31), EE_ESHAPE, "%s: too large",
+               what);
+    return EE_OK;
+}
+
+}  // namespace
+
+extern "C" int ee_linear_fwd(const void* X, const void* W, int64_t T, int64_t K, int64_t N,
+                             const void* R, void* Y, void* stream) {
+    int rc;
+    if ((rc = check("linear_fwd", T, K, N))) return rc;
+    return tc::launch_tc_gemm2<kBN, false, true, false>(
+        X, W, (int)T, (int)N, (int)K, EpiBf16{(bf16*)Y, (const bf16*)R, (int)N}, as_stream(stream));
+}
+
+extern "C" int ee_linear_dgrad(const void* dY, const void* W, int64_t T, int64_t K, int64_t N,
+                               const void* R, void* dX, void* stream) {
+    int rc;
+    if ((rc = check("linear_dgrad", T, K, N))) return rc;
+    return tc::launch_tc_gemm2<kBN, false, false, false>(
+        dY, W, (int)T, (int)K, (int)N, EpiBf16{(bf16*)dX, (const bf16*)R, (int)K},
+        as_stream(stream));
+}

@@ -273,10 +273,39 @@ def join_wgrad(device=None):
         cur.wait_stream(side)
 
 
+_OWN_LINEAR = os.environ.get("EE_LINEAR", "1") != "0"  # A/B switch: 0 = cuBLAS (torch)
+
+
+def _linear_fwd(x2, w, res2=None):
+    """(T, N) bf16 = x2 (T, K) @ w (K, N) [+ res2] on the CTA-pair tcgen05
+    GEMM (ee_linear_fwd; the residual is added before the one rounding)."""
+    torch = _torch()
+    T, K = x2.shape
+    N = w.shape[1]
+    if not _OWN_LINEAR:
+        return x2 @ w if res2 is None else torch.addmm(res2, x2, w)
+    out = torch.empty((T, N), dtype=x2.dtype, device=x2.device)
+    call("ee_linear_fwd", ptr(x2), ptr(w), T, K, N, ptr(res2), ptr(out), stream_ptr())
+    return out
+
+
+def _linear_dgrad(g2, w):
+    """(T, K) bf16 = g2 (T, N) @ w (K, N)^T (ee_linear_dgrad)."""
+    torch = _torch()
+    T, N = g2.shape
+    K = w.shape[0]
+    if not _OWN_LINEAR:
+        return g2 @ w.t()
+    out = torch.empty((T, K), dtype=g2.dtype, device=g2.device)
+    call("ee_linear_dgrad", ptr(g2), ptr(w), T, K, N, None, ptr(out), stream_ptr())
+    return out
+
+
 class _LinearFn:
-    """y = x @ W (bf16) whose backward computes dX with torch and accumulates
-    dW = X^T dY into the float32 main gradient with the CTA-pair tcgen05 GEMM
-    (no bf16 weight gradient; returns None for W)."""
+    """y = x @ W (bf16) on the tcgen05 GEMM (ee_linear_fwd, residual folded
+    in); the backward forms dX with ee_linear_dgrad and accumulates
+    dW = X^T dY into the float32 main gradient (ee_wgrad_accum): no bf16
+    weight gradient, returns None for W."""
 
     _fn = None
 
@@ -291,20 +320,19 @@ class _LinearFn:
                     ctx.save_for_backward(x, w)
                     ctx.acc = acc
                     ctx.has_res = res is not None
-                    if res is None:
-                        return x @ w
+                    x2 = x.reshape(-1, x.shape[-1]).contiguous()
                     # residual added by the GEMM itself (beta = 1): one rounding,
                     # no separate add pass over the (T, h) rows
-                    out = torch.addmm(res.reshape(-1, res.shape[-1]),
-                                      x.reshape(-1, x.shape[-1]), w)
-                    return out.view(res.shape)
+                    r2 = res.reshape(-1, res.shape[-1]).contiguous() if res is not None else None
+                    out = _linear_fwd(x2, w, r2)
+                    return out.view(*x.shape[:-1], w.shape[1])
 
                 @staticmethod
                 def backward(ctx, gy):
                     x, w = ctx.saved_tensors
-                    gx = gy @ w.t()
                     x2 = x.reshape(-1, x.shape[-1]).contiguous()
                     g2 = gy.reshape(-1, gy.shape[-1]).to(x2.dtype).contiguous()
+                    gx = _linear_dgrad(g2, w).view(x.shape)
                     _wgrad_accum(x2, g2, ctx.acc)
                     return gx, None, None, (gy if ctx.has_res else None)
 
@@ -340,9 +368,8 @@ class _MLPFn:
                     ctx.acc = (acc1, acc2)
                     ctx.shape = x.shape
                     ctx.has_res = res is not None
-                    if res is None:
-                        return (act @ w2).view(*x.shape[:-1], w2.shape[1])
-                    return torch.addmm(res.reshape(-1, res.shape[-1]), act, w2).view(res.shape)
+                    r2 = res.reshape(-1, res.shape[-1]).contiguous() if res is not None else None
+                    return _linear_fwd(act, w2, r2).view(*x.shape[:-1], w2.shape[1])
 
                 @staticmethod
                 def backward(ctx, gy):
@@ -355,7 +382,7 @@ class _MLPFn:
                     call("ee_mlp_gelu_bwd", ptr(g2), ptr(w2), T, h, N, ptr(pre), ptr(dpre),
                          stream_ptr())
                     _wgrad_accum(act, g2, acc2)
-                    gx = dpre @ w1.t()
+                    gx = _linear_dgrad(dpre, w1)
                     _wgrad_accum(x2, dpre, acc1)
                     return (gx.view(ctx.shape), None, None, None, None,
                             gy if ctx.has_res else None)

@@ -60,3 +60,35 @@ def test_rmsnorm_inv_rms_statistics():
          stream_ptr())
     _, rinv = O.rmsnorm_fwd(x.double().cpu().numpy(), np.ones(h))
     assert np.abs(inv.cpu().numpy() - rinv).max() / rinv.max() < 1e-5
+
+
+@pytest.mark.parametrize("T,K,N", [(5, 32, 32), (4096, 2048, 2048), (4096, 8192, 2048),
+                                   (2048, 5120, 15360), (300, 264, 776)])
+def test_linear_fwd_dgrad_match_fp32(T, K, N):
+    """Backbone linears on the tcgen05 GEMM (ee_linear_fwd / ee_linear_dgrad,
+    csrc/linear_train.cu) against a float32 torch reference on the same bf16
+    inputs: Y = X W + R and dX = dY W^T within 1e-2 relative (Frobenius; one
+    bf16 rounding of a float32 accumulation), the residual added before the
+    rounding."""
+    import torch
+    from paper_2312_04916_b200 import _lib
+    from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+    g = torch.Generator(device="cuda").manual_seed(T + K + N)
+    x = torch.randn(T, K, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(K, N, device="cuda", generator=g) * 0.02).bfloat16()
+    r = torch.randn(T, N, device="cuda", generator=g).bfloat16()
+    gy = torch.randn(T, N, device="cuda", generator=g).bfloat16()
+    y = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
+    gx = torch.empty(T, K, device="cuda", dtype=torch.bfloat16)
+    _lib.load()
+    call("ee_linear_fwd", ptr(x), ptr(w), T, K, N, ptr(r), ptr(y), stream_ptr())
+    call("ee_linear_dgrad", ptr(gy), ptr(w), T, K, N, None, ptr(gx), stream_ptr())
+    torch.cuda.synchronize()
+    ry = x.float() @ w.float() + r.float()
+    rgx = gy.float() @ w.float().t()
+    assert _rel(y.double().cpu().numpy(), ry.double().cpu().numpy()) < 1e-2
+    assert _rel(gx.double().cpu().numpy(), rgx.double().cpu().numpy()) < 1e-2
+    y0 = torch.empty_like(y)
+    call("ee_linear_fwd", ptr(x), ptr(w), T, K, N, None, ptr(y0), stream_ptr())
+    torch.cuda.synchronize()
+    assert _rel(y0.double().cpu().numpy(), (x.float() @ w.float()).double().cpu().numpy()) < 1e-2
