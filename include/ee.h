@@ -352,6 +352,23 @@ int ee_linear_fwd(const void* X, const void* W, int64_t T, int64_t K, int64_t N,
 int ee_linear_dgrad(const void* dY, const void* W, int64_t T, int64_t K, int64_t N, const void* R,
                     void* dX, void* stream);
 
+/* ---- training backbone causal attention (tcgen05, flash-style) ---------
+ * `causal_attention` forward / backward (eepipe/autodiff.py:265-298) and the
+ * boundary kernels attention_fwd / attention_bwd (eepipe/_pykernels.py:52-62,
+ * eepipe/_ckernels.pyx:170-236) without the (S x S) probabilities in HBM.
+ * Q, K, V, O, dO, dQ, dK, dV: (B*S, ld) bf16 row-major, head h in columns
+ * [128 h, 128 h + 128) (head_dim 128; the projections' own layout, e.g. the
+ * q / k / v column blocks of one fused output); S a multiple of 128.  lse
+ * (forward output, backward input) and dsum (backward scratch) are float32
+ * [B][H][S].  Deterministic (no atomics); scale 1/sqrt(128). */
+int ee_attn_train_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                      int64_t ldv, int64_t B, int64_t S, int64_t H, void* out, int64_t ldo,
+                      float* lse, void* stream);
+int ee_attn_train_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                      int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t ldd,
+                      const float* lse, int64_t B, int64_t S, int64_t H, void* dq, int64_t lddq,
+                      void* dk, int64_t lddk, void* dv, int64_t lddv, float* dsum, void* stream);
+
 /* ---- training RMSNorm (bf16 activations, float32 statistics) ---------- */
 
 /* y = x * (mean(x^2) + eps)^-1/2 * w row-wise; x, y (n, h) bf16, w (h) float32,

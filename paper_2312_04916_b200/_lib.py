@@ -122,6 +122,12 @@ SIGNATURES = {
                               c_void_p]),
     "ee_linear_dgrad": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p,
                                 c_void_p]),
+    "ee_attn_train_fwd": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
+                                  c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
+    "ee_attn_train_bwd": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+                                  c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                  c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+                                  c_void_p]),
     "ee_exit_head_train_fwd": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                                        c_float, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "ee_exit_head_train_bwd": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,

@@ -344,10 +344,15 @@ __global__ void k_loss_sum(const float* __restrict__ rowloss, int n, float scale
 
 namespace tc {
 int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
-    EE_REQUIRE(((uintptr_t)base & 15) == 0 && cols % 8 == 0, EE_ESHAPE,
-               "tensor map: base must be 16-B aligned and cols %% 8 == 0");
+    return make_tmap_bf16_ld(map, base, rows, cols, cols, box_rows);
+}
+
+int make_tmap_bf16_ld(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                      int box_rows) {
+    EE_REQUIRE(((uintptr_t)base & 15) == 0 && cols % 8 == 0 && ld % 8 == 0 && ld >= cols,
+               EE_ESHAPE, "tensor map: base must be 16-B aligned, cols and ld multiples of 8");
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
     cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     // resolved through the runtime so libee.so does not link libcuda (the

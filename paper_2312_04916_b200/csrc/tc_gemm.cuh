@@ -585,6 +585,9 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
 // Host: 2-D bf16 tensor map of a row-major (rows x cols) matrix, box
 // (64 cols x box_rows rows), 128-byte swizzle, zero fill out of bounds.
 int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows);
+// the same over a matrix with row stride ld >= cols (elements)
+int make_tmap_bf16_ld(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                      int box_rows);
 
 // C[M, N] = A . B^T with A given as (M, K) row-major (A_MN = false) or as
 // (K, M) row-major (A_MN = true); B likewise as (N, K) or (K, N).

@@ -636,18 +636,75 @@ def _sdpa_backend():
                         "cudnn": SDPBackend.CUDNN_ATTENTION}[_SDPA])
 
 
-def run_layer(params, prefix, x, num_heads):
-    """One pre-norm block (`eepipe/model.py:207-216`)."""
+_OWN_ATTN = os.environ.get("EE_ATTN_TRAIN", "1") != "0"  # A/B switch: 0 = torch SDPA
+
+
+class _AttnFn:
+    """Causal attention of the training backbone on the tcgen05 kernels
+    (ee_attn_train_fwd / _bwd, csrc/attention_train.cu): q, k, v (B, S, h)
+    bf16 in the projections' own layout, output (B, S, h) straight into the
+    wo GEMM (no (B, H, S, dh) transposes); lse saved for the backward
+    (eepipe/autodiff.py:265-298)."""
+
+    _fn = None
+
+    @classmethod
+    def get(cls):
+        if cls._fn is None:
+            torch = _torch()
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, q, k, v, num_heads):
+                    B, S, h = q.shape
+                    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+                    o = torch.empty_like(q)
+                    lse = torch.empty((B, num_heads, S), dtype=torch.float32, device=q.device)
+                    call("ee_attn_train_fwd", ptr(q), h, ptr(k), h, ptr(v), h, B, S, num_heads,
+                         ptr(o), h, ptr(lse), stream_ptr())
+                    ctx.save_for_backward(q, k, v, o, lse)
+                    ctx.nh = num_heads
+                    return o
+
+                @staticmethod
+                def backward(ctx, do):
+                    q, k, v, o, lse = ctx.saved_tensors
+                    B, S, h = q.shape
+                    do = do.to(q.dtype).contiguous()
+                    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+                    dsum = torch.empty_like(lse)
+                    call("ee_attn_train_bwd", ptr(q), h, ptr(k), h, ptr(v), h, ptr(o), h, ptr(do),
+                         h, ptr(lse), B, S, ctx.nh, ptr(dq), h, ptr(dk), h, ptr(dv), h, ptr(dsum),
+                         stream_ptr())
+                    return dq, dk, dv, None
+
+            cls._fn = _F
+        return cls._fn
+
+
+def causal_attention(q, k, v, num_heads):
+    """(B, S, h) causal multi-head attention (`eepipe/autodiff.py:265-298`):
+    the tcgen05 kernels for bf16, head_dim 128, S a multiple of 128 (every
+    config's training shape); other shapes (the tests' tiny models) and
+    float32 go through torch SDPA."""
     torch = _torch()
-    F = torch.nn.functional
-    B, S, h = x.shape
+    B, S, h = q.shape
     dh = h // num_heads
-    h1 = rmsnorm(x, params[f"{prefix}.attn_norm"])
-    q, k, v = (_matmul(params, f"{prefix}.{w}", h1) for w in ("wq", "wk", "wv"))
+    if (_OWN_ATTN and q.is_cuda and q.dtype == torch.bfloat16 and dh == 128 and S % 128 == 0):
+        return _AttnFn.get().apply(q, k, v, num_heads)
+    F = torch.nn.functional
     split = lambda t: t.view(B, S, num_heads, dh).transpose(1, 2)  # noqa: E731
     with _sdpa_backend():
         a = F.scaled_dot_product_attention(split(q), split(k), split(v), is_causal=True)
-    x = _matmul(params, f"{prefix}.wo", a.transpose(1, 2).reshape(B, S, h), residual=x)
+    return a.transpose(1, 2).reshape(B, S, h)
+
+
+def run_layer(params, prefix, x, num_heads):
+    """One pre-norm block (`eepipe/model.py:207-216`)."""
+    h1 = rmsnorm(x, params[f"{prefix}.attn_norm"])
+    q, k, v = (_matmul(params, f"{prefix}.{w}", h1) for w in ("wq", "wk", "wv"))
+    a = causal_attention(q, k, v, num_heads)
+    x = _matmul(params, f"{prefix}.wo", a, residual=x)
     h2 = rmsnorm(x, params[f"{prefix}.mlp_norm"])
     return _mlp(params, prefix, h2, residual=x)
 
