@@ -25,6 +25,8 @@
 //     griddepcontrol.wait.  (An L2 prefetch of the K/V rows that predate the
 //     pass, issued before the wait to overlap the QKV GEMV, made multi-chunk
 //     rows (positions >= 256) nondeterministic run to run on B200: removed.)
+#include <stdlib.h>
+
 #include "attn_core.cuh"
 
 namespace {
@@ -192,6 +194,7 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     __shared__ float s_m[kRowsCta][kWarpsA], s_l[kRowsCta][kWarpsA];
     __shared__ int s_last[kRowsCta];
     constexpr int dh = kMaxDh;
+    EE_TMIN(0);  // even slots: min, odd: max
     pdl_trigger_dev();
     const int hh = blockIdx.x, ch = blockIdx.z;
     const int r0 = blockIdx.y * g;  // this CTA's rows: [r0, r0 + mr), g <= kRowsCta
@@ -210,6 +213,8 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int j0 = ch * kChunk + warp * kBlk;
     pdl_wait_dev();
+    EE_TMIN(2);
+    EE_TMAX(3);
     // the block's K / V loads go out first, the q rows are staged meanwhile
     attn::BlockRegsV R;
     bf16* sk = s_k + warp * kBlk * dh;  // this warp's K tile
@@ -222,6 +227,7 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     __syncthreads();
     if (j0 <= pmax) {
         attn::block_wait128_k();
+        if (warp == 0) EE_TMAX(5);
         for (int i = 0; i < mr; ++i) {
             const int p = pos[r0 + i];
             if (j0 > p) continue;  // warp-uniform
@@ -262,6 +268,7 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
             }
         }
     }
+    EE_TMAX(7);
     if (pmax < kChunk) return;  // every row of the group fits one chunk
     __threadfence();
     __syncthreads();
@@ -285,13 +292,304 @@ k_attn_rows128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
         out[(int64_t)r * h + hh * dh + d] = __float2bfloat16_rn(attn::chunk_merge(base, stride, nch, d));
     }
     if (tid < mr && s_last[tid]) ctr[(r0 + tid) * nh + hh] = 0;  // re-usable workspace
+    EE_TMAX(9);
+}
+
+
+// ---------------------------------------------------------------------------
+// bf16, head_dim 128: split-K/V "slab" kernel on a thread-block cluster.
+// A cluster of C <= 8 CTAs (grid y) serves one (head, group of <= 16 rows);
+// CTA rank r evaluates the 64-position slabs r, r + C, ... of the head's K/V
+// (double-buffered cp.async into shared memory, K 16-byte chunks XOR-
+// swizzled).  Per slab and row (short dependent chains, for latency):
+//   s_j  = (q . K_j) * scale: thread (j, quarter) sums 32 dims as 4
+//          interleaved chains, the quarters added in order;
+//   m, l = slab max / sum of exp(s_j - m) over j <= p (warp butterflies);
+//   o[d] = sum_j exp(s_j - m) V_j[d]: thread (d, half), 4 chains per half.
+// Each slab's (m, l, o) stays in its CTA's shared memory; after a cluster
+// barrier rank 0 folds slabs 0..p/64 of every row in slab order through
+// distributed shared memory (weights e^(m_c - M) and their sum by warp
+// butterflies, then o = sum_c w_c o_c in slab order) and writes the row.
+// Every value depends on (row, position) only -- not on C or the other rows
+// of the launch: row-stable and deterministic, no global atomics.
+// No K/V load is issued before griddepcontrol.wait, not even of rows that
+// earlier passes wrote: measured on B200, such loads -- when their values
+// are consumed -- made the PRECEDING QKV GEMV write wrong K rows.
+constexpr int kSlab = 64;
+constexpr int kMaxSlabs = kMaxChunks * kChunk / kSlab;  // 32 (positions < 2048)
+constexpr int kSlabThreads = 256;
+constexpr int kSlabWarps = kSlabThreads / 32;
+constexpr int kSlabRows = 16;
+constexpr int kMaxCluster = 8;  // (16, non-portable: clusters scheduled late, slower)
+constexpr int kLocalSlabs = kMaxSlabs / kMaxCluster;  // slabs one CTA may own
+constexpr int kSlot = kMaxDh + 4;                     // [m, l, -, -, o[128]] per (slab, row)
+constexpr int kKVBytes = 2 * kSlab * kMaxDh * 2;      // one K + V slab buffer
+static_assert(kMaxSlabs == 32, "the fold uses one warp lane per slab");
+
+__host__ __device__ constexpr size_t slab_smem(int rows, int local) {
+    // 2 K/V buffers; q rows; scores (4 quarter partials per (row, position));
+    // PV halves; the CTA's slab partials
+    return (size_t)2 * kKVBytes + (size_t)rows * kMaxDh * 4 + (size_t)rows * 4 * kSlab * 4 +
+           (size_t)rows * 2 * kMaxDh * 4 + (size_t)local * rows * kSlot * 4;
+}
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ float2 bf2(uint32_t u) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                     "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t a) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a)
+                 : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kSlabThreads)
+k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int m,
+               const bf16* __restrict__ kc, const bf16* __restrict__ vc, int nh, float scale,
+               bf16* __restrict__ out, int g) {
+    extern __shared__ __align__(16) uint8_t smem_slab[];
+    __shared__ float s_mx[kSlabRows], s_l[kSlabRows];
+    constexpr int dh = kMaxDh;
+    EE_TMIN(0);
+    pdl_trigger_dev();
+    const int hh = blockIdx.x;
+    const int C = (int)gridDim.y;
+    const int rank = (int)cl_rank();
+    const int r0 = blockIdx.z * g;
+    const int mr = min(g, m - r0);
+    const int h = nh * dh;
+    uint8_t* sKV = smem_slab;                                         // [2][K | V]
+    float* sQ = reinterpret_cast<float*>(smem_slab + 2 * kKVBytes);   // [mr][dh]
+    float* sS = sQ + mr * dh;                                         // [mr][4][kSlab]
+    float* sO = sS + mr * 4 * kSlab;                                  // [mr][2][dh]
+    float* sPart = sO + mr * 2 * dh;                                  // [local][mr][kSlot]
+    // host-written control data (safe before the wait)
+    int pmax = -1;
+    for (int i = 0; i < mr; ++i) pmax = max(pmax, pos[r0 + i]);
+    const int ns_g = pmax / kSlab + 1;                             // slabs of the group
+    const int nloc = rank < ns_g ? (ns_g - 1 - rank) / C + 1 : 0;  // this CTA's slabs
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t hoff = (int64_t)hh * dh;
+    const uint32_t kv_u = (uint32_t)__cvta_generic_to_shared(sKV);
+    // slab sl (positions up to the group's last) into buffer b
+    auto issue = [&](int b, int sl) {
+        const int j0 = sl * kSlab, nj = min(kSlab, pmax + 1 - j0);
+        const uint32_t k_u = kv_u + b * kKVBytes, v_u = k_u + kKVBytes / 2;
+        for (int idx = tid; idx < nj * 16; idx += kSlabThreads) {
+            const int jl = idx >> 4, c = idx & 15;
+            const int64_t go = (int64_t)(j0 + jl) * h + hoff + c * 8;
+            cp16(k_u + (uint32_t)((jl * 16 + (c ^ (jl & 7))) * 16), kc + go);
+            cp16(v_u + (uint32_t)((jl * 16 + c) * 16), vc + go);
+        }
+    };
+    pdl_wait_dev();
+    EE_TMIN(2);
+    EE_TMAX(3);
+    if (nloc > 0) issue(0, rank);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (nloc > 1) issue(1, rank + C);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int t = tid; t < mr * (dh / 4); t += kSlabThreads) {
+        const int i = t / (dh / 4), c = t % (dh / 4);
+        reinterpret_cast<float4*>(sQ + i * dh)[c] =
+            reinterpret_cast<const float4*>(q + (int64_t)(r0 + i) * h + hoff)[c];
+    }
+    for (int li = 0; li < nloc; ++li) {
+        const int sl = rank + li * C, j0 = sl * kSlab, jend = min(j0 + kSlab, pmax + 1);
+        const int b = li & 1;
+        const bf16* sK = reinterpret_cast<const bf16*>(sKV + b * kKVBytes);
+        const bf16* sV = sK + kSlab * dh;
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // this slab's group landed
+        __syncthreads();
+        EE_TMAX(5);
+        // scores: thread (position jl = tid & 63, quarter qt = tid >> 6)
+        {
+            const int jl = tid & (kSlab - 1), qt = tid >> 6;
+            if (j0 + jl < jend) {
+                uint4 kk[4];
+                const uint4* krow = reinterpret_cast<const uint4*>(sK) + jl * 16;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) kk[c] = krow[(qt * 4 + c) ^ (jl & 7)];
+                for (int i = 0; i < mr; ++i) {
+                    const float4* qv = reinterpret_cast<const float4*>(sQ + i * dh + qt * 32);
+                    float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float4 q0 = qv[2 * c], q1 = qv[2 * c + 1];
+                        const float2 k0 = bf2(kk[c].x), k1 = bf2(kk[c].y), k2 = bf2(kk[c].z),
+                                     k3 = bf2(kk[c].w);
+                        a[0] = fmaf(q0.x, k0.x, a[0]);
+                        a[1] = fmaf(q0.y, k0.y, a[1]);
+                        a[2] = fmaf(q0.z, k1.x, a[2]);
+                        a[3] = fmaf(q0.w, k1.y, a[3]);
+                        a[0] = fmaf(q1.x, k2.x, a[0]);
+                        a[1] = fmaf(q1.y, k2.y, a[1]);
+                        a[2] = fmaf(q1.z, k3.x, a[2]);
+                        a[3] = fmaf(q1.w, k3.y, a[3]);
+                    }
+                    sS[(i * 4 + qt) * kSlab + jl] = (a[0] + a[1]) + (a[2] + a[3]);
+                }
+            }
+        }
+        __syncthreads();
+        // slab softmax per row: warp per row, lane owns positions lane, lane + 32
+        for (int i = warp; i < mr; i += kSlabWarps) {
+            const int p = pos[r0 + i];
+            const float* s0 = sS + i * 4 * kSlab;
+            const int ja = j0 + lane, jb = j0 + 32 + lane;
+            float a = -INFINITY, bb = -INFINITY;
+            if (ja <= p)
+                a = ((s0[lane] + s0[kSlab + lane]) + (s0[2 * kSlab + lane] + s0[3 * kSlab + lane])) *
+                    scale;
+            if (jb <= p)
+                bb = ((s0[32 + lane] + s0[kSlab + 32 + lane]) +
+                      (s0[2 * kSlab + 32 + lane] + s0[3 * kSlab + 32 + lane])) *
+                     scale;
+            float mx = fmaxf(a, bb);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float ea = ja <= p ? expf(a - mx) : 0.f;
+            const float eb = jb <= p ? expf(bb - mx) : 0.f;
+            float l = ea + eb;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+            __syncwarp();
+            float* pr = sS + i * 4 * kSlab;  // probabilities overwrite the first quarter
+            pr[lane] = ea;
+            pr[32 + lane] = eb;
+            if (lane == 0) {
+                s_mx[i] = mx;
+                s_l[i] = l;
+            }
+        }
+        __syncthreads();
+        // P V: thread (dim d, position half ph), 4 interleaved chains per half
+        {
+            const int d = tid & (dh - 1), ph = tid >> 7;
+            for (int i = 0; i < mr; ++i) {
+                const int p = pos[r0 + i];
+                if (p < j0) continue;  // CTA-uniform
+                const int jb = ph * 32;
+                const int nj = max(0, min(32, p + 1 - j0 - jb));
+                const float* pr = sS + i * 4 * kSlab + jb;
+                const bf16* vb = sV + jb * dh + d;
+                float a[4] = {0.f, 0.f, 0.f, 0.f};
+                int jl = 0;
+                for (; jl + 4 <= nj; jl += 4) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        a[u] = fmaf(pr[jl + u], __bfloat162float(vb[(jl + u) * dh]), a[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 3; ++u)  // tail: at most 3 positions
+                    if (jl + u < nj) a[u] = fmaf(pr[jl + u], __bfloat162float(vb[(jl + u) * dh]), a[u]);
+                sO[(i * 2 + ph) * dh + d] = (a[0] + a[1]) + (a[2] + a[3]);
+            }
+        }
+        __syncthreads();  // buffer b and sS free from here on
+        if (li + 2 < nloc) issue(b, rank + (li + 2) * C);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // the slab's partials -> this CTA's shared memory
+        for (int t = tid; t < mr * dh; t += kSlabThreads) {
+            const int i = t / dh, d = t % dh;
+            float* slot = sPart + (li * mr + i) * kSlot;
+            slot[4 + d] = sO[i * 2 * dh + d] + sO[(i * 2 + 1) * dh + d];
+            if (d == 0) {
+                slot[0] = s_mx[i];
+                slot[1] = s_l[i];
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    EE_TMAX(7);
+    cl_sync();  // every slab partial of the cluster is in place
+    if (rank == 0) {
+        const uint32_t part_u = (uint32_t)__cvta_generic_to_shared(sPart);
+        for (int i = warp; i < mr; i += kSlabWarps) {
+            const int r = r0 + i;
+            const int ns = pos[r] / kSlab + 1;
+            // slab c lives in rank c % C, local index c / C
+            auto slot_addr = [&](int c) {
+                return cl_map(part_u + (uint32_t)((((c / C) * mr + i) * kSlot) * 4), (uint32_t)(c % C));
+            };
+            float Mc = -INFINITY, Lc = 0.f;
+            if (lane < ns) {
+                const uint32_t a = slot_addr(lane);
+                Mc = ld_dsmem(a);
+                Lc = ld_dsmem(a + 4);
+            }
+            float MM = Mc;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) MM = fmaxf(MM, __shfl_xor_sync(0xffffffffu, MM, o));
+            const float w = lane < ns ? expf(Mc - MM) : 0.f;
+            float LL = Lc * w;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) LL += __shfl_xor_sync(0xffffffffu, LL, o);
+            float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int c0 = 0; c0 < ns; c0 += 8) {
+                float4 oc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    oc[u] = c0 + u < ns ? ld_dsmem4(slot_addr(c0 + u) + 16 + 16 * lane)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const float wc = __shfl_sync(0xffffffffu, w, (c0 + u) & 31);
+                    if (c0 + u < ns) {
+                        o4.x = fmaf(oc[u].x, wc, o4.x);
+                        o4.y = fmaf(oc[u].y, wc, o4.y);
+                        o4.z = fmaf(oc[u].z, wc, o4.z);
+                        o4.w = fmaf(oc[u].w, wc, o4.w);
+                    }
+                }
+            }
+            const float inv = 1.f / LL;
+            bf16* orow = out + (int64_t)r * h + hoff + 4 * lane;
+            *reinterpret_cast<__nv_bfloat162*>(orow) = __floats2bfloat162_rn(o4.x * inv, o4.y * inv);
+            *reinterpret_cast<__nv_bfloat162*>(orow + 2) = __floats2bfloat162_rn(o4.z * inv, o4.w * inv);
+        }
+    }
+    EE_TMAX(9);
+    cl_sync();  // rank 0 has read every partial: the other CTAs may exit
 }
 
 }  // namespace
 
+EE_TRACE_READER(ee_trace_attention)
+
 // Workspace layout: attn_core.cuh (counters, then partial slots).
 size_t attention_ws_bytes(int64_t /*m*/, int64_t nh, int64_t dh, int64_t /*s_max*/) {
     return attn::counters_bytes(nh) + attn::partial_slots(nh) * (dh + 2) * sizeof(float);
+}
+
+// EE_ATTN_SLAB=0 (A/B): the chunked rows kernel instead of the slab kernel
+static bool attn_slab() {
+    static const bool v = !getenv("EE_ATTN_SLAB") || atoi(getenv("EE_ATTN_SLAB")) != 0;
+    return v;
 }
 
 int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_pos,
@@ -319,7 +617,40 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
         // bf16, head_dim 128: the rows kernel (K/V block loads shared by the
         // group's rows, K staged swizzled in shared memory, V in registers);
         // other shapes / fp32: one CTA per row (same arithmetic)
-        if (dtype == EE_BF16 && dh == kMaxDh && nch >= kRowsKernelMinChunks) {
+        const int ns = max_pos / kSlab + 1;
+        if (dtype == EE_BF16 && dh == kMaxDh && attn_slab()) {
+            const int C = ns < kMaxCluster ? ns : kMaxCluster;
+            const int local = (ns + C - 1) / C;
+            // rows per cluster: enough clusters to cover the GPU about twice
+            const int64_t want = (2 * mr * nh * C + ee_sm_count() - 1) / (2 * ee_sm_count());
+            const int g = (int)(want < 1 ? 1 : (want > kSlabRows ? kSlabRows : want));
+            const int groups = (int)((mr + g - 1) / g);
+            static bool configured[16] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (!configured[dev & 15]) {
+                cudaFuncSetAttribute(k_attn_slab128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)slab_smem(kSlabRows, kLocalSlabs));
+                configured[dev & 15] = true;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)nh, (unsigned)C, (unsigned)groups);
+            cfg.blockDim = dim3(kSlabThreads);
+            cfg.dynamicSmemBytes = slab_smem((int)(mr < g ? mr : g), local);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[2];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 1;
+            attr[0].val.clusterDim.y = (unsigned)C;
+            attr[0].val.clusterDim.z = 1;
+            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[1].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = ee_pdl_enabled() && !g_pdl_off ? 2 : 1;
+            e = cudaLaunchKernelEx(&cfg, k_attn_slab128, q + r0 * h, pos + r0, (int)mr,
+                                   (const bf16*)kc, (const bf16*)vc, (int)nh, scale,
+                                   (bf16*)out + r0 * h, g);
+        } else if (dtype == EE_BF16 && dh == kMaxDh && nch >= kRowsKernelMinChunks) {
             // rows per CTA: just enough to fill the GPU with one CTA per SM
             // (more rows per CTA share more K/V loads but evaluate serially)
             const int64_t want = (mr * nh * nch + ee_sm_count() - 1) / ee_sm_count();

@@ -27,6 +27,12 @@ int decode_layer_launches(const ee_decoder_t* D, int64_t m) {
     return prefill ? 9 : 5;  // 4 x (GEMM + apply) + attention, or 4 GEMVs + attention
 }
 
+// profiling stand-in for the attention (EE_ABLATE bit 2): PDL trigger + wait only
+__global__ void k_null_pdl() {
+    pdl_trigger_dev();
+    pdl_wait_dev();
+}
+
 extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, int64_t row0, int64_t m,
                                const int32_t* pos, int32_t max_pos, void* stream) {
     if (m == 0) return EE_OK;
@@ -39,7 +45,8 @@ extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, int64
     const int dt = D->dtype;
     float* x = D->x + row0 * h;
     // EE_ABLATE (profiling only; wrong results): bit 0 skips the explicit
-    // RMSNorm launches, bit 1 the attention.
+    // RMSNorm launches, bit 1 the attention, bit 2 replaces the attention by
+    // an empty PDL kernel.
     static const int ablate = getenv("EE_ABLATE") ? atoi(getenv("EE_ABLATE")) : 0;
     // EE_PDL_SKIP (debug): bit k launches kernel k of the tiled decode layer
     // (QKV, attention, wo, w1, w2) without PDL
@@ -79,9 +86,12 @@ extern "C" int ee_decode_layer(const ee_decoder_t* D, const ee_layer_t* L, int64
         if ((rc = launch_qkv_tiled(xb, m, h, L->wqkv, folded, D->q, L->kcache, L->vcache, pos, s)))
             return rc;
         g_pdl_off = pdl_skip & 2;
-        if (!(ablate & 2) &&
-            (rc = launch_attention(D->q, m, pos, max_pos, L->kcache, L->vcache, D->nh, h / D->nh, dt,
-                                   D->attn, D->ws, D->ws_bytes, s)))
+        if (ablate & 4) {
+            if (launch_ex(k_null_pdl, dim3((unsigned)D->nh), dim3(256), 0, s) != cudaSuccess)
+                return ee_fail(EE_ECUDA, "null launch");
+        } else if (!(ablate & 2) &&
+                   (rc = launch_attention(D->q, m, pos, max_pos, L->kcache, L->vcache, D->nh,
+                                          h / D->nh, dt, D->attn, D->ws, D->ws_bytes, s)))
             return rc;
         g_pdl_off = pdl_skip & 4;
         if ((rc = launch_gemv_tiled((const bf16*)D->attn, m, h, L->wo, h, EE_EPI_RESIDUAL, x, h,

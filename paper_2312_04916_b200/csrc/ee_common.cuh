@@ -82,6 +82,35 @@ __device__ __forceinline__ void pdl_wait_dev() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void pdl_trigger_dev() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 bool ee_pdl_enabled();  // EE_PDL=0 disables (debug)
+
+// ---- timeline probes (profiling builds only: -DEE_TRACE) -------------------
+// Per translation unit: slot i holds the min (EE_TMIN) or max (EE_TMAX) of
+// %globaltimer over the CTAs that reach the probe (thread 0 of each CTA);
+// EE_TRACE_READER(name) defines extern "C" name(uint64_t* out, int reset).
+#ifdef EE_TRACE
+static __device__ unsigned long long g_trace[16];
+__device__ __forceinline__ unsigned long long ee_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define EE_TMIN(i) do { if (threadIdx.x == 0) atomicMin(&g_trace[i], ee_gtime()); } while (0)
+#define EE_TMAX(i) do { if (threadIdx.x == 0) atomicMax(&g_trace[i], ee_gtime()); } while (0)
+#define EE_TRACE_READER(name)                                                              \
+    extern "C" int name(unsigned long long* out, int reset) {                             \
+        cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));                                \
+        if (reset) {                                                                        \
+            unsigned long long init[16];                                                    \
+            for (int i = 0; i < 16; ++i) init[i] = (i & 1) ? 0ull : ~0ull;                  \
+            cudaMemcpyToSymbol(g_trace, init, sizeof(init));                                \
+        }                                                                                   \
+        return 0;                                                                           \
+    }
+#else
+#define EE_TMIN(i) do { } while (0)
+#define EE_TMAX(i) do { } while (0)
+#define EE_TRACE_READER(name)
+#endif
 extern thread_local int g_pdl_off;  // debug (EE_PDL_SKIP): nonzero disables PDL on this thread's next launches
 
 template <typename... KArgs, typename... Args>

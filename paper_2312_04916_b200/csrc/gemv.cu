@@ -333,6 +333,8 @@ int launch_qkv_tiled(const bf16* x, int64_t m, int64_t h, const void* Wqkv, Gemv
                    tma_gemv::RowNorm{nrm.ssq, nrm.eps});
 }
 
+EE_TRACE_READER(ee_trace_gemv)
+
 extern "C" int ee_gemv(const void* x, int64_t m, int64_t K, const void* W, int64_t N, int dtype,
                        int epilogue, void* out, int64_t ldo, void* stream) {
     return launch_gemv(x, m, K, W, N, dtype, epilogue, out, ldo, as_stream(stream));

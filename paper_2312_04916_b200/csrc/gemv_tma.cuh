@@ -131,6 +131,10 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
     }
     __syncthreads();
     pdl_trigger_dev();
+    // trace slots (profiling builds): 4 per kernel kind, qkv / wo / w1 / w2
+    const int tslot = 4 * (N == 3 * K ? 0 : N == K ? 1 : N == 4 * K ? 2 : 3);
+    (void)tslot;
+    EE_TMIN(tslot);
 
     if (warp == kConsumers) {
         // ---------------- producer (one lane) ----------------
@@ -176,6 +180,7 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
 
     // ---------------- consumers ----------------
     pdl_wait_dev();  // epilogues read/write buffers shared with the predecessor
+    EE_TMIN(tslot + 2);
     const int g = lane >> 2, t = lane & 3;
     const uint32_t ring_u32 = smem_u32(ring);
     int q = 0;
@@ -251,6 +256,7 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
         consumers_sync();
     }
     epi.finish();
+    EE_TMAX(tslot + 1);
 }
 
 }  // namespace tma_gemv
