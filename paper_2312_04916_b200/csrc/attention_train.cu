@@ -60,6 +60,22 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
 __device__ __forceinline__ void tmem_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_st8u(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+        : "memory");
+}
+// D (TMEM) (+)= A (TMEM: row = lane, K-major bf16 pairs per column) . B (smem)
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -99,42 +115,79 @@ __device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* m, in
 }
 
 // ============================================================================
-// forward: CTA = (q tile, head, batch); key tiles 0..qt, double-buffered S
+// forward: CTA = (pair of q tiles A = qt, B = qt - 1, head, batch), key tiles
+// 0..qt streamed once for both (K and V through a 3-slot ring).  Two softmax
+// warpgroups (A: warps 2-5, B: warps 6-9; warp w owns TMEM lanes of quarter
+// w % 4) so that one tile's exponentials overlap the other tile's MMAs:
+//   MMA issue order per key tile j:  S_A(j+1), PV_A(j), S_B(j+1), PV_B(j)
+//   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
+// P goes through shared memory (K-major SW128), so S_t(j+1) can be computed
+// while the softmax of tile j still works on its registers.  Lazy
+// rescaling: a row keeps its exponent offset m until its running max
+// exceeds m by more than 8 (log2 units; P <= 256), so O is rewritten in TMEM
+// only when the max jumps.  (Measured alternatives, B200, C2 shape: P in
+// TMEM read by a TS-MMA 84 us -- S_t(j+1) then has to wait for PV_t(j);
+// event-driven MMA issue 76 us; this order 73 us.)
 // ============================================================================
+#ifdef EE_TRACE
+// per-event timestamps of CTA 0 (events: 0 S issued, 1 PV issued, 2 S seen by
+// the softmax, 3 P published) x tile x key tile
+__device__ unsigned long long g_fwd_tl[4][2][32];
+#define FWD_TL(e, t, j)                                                  \
+    do {                                                                 \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 32) \
+            g_fwd_tl[e][t][j] = ee_gtime();                              \
+    } while (0)
+#else
+#define FWD_TL(e, t, j) do { } while (0)
+#endif
+constexpr int kFwdThreads = 320;
+constexpr int kRing = 3;                 // K / V ring slots (one 32 KB tile each)
+constexpr float kRescaleLog2 = 8.f;
+
 struct FwdBars {
-    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, o_done;
+    uint64_t q_full, full[kRing], empty[kRing];
+    uint64_t s_full[2], s_free[2], p_full[2], o_done[2];
     uint32_t tmem;
 };
-constexpr size_t kFwdSmem = 1024 + 6 * (size_t)kTile + sizeof(FwdBars) + 64;
+// Q_A, Q_B, ring, P_A, P_B
+constexpr size_t kFwdSmem = 1024 + (4 + kRing) * (size_t)kTile + sizeof(FwdBars) + 64;
 
-__global__ void __launch_bounds__(kAttnThreads, 1)
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
 k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
            const __grid_constant__ CUtensorMap tv, int S, int H, bf16* __restrict__ out, int ldo,
            float* __restrict__ lse, float scale) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* sQ = sm;
-    uint8_t* sK = sm + kTile;          // [2]
-    uint8_t* sV = sm + 3 * kTile;      // [2]
-    uint8_t* sP = sm + 5 * kTile;
-    FwdBars* bar = reinterpret_cast<FwdBars*>(sm + 6 * kTile);
+    uint8_t* sm = tc::align1024(smem_raw);
+    uint8_t* sQ = sm;                        // [2] (A, B)
+    uint8_t* sRing = sm + 2 * kTile;         // [kRing]
+    uint8_t* sP = sm + (2 + kRing) * kTile;  // [2]
+    FwdBars* bar = reinterpret_cast<FwdBars*>(sm + (4 + kRing) * kTile);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqt = S / kT;
-    const int qt = nqt - 1 - (int)blockIdx.x;  // longest rows first
+    const int qa = nqt - 1 - 2 * (int)blockIdx.x;   // longest rows first
+    const int qb = qa - 1;                          // -1: no second tile
     const int hh = blockIdx.y, b = blockIdx.z;
-    const int row0 = b * S + qt * kT;
     const int col = hh * kDh;
-    const int nkt = qt + 1;
+    const int na = qa + 1, nb = qb + 1;             // key tiles of A / B
     if (threadIdx.x == 0) {
         mb_init(&bar->q_full, 1);
-        for (int i = 0; i < 2; ++i) {
-            mb_init(&bar->kv_full[i], 1);
-            mb_init(&bar->kv_empty[i], 1);
-            mb_init(&bar->s_full[i], 1);
-            mb_init(&bar->s_free[i], 128);
+        for (int i = 0; i < kRing; ++i) {
+            mb_init(&bar->full[i], 1);
+            mb_init(&bar->empty[i], 1);
         }
-        mb_init(&bar->p_full, 128);
-        mb_init(&bar->o_done, 1);
+        for (int t = 0; t < 2; ++t) {
+            mb_init(&bar->s_full[t], 1);
+            mb_init(&bar->s_free[t], 128);
+            mb_init(&bar->p_full[t], 128);
+            mb_init(&bar->o_done[t], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) alloc_tmem512(&bar->tmem);
@@ -145,124 +198,167 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 
     if (warp == 0) {
         if (lane == 0) {
-            mb_expect_tx(&bar->q_full, kTile);
-            load_tile(sQ, &tq, col, row0, &bar->q_full);
-            for (int kt = 0; kt < nkt; ++kt) {
-                const int s = kt & 1;
-                if (kt >= 2) mb_wait(&bar->kv_empty[s], ((kt >> 1) - 1) & 1);
-                mb_expect_tx(&bar->kv_full[s], 2 * kTile);
-                load_tile(sK + s * kTile, &tk, col, b * S + kt * kT, &bar->kv_full[s]);
-                load_tile(sV + s * kTile, &tv, col, b * S + kt * kT, &bar->kv_full[s]);
+            // ---------------- TMA producer ----------------
+            mb_expect_tx(&bar->q_full, (nb > 0 ? 2 : 1) * kTile);
+            load_tile(sQ, &tq, col, b * S + qa * kT, &bar->q_full);
+            if (nb > 0) load_tile(sQ + kTile, &tq, col, b * S + qb * kT, &bar->q_full);
+            for (int L = 0; L < 2 * na; ++L) {  // K(0) V(0) K(1) V(1) ...
+                const int s = L % kRing, u = L / kRing;
+                if (u > 0) mb_wait(&bar->empty[s], (u - 1) & 1);
+                mb_expect_tx(&bar->full[s], kTile);
+                load_tile(sRing + s * kTile, (L & 1) ? &tv : &tk, col, b * S + (L >> 1) * kT,
+                          &bar->full[s]);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
+            // ---------------- MMA issuer ----------------
             mb_wait(&bar->q_full, 0);
             tc_fence_after();
-            const uint32_t q = su32(sQ);
-            auto issue_s = [&](int kt) {
-                const int s = kt & 1;
-                mb_wait(&bar->kv_full[s], (kt >> 1) & 1);
-                if (kt >= 2) mb_wait(&bar->s_free[s], ((kt >> 1) - 1) & 1);
+            auto slot = [&](int L) { return L % kRing; };
+            auto wait_full = [&](int L) {
+                mb_wait(&bar->full[slot(L)], (L / kRing) & 1);
                 tc_fence_after();
-                const uint32_t kk = su32(sK + s * kTile);
-#pragma unroll
-                for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        tc_mma(tmem + s * kT, desc_k(q, kb, k), desc_k(kk, kb, k), kIdescKK,
-                               (kb | k) != 0);
-                tc_commit(&bar->s_full[s]);
             };
-            issue_s(0);
-            const uint32_t p = su32(sP);
-            for (int kt = 0; kt < nkt; ++kt) {
-                if (kt + 1 < nkt) issue_s(kt + 1);
-                mb_wait(&bar->p_full, kt & 1);
-                tc_fence_after();
-                const uint32_t v = su32(sV + (kt & 1) * kTile);
+            auto issue_s = [&](int t, int j) {  // S_t = Q_t K(j)^T
+                const uint32_t q = su32(sQ + t * kTile), kk = su32(sRing + slot(2 * j) * kTile);
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        tc_mma(tmem + 2 * kT, desc_k(p, kb, k), desc_mn(v, kb * 4 + k), kIdescKM,
-                               (kt | kb | k) != 0);
-                tc_commit(&bar->o_done);
-                tc_commit(&bar->kv_empty[kt & 1]);
+                        tc_mma(tmem + t * kT, desc_k(q, kb, k), desc_k(kk, kb, k), kIdescKK,
+                               (kb | k) != 0);
+                tc_commit(&bar->s_full[t]);
+                FWD_TL(0, t, j);
+            };
+            auto issue_pv = [&](int t, int j) {  // O_t += P_t V(j)
+                const uint32_t p = su32(sP + t * kTile), v = su32(sRing + slot(2 * j + 1) * kTile);
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        tc_mma(tmem + (2 + t) * kT, desc_k(p, kb, k), desc_mn(v, kb * 4 + k), kIdescKM,
+                               (j | kb | k) != 0);
+                tc_commit(&bar->o_done[t]);
+                FWD_TL(1, t, j);
+            };
+            wait_full(0);
+            issue_s(0, 0);
+            if (nb > 0) issue_s(1, 0);
+            tc_commit(&bar->empty[slot(0)]);
+            for (int j = 0; j < na; ++j) {
+                const bool nxt = j + 1 < na, bnow = j < nb, bnxt = j + 1 < nb;
+                if (nxt) {
+                    wait_full(2 * j + 2);
+                    mb_wait(&bar->s_free[0], j & 1);  // softmax A has read S_A(j)
+                    tc_fence_after();
+                    issue_s(0, j + 1);
+                }
+                wait_full(2 * j + 1);
+                mb_wait(&bar->p_full[0], j & 1);
+                tc_fence_after();
+                issue_pv(0, j);
+                if (bnxt) {
+                    mb_wait(&bar->s_free[1], j & 1);
+                    tc_fence_after();
+                    issue_s(1, j + 1);
+                }
+                if (nxt) tc_commit(&bar->empty[slot(2 * j + 2)]);  // K(j+1) read by both S
+                if (bnow) {
+                    mb_wait(&bar->p_full[1], j & 1);
+                    tc_fence_after();
+                    issue_pv(1, j);
+                }
+                tc_commit(&bar->empty[slot(2 * j + 1)]);  // V(j) read by both PV
             }
         }
     } else {
+        // ---------------- softmax warpgroups ----------------
+        const int t = (warp - 2) >> 2;   // 0: tile A, 1: tile B
+        const int qt = t == 0 ? qa : qb;
+        const int n = t == 0 ? na : nb;
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;  // tile row = TMEM lane
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        const uint32_t tS = tmem + lane_off + t * kT, tO = tmem + lane_off + (2 + t) * kT;
+        uint8_t* myP = sP + t * kTile;
         const float sl2 = scale * kLog2e;
         float m = -INFINITY, l = 0.f;
         float v[kT];
-        for (int kt = 0; kt < nkt; ++kt) {
-            const int s = kt & 1;
-            mb_wait(&bar->s_full[s], (kt >> 1) & 1);
+        for (int j = 0; j < n; ++j) {
+            mb_wait(&bar->s_full[t], j & 1);
             tc_fence_after();
+            if (threadIdx.x == 64 + 128 * t) FWD_TL(2, t, j);
 #pragma unroll
-            for (int c = 0; c < kT; c += 16) tmem_ld16_nowait(tmem + lane_off + s * kT + c, v + c);
+            for (int c = 0; c < kT; c += 16) tmem_ld16_nowait(tS + c, v + c);
             tmem_wait_ld();
             tc_fence_before();
-            mb_arrive(&bar->s_free[s]);
-            const bool diag = kt == qt;
+            mb_arrive(&bar->s_free[t]);
+            const bool diag = j == qt;
             float mx = -INFINITY;
+            if (diag) {
 #pragma unroll
-            for (int j = 0; j < kT; ++j) {
-                const float x = (diag && j > r) ? -INFINITY : v[j] * sl2;
-                v[j] = x;
-                mx = fmaxf(mx, x);
-            }
-            const float mn = fmaxf(m, mx);
-            const float alpha = exp2f(m - mn);
-            float sum = 0.f;
+                for (int c = 0; c < kT; ++c) {
+                    if (c > r) v[c] = -INFINITY;
+                    mx = fmaxf(mx, v[c]);
+                }
+            } else {
 #pragma unroll
-            for (int j = 0; j < kT; ++j) {
-                const float e = exp2f(v[j] - mn);
-                v[j] = e;
-                sum += e;
+                for (int c = 0; c < kT; ++c) mx = fmaxf(mx, v[c]);
             }
-            l = l * alpha + sum;
-            m = mn;
-            if (kt > 0) {
-                mb_wait(&bar->o_done, (kt - 1) & 1);  // PV(kt-1) done: O stable, P free
+            const float mrow = mx * sl2;
+            // lazy rescale: move the offset only when the max outgrows it
+            const bool move = j == 0 || mrow > m + kRescaleLog2;
+            const float mnew = move ? mrow : m;
+            const float alpha = j == 0 ? 0.f : ex2(m - mnew);
+            float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c = 0; c < kT; ++c) {
+                v[c] = ex2(fmaf(v[c], sl2, -mnew));
+                s4[c & 3] += v[c];
+            }
+            l = fmaf(l, alpha, (s4[0] + s4[1]) + (s4[2] + s4[3]));
+            m = mnew;
+            if (j > 0) {
+                mb_wait(&bar->o_done[t], (j - 1) & 1);  // PV(j-1) done: O stable, P free
                 tc_fence_after();
-                if (__any_sync(0xffffffffu, alpha != 1.f)) {
+                if (__any_sync(0xffffffffu, move)) {
 #pragma unroll 1
                     for (int c = 0; c < kDh; c += 16) {
                         float o[16];
-                        tmem_ld16(tmem + lane_off + 2 * kT + c, o);
+                        tmem_ld16(tO + c, o);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) o[j] *= alpha;
-                        tmem_st16(tmem + lane_off + 2 * kT + c, o);
+                        for (int q = 0; q < 16; ++q) o[q] *= alpha;
+                        tmem_st16(tO + c, o);
                     }
                     tmem_wait_st();
                 }
             }
 #pragma unroll
-            for (int c = 0; c < kT; c += 16) store_row16(sP, r, c, v + c);
+            for (int c = 0; c < kT; c += 16) store_row16(myP, r, c, v + c);
             fence_async_smem();
             tc_fence_before();
-            mb_arrive(&bar->p_full);
+            if (threadIdx.x == 64 + 128 * t) FWD_TL(3, t, j);
+            mb_arrive(&bar->p_full[t]);
         }
-        mb_wait(&bar->o_done, (nkt - 1) & 1);
-        tc_fence_after();
-        const float inv = 1.f / l;
-        bf16* orow = out + (int64_t)(row0 + r) * ldo + col;
+        if (n > 0) {
+            mb_wait(&bar->o_done[t], (n - 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / l;
+            bf16* orow = out + (int64_t)(b * S + qt * kT + r) * ldo + col;
 #pragma unroll 1
-        for (int c = 0; c < kDh; c += 16) {
-            float o[16];
-            tmem_ld16(tmem + lane_off + 2 * kT + c, o);
-            uint4 u0 = make_uint4(pack2(o[0] * inv, o[1] * inv), pack2(o[2] * inv, o[3] * inv),
-                                  pack2(o[4] * inv, o[5] * inv), pack2(o[6] * inv, o[7] * inv));
-            uint4 u1 = make_uint4(pack2(o[8] * inv, o[9] * inv), pack2(o[10] * inv, o[11] * inv),
-                                  pack2(o[12] * inv, o[13] * inv), pack2(o[14] * inv, o[15] * inv));
-            reinterpret_cast<uint4*>(orow + c)[0] = u0;
-            reinterpret_cast<uint4*>(orow + c)[1] = u1;
+            for (int c = 0; c < kDh; c += 16) {
+                float o[16];
+                tmem_ld16(tO + c, o);
+                uint4 u0 = make_uint4(pack2(o[0] * inv, o[1] * inv), pack2(o[2] * inv, o[3] * inv),
+                                      pack2(o[4] * inv, o[5] * inv), pack2(o[6] * inv, o[7] * inv));
+                uint4 u1 = make_uint4(pack2(o[8] * inv, o[9] * inv), pack2(o[10] * inv, o[11] * inv),
+                                      pack2(o[12] * inv, o[13] * inv), pack2(o[14] * inv, o[15] * inv));
+                reinterpret_cast<uint4*>(orow + c)[0] = u0;
+                reinterpret_cast<uint4*>(orow + c)[1] = u1;
+            }
+            lse[((int64_t)b * H + hh) * S + qt * kT + r] = (m + log2f(l)) * kLn2;
         }
-        lse[((int64_t)b * H + hh) * S + qt * kT + r] = (m + log2f(l)) * kLn2;
     }
     tc_fence_before();
     __syncthreads();
@@ -293,61 +389,70 @@ __global__ void k_attn_dot(const bf16* __restrict__ dout, int ldd, const bf16* _
     }
 }
 
-// P (and dS) of one 16-column chunk of tile row r from S and dP in TMEM
-struct RowGrad {
-    float lse2;  // lse * log2(e)
-    float d;     // rowsum(dO o O)
-    float sl2;   // scale * log2(e)
-    float scale;
-};
-__device__ __forceinline__ void p_ds_chunk(const RowGrad& g, const float* sv, const float* dpv,
-                                           bool diag, int r, int c0, float* p, float* ds) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const bool masked = diag && (c0 + j) > r;
-        const float pj = masked ? 0.f : exp2f(sv[j] * g.sl2 - g.lse2);
-        p[j] = pj;
-        ds[j] = pj * (dpv[j] - g.d) * g.scale;
-    }
-}
-
 // ============================================================================
-// backward dK, dV: CTA = (key tile, head, batch); q tiles kt..nqt-1
-//   TMEM: S [0,128) dP [128,256) dV [256,384) dK [384,512)
+// backward dK, dV: CTA = (key tile, head, batch); q tiles kt..nqt-1, in the
+// TRANSPOSED formulation (rows = keys = TMEM lanes), each q tile as two
+// 64-row halves h handled by two warpgroups (h = 0: warps 2-5, h = 1: warps
+// 6-9) so one half's exponentials overlap the other half's MMAs:
+//   S_h^T = K Q_h^T,  dP_h^T = V dO_h^T                    (M = keys, N = 64)
+//   P_h^T = exp2(S_h^T c - lse_q),  dS_h^T = P_h^T (dP_h^T - D_q) / sqrt(dh)
+//   dV += P_h^T dO_h,  dK += dS_h^T Q_h    (A = P^T / dS^T straight from TMEM)
+// P and dS never touch shared memory; (Q_i, dO_i) plus the q tile's lse / D
+// stream through a 2-stage ring.  TMEM: S_0^T [0,64) dP_0^T [64,128)
+// S_1^T [128,192) dP_1^T [192,256) dV [256,384) dK [384,512); P^T / dS^T
+// overwrite the first 32 columns of S^T / dP^T, so S_h^T(i+1) is issued once
+// the dV / dK MMAs of half h of tile i completed.
 // ============================================================================
+constexpr int kBwdStages = 2;
+constexpr int kHalf = kT / 2;
+constexpr int kBwdThreads = 320;
 struct BwdBars {
-    uint64_t kv_full, qd_full, qd_empty, s_full, st_free, p_full;
+    uint64_t kv_full, full[kBwdStages], empty[kBwdStages], s_full[2], p_full[2], mma_done[2];
     uint32_t tmem;
 };
-constexpr size_t kBwdKvSmem = 1024 + 6 * (size_t)kTile + sizeof(BwdBars) + 64;
+constexpr int kBwdStage = 2 * kTile + 2 * kT * 4;  // Q, dO tiles + lse, D of the q tile
+constexpr size_t kBwdKvSmem = 1024 + 2 * (size_t)kTile + kBwdStages * (size_t)kBwdStage +
+                              sizeof(BwdBars) + 64;
+constexpr uint32_t kIdescKK64 = idesc_bf16(128, 64, false, false);  // N = 64 q rows
 
-__global__ void __launch_bounds__(kAttnThreads, 1)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
 k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
               const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
               int S, int H, const float* __restrict__ lse, const float* __restrict__ D,
               bf16* __restrict__ dk, int lddk, bf16* __restrict__ dv, int lddv, float scale) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sm = tc::align1024(smem_raw);
     uint8_t* sK = sm;
     uint8_t* sV = sm + kTile;
-    uint8_t* sQ = sm + 2 * kTile;
-    uint8_t* sDO = sm + 3 * kTile;
-    uint8_t* sP = sm + 4 * kTile;
-    uint8_t* sDS = sm + 5 * kTile;
-    BwdBars* bar = reinterpret_cast<BwdBars*>(sm + 6 * kTile);
+    uint8_t* sStage = sm + 2 * kTile;  // [kBwdStages] x (Q, dO, lse, D)
+    BwdBars* bar = reinterpret_cast<BwdBars*>(sm + 2 * kTile + kBwdStages * kBwdStage);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqt = S / kT;
-    const int kt = (int)blockIdx.x;  // key tile
+    const int kt = (int)blockIdx.x;  // key tile (0 = most q tiles: scheduled first)
     const int hh = blockIdx.y, b = blockIdx.z;
     const int col = hh * kDh;
     const int n = nqt - kt;  // q tiles kt .. nqt-1
+    const float* lse_bh = lse + ((int64_t)b * H + hh) * S;
+    const float* d_bh = D + ((int64_t)b * H + hh) * S;
     if (threadIdx.x == 0) {
         mb_init(&bar->kv_full, 1);
-        mb_init(&bar->qd_full, 1);
-        mb_init(&bar->qd_empty, 1);
-        mb_init(&bar->s_full, 1);
-        mb_init(&bar->st_free, 128);
-        mb_init(&bar->p_full, 128);
+        for (int i = 0; i < kBwdStages; ++i) {
+            mb_init(&bar->full[i], 1);
+            mb_init(&bar->empty[i], 1);
+        }
+        for (int h = 0; h < 2; ++h) {
+            mb_init(&bar->s_full[h], 1);
+            mb_init(&bar->p_full[h], 128);
+            mb_init(&bar->mma_done[h], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) alloc_tmem512(&bar->tmem);
@@ -362,91 +467,136 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
             load_tile(sK, &tk, col, b * S + kt * kT, &bar->kv_full);
             load_tile(sV, &tv, col, b * S + kt * kT, &bar->kv_full);
             for (int i = 0; i < n; ++i) {
-                if (i > 0) mb_wait(&bar->qd_empty, (i - 1) & 1);
-                const int q0 = b * S + (kt + i) * kT;
-                mb_expect_tx(&bar->qd_full, 2 * kTile);
-                load_tile(sQ, &tq, col, q0, &bar->qd_full);
-                load_tile(sDO, &tdo, col, q0, &bar->qd_full);
+                const int st = i % kBwdStages, u = i / kBwdStages;
+                if (u > 0) mb_wait(&bar->empty[st], (u - 1) & 1);
+                uint8_t* g = sStage + st * kBwdStage;
+                const int qt = kt + i, q0 = b * S + qt * kT;
+                mb_expect_tx(&bar->full[st], kBwdStage);
+                load_tile(g, &tq, col, q0, &bar->full[st]);
+                load_tile(g + kTile, &tdo, col, q0, &bar->full[st]);
+                bulk_g2s(g + 2 * kTile, lse_bh + qt * kT, kT * 4, &bar->full[st]);
+                bulk_g2s(g + 2 * kTile + kT * 4, d_bh + qt * kT, kT * 4, &bar->full[st]);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             mb_wait(&bar->kv_full, 0);
-            const uint32_t k = su32(sK), v = su32(sV), q = su32(sQ), dO = su32(sDO);
-            const uint32_t p = su32(sP), ds = su32(sDS);
-            for (int i = 0; i < n; ++i) {
-                mb_wait(&bar->qd_full, i & 1);
-                if (i > 0) mb_wait(&bar->st_free, (i - 1) & 1);
-                tc_fence_after();
+            tc_fence_after();
+            const uint32_t k = su32(sK), v = su32(sV);
+            // S_h^T, dP_h^T of tile i: K-major B = rows [64h, 64h+64) of Q / dO
+            auto issue_s = [&](int i, int h) {
+                const int st = i % kBwdStages;
+                const uint32_t q = su32(sStage + st * kBwdStage) + h * kHalf * 128, dO = q + kTile;
+                const uint32_t ts = tmem + h * kT;
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        tc_mma(tmem, desc_k(q, kb, kk), desc_k(k, kb, kk), kIdescKK, (kb | kk) != 0);
-                        tc_mma(tmem + kT, desc_k(dO, kb, kk), desc_k(v, kb, kk), kIdescKK,
+                        tc_mma(ts, desc_k(k, kb, kk), desc_k(q, kb, kk), kIdescKK64, (kb | kk) != 0);
+                        tc_mma(ts + kHalf, desc_k(v, kb, kk), desc_k(dO, kb, kk), kIdescKK64,
                                (kb | kk) != 0);
                     }
-                tc_commit(&bar->s_full);
-                mb_wait(&bar->p_full, i & 1);
-                tc_fence_after();
-                // dV += P^T dO, dK += dS^T Q  (M = keys, K = q rows, N = dh)
+                tc_commit(&bar->s_full[h]);
+                FWD_TL(0, h, i);
+            };
+            // dV += P_h^T dO_h, dK += dS_h^T Q_h  (K = the half's 64 q rows)
+            auto issue_acc = [&](int i, int h) {
+                const int st = i % kBwdStages;
+                const uint32_t q = su32(sStage + st * kBwdStage), dO = q + kTile;
+                const uint32_t ts = tmem + h * kT;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    tc_mma(tmem + 2 * kT, desc_mn(p, kk), desc_mn(dO, kk), kIdescMM, (i | kk) != 0);
-                    tc_mma(tmem + 3 * kT, desc_mn(ds, kk), desc_mn(q, kk), kIdescMM, (i | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk) {
+                    tc_mma_ts(tmem + 2 * kT, ts + kk * 8, desc_mn(dO, 4 * h + kk), kIdescKM,
+                              (i | h | kk) != 0);
+                    tc_mma_ts(tmem + 3 * kT, ts + kHalf + kk * 8, desc_mn(q, 4 * h + kk), kIdescKM,
+                              (i | h | kk) != 0);
                 }
-                tc_commit(&bar->qd_empty);
+                tc_commit(&bar->mma_done[h]);
+                FWD_TL(1, h, i);
+            };
+            mb_wait(&bar->full[0], 0);
+            tc_fence_after();
+            issue_s(0, 0);
+            issue_s(0, 1);
+            for (int i = 0; i < n; ++i) {
+                const bool nxt = i + 1 < n;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    mb_wait(&bar->p_full[h], i & 1);
+                    tc_fence_after();
+                    issue_acc(i, h);
+                    if (h == 1) tc_commit(&bar->empty[i % kBwdStages]);  // Q / dO of tile i read
+                    if (nxt) {
+                        mb_wait(&bar->full[(i + 1) % kBwdStages], ((i + 1) / kBwdStages) & 1);
+                        mb_wait(&bar->mma_done[h], i & 1);  // P_h^T / dS_h^T(i) consumed
+                        tc_fence_after();
+                        issue_s(i + 1, h);
+                    }
+                }
             }
         }
     } else {
+        const int hf = (warp - 2) >> 2;  // this warpgroup's q half
         const int quarter = warp & 3;
-        const int r = quarter * 32 + lane;
+        const int r = quarter * 32 + lane;  // key row = TMEM lane
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        RowGrad g;
-        g.sl2 = scale * kLog2e;
-        g.scale = scale;
+        const uint32_t tS = tmem + lane_off + hf * kT, tP = tS + kHalf;
+        const float sl2 = scale * kLog2e;
         for (int i = 0; i < n; ++i) {
-            const int qt = kt + i;
-            const int64_t si = ((int64_t)b * H + hh) * S + qt * kT + r;
-            g.lse2 = lse[si] * kLog2e;
-            g.d = D[si];
-            mb_wait(&bar->s_full, i & 1);
+            const float* sLse = reinterpret_cast<const float*>(sStage + (i % kBwdStages) * kBwdStage +
+                                                                 2 * kTile) + hf * kHalf;
+            const float* sD = sLse + kT;
+            mb_wait(&bar->full[i % kBwdStages], (i / kBwdStages) & 1);  // lse / D landed
+            mb_wait(&bar->s_full[hf], i & 1);
             tc_fence_after();
-            const bool diag = i == 0;  // q tile == key tile
+            if (threadIdx.x == 64 + 128 * hf) FWD_TL(2, hf, i);
+            const bool diag = i == 0;  // q tile == key tile: q index < key r is masked
+            const int c0 = hf * kHalf;   // q index of this half's first column
 #pragma unroll 1
-            for (int c = 0; c < kT; c += 16) {
-                float sv[16], dpv[16], p[16], ds[16];
-                tmem_ld16_nowait(tmem + lane_off + c, sv);
-                tmem_ld16_nowait(tmem + lane_off + kT + c, dpv);
+            for (int c = 0; c < kHalf; c += 16) {
+                float sv[16], dpv[16];
+                tmem_ld16_nowait(tS + c, sv);
+                tmem_ld16_nowait(tP + c, dpv);
                 tmem_wait_ld();
-                p_ds_chunk(g, sv, dpv, diag, r, c, p, ds);
-                store_row16(sP, r, c, p);
-                store_row16(sDS, r, c, ds);
+                uint32_t pk[8], dk8[8];
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    const float4 l4 = *reinterpret_cast<const float4*>(sLse + c + (j & ~3));
+                    const float4 d4 = *reinterpret_cast<const float4*>(sD + c + (j & ~3));
+                    const float la = (j & 2) ? l4.z : l4.x, lb = (j & 2) ? l4.w : l4.y;
+                    const float da = (j & 2) ? d4.z : d4.x, db = (j & 2) ? d4.w : d4.y;
+                    float p0 = ex2(fmaf(sv[j], sl2, -la * kLog2e));
+                    float p1 = ex2(fmaf(sv[j + 1], sl2, -lb * kLog2e));
+                    if (diag && c0 + c + j < r) p0 = 0.f;
+                    if (diag && c0 + c + j + 1 < r) p1 = 0.f;
+                    pk[j / 2] = pack2(p0, p1);
+                    dk8[j / 2] = pack2(p0 * (dpv[j] - da) * scale, p1 * (dpv[j + 1] - db) * scale);
+                }
+                // P^T over S^T columns [c/2, c/2 + 8), dS^T over dP^T's (already read)
+                tmem_st8u(tS + c / 2, pk);
+                tmem_st8u(tP + c / 2, dk8);
             }
+            tmem_wait_st();
             tc_fence_before();
-            mb_arrive(&bar->st_free);
-            fence_async_smem();
-            tc_fence_before();
-            mb_arrive(&bar->p_full);
+            if (threadIdx.x == 64 + 128 * hf) FWD_TL(3, hf, i);
+            mb_arrive(&bar->p_full[hf]);
         }
-        // the final dV / dK: wait for the last accumulation (qd_empty of i = n-1)
-        mb_wait(&bar->qd_empty, (n - 1) & 1);
+        // the final dV (warpgroup 0) / dK (warpgroup 1)
+        mb_wait(&bar->mma_done[0], (n - 1) & 1);
+        mb_wait(&bar->mma_done[1], (n - 1) & 1);
         tc_fence_after();
         const int64_t row = (int64_t)b * S + kt * kT + r;
+        bf16* dst = hf == 0 ? dv + row * lddv + col : dk + row * lddk + col;
 #pragma unroll 1
-        for (int which = 0; which < 2; ++which) {
-            bf16* dst = which == 0 ? dv + row * lddv + col : dk + row * lddk + col;
-#pragma unroll 1
-            for (int c = 0; c < kDh; c += 16) {
-                float o[16];
-                tmem_ld16(tmem + lane_off + (2 + which) * kT + c, o);
-                uint4 u0 = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]),
-                                      pack2(o[6], o[7]));
-                uint4 u1 = make_uint4(pack2(o[8], o[9]), pack2(o[10], o[11]), pack2(o[12], o[13]),
-                                      pack2(o[14], o[15]));
-                reinterpret_cast<uint4*>(dst + c)[0] = u0;
-                reinterpret_cast<uint4*>(dst + c)[1] = u1;
-            }
+        for (int c = 0; c < kDh; c += 16) {
+            float o[16];
+            tmem_ld16(tmem + lane_off + (2 + hf) * kT + c, o);
+            uint4 u0 = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]),
+                                  pack2(o[6], o[7]));
+            uint4 u1 = make_uint4(pack2(o[8], o[9]), pack2(o[10], o[11]), pack2(o[12], o[13]),
+                                  pack2(o[14], o[15]));
+            reinterpret_cast<uint4*>(dst + c)[0] = u0;
+            reinterpret_cast<uint4*>(dst + c)[1] = u1;
         }
     }
     tc_fence_before();
@@ -458,14 +608,18 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
 }
 
 // ============================================================================
-// backward dQ: CTA = (q tile, head, batch); key tiles 0..qt, K/V double-buffered
+// backward dQ: CTA = (q tile, head, batch); key tiles 0..qt through a 2-stage
+// K / V ring.  S = Q K_j^T, dP = dO V_j^T (M = q rows = TMEM lanes), dS =
+// P (dP - D) / sqrt(dh) written as bf16 pairs over the first 64 columns of
+// dP, dQ += dS K_j with A = dS straight from TMEM (K_j read MN-major).
 //   TMEM: S [0,128) dP [128,256) dQ [256,384)
 // ============================================================================
 struct BwdQBars {
-    uint64_t qd_full, kv_full[2], kv_empty[2], s_full, st_free, ds_full, ds_free;
+    uint64_t qd_full, full[kBwdStages], empty[kBwdStages], s_full, ds_full, mma_done;
     uint32_t tmem;
 };
-constexpr size_t kBwdQSmem = 1024 + 7 * (size_t)kTile + sizeof(BwdQBars) + 64;
+constexpr size_t kBwdQSmem = 1024 + 2 * (size_t)kTile + 2 * kBwdStages * (size_t)kTile +
+                             sizeof(BwdQBars) + 64;
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
 k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -473,29 +627,26 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
              int S, int H, const float* __restrict__ lse, const float* __restrict__ D,
              bf16* __restrict__ dq, int lddq, float scale) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sm = tc::align1024(smem_raw);
     uint8_t* sQ = sm;
     uint8_t* sDO = sm + kTile;
-    uint8_t* sK = sm + 2 * kTile;  // [2]
-    uint8_t* sV = sm + 4 * kTile;  // [2]
-    uint8_t* sDS = sm + 6 * kTile;
-    BwdQBars* bar = reinterpret_cast<BwdQBars*>(sm + 7 * kTile);
+    uint8_t* sKV = sm + 2 * kTile;  // [kBwdStages] x (K, V)
+    BwdQBars* bar = reinterpret_cast<BwdQBars*>(sm + 2 * kTile + 2 * kBwdStages * kTile);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqt = S / kT;
-    const int qt = nqt - 1 - (int)blockIdx.x;
+    const int qt = nqt - 1 - (int)blockIdx.x;  // longest rows first
     const int hh = blockIdx.y, b = blockIdx.z;
     const int col = hh * kDh;
     const int nkt = qt + 1;
     if (threadIdx.x == 0) {
         mb_init(&bar->qd_full, 1);
-        for (int i = 0; i < 2; ++i) {
-            mb_init(&bar->kv_full[i], 1);
-            mb_init(&bar->kv_empty[i], 1);
+        for (int i = 0; i < kBwdStages; ++i) {
+            mb_init(&bar->full[i], 1);
+            mb_init(&bar->empty[i], 1);
         }
         mb_init(&bar->s_full, 1);
-        mb_init(&bar->st_free, 128);
         mb_init(&bar->ds_full, 128);
-        mb_init(&bar->ds_free, 1);
+        mb_init(&bar->mma_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) alloc_tmem512(&bar->tmem);
@@ -511,23 +662,24 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
             load_tile(sQ, &tq, col, q0, &bar->qd_full);
             load_tile(sDO, &tdo, col, q0, &bar->qd_full);
             for (int kt = 0; kt < nkt; ++kt) {
-                const int s = kt & 1;
-                if (kt >= 2) mb_wait(&bar->kv_empty[s], ((kt >> 1) - 1) & 1);
-                mb_expect_tx(&bar->kv_full[s], 2 * kTile);
-                load_tile(sK + s * kTile, &tk, col, b * S + kt * kT, &bar->kv_full[s]);
-                load_tile(sV + s * kTile, &tv, col, b * S + kt * kT, &bar->kv_full[s]);
+                const int st = kt % kBwdStages, u = kt / kBwdStages;
+                if (u > 0) mb_wait(&bar->empty[st], (u - 1) & 1);
+                uint8_t* g = sKV + st * 2 * kTile;
+                mb_expect_tx(&bar->full[st], 2 * kTile);
+                load_tile(g, &tk, col, b * S + kt * kT, &bar->full[st]);
+                load_tile(g + kTile, &tv, col, b * S + kt * kT, &bar->full[st]);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             mb_wait(&bar->qd_full, 0);
-            const uint32_t q = su32(sQ), dO = su32(sDO), ds = su32(sDS);
+            const uint32_t q = su32(sQ), dO = su32(sDO);
             for (int kt = 0; kt < nkt; ++kt) {
-                const int s = kt & 1;
-                mb_wait(&bar->kv_full[s], (kt >> 1) & 1);
-                if (kt > 0) mb_wait(&bar->st_free, (kt - 1) & 1);
+                const int st = kt % kBwdStages;
+                const uint32_t k = su32(sKV + st * 2 * kTile), v = k + kTile;
+                mb_wait(&bar->full[st], (kt / kBwdStages) & 1);
+                if (kt > 0) mb_wait(&bar->mma_done, (kt - 1) & 1);  // dS(kt-1) consumed
                 tc_fence_after();
-                const uint32_t k = su32(sK + s * kTile), v = su32(sV + s * kTile);
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
@@ -539,48 +691,49 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
                 tc_commit(&bar->s_full);
                 mb_wait(&bar->ds_full, kt & 1);
                 tc_fence_after();
-                // dQ += dS K   (A = dS K-major over keys, B = K tile MN-major)
+                // dQ += dS K   (A = dS from TMEM, B = K tile MN-major, K = keys)
 #pragma unroll
-                for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        tc_mma(tmem + 2 * kT, desc_k(ds, kb, kk), desc_mn(k, kb * 4 + kk), kIdescKM,
-                               (kt | kb | kk) != 0);
-                tc_commit(&bar->ds_free);
-                tc_commit(&bar->kv_empty[s]);
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 2 * kT, tmem + kT + kk * 8, desc_mn(k, kk), kIdescKM,
+                              (kt | kk) != 0);
+                tc_commit(&bar->empty[st]);
+                tc_commit(&bar->mma_done);
             }
         }
     } else {
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        const uint32_t tS = tmem + lane_off, tP = tmem + lane_off + kT;
         const int64_t si = ((int64_t)b * H + hh) * S + qt * kT + r;
-        RowGrad g;
-        g.sl2 = scale * kLog2e;
-        g.scale = scale;
-        g.lse2 = lse[si] * kLog2e;
-        g.d = D[si];
+        const float sl2 = scale * kLog2e;
+        const float lse2 = lse[si] * kLog2e, d = D[si];
         for (int kt = 0; kt < nkt; ++kt) {
             mb_wait(&bar->s_full, kt & 1);
-            if (kt > 0) mb_wait(&bar->ds_free, (kt - 1) & 1);  // dQ MMA of kt-1 read dS
             tc_fence_after();
             const bool diag = kt == qt;
 #pragma unroll 1
             for (int c = 0; c < kT; c += 16) {
-                float sv[16], dpv[16], p[16], d[16];
-                tmem_ld16_nowait(tmem + lane_off + c, sv);
-                tmem_ld16_nowait(tmem + lane_off + kT + c, dpv);
+                float sv[16], dpv[16];
+                tmem_ld16_nowait(tS + c, sv);
+                tmem_ld16_nowait(tP + c, dpv);
                 tmem_wait_ld();
-                p_ds_chunk(g, sv, dpv, diag, r, c, p, d);
-                store_row16(sDS, r, c, d);
+                uint32_t dk8[8];
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    float p0 = ex2(fmaf(sv[j], sl2, -lse2));
+                    float p1 = ex2(fmaf(sv[j + 1], sl2, -lse2));
+                    if (diag && c + j > r) p0 = 0.f;
+                    if (diag && c + j + 1 > r) p1 = 0.f;
+                    dk8[j / 2] = pack2(p0 * (dpv[j] - d) * scale, p1 * (dpv[j + 1] - d) * scale);
+                }
+                tmem_st8u(tP + c / 2, dk8);  // dS over dP columns already read
             }
-            tc_fence_before();
-            mb_arrive(&bar->st_free);
-            fence_async_smem();
+            tmem_wait_st();
             tc_fence_before();
             mb_arrive(&bar->ds_full);
         }
-        mb_wait(&bar->ds_free, (nkt - 1) & 1);
+        mb_wait(&bar->mma_done, (nkt - 1) & 1);
         tc_fence_after();
         bf16* dst = dq + ((int64_t)b * S + qt * kT + r) * lddq + col;
 #pragma unroll 1
@@ -626,6 +779,12 @@ void set_smem(K kern, size_t bytes) {
 
 }  // namespace
 
+#ifdef EE_TRACE
+extern "C" int ee_trace_attn_fwd(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_fwd_tl, sizeof(g_fwd_tl));
+}
+#endif
+
 extern "C" int ee_attn_train_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk,
                                  const void* v, int64_t ldv, int64_t B, int64_t S, int64_t H,
                                  void* out, int64_t ldo, float* lse, void* stream) {
@@ -641,8 +800,8 @@ extern "C" int ee_attn_train_fwd(const void* q, int64_t ldq, const void* k, int6
         (rc = make_tmap_bf16_ld(&tv, v, rows, cols, ldv, kT)))
         return rc;
     set_smem(k_attn_fwd, kFwdSmem);
-    const dim3 grid((unsigned)(S / kT), (unsigned)H, (unsigned)B);
-    k_attn_fwd<<<grid, kAttnThreads, kFwdSmem, as_stream(stream)>>>(
+    const dim3 grid((unsigned)((S / kT + 1) / 2), (unsigned)H, (unsigned)B);
+    k_attn_fwd<<<grid, kFwdThreads, kFwdSmem, as_stream(stream)>>>(
         tq, tk, tv, (int)S, (int)H, (bf16*)out, (int)ldo, lse, 1.0f / sqrtf((float)kDh));
     return ee_check_launch("attn_train_fwd");
 }
@@ -676,7 +835,7 @@ extern "C" int ee_attn_train_bwd(const void* q, int64_t ldq, const void* k, int6
     const float scale = 1.0f / sqrtf((float)kDh);
     const dim3 grid((unsigned)(S / kT), (unsigned)H, (unsigned)B);
     set_smem(k_attn_bwd_kv, kBwdKvSmem);
-    k_attn_bwd_kv<<<grid, kAttnThreads, kBwdKvSmem, s>>>(tq, tk, tv, tdo, (int)S, (int)H, lse, dsum,
+    k_attn_bwd_kv<<<grid, kBwdThreads, kBwdKvSmem, s>>>(tq, tk, tv, tdo, (int)S, (int)H, lse, dsum,
                                                           (bf16*)dk, (int)lddk, (bf16*)dv,
                                                           (int)lddv, scale);
     if ((rc = ee_check_launch("attn_train_bwd_kv"))) return rc;

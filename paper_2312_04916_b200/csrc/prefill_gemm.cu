@@ -53,7 +53,7 @@ k_prefill_gemm(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                int N, int m, int K, int splits, float* __restrict__ part) {
     using namespace tc;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = tc::align1024(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPStages * kPStageBytes);
     uint64_t* empty = full + kPStages;
     uint64_t* tfull = empty + kPStages;

@@ -42,6 +42,12 @@ struct Cfg {
 
 // ---- PTX wrappers -----------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// dynamic shared memory rounded up to 1024 B (SW128 atoms) by pointer
+// arithmetic on the shared array itself, so the compiler keeps the shared
+// address space (an integer round trip would turn every access generic)
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+    return p + ((1024u - (su32(p) & 1023u)) & 1023u);
+}
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
 }
@@ -202,7 +208,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
           int N, int K, Epi epi) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = align1024(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
@@ -423,7 +429,7 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     using C = Cfg2<BN>;
     constexpr int BM2 = 2 * BM;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = align1024(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * C::kStageBytes);
     uint64_t* empty = full + kStages2;
     uint64_t* tfull = empty + kStages2;
