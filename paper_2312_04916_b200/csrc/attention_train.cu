@@ -609,19 +609,22 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
 
 // ============================================================================
 // backward dQ: CTA = (q tile, head, batch); key tiles 0..qt through a 2-stage
-// K / V ring.  S = Q K_j^T, dP = dO V_j^T (M = q rows = TMEM lanes), dS =
-// P (dP - D) / sqrt(dh) written as bf16 pairs over the first 64 columns of
-// dP, dQ += dS K_j with A = dS straight from TMEM (K_j read MN-major).
-//   TMEM: S [0,128) dP [128,256) dQ [256,384)
+// K / V ring, each as two 64-key halves h handled by two warpgroups (h = 0:
+// warps 2-5, h = 1: warps 6-9) so one half's exponentials overlap the other
+// half's MMAs.  S_h = Q K_h^T, dP_h = dO V_h^T (M = q rows = TMEM lanes,
+// N = 64), dS_h = P_h (dP_h - D) / sqrt(dh) written as bf16 pairs over the
+// first 32 columns of dP_h, dQ += dS_h K_h with A = dS_h straight from TMEM
+// (K_h read MN-major).
+//   TMEM: S_0 [0,64) dP_0 [64,128) S_1 [128,192) dP_1 [192,256) dQ [256,384)
 // ============================================================================
 struct BwdQBars {
-    uint64_t qd_full, full[kBwdStages], empty[kBwdStages], s_full, ds_full, mma_done;
+    uint64_t qd_full, full[kBwdStages], empty[kBwdStages], s_full[2], ds_full[2], mma_done[2];
     uint32_t tmem;
 };
 constexpr size_t kBwdQSmem = 1024 + 2 * (size_t)kTile + 2 * kBwdStages * (size_t)kTile +
                              sizeof(BwdQBars) + 64;
 
-__global__ void __launch_bounds__(kAttnThreads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
 k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
              const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
              int S, int H, const float* __restrict__ lse, const float* __restrict__ D,
@@ -644,9 +647,11 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
             mb_init(&bar->full[i], 1);
             mb_init(&bar->empty[i], 1);
         }
-        mb_init(&bar->s_full, 1);
-        mb_init(&bar->ds_full, 128);
-        mb_init(&bar->mma_done, 1);
+        for (int h = 0; h < 2; ++h) {
+            mb_init(&bar->s_full[h], 1);
+            mb_init(&bar->ds_full[h], 128);
+            mb_init(&bar->mma_done[h], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) alloc_tmem512(&bar->tmem);
@@ -674,46 +679,68 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
         if (lane == 0) {
             mb_wait(&bar->qd_full, 0);
             const uint32_t q = su32(sQ), dO = su32(sDO);
-            for (int kt = 0; kt < nkt; ++kt) {
-                const int st = kt % kBwdStages;
-                const uint32_t k = su32(sKV + st * 2 * kTile), v = k + kTile;
-                mb_wait(&bar->full[st], (kt / kBwdStages) & 1);
-                if (kt > 0) mb_wait(&bar->mma_done, (kt - 1) & 1);  // dS(kt-1) consumed
-                tc_fence_after();
+            // S_h, dP_h of key tile kt: K-major B = rows [64h, 64h+64) of K / V
+            auto issue_s = [&](int kt, int h) {
+                const uint32_t k = su32(sKV + (kt % kBwdStages) * 2 * kTile) + h * kHalf * 128,
+                               v = k + kTile;
+                const uint32_t ts = tmem + h * kT;
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        tc_mma(tmem, desc_k(q, kb, kk), desc_k(k, kb, kk), kIdescKK, (kb | kk) != 0);
-                        tc_mma(tmem + kT, desc_k(dO, kb, kk), desc_k(v, kb, kk), kIdescKK,
+                        tc_mma(ts, desc_k(q, kb, kk), desc_k(k, kb, kk), kIdescKK64, (kb | kk) != 0);
+                        tc_mma(ts + kHalf, desc_k(dO, kb, kk), desc_k(v, kb, kk), kIdescKK64,
                                (kb | kk) != 0);
                     }
-                tc_commit(&bar->s_full);
-                mb_wait(&bar->ds_full, kt & 1);
-                tc_fence_after();
-                // dQ += dS K   (A = dS from TMEM, B = K tile MN-major, K = keys)
+                tc_commit(&bar->s_full[h]);
+            };
+            // dQ += dS_h K_h   (K = the half's 64 keys, K tile MN-major)
+            auto issue_acc = [&](int kt, int h) {
+                const uint32_t k = su32(sKV + (kt % kBwdStages) * 2 * kTile);
+                const uint32_t ts = tmem + h * kT;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 2 * kT, tmem + kT + kk * 8, desc_mn(k, kk), kIdescKM,
-                              (kt | kk) != 0);
-                tc_commit(&bar->empty[st]);
-                tc_commit(&bar->mma_done);
+                for (int kk = 0; kk < 4; ++kk)
+                    tc_mma_ts(tmem + 2 * kT, ts + kHalf + kk * 8, desc_mn(k, 4 * h + kk), kIdescKM,
+                              (kt | h | kk) != 0);
+                tc_commit(&bar->mma_done[h]);
+            };
+            mb_wait(&bar->full[0], 0);
+            tc_fence_after();
+            issue_s(0, 0);
+            issue_s(0, 1);
+            for (int kt = 0; kt < nkt; ++kt) {
+                const bool nxt = kt + 1 < nkt;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    mb_wait(&bar->ds_full[h], kt & 1);
+                    tc_fence_after();
+                    issue_acc(kt, h);
+                    if (h == 1) tc_commit(&bar->empty[kt % kBwdStages]);  // K / V of tile kt read
+                    if (nxt) {
+                        mb_wait(&bar->full[(kt + 1) % kBwdStages], ((kt + 1) / kBwdStages) & 1);
+                        mb_wait(&bar->mma_done[h], kt & 1);  // dS_h(kt) consumed
+                        tc_fence_after();
+                        issue_s(kt + 1, h);
+                    }
+                }
             }
         }
     } else {
+        const int hf = (warp - 2) >> 2;  // this warpgroup's key half
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        const uint32_t tS = tmem + lane_off, tP = tmem + lane_off + kT;
+        const uint32_t tS = tmem + lane_off + hf * kT, tP = tS + kHalf;
         const int64_t si = ((int64_t)b * H + hh) * S + qt * kT + r;
         const float sl2 = scale * kLog2e;
         const float lse2 = lse[si] * kLog2e, d = D[si];
+        const int c0 = hf * kHalf;  // key index of this half's first column
         for (int kt = 0; kt < nkt; ++kt) {
-            mb_wait(&bar->s_full, kt & 1);
+            mb_wait(&bar->s_full[hf], kt & 1);
             tc_fence_after();
             const bool diag = kt == qt;
 #pragma unroll 1
-            for (int c = 0; c < kT; c += 16) {
+            for (int c = 0; c < kHalf; c += 16) {
                 float sv[16], dpv[16];
                 tmem_ld16_nowait(tS + c, sv);
                 tmem_ld16_nowait(tP + c, dpv);
@@ -723,29 +750,32 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
                 for (int j = 0; j < 16; j += 2) {
                     float p0 = ex2(fmaf(sv[j], sl2, -lse2));
                     float p1 = ex2(fmaf(sv[j + 1], sl2, -lse2));
-                    if (diag && c + j > r) p0 = 0.f;
-                    if (diag && c + j + 1 > r) p1 = 0.f;
+                    if (diag && c0 + c + j > r) p0 = 0.f;
+                    if (diag && c0 + c + j + 1 > r) p1 = 0.f;
                     dk8[j / 2] = pack2(p0 * (dpv[j] - d) * scale, p1 * (dpv[j + 1] - d) * scale);
                 }
                 tmem_st8u(tP + c / 2, dk8);  // dS over dP columns already read
             }
             tmem_wait_st();
             tc_fence_before();
-            mb_arrive(&bar->ds_full);
+            mb_arrive(&bar->ds_full[hf]);
         }
-        mb_wait(&bar->mma_done, (nkt - 1) & 1);
-        tc_fence_after();
-        bf16* dst = dq + ((int64_t)b * S + qt * kT + r) * lddq + col;
+        if (hf == 0) {
+            mb_wait(&bar->mma_done[0], (nkt - 1) & 1);
+            mb_wait(&bar->mma_done[1], (nkt - 1) & 1);
+            tc_fence_after();
+            bf16* dst = dq + ((int64_t)b * S + qt * kT + r) * lddq + col;
 #pragma unroll 1
-        for (int c = 0; c < kDh; c += 16) {
-            float o[16];
-            tmem_ld16(tmem + lane_off + 2 * kT + c, o);
-            uint4 u0 = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]),
-                                  pack2(o[6], o[7]));
-            uint4 u1 = make_uint4(pack2(o[8], o[9]), pack2(o[10], o[11]), pack2(o[12], o[13]),
-                                  pack2(o[14], o[15]));
-            reinterpret_cast<uint4*>(dst + c)[0] = u0;
-            reinterpret_cast<uint4*>(dst + c)[1] = u1;
+            for (int c = 0; c < kDh; c += 16) {
+                float o[16];
+                tmem_ld16(tmem + lane_off + 2 * kT + c, o);
+                uint4 u0 = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]),
+                                      pack2(o[6], o[7]));
+                uint4 u1 = make_uint4(pack2(o[8], o[9]), pack2(o[10], o[11]), pack2(o[12], o[13]),
+                                      pack2(o[14], o[15]));
+                reinterpret_cast<uint4*>(dst + c)[0] = u0;
+                reinterpret_cast<uint4*>(dst + c)[1] = u1;
+            }
         }
     }
     tc_fence_before();
@@ -840,7 +870,7 @@ extern "C" int ee_attn_train_bwd(const void* q, int64_t ldq, const void* k, int6
                                                           (int)lddv, scale);
     if ((rc = ee_check_launch("attn_train_bwd_kv"))) return rc;
     set_smem(k_attn_bwd_q, kBwdQSmem);
-    k_attn_bwd_q<<<grid, kAttnThreads, kBwdQSmem, s>>>(tq, tk, tv, tdo, (int)S, (int)H, lse, dsum,
+    k_attn_bwd_q<<<grid, kBwdThreads, kBwdQSmem, s>>>(tq, tk, tv, tdo, (int)S, (int)H, lse, dsum,
                                                         (bf16*)dq, (int)lddq, scale);
     return ee_check_launch("attn_train_bwd_q");
 }
