@@ -380,12 +380,14 @@ int ee_rmsnorm_fwd(const void* x, int64_t n, int64_t h, const float* w, float ep
 
 /* gx (n, h) bf16 and gw (h) float32 (overwritten, or accumulated when
  * accumulate_gw != 0) from x, w, inv_rms and gy (n, h) bf16; gw is reduced in
- * a fixed order (deterministic).  Workspace: ee_workspace_bytes(
+ * a fixed order (deterministic).  gres (n, h) bf16, optional (NULL): a second
+ * gradient of x (the residual branch of a pre-norm block) added into gx in the
+ * same pass.  Workspace: ee_workspace_bytes(
  * EE_OP_RMSNORM_BWD, n, h, 0, 0, 0).  Replaces `rmsnorm_bwd`
  * (eepipe/_pykernels.py:44-49, eepipe/_ckernels.pyx:68-89). */
-int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rms, const void* gy, int64_t n,
-                   int64_t h, void* gx, float* gw, int accumulate_gw, void* ws, size_t ws_bytes,
-                   void* stream);
+int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rms, const void* gy,
+                   const void* gres, int64_t n, int64_t h, void* gx, float* gw, int accumulate_gw,
+                   void* ws, size_t ws_bytes, void* stream);
 
 /* ---- optimizer step (fused, multi-tensor) ----------------------------- */
 

@@ -112,8 +112,8 @@ SIGNATURES = {
                                c_void_p]),
     "ee_rmsnorm_fwd": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_float, c_void_p, c_void_p,
                                c_void_p]),
-    "ee_rmsnorm_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p,
-                               c_void_p, c_int, c_void_p, c_size_t, c_void_p]),
+    "ee_rmsnorm_bwd": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                               c_void_p, c_void_p, c_int, c_void_p, c_size_t, c_void_p]),
     "ee_mlp_up_gelu": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p,
                                c_void_p]),
     "ee_mlp_gelu_bwd": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p,

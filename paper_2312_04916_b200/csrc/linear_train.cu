@@ -30,7 +30,16 @@ struct EpiBf16 {
     bf16* out;
     const bf16* res;  // nullable
     int ld;
-    __device__ void begin_tile(int, int, int, bool) {}
+    // the half-row's residual (BN/2 bf16 = 256 B, two lines) is pulled into
+    // L1 before the accumulator chunks stream out of TMEM, so the per-chunk
+    // residual loads hit L1 instead of waiting on HBM one chunk at a time
+    __device__ void begin_tile(int row, int col0, int, bool valid) {
+        if (res && valid) {
+            const bf16* p = res + (int64_t)row * ld + col0;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 64));
+        }
+    }
     __device__ void end_tile(int, int, int, bool) {}
     __device__ void chunk(int row, int col, const float* v0, int nvalid) {
         float v[16];

@@ -76,10 +76,16 @@ k_rms_fwd(const bf16* __restrict__ x, const float* __restrict__ w, int64_t n, in
     if (lane == 0) inv_out[row] = inv;
 }
 
+// One warp per row.  The row's x and g chunks are loaded 8 per lane at a time
+// (8 independent 16-byte loads in flight) and kept in registers for the
+// second sweep when the row fits (h <= 2048); gres (optional) is a second
+// incoming gradient of x added to gx in the same pass (the residual branch of
+// a pre-norm block), so no separate element-wise add reads / writes (n, h).
+constexpr int kChunkRegs = 8;  // 16-byte chunks per lane held in registers
 __global__ void __launch_bounds__(kThreads)
 k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* __restrict__ inv_in,
-          const bf16* __restrict__ g, int64_t n, int h, bf16* __restrict__ gx,
-          float* __restrict__ gw_part) {
+          const bf16* __restrict__ g, const bf16* __restrict__ gres, int64_t n, int h,
+          bf16* __restrict__ gx, float* __restrict__ gw_part) {
     __shared__ float part[kWarps][256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
@@ -87,21 +93,38 @@ k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* 
     const int nvec = h / 8;
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
     const uint4* gr = reinterpret_cast<const uint4*>(g + row * h);
+    const bool held = nvec <= 32 * kChunkRegs;  // whole row in registers
+    uint4 xs[kChunkRegs], gs[kChunkRegs];
     float dot = 0.f, inv = 0.f;
     if (valid) {
         inv = inv_in[row];
-        for (int c = lane; c < nvec; c += 32) {
-            float xv[8], gv[8], ww[8];
-            unpack8(xr[c], xv);
-            unpack8(gr[c], gv);
-            load_w8(w, c, ww);
+        for (int c0 = 0; c0 < nvec; c0 += 32 * kChunkRegs) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) dot += gv[k] * ww[k] * xv[k];
+            for (int u = 0; u < kChunkRegs; ++u) {
+                const int c = c0 + u * 32 + lane;
+                if (c < nvec) {
+                    xs[u] = xr[c];
+                    gs[u] = gr[c];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kChunkRegs; ++u) {
+                const int c = c0 + u * 32 + lane;
+                if (c < nvec) {
+                    float xv[8], gv[8], ww[8];
+                    unpack8(xs[u], xv);
+                    unpack8(gs[u], gv);
+                    load_w8(w, c, ww);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) dot += gv[k] * ww[k] * xv[k];
+                }
+            }
         }
         dot = warp_sum(dot);
     }
     const float coef = inv * inv * inv * dot / (float)h;
     uint4* gxr = reinterpret_cast<uint4*>(gx + row * h);
+    const uint4* rr = gres ? reinterpret_cast<const uint4*>(gres + row * h) : nullptr;
     // second sweep, 256 columns per step for the whole CTA: gx, and this
     // CTA's weight-gradient partial (rows summed in warp order)
     for (int c0 = 0; c0 < nvec; c0 += 32) {
@@ -109,13 +132,33 @@ k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* 
         float gwv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (valid && c < nvec) {
             float xv[8], gv[8], ww[8], o[8];
-            unpack8(xr[c], xv);
-            unpack8(gr[c], gv);
+            const int u = c0 / 32;
+            if (held) {
+                // u < kChunkRegs: register-resident chunk (indices unrolled below)
+                uint4 xu = xs[0], gu = gs[0];
+#pragma unroll
+                for (int q = 1; q < kChunkRegs; ++q)
+                    if (q == u) {
+                        xu = xs[q];
+                        gu = gs[q];
+                    }
+                unpack8(xu, xv);
+                unpack8(gu, gv);
+            } else {
+                unpack8(xr[c], xv);
+                unpack8(gr[c], gv);
+            }
             load_w8(w, c, ww);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 o[k] = gv[k] * ww[k] * inv - xv[k] * coef;
                 gwv[k] = gv[k] * xv[k] * inv;
+            }
+            if (rr) {
+                float rv[8];
+                unpack8(rr[c], rv);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o[k] += rv[k];
             }
             gxr[c] = pack8(o);
         }
@@ -175,8 +218,8 @@ extern "C" int ee_rmsnorm_fwd(const void* x, int64_t n, int64_t h, const float* 
 }
 
 extern "C" int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rms, const void* gy,
-                              int64_t n, int64_t h, void* gx, float* gw, int accumulate_gw,
-                              void* ws, size_t ws_bytes, void* stream) {
+                              const void* gres, int64_t n, int64_t h, void* gx, float* gw,
+                              int accumulate_gw, void* ws, size_t ws_bytes, void* stream) {
     EE_REQUIRE(n >= 0 && h > 0 && h % 8 == 0, EE_ESHAPE, "rmsnorm_bwd: need h %% 8 == 0 (h=%lld)",
                (long long)h);
     EE_REQUIRE(ws_bytes >= rmsnorm_train_ws_bytes(n, h), EE_ESHAPE,
@@ -184,8 +227,8 @@ extern "C" int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rm
     cudaStream_t s = as_stream(stream);
     const int nparts = (int)((n + kWarps - 1) / kWarps);
     if (n > 0) {
-        k_rms_bwd<<<nparts, kThreads, 0, s>>>((const bf16*)x, w, inv_rms, (const bf16*)gy, n,
-                                              (int)h, (bf16*)gx, (float*)ws);
+        k_rms_bwd<<<nparts, kThreads, 0, s>>>((const bf16*)x, w, inv_rms, (const bf16*)gy,
+                                              (const bf16*)gres, n, (int)h, (bf16*)gx, (float*)ws);
         int rc;
         if ((rc = ee_check_launch("rmsnorm_bwd"))) return rc;
     }

@@ -289,15 +289,17 @@ def _linear_fwd(x2, w, res2=None):
     return out
 
 
-def _linear_dgrad(g2, w):
-    """(T, K) bf16 = g2 (T, N) @ w (K, N)^T (ee_linear_dgrad)."""
+def _linear_dgrad(g2, w, res2=None):
+    """(T, K) bf16 = g2 (T, N) @ w (K, N)^T [+ res2] (ee_linear_dgrad; the
+    addend is summed before the one rounding)."""
     torch = _torch()
     T, N = g2.shape
     K = w.shape[0]
     if not _OWN_LINEAR:
-        return g2 @ w.t()
+        return g2 @ w.t() if res2 is None else torch.addmm(res2, g2, w.t())
     out = torch.empty((T, K), dtype=g2.dtype, device=g2.device)
-    call("ee_linear_dgrad", ptr(g2), ptr(w), T, K, N, None, ptr(out), stream_ptr())
+    call("ee_linear_dgrad", ptr(g2), ptr(w), T, K, N, ptr(res2) if res2 is not None else None,
+         ptr(out), stream_ptr())
     return out
 
 
@@ -335,6 +337,48 @@ class _LinearFn:
                     gx = _linear_dgrad(g2, w).view(x.shape)
                     _wgrad_accum(x2, g2, ctx.acc)
                     return gx, None, None, (gy if ctx.has_res else None)
+
+            cls._fn = _F
+        return cls._fn
+
+
+class _QKVFn:
+    """q, k, v = h1 @ wq, h1 @ wk, h1 @ wv on the tcgen05 GEMM; the backward
+    chains the three input-gradient GEMMs through the residual epilogue
+    (dX = ((gq wq^T) + gk wk^T) + gv wv^T, one rounding per step, no
+    separate add kernels) and accumulates the three weight gradients into
+    their float32 sums (ee_wgrad_accum)."""
+
+    _fn = None
+
+    @classmethod
+    def get(cls):
+        if cls._fn is None:
+            torch = _torch()
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, x, wq, wk, wv, aq, ak, av):
+                    x2 = x.reshape(-1, x.shape[-1]).contiguous()
+                    ctx.save_for_backward(x2, wq, wk, wv)
+                    ctx.acc = (aq, ak, av)
+                    ctx.shape = x.shape
+                    return tuple(_linear_fwd(x2, w).view(*x.shape[:-1], w.shape[1])
+                                 for w in (wq, wk, wv))
+
+                @staticmethod
+                def backward(ctx, gq, gk, gv):
+                    x2, wq, wk, wv = ctx.saved_tensors
+                    gx = None
+                    for g, w, acc in zip((gq, gk, gv), (wq, wk, wv), ctx.acc):
+                        if g is None:
+                            continue
+                        g2 = g.reshape(-1, g.shape[-1]).to(x2.dtype).contiguous()
+                        gx = _linear_dgrad(g2, w, gx)
+                        _wgrad_accum(x2, g2, acc)
+                    if gx is not None:
+                        gx = gx.view(ctx.shape)
+                    return gx, None, None, None, None, None, None
 
             cls._fn = _F
         return cls._fn
@@ -603,12 +647,68 @@ class _RMSNormFn:
                     gw = torch.empty(h, dtype=torch.float32, device=x2.device)
                     ws = _workspace(x2.device, _lib.load().ee_workspace_bytes(
                         _lib.EE_OP_RMSNORM_BWD, n, h, 0, 0, 0), tag="rmsnorm")
-                    call("ee_rmsnorm_bwd", ptr(x2), ptr(wf), ptr(inv), ptr(gy2), n, h, ptr(gx),
-                         ptr(gw), 0, ptr(ws), ws.numel(), stream_ptr())
+                    call("ee_rmsnorm_bwd", ptr(x2), ptr(wf), ptr(inv), ptr(gy2), None, n, h,
+                         ptr(gx), ptr(gw), 0, ptr(ws), ws.numel(), stream_ptr())
                     return gx.view(gy.shape), gw.to(ctx.wdtype), None
 
             cls._fn = _F
         return cls._fn
+
+
+class _NormForkFn:
+    """(RMSNorm(x), x) of a pre-norm block: the second output is x itself for
+    the block's residual branch, so the backward receives both gradients of x
+    and `ee_rmsnorm_bwd` adds the residual one into gx in the same pass
+    (no separate element-wise add over the (T, h) rows)."""
+
+    _fn = None
+
+    @classmethod
+    def get(cls):
+        if cls._fn is None:
+            torch = _torch()
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, x, w, eps):
+                    h = x.shape[-1]
+                    x2 = x.reshape(-1, h).contiguous()
+                    wf = w.detach().float().contiguous()
+                    y = torch.empty_like(x2)
+                    inv = torch.empty(x2.shape[0], dtype=torch.float32, device=x.device)
+                    call("ee_rmsnorm_fwd", ptr(x2), x2.shape[0], h, ptr(wf), float(eps), ptr(y),
+                         ptr(inv), stream_ptr())
+                    ctx.save_for_backward(x2, wf, inv)
+                    ctx.wdtype = w.dtype
+                    return y.view(x.shape), x.view(x.shape)
+
+                @staticmethod
+                def backward(ctx, gy, gres):
+                    x2, wf, inv = ctx.saved_tensors
+                    n, h = x2.shape
+                    gy2 = gy.reshape(n, h).to(torch.bfloat16).contiguous()
+                    gr2 = (gres.reshape(n, h).to(torch.bfloat16).contiguous()
+                           if gres is not None else None)
+                    gx = torch.empty_like(x2)
+                    gw = torch.empty(h, dtype=torch.float32, device=x2.device)
+                    ws = _workspace(x2.device, _lib.load().ee_workspace_bytes(
+                        _lib.EE_OP_RMSNORM_BWD, n, h, 0, 0, 0), tag="rmsnorm")
+                    call("ee_rmsnorm_bwd", ptr(x2), ptr(wf), ptr(inv), ptr(gy2),
+                         ptr(gr2) if gr2 is not None else None, n, h, ptr(gx), ptr(gw), 0,
+                         ptr(ws), ws.numel(), stream_ptr())
+                    return gx.view(gy.shape), gw.to(ctx.wdtype), None
+
+            cls._fn = _F
+        return cls._fn
+
+
+def rmsnorm_fork(x, w, eps=NORM_EPS):
+    """(rmsnorm(x, w), x) with both gradients of x joined inside the fused
+    backward (bf16 on the GPU); elsewhere plain (rmsnorm(x, w), x)."""
+    torch = _torch()
+    if x.dtype == torch.bfloat16 and x.is_cuda and x.shape[-1] % 8 == 0:
+        return _NormForkFn.get().apply(x, w, eps)
+    return rmsnorm(x, w, eps), x
 
 
 def rmsnorm(x, w, eps=NORM_EPS):
@@ -699,13 +799,28 @@ def causal_attention(q, k, v, num_heads):
     return a.transpose(1, 2).reshape(B, S, h)
 
 
+def _qkv(params, prefix, h1):
+    """q, k, v projections; in mixed mode one autograd node (_QKVFn: chained
+    input-gradient GEMMs, no add kernels)."""
+    acc = getattr(params, "main_grads", None)
+    names = [f"{prefix}.{w}" for w in ("wq", "wk", "wv")]
+    ws = [params[n] for n in names]
+    if (acc is not None and all(n in acc for n in names) and _OWN_LINEAR
+            and all(w.dtype == h1.dtype and w.shape[0] % 8 == 0 and w.shape[1] % 8 == 0
+                    for w in ws)):
+        return _QKVFn.get().apply(h1, *ws, *(acc[n] for n in names))
+    return tuple(_matmul(params, n, h1) for n in names)
+
+
 def run_layer(params, prefix, x, num_heads):
-    """One pre-norm block (`eepipe/model.py:207-216`)."""
-    h1 = rmsnorm(x, params[f"{prefix}.attn_norm"])
-    q, k, v = (_matmul(params, f"{prefix}.{w}", h1) for w in ("wq", "wk", "wv"))
+    """One pre-norm block (`eepipe/model.py:207-216`).  The norms fork x so
+    that the residual branch's gradient joins the norm's inside its backward
+    kernel."""
+    h1, x = rmsnorm_fork(x, params[f"{prefix}.attn_norm"])
+    q, k, v = _qkv(params, prefix, h1)
     a = causal_attention(q, k, v, num_heads)
     x = _matmul(params, f"{prefix}.wo", a, residual=x)
-    h2 = rmsnorm(x, params[f"{prefix}.mlp_norm"])
+    h2, x = rmsnorm_fork(x, params[f"{prefix}.mlp_norm"])
     return _mlp(params, prefix, h2, residual=x)
 
 
