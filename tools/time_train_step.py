@@ -64,4 +64,5 @@ def train_step_bench(M=8, mb=2, seq=2048, steps=3, warmup=2, stages=1):
 
 if __name__ == "__main__":
     M = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-    print(train_step_bench(M=M))
+    mb = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    print(train_step_bench(M=M, mb=mb))
