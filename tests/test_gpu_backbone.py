@@ -92,3 +92,28 @@ def test_linear_fwd_dgrad_match_fp32(T, K, N):
     call("ee_linear_fwd", ptr(x), ptr(w), T, K, N, None, ptr(y0), stream_ptr())
     torch.cuda.synchronize()
     assert _rel(y0.double().cpu().numpy(), (x.float() @ w.float()).double().cpu().numpy()) < 1e-2
+
+
+@pytest.mark.parametrize("n,h", [(37, 264), (4096, 2048), (1000, 5120)])
+def test_rmsnorm_fork_joins_residual_gradient(n, h):
+    """`rmsnorm_fork` (ee_rmsnorm_bwd with gres): the residual branch's
+    gradient of x is added inside the RMSNorm backward kernel.  x.grad must
+    equal the float64 oracle's rmsnorm_bwd + the residual gradient (1e-2,
+    bf16 output), and the weight gradient must not change (1e-4)."""
+    import torch
+    from paper_2312_04916_b200.training import rmsnorm_fork
+    rng = np.random.default_rng(n + h)
+    x = torch.tensor(rng.normal(size=(n, h)) * 2.0, dtype=torch.bfloat16, device="cuda")
+    w = torch.tensor(rng.normal(1.0, 0.2, size=h), dtype=torch.float32, device="cuda")
+    g = torch.tensor(rng.normal(size=(n, h)), dtype=torch.bfloat16, device="cuda")
+    gr = torch.tensor(rng.normal(size=(n, h)), dtype=torch.bfloat16, device="cuda")
+    xr = x.clone().requires_grad_()
+    wr = w.clone().requires_grad_()
+    y, xa = rmsnorm_fork(xr, wr)
+    torch.autograd.backward([y, xa], [g, gr])
+    x64, w64, g64 = (t.double().cpu().numpy() for t in (x, w, g))
+    _, rinv = O.rmsnorm_fwd(x64, w64)
+    rgx, rgw = O.rmsnorm_bwd(x64, w64, rinv, g64)
+    rgx = rgx + gr.double().cpu().numpy()
+    assert _rel(xr.grad.double().cpu().numpy(), rgx) < 1e-2
+    assert _rel(wr.grad.double().cpu().numpy(), rgw) < 1e-4
