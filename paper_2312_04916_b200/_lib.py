@@ -14,7 +14,8 @@ import os
 from .errors import ConfigError, NonFiniteError, ShapeError, TokenError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libee.so")
+# EE_LIB_PATH (profiling A/B only): load another in-tree build of the same ABI
+LIB_PATH = os.environ.get("EE_LIB_PATH") or os.path.join(HERE, "libee.so")
 
 EE_OK, EE_ESHAPE, EE_ETOKEN, EE_ENONFINITE, EE_ECONFIG, EE_ECUDA = range(6)
 EE_F32, EE_BF16, EE_BF16_TILED = 0, 1, 2

@@ -211,7 +211,8 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {
+            const bool leader = elect_one();
             // ---------------- MMA issuer ----------------
             mb_wait(&bar->q_full, 0);
             tc_fence_after();
@@ -226,9 +227,9 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        tc_mma(tmem + t * kT, desc_k(q, kb, k), desc_k(kk, kb, k), kIdescKK,
+                        if (leader) tc_mma(tmem + t * kT, desc_k(q, kb, k), desc_k(kk, kb, k), kIdescKK,
                                (kb | k) != 0);
-                tc_commit(&bar->s_full[t]);
+                if (leader) tc_commit(&bar->s_full[t]);
                 FWD_TL(0, t, j);
             };
             auto issue_pv = [&](int t, int j) {  // O_t += P_t V(j)
@@ -237,15 +238,15 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        tc_mma(tmem + (2 + t) * kT, desc_k(p, kb, k), desc_mn(v, kb * 4 + k), kIdescKM,
+                        if (leader) tc_mma(tmem + (2 + t) * kT, desc_k(p, kb, k), desc_mn(v, kb * 4 + k), kIdescKM,
                                (j | kb | k) != 0);
-                tc_commit(&bar->o_done[t]);
+                if (leader) tc_commit(&bar->o_done[t]);
                 FWD_TL(1, t, j);
             };
             wait_full(0);
             issue_s(0, 0);
             if (nb > 0) issue_s(1, 0);
-            tc_commit(&bar->empty[slot(0)]);
+            if (leader) tc_commit(&bar->empty[slot(0)]);
             for (int j = 0; j < na; ++j) {
                 const bool nxt = j + 1 < na, bnow = j < nb, bnxt = j + 1 < nb;
                 if (nxt) {
@@ -263,13 +264,13 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
                     tc_fence_after();
                     issue_s(1, j + 1);
                 }
-                if (nxt) tc_commit(&bar->empty[slot(2 * j + 2)]);  // K(j+1) read by both S
+                if (nxt) if (leader) tc_commit(&bar->empty[slot(2 * j + 2)]);  // K(j+1) read by both S
                 if (bnow) {
                     mb_wait(&bar->p_full[1], j & 1);
                     tc_fence_after();
                     issue_pv(1, j);
                 }
-                tc_commit(&bar->empty[slot(2 * j + 1)]);  // V(j) read by both PV
+                if (leader) tc_commit(&bar->empty[slot(2 * j + 1)]);  // V(j) read by both PV
             }
         }
     } else {
@@ -479,7 +480,8 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {
+            const bool leader = elect_one();
             mb_wait(&bar->kv_full, 0);
             tc_fence_after();
             const uint32_t k = su32(sK), v = su32(sV);
@@ -492,11 +494,11 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        tc_mma(ts, desc_k(k, kb, kk), desc_k(q, kb, kk), kIdescKK64, (kb | kk) != 0);
-                        tc_mma(ts + kHalf, desc_k(v, kb, kk), desc_k(dO, kb, kk), kIdescKK64,
+                        if (leader) tc_mma(ts, desc_k(k, kb, kk), desc_k(q, kb, kk), kIdescKK64, (kb | kk) != 0);
+                        if (leader) tc_mma(ts + kHalf, desc_k(v, kb, kk), desc_k(dO, kb, kk), kIdescKK64,
                                (kb | kk) != 0);
                     }
-                tc_commit(&bar->s_full[h]);
+                if (leader) tc_commit(&bar->s_full[h]);
                 FWD_TL(0, h, i);
             };
             // dV += P_h^T dO_h, dK += dS_h^T Q_h  (K = the half's 64 q rows)
@@ -506,12 +508,12 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
                 const uint32_t ts = tmem + h * kT;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    tc_mma_ts(tmem + 2 * kT, ts + kk * 8, desc_mn(dO, 4 * h + kk), kIdescKM,
+                    if (leader) tc_mma_ts(tmem + 2 * kT, ts + kk * 8, desc_mn(dO, 4 * h + kk), kIdescKM,
                               (i | h | kk) != 0);
-                    tc_mma_ts(tmem + 3 * kT, ts + kHalf + kk * 8, desc_mn(q, 4 * h + kk), kIdescKM,
+                    if (leader) tc_mma_ts(tmem + 3 * kT, ts + kHalf + kk * 8, desc_mn(q, 4 * h + kk), kIdescKM,
                               (i | h | kk) != 0);
                 }
-                tc_commit(&bar->mma_done[h]);
+                if (leader) tc_commit(&bar->mma_done[h]);
                 FWD_TL(1, h, i);
             };
             mb_wait(&bar->full[0], 0);
@@ -525,7 +527,7 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
                     mb_wait(&bar->p_full[h], i & 1);
                     tc_fence_after();
                     issue_acc(i, h);
-                    if (h == 1) tc_commit(&bar->empty[i % kBwdStages]);  // Q / dO of tile i read
+                    if (h == 1) if (leader) tc_commit(&bar->empty[i % kBwdStages]);  // Q / dO of tile i read
                     if (nxt) {
                         mb_wait(&bar->full[(i + 1) % kBwdStages], ((i + 1) / kBwdStages) & 1);
                         mb_wait(&bar->mma_done[h], i & 1);  // P_h^T / dS_h^T(i) consumed
@@ -552,29 +554,50 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
             if (threadIdx.x == 64 + 128 * hf) FWD_TL(2, hf, i);
             const bool diag = i == 0;  // q tile == key tile: q index < key r is masked
             const int c0 = hf * kHalf;   // q index of this half's first column
-#pragma unroll 1
-            for (int c = 0; c < kHalf; c += 16) {
-                float sv[16], dpv[16];
-                tmem_ld16_nowait(tS + c, sv);
-                tmem_ld16_nowait(tP + c, dpv);
-                tmem_wait_ld();
+            {   // this half's lse -> lse * log2(e) and D -> D / sqrt(dh), in place
+                // (one multiply per column instead of one per element)
+                const int tw = threadIdx.x - 64 - 128 * hf;
+                if (tw < kHalf) {
+                    float* l = const_cast<float*>(sLse) + tw;
+                    float* d = const_cast<float*>(sD) + tw;
+                    *l *= kLog2e;
+                    *d *= scale;
+                }
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + hf) : "memory");
+            }
+            float sv[2][16], dpv[2][16];
+            tmem_ld16_nowait(tS, sv[0]);
+            tmem_ld16_nowait(tP, dpv[0]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int cc = 0; cc < kHalf / 16; ++cc) {
+                const int c = cc * 16, cur = cc & 1;
+                if (cc + 1 < kHalf / 16) {  // next chunk's S^T / dP^T in flight meanwhile
+                    tmem_ld16_nowait(tS + c + 16, sv[cur ^ 1]);
+                    tmem_ld16_nowait(tP + c + 16, dpv[cur ^ 1]);
+                }
                 uint32_t pk[8], dk8[8];
 #pragma unroll
-                for (int j = 0; j < 16; j += 2) {
-                    const float4 l4 = *reinterpret_cast<const float4*>(sLse + c + (j & ~3));
-                    const float4 d4 = *reinterpret_cast<const float4*>(sD + c + (j & ~3));
-                    const float la = (j & 2) ? l4.z : l4.x, lb = (j & 2) ? l4.w : l4.y;
-                    const float da = (j & 2) ? d4.z : d4.x, db = (j & 2) ? d4.w : d4.y;
-                    float p0 = ex2(fmaf(sv[j], sl2, -la * kLog2e));
-                    float p1 = ex2(fmaf(sv[j + 1], sl2, -lb * kLog2e));
-                    if (diag && c0 + c + j < r) p0 = 0.f;
-                    if (diag && c0 + c + j + 1 < r) p1 = 0.f;
-                    pk[j / 2] = pack2(p0, p1);
-                    dk8[j / 2] = pack2(p0 * (dpv[j] - da) * scale, p1 * (dpv[j + 1] - db) * scale);
+                for (int j = 0; j < 16; j += 4) {
+                    const float4 l4 = *reinterpret_cast<const float4*>(sLse + c + j);
+                    const float4 d4 = *reinterpret_cast<const float4*>(sD + c + j);
+                    const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+                    float pe[4], de[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        pe[e] = ex2(fmaf(sv[cur][j + e], sl2, -lv[e]));
+                        if (diag && c0 + c + j + e < r) pe[e] = 0.f;
+                        de[e] = pe[e] * fmaf(dpv[cur][j + e], scale, -dv4[e]);
+                    }
+                    pk[j / 2] = pack2(pe[0], pe[1]);
+                    pk[j / 2 + 1] = pack2(pe[2], pe[3]);
+                    dk8[j / 2] = pack2(de[0], de[1]);
+                    dk8[j / 2 + 1] = pack2(de[2], de[3]);
                 }
                 // P^T over S^T columns [c/2, c/2 + 8), dS^T over dP^T's (already read)
                 tmem_st8u(tS + c / 2, pk);
                 tmem_st8u(tP + c / 2, dk8);
+                tmem_wait_ld();
             }
             tmem_wait_st();
             tc_fence_before();
@@ -676,7 +699,8 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {
+            const bool leader = elect_one();
             mb_wait(&bar->qd_full, 0);
             const uint32_t q = su32(sQ), dO = su32(sDO);
             // S_h, dP_h of key tile kt: K-major B = rows [64h, 64h+64) of K / V
@@ -688,11 +712,11 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        tc_mma(ts, desc_k(q, kb, kk), desc_k(k, kb, kk), kIdescKK64, (kb | kk) != 0);
-                        tc_mma(ts + kHalf, desc_k(dO, kb, kk), desc_k(v, kb, kk), kIdescKK64,
+                        if (leader) tc_mma(ts, desc_k(q, kb, kk), desc_k(k, kb, kk), kIdescKK64, (kb | kk) != 0);
+                        if (leader) tc_mma(ts + kHalf, desc_k(dO, kb, kk), desc_k(v, kb, kk), kIdescKK64,
                                (kb | kk) != 0);
                     }
-                tc_commit(&bar->s_full[h]);
+                if (leader) tc_commit(&bar->s_full[h]);
             };
             // dQ += dS_h K_h   (K = the half's 64 keys, K tile MN-major)
             auto issue_acc = [&](int kt, int h) {
@@ -700,9 +724,9 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
                 const uint32_t ts = tmem + h * kT;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    tc_mma_ts(tmem + 2 * kT, ts + kHalf + kk * 8, desc_mn(k, 4 * h + kk), kIdescKM,
+                    if (leader) tc_mma_ts(tmem + 2 * kT, ts + kHalf + kk * 8, desc_mn(k, 4 * h + kk), kIdescKM,
                               (kt | h | kk) != 0);
-                tc_commit(&bar->mma_done[h]);
+                if (leader) tc_commit(&bar->mma_done[h]);
             };
             mb_wait(&bar->full[0], 0);
             tc_fence_after();
@@ -715,7 +739,7 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
                     mb_wait(&bar->ds_full[h], kt & 1);
                     tc_fence_after();
                     issue_acc(kt, h);
-                    if (h == 1) tc_commit(&bar->empty[kt % kBwdStages]);  // K / V of tile kt read
+                    if (h == 1) if (leader) tc_commit(&bar->empty[kt % kBwdStages]);  // K / V of tile kt read
                     if (nxt) {
                         mb_wait(&bar->full[(kt + 1) % kBwdStages], ((kt + 1) / kBwdStages) & 1);
                         mb_wait(&bar->mma_done[h], kt & 1);  // dS_h(kt) consumed
@@ -733,28 +757,35 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
         const uint32_t tS = tmem + lane_off + hf * kT, tP = tS + kHalf;
         const int64_t si = ((int64_t)b * H + hh) * S + qt * kT + r;
         const float sl2 = scale * kLog2e;
-        const float lse2 = lse[si] * kLog2e, d = D[si];
+        const float lse2 = lse[si] * kLog2e, ds_off = D[si] * scale;
         const int c0 = hf * kHalf;  // key index of this half's first column
         for (int kt = 0; kt < nkt; ++kt) {
             mb_wait(&bar->s_full[hf], kt & 1);
             tc_fence_after();
             const bool diag = kt == qt;
-#pragma unroll 1
-            for (int c = 0; c < kHalf; c += 16) {
-                float sv[16], dpv[16];
-                tmem_ld16_nowait(tS + c, sv);
-                tmem_ld16_nowait(tP + c, dpv);
-                tmem_wait_ld();
+            float sv[2][16], dpv[2][16];
+            tmem_ld16_nowait(tS, sv[0]);
+            tmem_ld16_nowait(tP, dpv[0]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int cc = 0; cc < kHalf / 16; ++cc) {
+                const int c = cc * 16, cur = cc & 1;
+                if (cc + 1 < kHalf / 16) {
+                    tmem_ld16_nowait(tS + c + 16, sv[cur ^ 1]);
+                    tmem_ld16_nowait(tP + c + 16, dpv[cur ^ 1]);
+                }
                 uint32_t dk8[8];
 #pragma unroll
                 for (int j = 0; j < 16; j += 2) {
-                    float p0 = ex2(fmaf(sv[j], sl2, -lse2));
-                    float p1 = ex2(fmaf(sv[j + 1], sl2, -lse2));
+                    float p0 = ex2(fmaf(sv[cur][j], sl2, -lse2));
+                    float p1 = ex2(fmaf(sv[cur][j + 1], sl2, -lse2));
                     if (diag && c0 + c + j > r) p0 = 0.f;
                     if (diag && c0 + c + j + 1 > r) p1 = 0.f;
-                    dk8[j / 2] = pack2(p0 * (dpv[j] - d) * scale, p1 * (dpv[j + 1] - d) * scale);
+                    dk8[j / 2] = pack2(p0 * fmaf(dpv[cur][j], scale, -ds_off),
+                                       p1 * fmaf(dpv[cur][j + 1], scale, -ds_off));
                 }
                 tmem_st8u(tP + c / 2, dk8);  // dS over dP columns already read
+                tmem_wait_ld();
             }
             tmem_wait_st();
             tc_fence_before();

@@ -127,8 +127,9 @@ k_prefill_gemm(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer ----------------
+        {
+            // ---------------- MMA issuer (warp-uniform, one elected lane issues) ----------------
+            const bool leader = elect_one();
             constexpr uint32_t idesc = idesc_bf16(PBM, PBN, false, false);
             int s = 0;
             uint32_t ph = 0;
@@ -148,15 +149,16 @@ k_prefill_gemm(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                     const uint32_t b0 = a0 + kPABytes;
 #pragma unroll
                     for (int k = 0; k < PBK / 16; ++k)
-                        tc_mma(d, op_desc<false>(a0, k), op_desc<false>(b0, k), idesc,
-                               (kb > k0 || k > 0) ? 1u : 0u);
-                    tc_commit(&empty[s]);
+                        if (leader)
+                            tc_mma(d, op_desc<false>(a0, k), op_desc<false>(b0, k), idesc,
+                                   (kb > k0 || k > 0) ? 1u : 0u);
+                    if (leader) tc_commit(&empty[s]);
                     if (++s == kPStages) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                tc_commit(&tfull[acc]);
+                if (leader) tc_commit(&tfull[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     aph ^= 1;

@@ -42,6 +42,20 @@ struct Cfg {
 
 // ---- PTX wrappers -----------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// one elected lane of a converged warp.  The MMA-issuing warps run their
+// loops warp-uniformly and only the elected lane issues tcgen05.mma /
+// commit: the operand descriptors then live in uniform registers (no
+// per-MMA R2UR conversion from a single divergent lane).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(p));
+    return p != 0;
+}
+
 // dynamic shared memory rounded up to 1024 B (SW128 atoms) by pointer
 // arithmetic on the shared array itself, so the compiler keeps the shared
 // address space (an integer round trip would turn every access generic)
@@ -277,8 +291,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer ----------------
+        {
+            // ---------------- MMA issuer (warp-uniform, one elected lane issues) ----------------
+            const bool leader = elect_one();
             constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
             int s = 0;
             uint32_t ph = 0;
@@ -295,14 +310,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtens
                     const uint32_t b0 = a0 + kABytes;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        tc_mma(d, op_desc<A_MN>(a0, k), op_desc<B_MN>(b0, k), idesc, (kb | k) != 0);
-                    tc_commit(&empty[s]);  // smem stage free once these MMAs completed
+                        if (leader) tc_mma(d, op_desc<A_MN>(a0, k), op_desc<B_MN>(b0, k), idesc, (kb | k) != 0);
+                    if (leader) tc_commit(&empty[s]);  // smem stage free once these MMAs completed
                     if (++s == kStages) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                if (leader) tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
                 if (++acc == 2) {
                     acc = 0;
                     aph ^= 1;
@@ -512,8 +527,9 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
-            // ---------------- MMA issuer (leader CTA only) ----------------
+        if (rank == 0) {
+            // ---------------- MMA issuer (leader CTA only; warp-uniform, one lane issues) ----------------
+            const bool leader = elect_one();
             constexpr uint32_t idesc = idesc_bf16(BM2, BN, A_MN, B_MN);
             int s = 0;
             uint32_t ph = 0;
@@ -532,15 +548,16 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                     const uint32_t b0 = a0 + kABytes;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        tc_mma2(d, op_desc<A_MN>(a0, k), op_desc<B_MN>(b0, k), idesc,
-                                (kb > k0 || k > 0) ? 1u : 0u);
-                    tc_commit2(&empty[s]);  // both CTAs' stage s free once these MMAs completed
+                        if (leader)
+                            tc_mma2(d, op_desc<A_MN>(a0, k), op_desc<B_MN>(b0, k), idesc,
+                                    (kb > k0 || k > 0) ? 1u : 0u);
+                    if (leader) tc_commit2(&empty[s]);  // both CTAs' stage s free once these MMAs completed
                     if (++s == kStages2) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                tc_commit2(&tfull[acc]);  // both CTAs' accumulators ready
+                if (leader) tc_commit2(&tfull[acc]);  // both CTAs' accumulators ready
                 if (++acc == 2) {
                     acc = 0;
                     aph ^= 1;
