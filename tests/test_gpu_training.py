@@ -137,3 +137,58 @@ def test_mlp_gelu_fused_gemms_match_torch(T, h, N):
     assert rel(pre, ref_pre) < 1e-2
     assert rel(act, ref_act) < 1e-2
     assert rel(dpre, p.grad) < 1e-2
+
+
+def test_mixed_precision_own_kernels_match_fp32_reference():
+    """The mixed-precision training path that the C2 bench times (bf16 leaves,
+    float32 gradient sums; every backbone linear, the causal attention
+    (head_dim 128, S = 128), the fused RMSNorm / residual-gradient kernels and
+    the fused exit heads are own sm_100a kernels) against a float32 torch
+    autograd reference of the SAME bf16-rounded weights.  Per-tensor
+    tolerance 3e-2 relative (Frobenius): bf16 activations between kernels,
+    float32 accumulation -- tight enough that a wrong scale factor on any
+    tensor (>= 2x) fails.  Per-exit losses within 1e-2."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2312_04916_b200.training import NORM_EPS, TrainModel, single_device_gradients
+    cfg = ModelConfig(2, 256, 2, 512, 256, exits=(ExitSpec(1, "minimalistic", 0.3),))
+    m = build_model(cfg, 5)
+    batch = np.random.default_rng(7).integers(0, 512, size=(2, 129))
+    weights = [0.3, 1.0]
+    tm = TrainModel(m, master_dtype=torch.float32)
+    grads, per_exit = single_device_gradients(tm, batch, weights, 2)
+
+    P = {n: p.detach().float().clone().requires_grad_() for n, p in tm.params.items()}
+
+    def rms(x, w):
+        return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + NORM_EPS) * w
+
+    tok = torch.as_tensor(batch, device="cuda")
+    inp, tgt = tok[:, :-1], tok[:, 1:]
+    B, S = inp.shape
+    x = P["tok_emb"][inp] + P["pos_emb"][torch.arange(S, device="cuda")][None]
+    taps = {}
+    for i in range(1, cfg.num_layers + 1):
+        pre = f"layer{i}"
+        h1 = rms(x, P[f"{pre}.attn_norm"])
+        split = lambda t: t.view(B, S, cfg.num_heads, -1).transpose(1, 2)  # noqa: E731
+        q, k, v = (split(h1 @ P[f"{pre}.{w}"]) for w in ("wq", "wk", "wv"))
+        a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        x = x + a.transpose(1, 2).reshape(B, S, -1) @ P[f"{pre}.wo"]
+        h2 = rms(x, P[f"{pre}.mlp_norm"])
+        x = x + F.gelu(h2 @ P[f"{pre}.w1"]) @ P[f"{pre}.w2"]
+        taps[i] = x
+    total, ref_exit = 0.0, {}
+    for hd, w in zip(tm.heads, weights):
+        xi = taps[hd.layer_index]
+        if "norm" in hd.param_names:
+            xi = rms(xi, P[hd.param_names["norm"]])
+        logits = xi @ P[hd.param_names["out"]].t()
+        ce = F.cross_entropy(logits.reshape(-1, logits.shape[-1]), tgt.reshape(-1))
+        ref_exit[hd.key] = float(ce.detach())
+        total = total + w * ce
+    total.backward()
+    for key, v in ref_exit.items():
+        assert per_exit[key] == pytest.approx(v, rel=1e-2), key
+    for name, g in grads.items():
+        assert _rel(g.float().cpu().numpy(), P[name].grad.double().cpu().numpy()) < 3e-2, name
