@@ -263,7 +263,8 @@ def model_from_arrays(config: ModelConfig, arrays: dict) -> EarlyExitModel:
         if name not in arrays:
             raise ConfigError(f"missing parameter {name}")
         arr = arrays[name]
-        arr = getattr(arr, "data", arr)
+        if not isinstance(arr, np.ndarray):  # a reference Tensor / Param (ndarray.data is a buffer)
+            arr = getattr(arr, "data", arr)
         if tuple(arr.shape) != tuple(shape):
             raise ConfigError(f"parameter {name} has shape {tuple(arr.shape)}, expected {shape}")
         params[name] = Param(arr)

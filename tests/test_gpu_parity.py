@@ -339,3 +339,33 @@ def test_tiled_modes_bitwise_equal_long_context(prompt_len, max_new, max_deferre
         assert reco.tokens == pipe.tokens, thr
         assert reco.exit_layers == pipe.exit_layers, thr
         assert reco.confidences == pipe.confidences, thr
+
+
+def test_bridge_runs_reference_model_objects(c1):
+    """`eepipe_bridge`: a model object with the reference's surface (`config`
+    with the reference fields, `named_arrays()` of float64 arrays) decodes on
+    the GPU through the bridge with the reference's own golden tokens, exit
+    layers and confidences (C1, threshold 0.8), and re-partitions for
+    pipeline mode (tokens equal to the recompute run)."""
+    from types import SimpleNamespace
+    from paper_2312_04916_b200 import eepipe_bridge as B
+    cfg = c1.config
+    ref_like = SimpleNamespace(
+        config=SimpleNamespace(num_layers=cfg.num_layers, hidden_dim=cfg.hidden_dim,
+                               num_heads=cfg.num_heads, vocab_size=cfg.vocab_size,
+                               max_seq_len=cfg.max_seq_len, tie_embeddings=cfg.tie_embeddings,
+                               exits=tuple(SimpleNamespace(layer_index=e.layer_index,
+                                                           head_kind=e.head_kind,
+                                                           loss_weight=e.loss_weight)
+                                           for e in cfg.exits)),
+        named_arrays=c1.named_arrays)
+    ref = gold()["c1_thr08"]
+    tr = B.generate_kv_recompute(ref_like, gold()["c1_prompt"], 0.8, 8)
+    _same_decisions(tr, ref)
+    _close_conf(tr.confidences, ref["confidences"])
+    # a reference-surface StagePartition: config + stages holding their params
+    part = partition(c1, 2)
+    part_like = SimpleNamespace(config=ref_like.config, num_stages=2,
+                                stages=[SimpleNamespace(params=st.params) for st in part.stages])
+    pipe = B.generate_pipeline(part_like, gold()["c1_prompt"], 0.8, 8)
+    assert pipe.tokens == tr.tokens and pipe.exit_layers == tr.exit_layers
