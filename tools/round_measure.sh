@@ -16,5 +16,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_at
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_attn_slab128 -s 130 -c 1 -o gpurun_out/slab_ctx2000_full python tools/prof_decode.py 3 1 1999 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemv_tma -s 40 -c 4 -o gpurun_out/gemv_tma_full python tools/prof_decode.py 1 1 192 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm2 -s 3 -c 3 -o gpurun_out/tc_gemm2_full python tools/time_train_head.py 4096 2048 50304 1 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_attn_fwd|k_attn_bwd_kv|k_attn_bwd_q" -s 3 -c 3 -o gpurun_out/attn_train_full python tools/time_attn_train.py > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_attn_fwd|k_attn_bwd_kv|k_attn_bwd_q" -s 6 -c 3 -o gpurun_out/attn_train_full python tools/time_attn_train.py > /dev/null 2>&1
+timeout 600 python tools/time_train_step.py 4 4 > gpurun_out/ts.txt 2>&1
+timeout 600 python tools/prof_train_step.py > gpurun_out/prof_ts_own.txt 2>&1
 ls -la gpurun_out
