@@ -171,9 +171,12 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     FwdBars* bar = reinterpret_cast<FwdBars*>(sm + (4 + kRing) * kTile);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqt = S / kT;
-    const int qa = nqt - 1 - 2 * (int)blockIdx.x;   // longest rows first
+    // grid (heads, pairs, batch): the pair index is the SLOW dimension, so the
+    // longest pairs of every head are dispatched first (longest-processing-
+    // time order across the whole grid)
+    const int qa = nqt - 1 - 2 * (int)blockIdx.y;
     const int qb = qa - 1;                          // -1: no second tile
-    const int hh = blockIdx.y, b = blockIdx.z;
+    const int hh = blockIdx.x, b = blockIdx.z;
     const int col = hh * kDh;
     const int na = qa + 1, nb = qb + 1;             // key tiles of A / B
     if (threadIdx.x == 0) {
@@ -437,8 +440,8 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
     BwdBars* bar = reinterpret_cast<BwdBars*>(sm + 2 * kTile + kBwdStages * kBwdStage);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqt = S / kT;
-    const int kt = (int)blockIdx.x;  // key tile (0 = most q tiles: scheduled first)
-    const int hh = blockIdx.y, b = blockIdx.z;
+    const int kt = (int)blockIdx.y;  // key tile; slow grid dimension: longest first
+    const int hh = blockIdx.x, b = blockIdx.z;
     const int col = hh * kDh;
     const int n = nqt - kt;  // q tiles kt .. nqt-1
     const float* lse_bh = lse + ((int64_t)b * H + hh) * S;
@@ -660,8 +663,8 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
     BwdQBars* bar = reinterpret_cast<BwdQBars*>(sm + 2 * kTile + 2 * kBwdStages * kTile);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqt = S / kT;
-    const int qt = nqt - 1 - (int)blockIdx.x;  // longest rows first
-    const int hh = blockIdx.y, b = blockIdx.z;
+    const int qt = nqt - 1 - (int)blockIdx.y;  // slow grid dimension: longest first
+    const int hh = blockIdx.x, b = blockIdx.z;
     const int col = hh * kDh;
     const int nkt = qt + 1;
     if (threadIdx.x == 0) {
@@ -861,7 +864,7 @@ extern "C" int ee_attn_train_fwd(const void* q, int64_t ldq, const void* k, int6
         (rc = make_tmap_bf16_ld(&tv, v, rows, cols, ldv, kT)))
         return rc;
     set_smem(k_attn_fwd, kFwdSmem);
-    const dim3 grid((unsigned)((S / kT + 1) / 2), (unsigned)H, (unsigned)B);
+    const dim3 grid((unsigned)H, (unsigned)((S / kT + 1) / 2), (unsigned)B);
     k_attn_fwd<<<grid, kFwdThreads, kFwdSmem, as_stream(stream)>>>(
         tq, tk, tv, (int)S, (int)H, (bf16*)out, (int)ldo, lse, 1.0f / sqrtf((float)kDh));
     return ee_check_launch("attn_train_fwd");
@@ -894,7 +897,7 @@ extern "C" int ee_attn_train_bwd(const void* q, int64_t ldq, const void* k, int6
         (rc = make_tmap_bf16_ld(&tdo, dout, rows, cols, ldd, kT)))
         return rc;
     const float scale = 1.0f / sqrtf((float)kDh);
-    const dim3 grid((unsigned)(S / kT), (unsigned)H, (unsigned)B);
+    const dim3 grid((unsigned)H, (unsigned)(S / kT), (unsigned)B);
     set_smem(k_attn_bwd_kv, kBwdKvSmem);
     k_attn_bwd_kv<<<grid, kBwdThreads, kBwdKvSmem, s>>>(tq, tk, tv, tdo, (int)S, (int)H, lse, dsum,
                                                           (bf16*)dk, (int)lddk, (bf16*)dv,
