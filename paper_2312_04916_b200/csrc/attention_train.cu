@@ -373,23 +373,39 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 }
 
 // D[b][h][s] = sum_d dO * O (float32), one warp per (row, head)
+// 16 lanes per (row, head): 8 dims each (16-byte loads), xor-butterfly over
+// the 16 lanes; a warp covers kDotPairs (row, head) pairs, two at a time
+constexpr int kDotPairs = 8;
 __global__ void k_attn_dot(const bf16* __restrict__ dout, int ldd, const bf16* __restrict__ o,
                            int ldo, int S, int H, int rows, float* __restrict__ D) {
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (w >= rows * H) return;
-    const int row = w / H, hh = w % H;
-    const uint2 a = *reinterpret_cast<const uint2*>(dout + (int64_t)row * ldd + hh * kDh + 4 * lane);
-    const uint2 c = *reinterpret_cast<const uint2*>(o + (int64_t)row * ldo + hh * kDh + 4 * lane);
-    const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.x));
-    const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.y));
-    const float2 c0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.x));
-    const float2 c1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.y));
-    float s = a0.x * c0.x + a0.y * c0.y + a1.x * c1.x + a1.y * c1.y;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int half = lane >> 4, l16 = lane & 15;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) {
-        const int b = row / S, si = row % S;
-        D[((int64_t)b * H + hh) * S + si] = s;
+    for (int it = 0; it < kDotPairs / 2; ++it) {
+        const int pidx = warp * kDotPairs + it * 2 + half;  // (row, head) pair
+        const bool ok = pidx < rows * H;
+        float sacc = 0.f;
+        int row = 0, hh = 0;
+        if (ok) {
+            row = pidx / H;
+            hh = pidx % H;
+            const uint4 a = *reinterpret_cast<const uint4*>(dout + (int64_t)row * ldd + hh * kDh + 8 * l16);
+            const uint4 c = *reinterpret_cast<const uint4*>(o + (int64_t)row * ldo + hh * kDh + 8 * l16);
+            const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 af = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&aw[q]));
+                const float2 cf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cw[q]));
+                sacc = fmaf(af.x, cf.x, sacc);
+                sacc = fmaf(af.y, cf.y, sacc);
+            }
+        }
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+        if (ok && l16 == 0) {
+            const int b = row / S, si = row % S;
+            D[((int64_t)b * H + hh) * S + si] = sacc;
+        }
     }
 }
 
@@ -886,7 +902,8 @@ extern "C" int ee_attn_train_bwd(const void* q, int64_t ldq, const void* k, int6
     const int64_t rows = B * S, cols = H * kDh;
     {
         const int64_t warps = rows * H;
-        k_attn_dot<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(
+        const int64_t dwarps = (warps + kDotPairs - 1) / kDotPairs;
+        k_attn_dot<<<(unsigned)((dwarps + 7) / 8), 256, 0, s>>>(
             (const bf16*)dout, (int)ldd, (const bf16*)o, (int)ldo, (int)S, (int)H, (int)rows, dsum);
         if ((rc = ee_check_launch("attn_train_dot"))) return rc;
     }
