@@ -26,20 +26,23 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force=False, verbose=False, trace=False):
+def build(force=False, verbose=False, trace=False, variant=None, defines=()):
     """trace=True: the profiling variant libee_trace.so (-DEE_TRACE timeline
-    probes, tools/attn_timeline.py); never loaded by the product path."""
-    target = OUT.replace("libee.so", "libee_trace.so") if trace else OUT
-    if not force and not trace and not needs_build():
+    probes, tools/attn_timeline.py); variant="name" with `defines` builds an
+    A/B copy libee_<name>.so (loaded through EE_LIB_PATH by the timing tools).
+    Neither is ever loaded by the product path."""
+    name = "trace" if trace else variant
+    target = OUT.replace("libee.so", f"libee_{name}.so") if name else OUT
+    if not force and not name and not needs_build():
         return OUT
-    objdir = os.path.join(HERE, "build_trace" if trace else "build")
+    objdir = os.path.join(HERE, f"build_{name}" if name else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     log = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *FLAGS, *(["-DEE_TRACE"] if trace else []), "-c", src, "-o", obj]
+        cmd = [NVCC, *FLAGS, *(["-DEE_TRACE"] if trace else []), *defines, "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     for cmd, p in procs:

@@ -95,6 +95,42 @@ __device__ __forceinline__ void store_row16(uint8_t* tile, int r, int c0, const 
     }
 }
 
+// store one 128 x 64 SW128 box of shared memory to (col, row0) of the map's
+// matrix (bulk group; the issuing thread waits for the smem reads before exit)
+__device__ __forceinline__ void tma_store_box(const CUtensorMap* m, const uint8_t* src, int col,
+                                              int row0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(m),
+        "r"(su32(src)), "r"(col), "r"(row0)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait_read() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// epilogue of an fp32 TMEM accumulator (lanes = tile rows) through shared
+// memory: this thread's row r, columns [c_lo, c_hi) -> bf16 SW128 boxes at
+// `tile`; then the `nthreads` threads that share named barrier `bar_id` sync
+// and the first of them stores boxes [box_lo, box_lo + nbox) with TMA.
+__device__ __forceinline__ void tmem_epilogue_tma(uint32_t tacc, uint8_t* tile, int r, int c_lo,
+                                                  int c_hi, int bar_id, int nthreads, bool issuer,
+                                                  const CUtensorMap* m, int col, int row0,
+                                                  int box_lo, int nbox) {
+#pragma unroll 1
+    for (int c = c_lo; c < c_hi; c += 16) {
+        float o[16];
+        tmem_ld16(tacc + c, o);
+        store_row16(tile, r, c, o);
+    }
+    fence_async_smem();
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+    if (issuer) {
+        for (int x = box_lo; x < box_lo + nbox; ++x)
+            tma_store_box(m, tile + x * kBox, col + 64 * x, row0);
+        tma_store_commit_wait_read();
+    }
+}
+
 __device__ __forceinline__ void alloc_tmem512(uint32_t* slot) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -138,8 +174,16 @@ __device__ unsigned long long g_fwd_tl[4][2][32];
         if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 32) \
             g_fwd_tl[e][t][j] = ee_gtime();                              \
     } while (0)
+// start / end of every CTA (kernel 0 fwd, 1 bwd_kv, 2 bwd_q; first 2048 CTAs)
+__device__ unsigned long long g_cta_tl[3][2048][4];
+#define CTA_TL(k, e)                                                                  \
+    do {                                                                              \
+        const unsigned id = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+        if ((threadIdx.x == ((e) == 0 ? 0u : 32u) || (e) >= 2) && id < 2048) g_cta_tl[k][id][e] = ee_gtime(); \
+    } while (0)
 #else
 #define FWD_TL(e, t, j) do { } while (0)
+#define CTA_TL(k, e) do { } while (0)
 #endif
 constexpr int kFwdThreads = 320;
 constexpr int kRing = 3;                 // K / V ring slots (one 32 KB tile each)
@@ -164,6 +208,7 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
            const __grid_constant__ CUtensorMap tv, int S, int H, bf16* __restrict__ out, int ldo,
            float* __restrict__ lse, float scale) {
     extern __shared__ uint8_t smem_raw[];
+    CTA_TL(0, 0);
     uint8_t* sm = tc::align1024(smem_raw);
     uint8_t* sQ = sm;                        // [2] (A, B)
     uint8_t* sRing = sm + 2 * kTile;         // [kRing]
@@ -369,6 +414,7 @@ k_attn_fwd(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     if (warp == 1) {
         tc_fence_after();
         free_tmem512(tmem);
+        CTA_TL(0, 1);
     }
 }
 
@@ -423,9 +469,19 @@ __global__ void k_attn_dot(const bf16* __restrict__ dout, int ldd, const bf16* _
 // overwrite the first 32 columns of S^T / dP^T, so S_h^T(i+1) is issued once
 // the dV / dK MMAs of half h of tile i completed.
 // ============================================================================
+#ifndef EE_ATTN_SPLIT_KV
+#define EE_ATTN_SPLIT_KV 1
+#endif
+#ifndef EE_ATTN_SPLIT_Q
+#define EE_ATTN_SPLIT_Q 2
+#endif
 constexpr int kBwdStages = 2;
 constexpr int kHalf = kT / 2;
-constexpr int kBwdThreads = 320;
+// softmax warps per TMEM lane quarter and half (each takes kHalf / split of
+// the half's columns); 2 for dQ, 1 for dK / dV (18 warps cap a thread at 96
+// registers, which the dK / dV kernel exceeds)
+constexpr int kSplitKv = EE_ATTN_SPLIT_KV, kSplitQ = EE_ATTN_SPLIT_Q;
+constexpr int kBwdKvThreads = 64 + 256 * kSplitKv, kBwdQThreads = 64 + 256 * kSplitQ;
 struct BwdBars {
     uint64_t kv_full, full[kBwdStages], empty[kBwdStages], s_full[2], p_full[2], mma_done[2];
     uint32_t tmem;
@@ -443,12 +499,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-__global__ void __launch_bounds__(kBwdThreads, 1)
+__global__ void __launch_bounds__(kBwdKvThreads, 1)
 k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
               const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+              const __grid_constant__ CUtensorMap tdk, const __grid_constant__ CUtensorMap tdv,
               int S, int H, const float* __restrict__ lse, const float* __restrict__ D,
-              bf16* __restrict__ dk, int lddk, bf16* __restrict__ dv, int lddv, float scale) {
+              float scale) {
+    constexpr int kSplit = kSplitKv, kCols = kHalf / kSplit;
     extern __shared__ uint8_t smem_raw[];
+    CTA_TL(1, 0);
     uint8_t* sm = tc::align1024(smem_raw);
     uint8_t* sK = sm;
     uint8_t* sV = sm + kTile;
@@ -470,7 +529,7 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
         }
         for (int h = 0; h < 2; ++h) {
             mb_init(&bar->s_full[h], 1);
-            mb_init(&bar->p_full[h], 128);
+            mb_init(&bar->p_full[h], 128 * kSplit);
             mb_init(&bar->mma_done[h], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -539,6 +598,7 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
             tc_fence_after();
             issue_s(0, 0);
             issue_s(0, 1);
+            if (lane == 0) CTA_TL(1, 2);
             for (int i = 0; i < n; ++i) {
                 const bool nxt = i + 1 < n;
 #pragma unroll
@@ -557,44 +617,50 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
             }
         }
     } else {
-        const int hf = (warp - 2) >> 2;  // this warpgroup's q half
+        // kSplit warps per TMEM lane quarter and half: sub-group `sub` owns the
+        // half's q columns [sub * kCols, sub * kCols + kCols)
+        const int sw = warp - 2;
+        const int hf = sw / (4 * kSplit);  // this group's q half
+        const int sub = (sw >> 2) % kSplit;
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;  // key row = TMEM lane
+        const int lead = 64 + hf * 128 * kSplit;  // first thread of the half's group
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        const uint32_t tS = tmem + lane_off + hf * kT, tP = tS + kHalf;
+        const uint32_t tS = tmem + lane_off + hf * kT + sub * kCols, tP = tS + kHalf;
         const float sl2 = scale * kLog2e;
         for (int i = 0; i < n; ++i) {
             const float* sLse = reinterpret_cast<const float*>(sStage + (i % kBwdStages) * kBwdStage +
-                                                                 2 * kTile) + hf * kHalf;
+                                                                 2 * kTile) + hf * kHalf + sub * kCols;
             const float* sD = sLse + kT;
             mb_wait(&bar->full[i % kBwdStages], (i / kBwdStages) & 1);  // lse / D landed
             mb_wait(&bar->s_full[hf], i & 1);
             tc_fence_after();
-            if (threadIdx.x == 64 + 128 * hf) FWD_TL(2, hf, i);
+            if (threadIdx.x == lead) FWD_TL(2, hf, i);
             const bool diag = i == 0;  // q tile == key tile: q index < key r is masked
-            const int c0 = hf * kHalf;   // q index of this half's first column
+            const int c0 = hf * kHalf + sub * kCols;  // q index of this thread's first column
+            float sv[kCols / 16][16], dpv[kCols / 16][16];
+#pragma unroll
+            for (int cc = 0; cc < kCols / 16; ++cc) {
+                tmem_ld16_nowait(tS + cc * 16, sv[cc]);
+                tmem_ld16_nowait(tP + cc * 16, dpv[cc]);
+            }
             {   // this half's lse -> lse * log2(e) and D -> D / sqrt(dh), in place
                 // (one multiply per column instead of one per element)
-                const int tw = threadIdx.x - 64 - 128 * hf;
+                const int tw = threadIdx.x - lead;
                 if (tw < kHalf) {
-                    float* l = const_cast<float*>(sLse) + tw;
-                    float* d = const_cast<float*>(sD) + tw;
+                    float* l = const_cast<float*>(sLse) - sub * kCols + tw;
+                    float* d = l + kT;
                     *l *= kLog2e;
                     *d *= scale;
                 }
-                asm volatile("bar.sync %0, 128;" ::"r"(1 + hf) : "memory");
+                tmem_wait_ld();
+                // also orders every sub-group's S^T / dP^T reads before any
+                // P^T / dS^T write (they pack over the other sub-group's columns)
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + hf), "r"(128 * kSplit) : "memory");
             }
-            float sv[2][16], dpv[2][16];
-            tmem_ld16_nowait(tS, sv[0]);
-            tmem_ld16_nowait(tP, dpv[0]);
-            tmem_wait_ld();
 #pragma unroll
-            for (int cc = 0; cc < kHalf / 16; ++cc) {
-                const int c = cc * 16, cur = cc & 1;
-                if (cc + 1 < kHalf / 16) {  // next chunk's S^T / dP^T in flight meanwhile
-                    tmem_ld16_nowait(tS + c + 16, sv[cur ^ 1]);
-                    tmem_ld16_nowait(tP + c + 16, dpv[cur ^ 1]);
-                }
+            for (int cc = 0; cc < kCols / 16; ++cc) {
+                const int c = cc * 16;
                 uint32_t pk[8], dk8[8];
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) {
@@ -604,48 +670,43 @@ k_attn_bwd_kv(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CU
                     float pe[4], de[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        pe[e] = ex2(fmaf(sv[cur][j + e], sl2, -lv[e]));
+                        pe[e] = ex2(fmaf(sv[cc][j + e], sl2, -lv[e]));
                         if (diag && c0 + c + j + e < r) pe[e] = 0.f;
-                        de[e] = pe[e] * fmaf(dpv[cur][j + e], scale, -dv4[e]);
+                        de[e] = pe[e] * fmaf(dpv[cc][j + e], scale, -dv4[e]);
                     }
                     pk[j / 2] = pack2(pe[0], pe[1]);
                     pk[j / 2 + 1] = pack2(pe[2], pe[3]);
                     dk8[j / 2] = pack2(de[0], de[1]);
                     dk8[j / 2 + 1] = pack2(de[2], de[3]);
                 }
-                // P^T over S^T columns [c/2, c/2 + 8), dS^T over dP^T's (already read)
-                tmem_st8u(tS + c / 2, pk);
-                tmem_st8u(tP + c / 2, dk8);
-                tmem_wait_ld();
+                // P^T over the half's S^T columns [(sub*kCols + c)/2, +8), dS^T
+                // likewise over dP^T's (all read before the barrier above)
+                const uint32_t po = tmem + lane_off + hf * kT + (sub * kCols + c) / 2;
+                tmem_st8u(po, pk);
+                tmem_st8u(po + kHalf, dk8);
             }
             tmem_wait_st();
             tc_fence_before();
-            if (threadIdx.x == 64 + 128 * hf) FWD_TL(3, hf, i);
+            if (threadIdx.x == lead) FWD_TL(3, hf, i);
             mb_arrive(&bar->p_full[hf]);
         }
         // the final dV (warpgroup 0) / dK (warpgroup 1)
         mb_wait(&bar->mma_done[0], (n - 1) & 1);
         mb_wait(&bar->mma_done[1], (n - 1) & 1);
         tc_fence_after();
-        const int64_t row = (int64_t)b * S + kt * kT + r;
-        bf16* dst = hf == 0 ? dv + row * lddv + col : dk + row * lddk + col;
-#pragma unroll 1
-        for (int c = 0; c < kDh; c += 16) {
-            float o[16];
-            tmem_ld16(tmem + lane_off + (2 + hf) * kT + c, o);
-            uint4 u0 = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]),
-                                  pack2(o[6], o[7]));
-            uint4 u1 = make_uint4(pack2(o[8], o[9]), pack2(o[10], o[11]), pack2(o[12], o[13]),
-                                  pack2(o[14], o[15]));
-            reinterpret_cast<uint4*>(dst + c)[0] = u0;
-            reinterpret_cast<uint4*>(dst + c)[1] = u1;
-        }
+        if (threadIdx.x == 64) CTA_TL(1, 3);
+        // dV (half 0) / dK (half 1) through the free stage-0 Q / dO buffers
+        const int c_lo = sub * (kDh / kSplit), c_hi = c_lo + kDh / kSplit;
+        tmem_epilogue_tma(tmem + lane_off + (2 + hf) * kT, sStage + hf * 2 * kBox, r, c_lo, c_hi,
+                          3 + hf * kSplit + sub, 128, threadIdx.x == 64 + 32 * (sw & ~3),
+                          hf == 0 ? &tdv : &tdk, col, b * S + kt * kT, c_lo / 64, (c_hi - c_lo) / 64);
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         free_tmem512(tmem);
+        CTA_TL(1, 1);
     }
 }
 
@@ -666,12 +727,14 @@ struct BwdQBars {
 constexpr size_t kBwdQSmem = 1024 + 2 * (size_t)kTile + 2 * kBwdStages * (size_t)kTile +
                              sizeof(BwdQBars) + 64;
 
-__global__ void __launch_bounds__(kBwdThreads, 1)
+__global__ void __launch_bounds__(kBwdQThreads, 1)
 k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
              const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
-             int S, int H, const float* __restrict__ lse, const float* __restrict__ D,
-             bf16* __restrict__ dq, int lddq, float scale) {
+             const __grid_constant__ CUtensorMap tdq, int S, int H,
+             const float* __restrict__ lse, const float* __restrict__ D, float scale) {
+    constexpr int kSplit = kSplitQ, kCols = kHalf / kSplit;
     extern __shared__ uint8_t smem_raw[];
+    CTA_TL(2, 0);
     uint8_t* sm = tc::align1024(smem_raw);
     uint8_t* sQ = sm;
     uint8_t* sDO = sm + kTile;
@@ -691,7 +754,7 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
         }
         for (int h = 0; h < 2; ++h) {
             mb_init(&bar->s_full[h], 1);
-            mb_init(&bar->ds_full[h], 128);
+            mb_init(&bar->ds_full[h], 128 * kSplit);
             mb_init(&bar->mma_done[h], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -769,63 +832,60 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
             }
         }
     } else {
-        const int hf = (warp - 2) >> 2;  // this warpgroup's key half
+        const int sw = warp - 2;
+        const int hf = sw / (4 * kSplit);  // this group's key half
+        const int sub = (sw >> 2) % kSplit;
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        const uint32_t tS = tmem + lane_off + hf * kT, tP = tS + kHalf;
+        const uint32_t tS = tmem + lane_off + hf * kT + sub * kCols, tP = tS + kHalf;
         const int64_t si = ((int64_t)b * H + hh) * S + qt * kT + r;
         const float sl2 = scale * kLog2e;
         const float lse2 = lse[si] * kLog2e, ds_off = D[si] * scale;
-        const int c0 = hf * kHalf;  // key index of this half's first column
+        const int c0 = hf * kHalf + sub * kCols;  // key index of this thread's first column
         for (int kt = 0; kt < nkt; ++kt) {
             mb_wait(&bar->s_full[hf], kt & 1);
             tc_fence_after();
             const bool diag = kt == qt;
-            float sv[2][16], dpv[2][16];
-            tmem_ld16_nowait(tS, sv[0]);
-            tmem_ld16_nowait(tP, dpv[0]);
-            tmem_wait_ld();
+            float sv[kCols / 16][16], dpv[kCols / 16][16];
 #pragma unroll
-            for (int cc = 0; cc < kHalf / 16; ++cc) {
-                const int c = cc * 16, cur = cc & 1;
-                if (cc + 1 < kHalf / 16) {
-                    tmem_ld16_nowait(tS + c + 16, sv[cur ^ 1]);
-                    tmem_ld16_nowait(tP + c + 16, dpv[cur ^ 1]);
-                }
+            for (int cc = 0; cc < kCols / 16; ++cc) {
+                tmem_ld16_nowait(tS + cc * 16, sv[cc]);
+                tmem_ld16_nowait(tP + cc * 16, dpv[cc]);
+            }
+            tmem_wait_ld();
+            if (kSplit > 1)  // every sub-group's reads before dS packs over them
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + hf), "r"(128 * kSplit) : "memory");
+#pragma unroll
+            for (int cc = 0; cc < kCols / 16; ++cc) {
+                const int c = cc * 16;
                 uint32_t dk8[8];
 #pragma unroll
                 for (int j = 0; j < 16; j += 2) {
-                    float p0 = ex2(fmaf(sv[cur][j], sl2, -lse2));
-                    float p1 = ex2(fmaf(sv[cur][j + 1], sl2, -lse2));
+                    float p0 = ex2(fmaf(sv[cc][j], sl2, -lse2));
+                    float p1 = ex2(fmaf(sv[cc][j + 1], sl2, -lse2));
                     if (diag && c0 + c + j > r) p0 = 0.f;
                     if (diag && c0 + c + j + 1 > r) p1 = 0.f;
-                    dk8[j / 2] = pack2(p0 * fmaf(dpv[cur][j], scale, -ds_off),
-                                       p1 * fmaf(dpv[cur][j + 1], scale, -ds_off));
+                    dk8[j / 2] = pack2(p0 * fmaf(dpv[cc][j], scale, -ds_off),
+                                       p1 * fmaf(dpv[cc][j + 1], scale, -ds_off));
                 }
-                tmem_st8u(tP + c / 2, dk8);  // dS over dP columns already read
-                tmem_wait_ld();
+                // dS over the half's dP columns [(sub*kCols + c)/2, +8)
+                tmem_st8u(tmem + lane_off + hf * kT + kHalf + (sub * kCols + c) / 2, dk8);
             }
             tmem_wait_st();
             tc_fence_before();
             mb_arrive(&bar->ds_full[hf]);
         }
-        if (hf == 0) {
+        {   // dQ: the 2 * kSplit groups take kDh / (2 * kSplit) columns each, through
+            // the free K / V stage 0; box x = hf is stored by its half group's first thread
+            constexpr int kEpi = kDh / (2 * kSplit);
+            const int g = hf * kSplit + sub;
             mb_wait(&bar->mma_done[0], (nkt - 1) & 1);
             mb_wait(&bar->mma_done[1], (nkt - 1) & 1);
             tc_fence_after();
-            bf16* dst = dq + ((int64_t)b * S + qt * kT + r) * lddq + col;
-#pragma unroll 1
-            for (int c = 0; c < kDh; c += 16) {
-                float o[16];
-                tmem_ld16(tmem + lane_off + 2 * kT + c, o);
-                uint4 u0 = make_uint4(pack2(o[0], o[1]), pack2(o[2], o[3]), pack2(o[4], o[5]),
-                                      pack2(o[6], o[7]));
-                uint4 u1 = make_uint4(pack2(o[8], o[9]), pack2(o[10], o[11]), pack2(o[12], o[13]),
-                                      pack2(o[14], o[15]));
-                reinterpret_cast<uint4*>(dst + c)[0] = u0;
-                reinterpret_cast<uint4*>(dst + c)[1] = u1;
-            }
+            tmem_epilogue_tma(tmem + lane_off + 2 * kT, sKV, r, g * kEpi, (g + 1) * kEpi, 1 + hf,
+                              128 * kSplit, threadIdx.x == 64 + 128 * kSplit * hf, &tdq, col,
+                              b * S + qt * kT, hf, 1);
         }
     }
     tc_fence_before();
@@ -833,6 +893,7 @@ k_attn_bwd_q(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUt
     if (warp == 1) {
         tc_fence_after();
         free_tmem512(tmem);
+        CTA_TL(2, 1);
     }
 }
 
@@ -862,6 +923,9 @@ void set_smem(K kern, size_t bytes) {
 #ifdef EE_TRACE
 extern "C" int ee_trace_attn_fwd(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_fwd_tl, sizeof(g_fwd_tl));
+}
+extern "C" int ee_trace_attn_cta(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_cta_tl, sizeof(g_cta_tl));
 }
 #endif
 
@@ -907,21 +971,23 @@ extern "C" int ee_attn_train_bwd(const void* q, int64_t ldq, const void* k, int6
             (const bf16*)dout, (int)ldd, (const bf16*)o, (int)ldo, (int)S, (int)H, (int)rows, dsum);
         if ((rc = ee_check_launch("attn_train_dot"))) return rc;
     }
-    CUtensorMap tq, tk, tv, tdo;
+    CUtensorMap tq, tk, tv, tdo, tdq, tdk, tdv;
     if ((rc = make_tmap_bf16_ld(&tq, q, rows, cols, ldq, kT)) ||
         (rc = make_tmap_bf16_ld(&tk, k, rows, cols, ldk, kT)) ||
         (rc = make_tmap_bf16_ld(&tv, v, rows, cols, ldv, kT)) ||
-        (rc = make_tmap_bf16_ld(&tdo, dout, rows, cols, ldd, kT)))
+        (rc = make_tmap_bf16_ld(&tdo, dout, rows, cols, ldd, kT)) ||
+        (rc = make_tmap_bf16_ld(&tdq, dq, rows, cols, lddq, kT)) ||
+        (rc = make_tmap_bf16_ld(&tdk, dk, rows, cols, lddk, kT)) ||
+        (rc = make_tmap_bf16_ld(&tdv, dv, rows, cols, lddv, kT)))
         return rc;
     const float scale = 1.0f / sqrtf((float)kDh);
     const dim3 grid((unsigned)H, (unsigned)(S / kT), (unsigned)B);
     set_smem(k_attn_bwd_kv, kBwdKvSmem);
-    k_attn_bwd_kv<<<grid, kBwdThreads, kBwdKvSmem, s>>>(tq, tk, tv, tdo, (int)S, (int)H, lse, dsum,
-                                                          (bf16*)dk, (int)lddk, (bf16*)dv,
-                                                          (int)lddv, scale);
+    k_attn_bwd_kv<<<grid, kBwdKvThreads, kBwdKvSmem, s>>>(tq, tk, tv, tdo, tdk, tdv, (int)S, (int)H,
+                                                          lse, dsum, scale);
     if ((rc = ee_check_launch("attn_train_bwd_kv"))) return rc;
     set_smem(k_attn_bwd_q, kBwdQSmem);
-    k_attn_bwd_q<<<grid, kBwdThreads, kBwdQSmem, s>>>(tq, tk, tv, tdo, (int)S, (int)H, lse, dsum,
-                                                        (bf16*)dq, (int)lddq, scale);
+    k_attn_bwd_q<<<grid, kBwdQThreads, kBwdQSmem, s>>>(tq, tk, tv, tdo, tdq, (int)S, (int)H, lse,
+                                                        dsum, scale);
     return ee_check_launch("attn_train_bwd_q");
 }

@@ -46,7 +46,10 @@ __device__ __forceinline__ void load_w8(const float* w, int c, float* ww) {
     ww[4] = w1.x; ww[5] = w1.y; ww[6] = w1.z; ww[7] = w1.w;
 }
 
-// two sweeps over the row (the second re-reads it from L1)
+// One warp per row.  Rows up to kHeld * 256 columns are loaded once into
+// registers (all 16-byte loads of the row in flight together); wider rows take
+// two sweeps, the second re-reading the row from L1 / L2.
+constexpr int kHeld = 8;  // 16-byte chunks per lane held in registers (h <= 2048)
 __global__ void __launch_bounds__(kThreads)
 k_rms_fwd(const bf16* __restrict__ x, const float* __restrict__ w, int64_t n, int h, float eps,
           bf16* __restrict__ y, float* __restrict__ inv_out) {
@@ -54,8 +57,39 @@ k_rms_fwd(const bf16* __restrict__ x, const float* __restrict__ w, int64_t n, in
     const int64_t row = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     if (row >= n) return;
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
+    uint4* yr = reinterpret_cast<uint4*>(y + row * h);
     const int nvec = h / 8;
     float ss = 0.f;
+    if (nvec <= 32 * kHeld) {
+        uint4 xs[kHeld];
+#pragma unroll
+        for (int u = 0; u < kHeld; ++u)
+            if (u * 32 + lane < nvec) xs[u] = xr[u * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < kHeld; ++u)
+            if (u * 32 + lane < nvec) {
+                float v[8];
+                unpack8(xs[u], v);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) ss += v[k] * v[k];
+            }
+        ss = warp_sum(ss);
+        const float inv = rsqrtf(ss / (float)h + eps);
+#pragma unroll
+        for (int u = 0; u < kHeld; ++u) {
+            const int c = u * 32 + lane;
+            if (c < nvec) {
+                float v[8], ww[8], o[8];
+                unpack8(xs[u], v);
+                load_w8(w, c, ww);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o[k] = v[k] * inv * ww[k];
+                yr[c] = pack8(o);
+            }
+        }
+        if (lane == 0) inv_out[row] = inv;
+        return;
+    }
     for (int c = lane; c < nvec; c += 32) {
         float v[8];
         unpack8(xr[c], v);
@@ -64,7 +98,6 @@ k_rms_fwd(const bf16* __restrict__ x, const float* __restrict__ w, int64_t n, in
     }
     ss = warp_sum(ss);
     const float inv = rsqrtf(ss / (float)h + eps);
-    uint4* yr = reinterpret_cast<uint4*>(y + row * h);
     for (int c = lane; c < nvec; c += 32) {
         float v[8], ww[8], o[8];
         unpack8(xr[c], v);
@@ -76,40 +109,67 @@ k_rms_fwd(const bf16* __restrict__ x, const float* __restrict__ w, int64_t n, in
     if (lane == 0) inv_out[row] = inv;
 }
 
-// One warp per row.  The row's x and g chunks are loaded 8 per lane at a time
-// (8 independent 16-byte loads in flight) and kept in registers for the
-// second sweep when the row fits (h <= 2048); gres (optional) is a second
-// incoming gradient of x added to gx in the same pass (the residual branch of
-// a pre-norm block), so no separate element-wise add reads / writes (n, h).
-constexpr int kChunkRegs = 8;  // 16-byte chunks per lane held in registers
-__global__ void __launch_bounds__(kThreads)
+// Backward: a grid of about one wave, each warp taking `rpw` consecutive rows.
+// Per row: x, g (and gres, a second incoming gradient of x -- the residual
+// branch of a pre-norm block -- added to gx in the same pass) are loaded with
+// every 16-byte load of the row in flight, the row's weight-gradient terms
+// g x inv are added into the warp's own float32 row of shared memory (no
+// synchronisation inside the row loop), and gx is written.  At the end the
+// CTA sums its warps' rows in warp order into its partial; k_gw_reduce adds
+// the partials in CTA order -- no atomics, repeated runs give identical bits.
+constexpr int kBwdWarps = 4;
+constexpr int kBwdThreads = kBwdWarps * 32;
+__device__ __forceinline__ void acc_gw8(float* a, const float* gv, const float* xv, float inv) {
+    float4* p = reinterpret_cast<float4*>(a);
+    float4 u0 = p[0], u1 = p[1];
+    u0.x += gv[0] * xv[0] * inv; u0.y += gv[1] * xv[1] * inv;
+    u0.z += gv[2] * xv[2] * inv; u0.w += gv[3] * xv[3] * inv;
+    u1.x += gv[4] * xv[4] * inv; u1.y += gv[5] * xv[5] * inv;
+    u1.z += gv[6] * xv[6] * inv; u1.w += gv[7] * xv[7] * inv;
+    p[0] = u0;
+    p[1] = u1;
+}
+#ifndef EE_RMS_BWD_MINB
+#define EE_RMS_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(kBwdThreads, EE_RMS_BWD_MINB)
 k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* __restrict__ inv_in,
-          const bf16* __restrict__ g, const bf16* __restrict__ gres, int64_t n, int h,
+          const bf16* __restrict__ g, const bf16* __restrict__ gres, int64_t n, int h, int rpw,
           bf16* __restrict__ gx, float* __restrict__ gw_part) {
-    __shared__ float part[kWarps][256];
+    extern __shared__ float4 acc_raw[];
+    float* acc = reinterpret_cast<float*>(acc_raw);  // [kBwdWarps][h]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
-    const bool valid = row < n;
     const int nvec = h / 8;
-    const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
-    const uint4* gr = reinterpret_cast<const uint4*>(g + row * h);
-    const bool held = nvec <= 32 * kChunkRegs;  // whole row in registers
-    uint4 xs[kChunkRegs], gs[kChunkRegs];
-    float dot = 0.f, inv = 0.f;
-    if (valid) {
-        inv = inv_in[row];
-        for (int c0 = 0; c0 < nvec; c0 += 32 * kChunkRegs) {
+    float* my = acc + (size_t)warp * h;
+    for (int c = lane; c < nvec; c += 32) {
+        reinterpret_cast<float4*>(my)[2 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4*>(my)[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const bool held = nvec <= 32 * kHeld;
+    const int64_t r0 = ((int64_t)blockIdx.x * kBwdWarps + warp) * rpw;
+    for (int i = 0; i < rpw; ++i) {
+        const int64_t row = r0 + i;
+        if (row >= n) break;
+        const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
+        const uint4* gr = reinterpret_cast<const uint4*>(g + row * h);
+        const uint4* rr = gres ? reinterpret_cast<const uint4*>(gres + row * h) : nullptr;
+        uint4* gxr = reinterpret_cast<uint4*>(gx + row * h);
+        const float inv = inv_in[row];
+        float dot = 0.f;
+        if (held) {
+            uint4 xs[kHeld], gs[kHeld], rs[kHeld];
 #pragma unroll
-            for (int u = 0; u < kChunkRegs; ++u) {
-                const int c = c0 + u * 32 + lane;
+            for (int u = 0; u < kHeld; ++u) {
+                const int c = u * 32 + lane;
                 if (c < nvec) {
                     xs[u] = xr[c];
                     gs[u] = gr[c];
+                    if (rr) rs[u] = rr[c];
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kChunkRegs; ++u) {
-                const int c = c0 + u * 32 + lane;
+            for (int u = 0; u < kHeld; ++u) {
+                const int c = u * 32 + lane;
                 if (c < nvec) {
                     float xv[8], gv[8], ww[8];
                     unpack8(xs[u], xv);
@@ -117,93 +177,174 @@ k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* 
                     load_w8(w, c, ww);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) dot += gv[k] * ww[k] * xv[k];
+                    acc_gw8(my + 8 * c, gv, xv, inv);
+                }
+            }
+            dot = warp_sum(dot);
+            const float coef = inv * inv * inv * dot / (float)h;
+#pragma unroll
+            for (int u = 0; u < kHeld; ++u) {
+                const int c = u * 32 + lane;
+                if (c < nvec) {
+                    float xv[8], gv[8], ww[8], o[8];
+                    unpack8(xs[u], xv);
+                    unpack8(gs[u], gv);
+                    load_w8(w, c, ww);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) o[k] = gv[k] * ww[k] * inv - xv[k] * coef;
+                    if (rr) {
+                        float rv[8];
+                        unpack8(rs[u], rv);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) o[k] += rv[k];
+                    }
+                    gxr[c] = pack8(o);
+                }
+            }
+        } else {
+            for (int c0 = 0; c0 < nvec; c0 += 32 * kHeld) {
+                uint4 xs[kHeld], gs[kHeld];
+#pragma unroll
+                for (int u = 0; u < kHeld; ++u) {
+                    const int c = c0 + u * 32 + lane;
+                    if (c < nvec) {
+                        xs[u] = xr[c];
+                        gs[u] = gr[c];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kHeld; ++u) {
+                    const int c = c0 + u * 32 + lane;
+                    if (c < nvec) {
+                        float xv[8], gv[8], ww[8];
+                        unpack8(xs[u], xv);
+                        unpack8(gs[u], gv);
+                        load_w8(w, c, ww);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) dot += gv[k] * ww[k] * xv[k];
+                        acc_gw8(my + 8 * c, gv, xv, inv);
+                    }
+                }
+            }
+            dot = warp_sum(dot);
+            const float coef = inv * inv * inv * dot / (float)h;
+            for (int c0 = 0; c0 < nvec; c0 += 32 * kHeld) {
+                uint4 xs[kHeld], gs[kHeld], rs[kHeld];
+#pragma unroll
+                for (int u = 0; u < kHeld; ++u) {
+                    const int c = c0 + u * 32 + lane;
+                    if (c < nvec) {
+                        xs[u] = xr[c];
+                        gs[u] = gr[c];
+                        if (rr) rs[u] = rr[c];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kHeld; ++u) {
+                    const int c = c0 + u * 32 + lane;
+                    if (c < nvec) {
+                        float xv[8], gv[8], ww[8], o[8];
+                        unpack8(xs[u], xv);
+                        unpack8(gs[u], gv);
+                        load_w8(w, c, ww);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) o[k] = gv[k] * ww[k] * inv - xv[k] * coef;
+                        if (rr) {
+                            float rv[8];
+                            unpack8(rs[u], rv);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) o[k] += rv[k];
+                        }
+                        gxr[c] = pack8(o);
+                    }
                 }
             }
         }
-        dot = warp_sum(dot);
     }
-    const float coef = inv * inv * inv * dot / (float)h;
-    uint4* gxr = reinterpret_cast<uint4*>(gx + row * h);
-    const uint4* rr = gres ? reinterpret_cast<const uint4*>(gres + row * h) : nullptr;
-    // second sweep, 256 columns per step for the whole CTA: gx, and this
-    // CTA's weight-gradient partial (rows summed in warp order)
-    for (int c0 = 0; c0 < nvec; c0 += 32) {
-        const int c = c0 + lane;
-        float gwv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (valid && c < nvec) {
-            float xv[8], gv[8], ww[8], o[8];
-            const int u = c0 / 32;
-            if (held) {
-                // u < kChunkRegs: register-resident chunk (indices unrolled below)
-                uint4 xu = xs[0], gu = gs[0];
+    __syncthreads();
+    // this CTA's partial: the warps' rows summed in warp order
+    for (int j4 = threadIdx.x; j4 < h / 4; j4 += kBwdThreads) {
+        float4 s4 = reinterpret_cast<const float4*>(acc)[j4];
 #pragma unroll
-                for (int q = 1; q < kChunkRegs; ++q)
-                    if (q == u) {
-                        xu = xs[q];
-                        gu = gs[q];
-                    }
-                unpack8(xu, xv);
-                unpack8(gu, gv);
-            } else {
-                unpack8(xr[c], xv);
-                unpack8(gr[c], gv);
-            }
-            load_w8(w, c, ww);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                o[k] = gv[k] * ww[k] * inv - xv[k] * coef;
-                gwv[k] = gv[k] * xv[k] * inv;
-            }
-            if (rr) {
-                float rv[8];
-                unpack8(rr[c], rv);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) o[k] += rv[k];
-            }
-            gxr[c] = pack8(o);
+        for (int r = 1; r < kBwdWarps; ++r) {
+            const float4 t = reinterpret_cast<const float4*>(acc + (size_t)r * h)[j4];
+            s4.x += t.x; s4.y += t.y; s4.z += t.z; s4.w += t.w;
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) part[warp][lane * 8 + k] = gwv[k];
-        __syncthreads();
-        const int j = c0 * 8 + threadIdx.x;
-        if (j < h) {
-            float acc = 0.f;
-#pragma unroll
-            for (int r = 0; r < kWarps; ++r) acc += part[r][threadIdx.x];
-            gw_part[(int64_t)blockIdx.x * h + j] = acc;
-        }
-        __syncthreads();
+        reinterpret_cast<float4*>(gw_part + (size_t)blockIdx.x * h)[j4] = s4;
     }
 }
 
-// gw_j (+)= sum over CTA partials in CTA order (deterministic), two levels:
-// k_gw_reduce1 sums consecutive groups of partials (grid.y groups) into
-// level-2 partials, k_gw_reduce2 sums those in group order
-constexpr int kGroups = 32;
-__global__ void k_gw_reduce1(const float* __restrict__ part, int nparts, int h,
-                             float* __restrict__ part2) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= h) return;
-    const int g = blockIdx.y;
-    const int p0 = (int)((int64_t)nparts * g / kGroups), p1 = (int)((int64_t)nparts * (g + 1) / kGroups);
+// gw_j (+)= sum over the CTA partials in CTA order (deterministic): a CTA per
+// 32 columns, warp v sums partials v, v + 8, v + 16, ... (lane = column), then
+// the 8 warp sums are added in warp order
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(kRedWarps * 32)
+k_gw_reduce(const float* __restrict__ part, int nparts, int h, int accumulate,
+            float* __restrict__ gw) {
+    __shared__ float red[kRedWarps][32];
+    const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + lane;
     float s = 0.f;
-    for (int p = p0; p < p1; ++p) s += part[(int64_t)p * h + j];
-    part2[(int64_t)g * h + j] = s;
-}
-__global__ void k_gw_reduce2(const float* __restrict__ part2, int h, int accumulate,
-                             float* __restrict__ gw) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= h) return;
-    float s = 0.f;
-#pragma unroll 8
-    for (int g = 0; g < kGroups; ++g) s += part2[(int64_t)g * h + j];
-    gw[j] = accumulate ? gw[j] + s : s;
+    if (j < h) {
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains, combined in order
+        int p = v;
+        for (; p + 3 * kRedWarps < nparts; p += 4 * kRedWarps) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s4[k] += part[(int64_t)(p + k * kRedWarps) * h + j];
+        }
+        for (; p < nparts; p += kRedWarps) s4[0] += part[(int64_t)p * h + j];
+        s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    }
+    red[v][lane] = s;
+    __syncthreads();
+    if (v == 0 && j < h) {
+        float t = red[0][lane];
+#pragma unroll
+        for (int r = 1; r < kRedWarps; ++r) t += red[r][lane];
+        gw[j] = accumulate ? gw[j] + t : t;
+    }
 }
 
 }  // namespace
 
+// backward grid: about one wave of CTAs (occupancy-limited by the per-warp
+// shared rows), never more CTAs than warps' worth of rows
+struct BwdGrid {
+    int ctas, rpw;
+    size_t smem;
+};
+BwdGrid bwd_grid(int64_t n, int64_t h) {
+    BwdGrid gr;
+    gr.smem = (size_t)kBwdWarps * h * sizeof(float);
+    static int64_t cached_h = -1;  // occupancy of the last width asked for
+    static int cached_per_sm = 1;
+    int per_sm = cached_per_sm;
+    if (h != cached_h) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_rms_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rms_bwd, kBwdThreads,
+                                                          gr.smem) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        cached_h = h;
+        cached_per_sm = per_sm;
+    }
+    const int64_t warps_needed = n;  // at most one row per warp
+    int64_t ctas = (int64_t)ee_sm_count() * per_sm;
+    const int64_t max_ctas = (warps_needed + kBwdWarps - 1) / kBwdWarps;
+    if (ctas > max_ctas) ctas = max_ctas;
+    if (ctas < 1) ctas = 1;
+    gr.rpw = (int)((n + ctas * kBwdWarps - 1) / (ctas * kBwdWarps));
+    if (gr.rpw < 1) gr.rpw = 1;
+    gr.ctas = (int)((n + (int64_t)gr.rpw * kBwdWarps - 1) / ((int64_t)gr.rpw * kBwdWarps));
+    return gr;
+}
+
 size_t rmsnorm_train_ws_bytes(int64_t n, int64_t h) {
-    return ((size_t)((n + kWarps - 1) / kWarps) + kGroups) * (size_t)h * sizeof(float);
+    // partials: at most one per kBwdWarps rows
+    return (size_t)((n + kBwdWarps - 1) / kBwdWarps) * (size_t)h * sizeof(float);
 }
 
 extern "C" int ee_rmsnorm_fwd(const void* x, int64_t n, int64_t h, const float* w, float eps,
@@ -224,19 +365,20 @@ extern "C" int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rm
                (long long)h);
     EE_REQUIRE(ws_bytes >= rmsnorm_train_ws_bytes(n, h), EE_ESHAPE,
                "rmsnorm_bwd: workspace too small");
+    EE_REQUIRE((size_t)kBwdWarps * h * sizeof(float) <= 227 * 1024, EE_ESHAPE,
+               "rmsnorm_bwd: h too large (%lld)", (long long)h);
     cudaStream_t s = as_stream(stream);
-    const int nparts = (int)((n + kWarps - 1) / kWarps);
+    int nparts = 0;
     if (n > 0) {
-        k_rms_bwd<<<nparts, kThreads, 0, s>>>((const bf16*)x, w, inv_rms, (const bf16*)gy,
-                                              (const bf16*)gres, n, (int)h, (bf16*)gx, (float*)ws);
+        const BwdGrid gr = bwd_grid(n, h);
+        nparts = gr.ctas;
+        k_rms_bwd<<<gr.ctas, kBwdThreads, gr.smem, s>>>((const bf16*)x, w, inv_rms, (const bf16*)gy,
+                                                        (const bf16*)gres, n, (int)h, gr.rpw,
+                                                        (bf16*)gx, (float*)ws);
         int rc;
         if ((rc = ee_check_launch("rmsnorm_bwd"))) return rc;
     }
-    float* part2 = (float*)ws + (size_t)nparts * h;
-    k_gw_reduce1<<<dim3((unsigned)((h + 255) / 256), kGroups), 256, 0, s>>>((const float*)ws, nparts,
-                                                                           (int)h, part2);
-    int rc;
-    if ((rc = ee_check_launch("rmsnorm_gw_reduce1"))) return rc;
-    k_gw_reduce2<<<(unsigned)((h + 255) / 256), 256, 0, s>>>(part2, (int)h, accumulate_gw, gw);
-    return ee_check_launch("rmsnorm_gw_reduce2");
+    k_gw_reduce<<<(unsigned)((h + 31) / 32), kRedWarps * 32, 0, s>>>((const float*)ws, nparts, (int)h,
+                                                                    accumulate_gw, gw);
+    return ee_check_launch("rmsnorm_gw_reduce");
 }
