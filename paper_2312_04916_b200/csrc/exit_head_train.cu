@@ -25,6 +25,8 @@
 // once.
 #include <cuda.h>
 
+#include <mutex>
+
 #include "tc_gemm.cuh"
 
 namespace {
@@ -68,6 +70,8 @@ size_t carve_bytes(int64_t n, int64_t V) {
 struct EpiProb {
     static constexpr bool kTwoPass = true;
     static constexpr bool kSplitK = false;
+    static constexpr bool kStreamK = false;  // stream-K tail allowed (tc_gemm.cuh)
+    static constexpr bool kStaged = false;
     const int64_t* targets;
     float *pmax, *psum, *tgt;
     bf16* g;
@@ -125,10 +129,19 @@ template <bool ACCUM>
 struct EpiF32 {  // K3 store / K4 accumulate, optionally scaled by *gs (device)
     static constexpr bool kTwoPass = false;
     static constexpr bool kSplitK = false;
+    static constexpr bool kStreamK = true;  // stream-K tail allowed (tc_gemm.cuh)
+    static constexpr bool kStaged = true;   // TMA-stored output boxes (tc_gemm.cuh)
+    static constexpr bool kReduceAdd = ACCUM;  // accumulate: TMA reduce-add in L2
+    using OutT = float;
     float* out;
     int ldo;
     const float* gs = nullptr;
     float g = 1.f;
+    int out_map(CUtensorMap* m, int M, int N) const { return tc::make_tmap_out(m, out, 4, M, N, ldo); }
+    __device__ void stage(int, int, const float* v, int, float* o) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = gs ? v[j] * g : v[j];
+    }
     __device__ void begin_tile(int, int, int, bool) {
         if (gs) g = __ldg(gs);
     }
@@ -170,6 +183,8 @@ struct EpiF32 {  // K3 store / K4 accumulate, optionally scaled by *gs (device)
 struct EpiF32Ordered {
     static constexpr bool kTwoPass = false;
     static constexpr bool kSplitK = true;
+    static constexpr bool kStreamK = false;  // stream-K tail allowed (tc_gemm.cuh)
+    static constexpr bool kStaged = false;
     float* out;
     int ldo;
     int* flags;  // [tiles][16 regions]
@@ -343,17 +358,98 @@ __global__ void k_loss_sum(const float* __restrict__ rowloss, int n, float scale
 }  // namespace
 
 namespace tc {
+bool sk_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("EE_GEMM_STREAMK");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+SkWs* sk_workspace(cudaStream_t s, size_t ws_bytes, int nflags) {
+    static SkWs table[32];
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SkWs* w = nullptr;
+    for (auto& e : table)
+        if (e.dev == dev && e.stream == s) {
+            w = &e;
+            break;
+        }
+    if (!w)
+        for (auto& e : table)
+            if (e.dev < 0) {
+                w = &e;
+                w->dev = dev;
+                w->stream = s;
+                break;
+            }
+    if (!w) return nullptr;
+    if (w->ws_bytes < ws_bytes) {
+        // grow: the stream's earlier launches may still read the old slots
+        if (w->ws) {
+            cudaStreamSynchronize(s);
+            cudaFree(w->ws);
+        }
+        w->ws = nullptr;
+        w->ws_bytes = 0;
+        if (cudaMalloc(&w->ws, ws_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            w->ws = nullptr;
+            return nullptr;
+        }
+        w->ws_bytes = ws_bytes;
+    }
+    if (w->nflags < nflags) {
+        if (w->flags) {
+            cudaStreamSynchronize(s);
+            cudaFree(w->flags);
+        }
+        w->flags = nullptr;
+        w->nflags = 0;
+        if (cudaMalloc(&w->flags, nflags * sizeof(uint32_t)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        cudaMemsetAsync(w->flags, 0, nflags * sizeof(uint32_t), s);
+        w->nflags = nflags;
+        w->epoch = 0;
+    }
+    return w;
+}
+
 int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
     return make_tmap_bf16_ld(map, base, rows, cols, cols, box_rows);
 }
 
+namespace {
+int encode_2d(CUtensorMap* map, const void* base, bool f32, int64_t rows, int64_t cols, int64_t ld,
+              int box_cols, int box_rows);
+}
 int make_tmap_bf16_ld(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
                       int box_rows) {
     EE_REQUIRE(((uintptr_t)base & 15) == 0 && cols % 8 == 0 && ld % 8 == 0 && ld >= cols,
                EE_ESHAPE, "tensor map: base must be 16-B aligned, cols and ld multiples of 8");
+    return encode_2d(map, base, false, rows, cols, ld, BK, box_rows);
+}
+
+int make_tmap_out(CUtensorMap* map, const void* base, int elem_bytes, int64_t rows, int64_t cols,
+                  int64_t ld) {
+    const int per16 = 16 / elem_bytes;
+    EE_REQUIRE(((uintptr_t)base & 15) == 0 && cols % per16 == 0 && ld % per16 == 0 && ld >= cols,
+               EE_ESHAPE, "output tensor map: base 16-B aligned, cols and ld 16-B multiples");
+    return encode_2d(map, base, elem_bytes == 4, rows, cols, ld, 128 / elem_bytes, 32);
+}
+
+namespace {
+int encode_2d(CUtensorMap* map, const void* base, bool f32, int64_t rows, int64_t cols, int64_t ld,
+              int box_cols, int box_rows) {
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * (f32 ? 4 : 2)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     // resolved through the runtime so libee.so does not link libcuda (the
     // build container has no driver; the GPU box does)
@@ -370,7 +466,8 @@ int make_tmap_bf16_ld(CUtensorMap* map, const void* base, int64_t rows, int64_t 
             return ee_fail(EE_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
         encode = (EncodeFn)fn;
     }
-    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)base, dims,
+    CUresult r = encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                        2, (void*)base, dims,
                                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                         CU_TENSOR_MAP_SWIZZLE_128B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -378,6 +475,7 @@ int make_tmap_bf16_ld(CUtensorMap* map, const void* base, int64_t rows, int64_t 
     EE_REQUIRE(r == CUDA_SUCCESS, EE_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return EE_OK;
 }
+}  // namespace
 }  // namespace tc
 
 size_t exit_head_train_ws_bytes(int64_t n, int64_t /*h*/, int64_t V) { return carve_bytes(n, V); }

@@ -27,9 +27,41 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 struct EpiBf16 {
     static constexpr bool kTwoPass = false;
     static constexpr bool kSplitK = false;
+    static constexpr bool kStreamK = true;  // stream-K tail allowed (tc_gemm.cuh)
+    static constexpr bool kStaged = true;   // TMA-stored output boxes (tc_gemm.cuh)
+    static constexpr bool kReduceAdd = false;
+    using OutT = bf16;
     bf16* out;
     const bf16* res;  // nullable
     int ld;
+    int out_map(CUtensorMap* m, int M, int N) const { return tc::make_tmap_out(m, out, 2, M, N, ld); }
+    // 16 outputs of a chunk: accumulator + residual, one rounding
+    __device__ void stage(int row, int col, const float* v0, int nvalid, bf16* o) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = v0[j];
+        if (res && nvalid > 0) {
+            const int64_t off = (int64_t)row * ld + col;
+            if (nvalid == 16) {
+                const uint4 r0 = reinterpret_cast<const uint4*>(res + off)[0];
+                const uint4 r1 = reinterpret_cast<const uint4*>(res + off)[1];
+                const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                    v[2 * q] += f.x;
+                    v[2 * q + 1] += f.y;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (j < nvalid) v[j] += __bfloat162float(res[off + j]);
+            }
+        }
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o32[q] = pack2(v[2 * q], v[2 * q + 1]);
+    }
     // the half-row's residual (BN/2 bf16 = 256 B, two lines) is pulled into
     // L1 before the accumulator chunks stream out of TMEM, so the per-chunk
     // residual loads hit L1 instead of waiting on HBM one chunk at a time
@@ -103,3 +135,10 @@ extern "C" int ee_linear_dgrad(const void* dY, const void* W, int64_t T, int64_t
         dY, W, (int)T, (int)K, (int)N, EpiBf16{(bf16*)dX, (const bf16*)R, (int)K},
         as_stream(stream));
 }
+
+#ifdef EE_TRACE
+extern "C" int ee_trace_gemm(unsigned long long* tl, int* units) {
+    cudaMemcpyFromSymbol(tl, tc::g_gemm_tl, sizeof(tc::g_gemm_tl));
+    return (int)cudaMemcpyFromSymbol(units, tc::g_gemm_unit, sizeof(tc::g_gemm_unit));
+}
+#endif

@@ -37,6 +37,8 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 struct EpiGeluUp {
     static constexpr bool kTwoPass = false;
     static constexpr bool kSplitK = false;
+    static constexpr bool kStreamK = true;  // stream-K tail allowed (tc_gemm.cuh)
+    static constexpr bool kStaged = false;  // two outputs: per-thread row stores
     bf16* pre;
     bf16* act;
     int ld;
@@ -78,9 +80,37 @@ struct EpiGeluUp {
 struct EpiGeluBwd {
     static constexpr bool kTwoPass = false;
     static constexpr bool kSplitK = false;
+    static constexpr bool kStreamK = true;  // stream-K tail allowed (tc_gemm.cuh)
+    static constexpr bool kStaged = true;   // TMA-stored output boxes (tc_gemm.cuh)
+    static constexpr bool kReduceAdd = false;
+    using OutT = bf16;
     const bf16* pre;
     bf16* dpre;
     int ld;
+    int out_map(CUtensorMap* m, int M, int N) const { return tc::make_tmap_out(m, dpre, 2, M, N, ld); }
+    __device__ void stage(int row, int col, const float* v, int nvalid, bf16* o) {
+        const bf16* pi = pre + (int64_t)row * ld + col;
+        float x[16];
+        if (nvalid == 16) {
+            const uint4 u0 = reinterpret_cast<const uint4*>(pi)[0];
+            const uint4 u1 = reinterpret_cast<const uint4*>(pi)[1];
+            const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+                x[2 * q] = f.x;
+                x[2 * q + 1] = f.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] = j < nvalid ? __bfloat162float(pi[j]) : 0.f;
+        }
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            o32[q] = pack2(__bfloat162float(__float2bfloat16_rn(v[2 * q])) * gelu_grad(x[2 * q]),
+                           __bfloat162float(__float2bfloat16_rn(v[2 * q + 1])) * gelu_grad(x[2 * q + 1]));
+    }
     __device__ void begin_tile(int, int, int, bool) {}
     __device__ void end_tile(int, int, int, bool) {}
     __device__ void chunk(int row, int col, const float* v, int nvalid) {

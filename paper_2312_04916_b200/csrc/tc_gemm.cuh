@@ -381,6 +381,9 @@ struct Cfg2 {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = 2 * BN;
     static constexpr size_t kSmem = (size_t)kStages2 * kStageBytes + 1024 + 256;
+    // + per-epilogue-warp 4 KB staging boxes for TMA-stored epilogues
+    static constexpr size_t kStageOff = (size_t)kStages2 * kStageBytes + 1024;  // from aligned base
+    static constexpr size_t kSmemStaged = kStageOff + kEpiWarps * 4096 + 1024;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -437,10 +440,285 @@ __device__ __forceinline__ void epi_set_split(Epi& epi, int s, int t) {
     if constexpr (Epi::kSplitK) epi.set_split(s, t);
 }
 
+// TMA-stored epilogues (Epi::kStaged): each epilogue warp converts its 32
+// rows x (128 B of output columns) into a 4 KB SW128 box in shared memory and
+// one lane stores the box with cp.async.bulk.tensor (or reduce-adds it:
+// Epi::kReduceAdd, float32 accumulation in L2 without a read in the SM) --
+// coalesced and asynchronous, instead of 32 scattered row segments per
+// store instruction.  Epi::stage(row, col, v[16], nvalid, o[16]) makes the
+// 16 outputs of a chunk; the box is clipped to the matrix by the TMA unit.
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <bool kAdd>
+__device__ __forceinline__ void tma_store_box2d(const CUtensorMap* m, const void* src, int c0, int r0) {
+    if constexpr (kAdd)
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(m),
+            "r"(su32(src)), "r"(c0), "r"(r0)
+            : "memory");
+    else
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(m),
+                     "r"(su32(src)), "r"(c0), "r"(r0)
+                     : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <class Epi>
+struct StagedOut {
+    static constexpr bool value = false;
+};
+
+// Stream-K tail.  A persistent grid of ncl clusters over T tiles leaves
+// 1 - (T mod ncl) / ncl of the last wave idle (the 256-tile backbone shapes
+// on 74 clusters: 86.5% busy).  With the tail on, the LAST sk_tiles tiles
+// (the partial wave plus one whole wave) have their k-blocks, flattened
+// tile-major, cut into ncl equal ranges of w blocks, one per cluster; the
+// first dp_items tiles run whole, round-robin, afterwards.  A cluster runs
+// its range first, one piece per tile touched:
+//   * the piece at the range's end, without the tile's last k-block, is a
+//     "writer" and runs first: fp32 partial into the cluster's own slot,
+//     then a release flag (= this launch's epoch);
+//   * the piece at the range's start, with the tile's last k-block but not
+//     its first, is the "owner" and runs last: it waits for the flags of
+//     the lower clusters holding the tile's earlier k-blocks, adds their
+//     partials (cluster order = k order) to its accumulator, then takes the
+//     normal epilogue;
+//   * pieces covering a whole tile take the normal epilogue.
+// Owners only wait on LOWER clusters' first pieces: no deadlock (clusters
+// are dispatched in index order) and no wait in practice.  The summation
+// order is a function of the shape only, so results are deterministic.
+// Used where it measured faster (tools/time_gemm.py, C2 shapes): a partial
+// last wave (plain schedule < 92% busy), at least one whole wave, and >= 64
+// k-blocks per tile -- e.g. the 256-tile dgrad / wgrad / W2 shapes (-3..-6%);
+// not the 2048 x 2048 (64 tiles) weight gradient or K = 2048 forwards, which
+// measured 2-10% slower with it.
+struct SkArgs {
+    int dp_items = 0;           // whole tiles first (all items when sk_tiles == 0)
+    int sk_tiles = 0;           // tiles in the stream-K region (0: off)
+    int w = 0;                  // k-blocks per cluster range
+    float* ws = nullptr;        // [ncl][2 ranks][128 x BN] fp32 partial slots
+    uint32_t* flags = nullptr;  // [ncl][2]
+    uint32_t epoch = 0;
+};
+enum : int { kUnitWhole = 0, kUnitWriter = 1, kUnitOwner = 2 };
+#ifdef EE_TRACE
+// per cluster (<= 80) and unit (<= 12): MMA start / MMA issued / epilogue
+// start / epilogue end (%globaltimer), and (tile, k0, k1, role) of the unit
+static __device__ unsigned long long g_gemm_tl[80][12][4];
+static __device__ int g_gemm_unit[80][12][4];
+#define GEMM_TL(c, j, e) do { if ((c) < 80 && (j) < 12) g_gemm_tl[c][j][e] = ee_gtime(); } while (0)
+#define GEMM_UNIT(c, j, u)                                                             \
+    do {                                                                               \
+        if ((c) < 80 && (j) < 12) {                                                    \
+            g_gemm_unit[c][j][0] = (u).t; g_gemm_unit[c][j][1] = (u).k0;                \
+            g_gemm_unit[c][j][2] = (u).k1; g_gemm_unit[c][j][3] = (u).role;             \
+        }                                                                              \
+    } while (0)
+#else
+#define GEMM_TL(c, j, e) do { } while (0)
+#define GEMM_UNIT(c, j, u) do { } while (0)
+#endif
+struct Unit {
+    int t, s, k0, k1, role;
+};
+// the unit sequence of one cluster; the producer, the MMA issuer and the
+// epilogue warps each walk an identical copy.  Stream-K pieces come first, in
+// the order [writer (range end), whole tiles, owner (range start)], then the
+// whole tiles of the round-robin part: the owner waits for the lower
+// cluster's FIRST piece, long finished by then.  (Owner second instead of
+// last, so that its epilogue overlaps later mainloops, measured slower: the
+// short owner piece then waits for the writer's epilogue.)
+struct UnitIter {
+    int cid, ncl, ntiles, nk, splits;
+    const SkArgs* sk;
+    int it;       // round-robin cursor
+    int j, np;    // stream-K piece cursor / count
+    int ta, tb;   // first / last tile of the range (stream-K tile numbering)
+    int64_t a, b; // range [a, b) of flattened k-blocks
+    __device__ UnitIter(int cid_, int ncl_, int ntiles_, int nk_, int splits_, const SkArgs* sk_)
+        : cid(cid_), ncl(ncl_), ntiles(ntiles_), nk(nk_), splits(splits_), sk(sk_), it(cid_), j(0),
+          np(0), ta(0), tb(0), a(0), b(0) {
+        if (sk->sk_tiles > 0) {
+            const int64_t total = (int64_t)sk->sk_tiles * nk;
+            a = min((int64_t)cid * sk->w, total);
+            b = min((int64_t)(cid + 1) * sk->w, total);
+            if (b > a) {
+                ta = (int)(a / nk);
+                tb = (int)((b - 1) / nk);
+                np = tb - ta + 1;
+            }
+        }
+    }
+    __device__ bool next(Unit& u) {
+        if (j < np) {
+            // piece order: tb, ta + 1, ..., tb - 1, ta
+            const int t = j == 0 ? tb : (j == np - 1 ? ta : ta + j);
+            ++j;
+            const int64_t ts = (int64_t)t * nk;
+            u.t = sk->dp_items + t;
+            u.s = 0;
+            u.k0 = (int)((a > ts ? a : ts) - ts);
+            u.k1 = (int)((b < ts + nk ? b : ts + nk) - ts);
+            u.role = u.k1 < nk ? kUnitWriter : (u.k0 > 0 ? kUnitOwner : kUnitWhole);
+            return true;
+        }
+        const int dp_limit = sk->sk_tiles > 0 ? sk->dp_items : ntiles * splits;
+        if (it < dp_limit) {
+            u.t = it % ntiles;
+            u.s = it / ntiles;
+            u.k0 = (int)((int64_t)nk * u.s / splits);
+            u.k1 = (int)((int64_t)nk * (u.s + 1) / splits);
+            u.role = kUnitWhole;
+            it += ncl;
+            return true;
+        }
+        return false;
+    }
+};
+// partial slot layout: [half][quarter][chunk][lane][16] fp32, so the writer's
+// and the owner's accesses (same thread -> same row) are contiguous per warp
+template <int BN>
+__device__ __forceinline__ float* sk_slot(const SkArgs& sk, int cl, uint32_t rank, int half,
+                                          int quarter, int lane) {
+    // chunk ch, quarter-of-chunk q of this lane at + ch * 512 + q * 128
+    return sk.ws + (size_t)(cl * 2 + (int)rank) * (128 * BN) +
+           (size_t)((half * 4 + quarter) * (BN / 32)) * 512 + lane * 4;
+}
+// the 16 partial values of chunk ch (4 coalesced 512-byte warp loads)
+template <int BN>
+__device__ __forceinline__ void sk_load(const SkArgs& sk, int c, uint32_t rank, int half, int quarter,
+                                        int lane, int ch, float4* f) {
+    const float4* p =
+        reinterpret_cast<const float4*>(sk_slot<BN>(sk, c, rank, half, quarter, lane) + (size_t)ch * 512);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f[q] = __ldcg(p + q * 32);
+}
+// chunk ch (16 columns) of the half-row += every contributing partial, in
+// cluster order
+template <int BN>
+__device__ __forceinline__ void sk_add(const SkArgs& sk, int c_first, int c_last, uint32_t rank,
+                                       int half, int quarter, int lane, int ch, float* v) {
+    for (int c = c_first; c <= c_last; ++c) {
+        float4 f[4];
+        sk_load<BN>(sk, c, rank, half, quarter, lane, ch, f);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[4 * q] += f[q].x;
+            v[4 * q + 1] += f[q].y;
+            v[4 * q + 2] += f[q].z;
+            v[4 * q + 3] += f[q].w;
+        }
+    }
+}
+__device__ __forceinline__ void sk_wait(const uint32_t* flag, uint32_t epoch) {
+    uint32_t f;
+    do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+    } while (f != epoch);
+}
+// the owner's epilogue: epilogue_half_row with the lower clusters' partials
+// added to the accumulator chunks first
+template <int BN, class Epi>
+__device__ __forceinline__ void epilogue_half_row_sk(Epi& epi, uint32_t base, int row, int M, int N,
+                                                     int col0, const SkArgs& sk, int c_first,
+                                                     int c_last, uint32_t rank, int half,
+                                                     int quarter, int lane) {
+    if constexpr (Epi::kTwoPass) {
+        float v[BN / 2];
+#pragma unroll
+        for (int c = 0; c < BN / 2; c += 16) tmem_ld16_nowait(base + c, v + c);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < BN / 2; c += 16)
+            sk_add<BN>(sk, c_first, c_last, rank, half, quarter, lane, c / 16, v + c);
+        if (row < M) {
+#pragma unroll
+            for (int c = 0; c < BN / 2; c += 16) {
+                const int nvalid = min(16, N - (col0 + c));
+                if (nvalid > 0) epi.pre(row, col0 + c, v + c, nvalid);
+            }
+#pragma unroll
+            for (int c = 0; c < BN / 2; c += 16) {
+                const int nvalid = min(16, N - (col0 + c));
+                if (nvalid > 0) epi.chunk(row, col0 + c, v + c, nvalid);
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 16) {
+            float v[16];
+            tmem_ld16(base + c, v);
+            sk_add<BN>(sk, c_first, c_last, rank, half, quarter, lane, c / 16, v);
+            if (row < M) {
+                const int nvalid = min(16, N - (col0 + c));
+                if (nvalid > 0) epi.chunk(row, col0 + c, v, nvalid);
+            }
+        }
+    }
+}
+
+// one (row, half-tile) through the warp's staging box: chunks of 16 columns
+// from TMEM (+ stream-K partials for an owner), Epi::stage, SW128 box writes,
+// one TMA store per 128 B of output columns
+template <int BN, class Epi>
+__device__ __forceinline__ void epilogue_half_row_staged(Epi& epi, uint32_t base, int row, int M, int N,
+                                                         int col0, int row0, uint8_t* stg,
+                                                         const CUtensorMap* tout, int lane, bool owner,
+                                                         const SkArgs& sk, int c_first, int c_last,
+                                                         uint32_t rank, int half, int quarter) {
+    using O = typename Epi::OutT;
+    constexpr int kBoxCols = 128 / (int)sizeof(O);  // 64 bf16 / 32 fp32 columns
+    constexpr int kUnits = 16 * (int)sizeof(O) / 16;  // 16-byte units per chunk
+    // owner: the partials of all chunks are loaded a whole box ahead of use
+    // (one cluster's partial in registers per chunk of the box; others, rare,
+    // are added with plain loads)
+    constexpr int kCh = kBoxCols / 16;
+    float4 pf[kCh][4];
+    if (Epi::kStreamK && owner)
+#pragma unroll
+        for (int cc = 0; cc < kCh; ++cc) sk_load<BN>(sk, c_first, rank, half, quarter, lane, cc, pf[cc]);
+#pragma unroll 1
+    for (int g = 0; g < (BN / 2) / kBoxCols; ++g) {
+        if (lane == 0) bulk_wait_read0();  // the previous box has left shared memory
+        __syncwarp();
+#pragma unroll
+        for (int cc = 0; cc < kCh; ++cc) {
+            const int c = g * kBoxCols + cc * 16;
+            float v[16];
+            tmem_ld16(base + c, v);
+            if (Epi::kStreamK && owner) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    v[4 * q] += pf[cc][q].x;
+                    v[4 * q + 1] += pf[cc][q].y;
+                    v[4 * q + 2] += pf[cc][q].z;
+                    v[4 * q + 3] += pf[cc][q].w;
+                }
+                if (g + 1 < (BN / 2) / kBoxCols)  // next box's chunk cc in flight
+                    sk_load<BN>(sk, c_first, rank, half, quarter, lane, c / 16 + kCh, pf[cc]);
+                if (c_last > c_first) sk_add<BN>(sk, c_first + 1, c_last, rank, half, quarter, lane, c / 16, v);
+            }
+            alignas(16) O o[16];
+            const int nvalid = row < M ? min(16, N - (col0 + c)) : 0;
+            epi.stage(row, col0 + c, v, nvalid, o);
+#pragma unroll
+            for (int k = 0; k < kUnits; ++k)
+                *reinterpret_cast<uint4*>(stg + lane * 128 + (((cc * kUnits + k) ^ (lane & 7)) << 4)) =
+                    reinterpret_cast<const uint4*>(o)[k];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && col0 + g * kBoxCols < N && row0 < M)
+            tma_store_box2d<Epi::kReduceAdd>(tout, stg, col0 + g * kBoxCols, row0);
+    }
+}
+
 template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M,
-           int N, int K, Epi epi, int splits) {
+           int N, int K, Epi epi, int splits, const __grid_constant__ SkArgs sk,
+           const __grid_constant__ CUtensorMap tout) {
     using C = Cfg2<BN>;
     constexpr int BM2 = 2 * BM;
     extern __shared__ uint8_t smem_raw[];
@@ -457,12 +735,6 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     const int tiles_m = (M + BM2 - 1) / BM2, tiles_n = (N + BN - 1) / BN;
     const int ntiles = tiles_m * tiles_n;
     const int nk = (K + BK - 1) / BK;
-    const int nitems = ntiles * splits;
-    auto kr = [&](int it, int& k0, int& k1) {
-        const int sp = it / ntiles;
-        k0 = (int)((int64_t)nk * sp / splits);
-        k1 = (int)((int64_t)nk * (sp + 1) / splits);
-    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages2; ++s) {
@@ -494,15 +766,15 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tb) : "memory");
             int s = 0;
             uint32_t ph = 0;
-            for (int it = cid; it < nitems; it += ncl) {
-                const int t = it % ntiles;
+            UnitIter ui(cid, ncl, ntiles, nk, splits, &sk);
+            Unit u;
+            while (ui.next(u)) {
+                const int t = u.t;
                 const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
                 const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
                 const int m0 = mb * BM2 + (int)rank * BM;
                 const int n0 = nb * BN + (int)rank * (BN / 2);
-                int k0, k1;
-                kr(it, k0, k1);
-                for (int kb = k0; kb < k1; ++kb) {
+                for (int kb = u.k0; kb < u.k1; ++kb) {
                     mb_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * C::kStageBytes;
                     const uint32_t bar = map_rank(&full[s], 0);
@@ -535,11 +807,17 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
             uint32_t ph = 0;
             int acc = 0;
             uint32_t aph = 0;
-            for (int it = cid; it < nitems; it += ncl) {
-                int k0, k1;
-                kr(it, k0, k1);
+            UnitIter ui(cid, ncl, ntiles, nk, splits, &sk);
+            Unit u;
+            int jt = 0;
+            while (ui.next(u)) {
+                const int k0 = u.k0, k1 = u.k1;
                 mb_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
+                if (lane == 0) {
+                    GEMM_TL(cid, jt, 0);
+                    GEMM_UNIT(cid, jt, u);
+                }
                 const uint32_t d = tmem + acc * BN;
                 for (int kb = k0; kb < k1; ++kb) {
                     mb_wait(&full[s], ph);
@@ -558,6 +836,8 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                     }
                 }
                 if (leader) tc_commit2(&tfull[acc]);  // both CTAs' accumulators ready
+                if (lane == 0) GEMM_TL(cid, jt, 1);
+                ++jt;
                 if (++acc == 2) {
                     acc = 0;
                     aph ^= 1;
@@ -572,30 +852,79 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         const uint32_t leader_tempty0 = map_rank(&tempty[0], 0);
         int acc = 0;
         uint32_t aph = 0;
-        for (int it = cid; it < nitems; it += ncl) {
-            const int t = it % ntiles;
+        UnitIter ui(cid, ncl, ntiles, nk, splits, &sk);
+        Unit u;
+        int jt = 0;
+        while (ui.next(u)) {
+            const int t = u.t;
             const int mb = N_FASTEST ? t / tiles_n : t % tiles_m;
             const int nb = N_FASTEST ? t % tiles_n : t / tiles_m;
-            epi_set_split(epi, it / ntiles, t);
+            epi_set_split(epi, u.s, t);
             mb_wait(&tfull[acc], aph);
             tc_fence_after();
+            if (rank == 0 && warp == 2 && lane == 0) GEMM_TL(cid, jt, 2);
             const int row = mb * BM2 + row_in_tile;
             const int col0 = nb * BN + half * (BN / 2);
             const int part = nb * 2 + half;
-            epi.begin_tile(row, col0, part, row < M);
             const uint32_t base =
                 tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * (BN / 2);
-            epilogue_half_row<BN>(epi, base, row, M, N, col0);
-            epi.end_tile(row, col0, part, row < M);
+            if (Epi::kStreamK && u.role == kUnitWriter) {
+                // this piece's fp32 partial into the cluster's slot
+                float* dst = sk_slot<BN>(sk, cid, rank, half, quarter, lane);
+#pragma unroll 1
+                for (int c = 0; c < BN / 2; c += 16) {
+                    float v[16];
+                    tmem_ld16(base + c, v);
+                    float4* d4 = reinterpret_cast<float4*>(dst + (size_t)(c / 16) * 512);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        __stcg(d4 + q * 32, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                }
+            } else {
+                epi.begin_tile(row, col0, part, row < M);
+                const bool owner = Epi::kStreamK && u.role == kUnitOwner;
+                int c_first = 0;
+                if (owner) {
+                    // the lower clusters holding k-blocks [0, k0) of this tile
+                    c_first = (int)((int64_t)(t - sk.dp_items) * nk / sk.w);
+                    for (int c = c_first; c < cid; ++c) sk_wait(sk.flags + c * 2 + rank, sk.epoch);
+                }
+                if constexpr (Epi::kStaged) {
+                    uint8_t* stg = smem + Cfg2<BN>::kStageOff + (size_t)(warp - 2) * 4096;
+                    epilogue_half_row_staged<BN>(epi, base, row, M, N, col0,
+                                                 mb * BM2 + (int)rank * BM + quarter * 32, stg, &tout,
+                                                 lane, owner, sk, c_first, cid - 1, rank, half, quarter);
+                } else if (owner) {
+                    epilogue_half_row_sk<BN>(epi, base, row, M, N, col0, sk, c_first, cid - 1, rank,
+                                             half, quarter, lane);
+                } else {
+                    epilogue_half_row<BN>(epi, base, row, M, N, col0);
+                }
+                epi.end_tile(row, col0, part, row < M);
+            }
             tc_fence_before();
             __syncwarp();
+            if (rank == 0 && warp == 2 && lane == 0) GEMM_TL(cid, jt, 3);
+            ++jt;
             if (lane == 0) mb_arrive_remote(leader_tempty0 + acc * 8);
+            if (Epi::kStreamK && u.role == kUnitWriter) {
+                // every epilogue warp of this CTA has stored its rows: publish
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                if (warp == 2 && lane == 0) {
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sk.flags + cid * 2 + rank),
+                                 "r"(sk.epoch)
+                                 : "memory");
+                }
+            }
             if (++acc == 2) {
                 acc = 0;
                 aph ^= 1;
             }
         }
     }
+    if constexpr (Epi::kStaged)
+        if (warp >= 2 && lane == 0) bulk_wait_all0();  // this warp's output boxes written
     tc_fence_before();
     cluster_sync_all();  // all MMAs consumed, all remote arrivals landed
     if (warp == 1) {
@@ -611,6 +940,10 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 // the same over a matrix with row stride ld >= cols (elements)
 int make_tmap_bf16_ld(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
                       int box_rows);
+// output map of a TMA-stored epilogue: (rows x cols) row stride ld, element
+// size 2 (bf16) or 4 (float32), box 128 B of columns x 32 rows, SW128
+int make_tmap_out(CUtensorMap* map, const void* base, int elem_bytes, int64_t rows, int64_t cols,
+                  int64_t ld);
 
 // C[M, N] = A . B^T with A given as (M, K) row-major (A_MN = false) or as
 // (K, M) row-major (A_MN = true); B likewise as (N, K) or (K, N).
@@ -635,7 +968,39 @@ int launch_tc_gemm(const void* A, const void* B, int M, int N, int K, Epi epi, c
 }
 
 
-// CTA-pair launch: M tiles of 256 rows, grid = 2 x min(tiles, SMs / 2).
+// Stream-K workspace of one stream: partial slots + flags, grown on demand;
+// the epoch makes flags from earlier launches stale without a memset.
+// Launches on one stream are ordered, so one workspace per stream suffices;
+// concurrent streams (the weight-gradient side stream) get their own.
+struct SkWs {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    float* ws = nullptr;
+    uint32_t* flags = nullptr;
+    size_t ws_bytes = 0;
+    int nflags = 0;
+    uint32_t epoch = 0;
+};
+SkWs* sk_workspace(cudaStream_t s, size_t ws_bytes, int nflags);  // nullptr: none free
+bool sk_enabled();  // EE_GEMM_STREAMK=0 turns the tail off (A/B)
+
+// the stream-K plan for T tiles of nk k-blocks on ncl clusters (sk_tiles = 0:
+// plain round-robin); see SkArgs
+inline SkArgs sk_plan(int tiles, int nk, int ncl) {
+    SkArgs a;
+    if (ncl <= 0 || tiles % ncl == 0 || tiles < ncl || nk < 64 || !sk_enabled()) return a;
+    const int full = tiles / ncl, rem = tiles % ncl;
+    if ((double)tiles / ((double)(full + 1) * ncl) >= 0.92) return a;  // tail already small
+    a.sk_tiles = rem + (full >= 1 ? ncl : 0);  // the partial wave plus one whole wave
+    a.dp_items = tiles - a.sk_tiles;
+    a.w = (int)(((int64_t)a.sk_tiles * nk + ncl - 1) / ncl);
+    if (a.w < 8) a.sk_tiles = 0;  // short k: not worth the partials
+    return a;
+}
+
+// CTA-pair launch: M tiles of 256 rows, grid = 2 x min(tiles, SMs / 2), or
+// 2 x SMs / 2 with the stream-K tail (epilogues with kStreamK, splits == 1,
+// not while the stream is being captured: the epoch is a launch argument).
 template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
 int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, cudaStream_t s,
                     int splits = 1) {
@@ -648,14 +1013,40 @@ int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, 
     static bool configured[16] = {};
     int dev = 0;
     cudaGetDevice(&dev);
+    constexpr size_t kSmemL = Epi::kStaged ? Cfg2<BN>::kSmemStaged : Cfg2<BN>::kSmem;
     if (!configured[dev & 15]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg2<BN>::kSmem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemL);
         configured[dev & 15] = true;
     }
-    const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * splits;
+    CUtensorMap tout;
+    memset(&tout, 0, sizeof(tout));
+    if constexpr (Epi::kStaged) {
+        if ((rc = epi.out_map(&tout, M, N))) return rc;
+    }
+    const int tiles1 = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+    const int tiles = tiles1 * splits;
     const int pairs = ee_sm_count() / 2;
-    const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    kern<<<grid, kThreads, Cfg2<BN>::kSmem, s>>>(ta, tb, M, N, K, epi, splits);
+    int ncl = tiles < pairs ? tiles : pairs;
+    SkArgs sk;
+    if constexpr (Epi::kStreamK) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (splits == 1 && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
+            cap == cudaStreamCaptureStatusNone) {
+            sk = sk_plan(tiles1, (K + BK - 1) / BK, pairs);
+            if (sk.sk_tiles > 0) {
+                SkWs* w = sk_workspace(s, (size_t)pairs * 2 * 128 * BN * sizeof(float), pairs * 2);
+                if (w) {
+                    sk.ws = w->ws;
+                    sk.flags = w->flags;
+                    sk.epoch = ++w->epoch;
+                    ncl = pairs;
+                } else {
+                    sk = SkArgs{};
+                }
+            }
+        }
+    }
+    kern<<<2 * ncl, kThreads, kSmemL, s>>>(ta, tb, M, N, K, epi, splits, sk, tout);
     return ee_check_launch("tc_gemm2");
 }
 

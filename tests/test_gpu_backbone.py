@@ -94,6 +94,44 @@ def test_linear_fwd_dgrad_match_fp32(T, K, N):
     assert _rel(y0.double().cpu().numpy(), (x.float() @ w.float()).double().cpu().numpy()) < 1e-2
 
 
+@pytest.mark.parametrize("kind,T,K,N", [("fwd", 8192, 4096, 1024), ("fwd", 8000, 4096, 1000),
+                                        ("wgrad", 4096, 4096, 1280), ("wgrad", 4000, 4096, 1272)])
+def test_gemm_stream_k_tail_matches_fp32_and_repeats(kind, T, K, N):
+    """The CTA-pair GEMM's stream-K tail (tc_gemm.cuh: the last wave's tiles'
+    k-blocks spread over all clusters, owners adding lower clusters' fp32
+    partials) on shapes that take it (a partial last wave, >= 64 k-blocks),
+    two with ragged edges: Y = X W (ee_linear_fwd, 128 tiles x 64 k-blocks)
+    against float32 torch within 1e-2, and dW += X^T dY (ee_wgrad_accum,
+    80 tiles, float32 TMA reduce-add in place) within 1e-3 of the float64
+    reference; a second run is bitwise equal (fixed summation order)."""
+    import torch
+    from paper_2312_04916_b200 import _lib
+    from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+    _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(7 * T + K + N)
+    x = torch.randn(T, K, device="cuda", generator=g).bfloat16()
+    if kind == "fwd":
+        w = (torch.randn(K, N, device="cuda", generator=g) * 0.02).bfloat16()
+        y1 = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
+        y2 = torch.empty_like(y1)
+        call("ee_linear_fwd", ptr(x), ptr(w), T, K, N, None, ptr(y1), stream_ptr())
+        call("ee_linear_fwd", ptr(x), ptr(w), T, K, N, None, ptr(y2), stream_ptr())
+        torch.cuda.synchronize()
+        ref = x.float() @ w.float()
+        assert _rel(y1.double().cpu().numpy(), ref.double().cpu().numpy()) < 1e-2
+        assert torch.equal(y1, y2)
+    else:
+        dy = torch.randn(T, N, device="cuda", generator=g).bfloat16()
+        dw0 = torch.randn(K, N, device="cuda", generator=g)
+        dw1, dw2 = dw0.clone(), dw0.clone()
+        call("ee_wgrad_accum", ptr(x), ptr(dy), T, K, N, ptr(dw1), stream_ptr())
+        call("ee_wgrad_accum", ptr(x), ptr(dy), T, K, N, ptr(dw2), stream_ptr())
+        torch.cuda.synchronize()
+        rdw = dw0.double() + x.double().t() @ dy.double()
+        assert _rel(dw1.double().cpu().numpy(), rdw.cpu().numpy()) < 1e-3
+        assert torch.equal(dw1, dw2)
+
+
 @pytest.mark.parametrize("n,h", [(37, 264), (4096, 2048), (1000, 5120)])
 def test_rmsnorm_fork_joins_residual_gradient(n, h):
     """`rmsnorm_fork` (ee_rmsnorm_bwd with gres): the residual branch's

@@ -1,4 +1,9 @@
-"""Kernel-time census (torch.profiler / CUPTI) of one C2 training step."""
+"""Kernel-time census (torch.profiler / CUPTI) of one C2 training step:
+per-kernel time, the step's span, and the span's GPU-idle share (no kernel
+of either stream running).
+
+    python tools/prof_train_step.py [M mb]      (default 4 4, as bench.py)
+"""
 import os
 import sys
 
@@ -16,7 +21,8 @@ from paper_2312_04916_b200.training import Adam, apply_update  # noqa: E402
 
 
 def main():
-    M, mb, seq = 8, 2, 2048
+    M, mb = (int(a) for a in sys.argv[1:3]) if len(sys.argv) > 2 else (4, 4)
+    seq = 2048
     cfg = T.c2_config()
     master = build_model(cfg, 0, init="device", dtype=torch.float32)
     opt = Adam(3e-4)
@@ -46,7 +52,18 @@ def main():
         a[0] += 1
         a[1] += e.time_range.end - e.time_range.start
     tot = sum(v[1] for v in agg.values())
-    print(f"span {span/1e3:.1f} ms, kernel time {tot/1e3:.1f} ms, {len(ev)} kernels")
+    busy, cur_s, cur_e = 0.0, None, None
+    for e in ev:  # union of kernel intervals
+        a, b = e.time_range.start, e.time_range.end
+        if cur_e is None or a > cur_e:
+            if cur_e is not None:
+                busy += cur_e - cur_s
+            cur_s, cur_e = a, b
+        else:
+            cur_e = max(cur_e, b)
+    busy += cur_e - cur_s
+    print(f"M={M} mb={mb}: span {span/1e3:.1f} ms, kernel time {tot/1e3:.1f} ms, {len(ev)} kernels, "
+          f"GPU idle {100 * (1 - busy / span):.1f}% of the span")
     for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
         print(f"{t/1e3:8.2f} ms {100*t/tot:5.1f}% {c:6d}  {k}")
 
