@@ -352,6 +352,23 @@ int ee_linear_fwd(const void* X, const void* W, int64_t T, int64_t K, int64_t N,
 int ee_linear_dgrad(const void* dY, const void* W, int64_t T, int64_t K, int64_t N, const void* R,
                     void* dX, void* stream);
 
+/* Stacked variants: `parts` same-shape (K x N) weight matrices adjacent in
+ * memory (W_j = W + j K N; the q / k / v projections of one block in the
+ * flat parameter buffer) as ONE GEMM each way (replaces the three h1 @ wq,
+ * h1 @ wk, h1 @ wv matmuls of eepipe/model.py:207-216 and their backward,
+ * eepipe/autodiff.py:158-179):
+ *   ee_linear_fwd_stacked:   Y (T x parts N) = X [W_0 | ... | W_{p-1}]
+ *   ee_linear_dgrad_stacked: dX (T x K) = dY (T x parts N) [W_0 | ...]^T [+ R]
+ *   ee_wgrad_accum_stacked:  dW_j (in x out, float32, dW_j = dW + j in out)
+ *                            += X^T dY[:, j out : (j + 1) out]
+ * N (out, in) multiples of 128, K a multiple of 64. */
+int ee_linear_fwd_stacked(const void* X, const void* W, int64_t T, int64_t K, int64_t N,
+                          int64_t parts, void* Y, void* stream);
+int ee_linear_dgrad_stacked(const void* dY, const void* W, int64_t T, int64_t K, int64_t N,
+                            int64_t parts, const void* R, void* dX, void* stream);
+int ee_wgrad_accum_stacked(const void* X, const void* dY, int64_t T, int64_t in, int64_t out,
+                           int64_t parts, float* dW, void* stream);
+
 /* ---- training backbone causal attention (tcgen05, flash-style) ---------
  * `causal_attention` forward / backward (eepipe/autodiff.py:265-298) and the
  * boundary kernels attention_fwd / attention_bwd (eepipe/_pykernels.py:52-62,

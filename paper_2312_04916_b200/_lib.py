@@ -123,6 +123,12 @@ SIGNATURES = {
                               c_void_p]),
     "ee_linear_dgrad": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p,
                                 c_void_p]),
+    "ee_linear_fwd_stacked": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                                      c_void_p, c_void_p]),
+    "ee_linear_dgrad_stacked": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                                        c_void_p, c_void_p, c_void_p]),
+    "ee_wgrad_accum_stacked": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                                       c_void_p, c_void_p]),
     "ee_attn_train_fwd": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64,
                                   c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
     "ee_attn_train_bwd": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p,

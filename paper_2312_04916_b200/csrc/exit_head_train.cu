@@ -597,3 +597,19 @@ extern "C" int ee_wgrad_accum(const void* X, const void* dY, int64_t T, int64_t 
     return tc::launch_tc_gemm2<kBN, true, true, true>(X, dY, (int)in, (int)out, (int)T,
                                                      EpiF32<true>{dW, (int)out}, as_stream(stream));
 }
+
+// Weight gradients of `parts` adjacent (in, out) matrices in one GEMM:
+// dW_j += X^T dY[:, j out : (j + 1) out], dW_j = dW + j in out (the float32
+// sums of q / k / v are adjacent in the flat gradient buffer): the output is
+// stored stacked (tc_gemm.cuh, osub), dY is one (T, parts out) matrix.
+extern "C" int ee_wgrad_accum_stacked(const void* X, const void* dY, int64_t T, int64_t in,
+                                      int64_t out, int64_t parts, float* dW, void* stream) {
+    EE_REQUIRE(T > 0 && parts >= 1 && in % 128 == 0 && out % 128 == 0, EE_ESHAPE,
+               "wgrad_accum_stacked: in and out must be multiples of 128 (T=%lld in=%lld out=%lld)",
+               (long long)T, (long long)in, (long long)out);
+    EE_REQUIRE(T < (1ll << 31) && in * parts < (1ll << 31) && out * parts < (1ll << 31), EE_ESHAPE,
+               "wgrad_accum_stacked: too large");
+    return tc::launch_tc_gemm2<kBN, true, true, true>(X, dY, (int)in, (int)(out * parts), (int)T,
+                                                     EpiF32<true>{dW, (int)out}, as_stream(stream),
+                                                     1, 0, (int)out);
+}

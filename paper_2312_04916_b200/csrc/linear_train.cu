@@ -136,6 +136,37 @@ extern "C" int ee_linear_dgrad(const void* dY, const void* W, int64_t T, int64_t
         as_stream(stream));
 }
 
+// q / k / v of one block as ONE GEMM each way: the three (K, N) weight
+// matrices are adjacent in the flat parameter buffer (W_j = W + j K N), so
+// they are read as one stacked operand (tc_gemm.cuh, bsub):
+//   fwd:    Y (T, parts N) = X [W_0 | ... | W_{p-1}]
+//   dgrad:  dX (T, K) = dY (T, parts N) [W_0 | ... | W_{p-1}]^T [+ R]
+// One wide GEMM instead of three 2048-wide ones: fewer partial waves and
+// epilogue tails (eepipe/model.py:207-216 computes h1 @ wq, h1 @ wk, h1 @ wv).
+extern "C" int ee_linear_fwd_stacked(const void* X, const void* W, int64_t T, int64_t K, int64_t N,
+                                     int64_t parts, void* Y, void* stream) {
+    int rc;
+    if ((rc = check("linear_fwd_stacked", T, K, N * parts))) return rc;
+    EE_REQUIRE(parts >= 1 && N % 128 == 0 && K % 64 == 0, EE_ESHAPE,
+               "linear_fwd_stacked: N %% 128 and K %% 64 must be 0 (K=%lld N=%lld)", (long long)K,
+               (long long)N);
+    return tc::launch_tc_gemm2<kBN, false, true, false>(
+        X, W, (int)T, (int)(N * parts), (int)K, EpiBf16{(bf16*)Y, nullptr, (int)(N * parts)},
+        as_stream(stream), 1, (int)N);
+}
+
+extern "C" int ee_linear_dgrad_stacked(const void* dY, const void* W, int64_t T, int64_t K,
+                                       int64_t N, int64_t parts, const void* R, void* dX,
+                                       void* stream) {
+    int rc;
+    if ((rc = check("linear_dgrad_stacked", T, K, N * parts))) return rc;
+    EE_REQUIRE(parts >= 1 && N % 128 == 0, EE_ESHAPE,
+               "linear_dgrad_stacked: N %% 128 must be 0 (N=%lld)", (long long)N);
+    return tc::launch_tc_gemm2<kBN, false, false, false>(
+        dY, W, (int)T, (int)K, (int)(N * parts), EpiBf16{(bf16*)dX, (const bf16*)R, (int)K},
+        as_stream(stream), 1, (int)N);
+}
+
 #ifdef EE_TRACE
 extern "C" int ee_trace_gemm(unsigned long long* tl, int* units) {
     cudaMemcpyFromSymbol(tl, tc::g_gemm_tl, sizeof(tc::g_gemm_tl));

@@ -666,7 +666,8 @@ __device__ __forceinline__ void epilogue_half_row_staged(Epi& epi, uint32_t base
                                                          int col0, int row0, uint8_t* stg,
                                                          const CUtensorMap* tout, int lane, bool owner,
                                                          const SkArgs& sk, int c_first, int c_last,
-                                                         uint32_t rank, int half, int quarter) {
+                                                         uint32_t rank, int half, int quarter,
+                                                         int osub) {
     using O = typename Epi::OutT;
     constexpr int kBoxCols = 128 / (int)sizeof(O);  // 64 bf16 / 32 fp32 columns
     constexpr int kUnits = 16 * (int)sizeof(O) / 16;  // 16-byte units per chunk
@@ -709,8 +710,12 @@ __device__ __forceinline__ void epilogue_half_row_staged(Epi& epi, uint32_t base
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0 && col0 + g * kBoxCols < N && row0 < M)
-            tma_store_box2d<Epi::kReduceAdd>(tout, stg, col0 + g * kBoxCols, row0);
+        if (lane == 0 && col0 + g * kBoxCols < N && row0 < M) {
+            // stacked output (osub > 0): column block j below block j - 1
+            const int c = col0 + g * kBoxCols;
+            tma_store_box2d<Epi::kReduceAdd>(tout, stg, osub ? c % osub : c,
+                                             osub ? (c / osub) * M + row0 : row0);
+        }
     }
 }
 
@@ -718,7 +723,7 @@ template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M,
            int N, int K, Epi epi, int splits, const __grid_constant__ SkArgs sk,
-           const __grid_constant__ CUtensorMap tout) {
+           const __grid_constant__ CUtensorMap tout, int bsub, int osub) {
     using C = Cfg2<BN>;
     constexpr int BM2 = 2 * BM;
     extern __shared__ uint8_t smem_raw[];
@@ -785,11 +790,17 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                     } else {
                         tma_load_2d_pair(st, &ta, kb * BK, m0, bar);
                     }
+                    // stacked B (bsub > 0, launch_tc_gemm2): logical column
+                    // block j of width bsub lives below block j - 1 in memory
                     if (B_MN) {
+                        const int bc = bsub ? n0 % bsub : n0;
+                        const int br = bsub ? (n0 / bsub) * K + kb * BK : kb * BK;
                         for (int c = 0; c < BN / 128; ++c)
-                            tma_load_2d_pair(st + kABytes + c * 8192, &tb, n0 + c * 64, kb * BK, bar);
+                            tma_load_2d_pair(st + kABytes + c * 8192, &tb, bc + c * 64, br, bar);
                     } else {
-                        tma_load_2d_pair(st + kABytes, &tb, kb * BK, n0, bar);
+                        const int kk = kb * BK;
+                        tma_load_2d_pair(st + kABytes, &tb, bsub ? kk % bsub : kk,
+                                         bsub ? (kk / bsub) * N + n0 : n0, bar);
                     }
                     if (++s == kStages2) {
                         s = 0;
@@ -893,7 +904,8 @@ k_tc_gemm2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                     uint8_t* stg = smem + Cfg2<BN>::kStageOff + (size_t)(warp - 2) * 4096;
                     epilogue_half_row_staged<BN>(epi, base, row, M, N, col0,
                                                  mb * BM2 + (int)rank * BM + quarter * 32, stg, &tout,
-                                                 lane, owner, sk, c_first, cid - 1, rank, half, quarter);
+                                                 lane, owner, sk, c_first, cid - 1, rank, half, quarter,
+                                                 osub);
                 } else if (owner) {
                     epilogue_half_row_sk<BN>(epi, base, row, M, N, col0, sk, c_first, cid - 1, rank,
                                              half, quarter, lane);
@@ -1001,14 +1013,31 @@ inline SkArgs sk_plan(int tiles, int nk, int ncl) {
 // CTA-pair launch: M tiles of 256 rows, grid = 2 x min(tiles, SMs / 2), or
 // 2 x SMs / 2 with the stream-K tail (epilogues with kStreamK, splits == 1,
 // not while the stream is being captured: the epoch is a launch argument).
+//
+// Stacked operands (several same-shape matrices adjacent in memory, e.g. the
+// q / k / v projections in the flat parameter buffer), one GEMM for all:
+//   bsub > 0: B is the logical concatenation along its N (B_MN) or K (K-major)
+//     axis of blocks of width bsub, block j stored below block j - 1
+//     (B_MN: (K, bsub) blocks; K-major: (N, bsub) blocks);
+//   osub > 0: the output likewise, (M, osub) blocks (staged epilogues only).
+// Tiles and TMA boxes never straddle a block: bsub / osub multiples of 128
+// (and K % 64 == 0 for a stacked B_MN, M % 32 == 0 for a stacked output).
 template <int BN, bool A_MN, bool B_MN, bool N_FASTEST, class Epi>
 int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, cudaStream_t s,
-                    int splits = 1) {
+                    int splits = 1, int bsub = 0, int osub = 0) {
     CUtensorMap ta, tb;
     int rc;
+    EE_REQUIRE(bsub == 0 || (bsub % 128 == 0 && (B_MN ? N % bsub == 0 && K % BK == 0 : K % bsub == 0)),
+               EE_ESHAPE, "tc_gemm2: bad stacked B (bsub %d, N %d, K %d)", bsub, N, K);
+    EE_REQUIRE(osub == 0 || (Epi::kStaged && osub % 128 == 0 && N % osub == 0 && M % 32 == 0),
+               EE_ESHAPE, "tc_gemm2: bad stacked output (osub %d, M %d, N %d)", osub, M, N);
     if ((rc = A_MN ? make_tmap_bf16(&ta, A, K, M, BK) : make_tmap_bf16(&ta, A, M, K, BM))) return rc;
-    if ((rc = B_MN ? make_tmap_bf16(&tb, B, K, N, BK) : make_tmap_bf16(&tb, B, N, K, BN / 2)))
-        return rc;
+    if (bsub)
+        rc = B_MN ? make_tmap_bf16(&tb, B, (int64_t)(N / bsub) * K, bsub, BK)
+                  : make_tmap_bf16(&tb, B, (int64_t)(K / bsub) * N, bsub, BN / 2);
+    else
+        rc = B_MN ? make_tmap_bf16(&tb, B, K, N, BK) : make_tmap_bf16(&tb, B, N, K, BN / 2);
+    if (rc) return rc;
     auto kern = k_tc_gemm2<BN, A_MN, B_MN, N_FASTEST, Epi>;
     static bool configured[16] = {};
     int dev = 0;
@@ -1021,7 +1050,8 @@ int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, 
     CUtensorMap tout;
     memset(&tout, 0, sizeof(tout));
     if constexpr (Epi::kStaged) {
-        if ((rc = epi.out_map(&tout, M, N))) return rc;
+        if ((rc = osub ? epi.out_map(&tout, (N / osub) * M, osub) : epi.out_map(&tout, M, N)))
+            return rc;
     }
     const int tiles1 = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
     const int tiles = tiles1 * splits;
@@ -1046,7 +1076,7 @@ int launch_tc_gemm2(const void* A, const void* B, int M, int N, int K, Epi epi, 
             }
         }
     }
-    kern<<<2 * ncl, kThreads, kSmemL, s>>>(ta, tb, M, N, K, epi, splits, sk, tout);
+    kern<<<2 * ncl, kThreads, kSmemL, s>>>(ta, tb, M, N, K, epi, splits, sk, tout, bsub, osub);
     return ee_check_launch("tc_gemm2");
 }
 

@@ -263,6 +263,62 @@ def _wgrad_accum(x2, g2, acc):
     g2.record_stream(side)
 
 
+def _wgrad_accum_stacked(x2, g2, acc0, parts):
+    """Weight gradients of `parts` adjacent matrices in one GEMM
+    (ee_wgrad_accum_stacked): acc_j += x2^T g2[:, j N : (j + 1) N], g2 one
+    (T, parts N) row-major matrix, acc_j = the float32 sums that follow acc0
+    in the flat gradient buffer.  Same side stream as `_wgrad_accum`."""
+    torch = _torch()
+    T, K = x2.shape
+    N = g2.shape[1] // parts
+    cur = torch.cuda.current_stream(x2.device)
+    side = None
+    if _WGRAD_OVERLAP:
+        key = cur.cuda_stream
+        side = _WGRAD_SIDE.get(key)
+        if side is None:
+            side = _WGRAD_SIDE[key] = torch.cuda.Stream(x2.device)
+        side.wait_stream(cur)
+    st = ctypes.c_void_p(side.cuda_stream) if side is not None else stream_ptr()
+    call("ee_wgrad_accum_stacked", ptr(x2), ptr(g2), T, K, N, parts, ptr(acc0), st)
+    if side is not None:
+        x2.record_stream(side)
+        g2.record_stream(side)
+
+
+def _adjacent(ts):
+    """Equal-shape contiguous tensors stored back to back (the q / k / v
+    weights, and their float32 sums, in the flat parameter buffers)."""
+    t0 = ts[0]
+    nb = t0.numel() * t0.element_size()
+    return all(t.shape == t0.shape and t.dtype == t0.dtype and t.is_contiguous()
+               and t.data_ptr() == t0.data_ptr() + i * nb for i, t in enumerate(ts))
+
+
+def _row_ld(t):
+    """Row stride of a (B, S, h) tensor whose rows are evenly spaced with
+    unit column stride (a column block of a wider row-major buffer), else
+    None."""
+    if t.stride(-1) != 1 or (t.shape[0] > 1 and t.stride(0) != t.shape[1] * t.stride(1)):
+        return None
+    return t.stride(1)
+
+
+def _column_blocks(gs):
+    """The 2-D (T, N) views are consecutive column blocks of ONE row-major
+    (T, len(gs) N) buffer (what the fused q / k / v projection and the
+    attention backward produce): returns that buffer as a (T, len N) view,
+    else None."""
+    g0 = gs[0]
+    T, N = g0.shape
+    P = len(gs)
+    for i, g in enumerate(gs):
+        if (g.shape != g0.shape or g.dtype != g0.dtype or g.stride() != (P * N, 1)
+                or g.data_ptr() != g0.data_ptr() + i * N * g0.element_size()):
+            return None
+    return g0.as_strided((T, P * N), (P * N, 1))
+
+
 def join_wgrad(device=None):
     """Order the current stream after every weight-gradient accumulation
     issued from it (call before reading the float32 gradient sums)."""
@@ -274,6 +330,9 @@ def join_wgrad(device=None):
 
 
 _OWN_LINEAR = os.environ.get("EE_LINEAR", "1") != "0"  # A/B switch: 0 = cuBLAS (torch)
+# A/B switch: 0 = three q / k / v GEMMs each way instead of one stacked GEMM
+_STACKED_QKV = os.environ.get("EE_STACKED_QKV", "1") != "0"
+_STACKED_USES = [0]  # forward calls that took the stacked path (tests)
 
 
 def _linear_fwd(x2, w, res2=None):
@@ -363,12 +422,37 @@ class _QKVFn:
                     ctx.save_for_backward(x2, wq, wk, wv)
                     ctx.acc = (aq, ak, av)
                     ctx.shape = x.shape
+                    T, K = x2.shape
+                    N = wq.shape[1]
+                    ctx.stacked = (_STACKED_QKV and _adjacent((wq, wk, wv)) and _adjacent((aq, ak, av))
+                                   and N % 128 == 0 and K % 128 == 0)
+                    if ctx.stacked:
+                        _STACKED_USES[0] += 1
+                        # one GEMM over the adjacent weights; q, k, v are
+                        # column blocks of one (T, 3N) buffer (the attention
+                        # reads them in place through its row stride)
+                        y = torch.empty((T, 3 * N), dtype=x2.dtype, device=x2.device)
+                        call("ee_linear_fwd_stacked", ptr(x2), ptr(wq), T, K, N, 3, ptr(y),
+                             stream_ptr())
+                        y3 = y.view(*x.shape[:-1], 3 * N)
+                        return y3[..., :N], y3[..., N:2 * N], y3[..., 2 * N:]
                     return tuple(_linear_fwd(x2, w).view(*x.shape[:-1], w.shape[1])
                                  for w in (wq, wk, wv))
 
                 @staticmethod
                 def backward(ctx, gq, gk, gv):
                     x2, wq, wk, wv = ctx.saved_tensors
+                    if ctx.stacked and gq is not None and gk is not None and gv is not None:
+                        gs = [g.reshape(-1, g.shape[-1]) for g in (gq, gk, gv)]
+                        G = _column_blocks(gs) if gs[0].dtype == x2.dtype else None
+                        if G is not None:
+                            T, K = x2.shape
+                            N = wq.shape[1]
+                            gx = torch.empty((T, K), dtype=x2.dtype, device=x2.device)
+                            call("ee_linear_dgrad_stacked", ptr(G), ptr(wq), T, K, N, 3, None,
+                                 ptr(gx), stream_ptr())
+                            _wgrad_accum_stacked(x2, G, ctx.acc[0], 3)
+                            return gx.view(ctx.shape), None, None, None, None, None, None
                     gx = None
                     for g, w, acc in zip((gq, gk, gv), (wq, wk, wv), ctx.acc):
                         if g is None:
@@ -757,13 +841,20 @@ class _AttnFn:
                 @staticmethod
                 def forward(ctx, q, k, v, num_heads):
                     B, S, h = q.shape
-                    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-                    o = torch.empty_like(q)
+                    # q / k / v read in place when their rows are evenly
+                    # spaced (column blocks of the fused projection's output)
+                    q, k, v = (t if _row_ld(t) is not None else t.contiguous() for t in (q, k, v))
+                    lq, lk, lv = (_row_ld(t) for t in (q, k, v))
+                    o = torch.empty((B, S, h), dtype=q.dtype, device=q.device)
                     lse = torch.empty((B, num_heads, S), dtype=torch.float32, device=q.device)
-                    call("ee_attn_train_fwd", ptr(q), h, ptr(k), h, ptr(v), h, B, S, num_heads,
+                    call("ee_attn_train_fwd", ptr(q), lq, ptr(k), lk, ptr(v), lv, B, S, num_heads,
                          ptr(o), h, ptr(lse), stream_ptr())
                     ctx.save_for_backward(q, k, v, o, lse)
                     ctx.nh = num_heads
+                    # gradients as column blocks of one (B, S, 3h) buffer when
+                    # the inputs were (the fused q / k / v backward reads it)
+                    ctx.packed = (lq == lk == lv == 3 * h and k.data_ptr() == q.data_ptr() + 2 * h
+                                  and v.data_ptr() == q.data_ptr() + 4 * h)
                     return o
 
                 @staticmethod
@@ -771,11 +862,18 @@ class _AttnFn:
                     q, k, v, o, lse = ctx.saved_tensors
                     B, S, h = q.shape
                     do = do.to(q.dtype).contiguous()
-                    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+                    if ctx.packed:
+                        g = torch.empty((B, S, 3 * h), dtype=q.dtype, device=q.device)
+                        dq, dk, dv = g[..., :h], g[..., h:2 * h], g[..., 2 * h:]
+                        ld = 3 * h
+                    else:
+                        dq, dk, dv = (torch.empty((B, S, h), dtype=q.dtype, device=q.device)
+                                      for _ in range(3))
+                        ld = h
                     dsum = torch.empty_like(lse)
-                    call("ee_attn_train_bwd", ptr(q), h, ptr(k), h, ptr(v), h, ptr(o), h, ptr(do),
-                         h, ptr(lse), B, S, ctx.nh, ptr(dq), h, ptr(dk), h, ptr(dv), h, ptr(dsum),
-                         stream_ptr())
+                    call("ee_attn_train_bwd", ptr(q), _row_ld(q), ptr(k), _row_ld(k), ptr(v),
+                         _row_ld(v), ptr(o), h, ptr(do), h, ptr(lse), B, S, ctx.nh, ptr(dq), ld,
+                         ptr(dk), ld, ptr(dv), ld, ptr(dsum), stream_ptr())
                     return dq, dk, dv, None
 
             cls._fn = _F

@@ -132,6 +132,82 @@ def test_gemm_stream_k_tail_matches_fp32_and_repeats(kind, T, K, N):
         assert torch.equal(dw1, dw2)
 
 
+@pytest.mark.parametrize("T,K,N,P", [(300, 256, 256, 3), (4096, 2048, 2048, 3),
+                                     (2000, 5120, 5120, 3), (8192, 2048, 2048, 2)])
+def test_stacked_linears_match_fp32(T, K, N, P):
+    """q / k / v as ONE GEMM each way over P adjacent (K, N) weight matrices
+    (ee_linear_fwd_stacked / ee_linear_dgrad_stacked / ee_wgrad_accum_stacked,
+    tc_gemm.cuh stacked operands): Y = X [W_0 | ...] and dX = dY [W_0 | ...]^T
+    within 1e-2 of float32 torch (one bf16 rounding), dW_j += X^T dY_j in
+    float32 within 1e-3 of float64 into P adjacent accumulators; the memory
+    around each block is untouched."""
+    import torch
+    from paper_2312_04916_b200 import _lib
+    from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+    _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(T + K + N + P)
+    x = torch.randn(T, K, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(P, K, N, device="cuda", generator=g) * 0.02).bfloat16()
+    wcat = torch.cat(list(w), dim=1).float()                      # (K, P N)
+    y = torch.empty(T, P * N, device="cuda", dtype=torch.bfloat16)
+    call("ee_linear_fwd_stacked", ptr(x), ptr(w), T, K, N, P, ptr(y), stream_ptr())
+    gy = torch.randn(T, P * N, device="cuda", generator=g).bfloat16()
+    r = torch.randn(T, K, device="cuda", generator=g).bfloat16()
+    gx = torch.empty(T, K, device="cuda", dtype=torch.bfloat16)
+    call("ee_linear_dgrad_stacked", ptr(gy), ptr(w), T, K, N, P, ptr(r), ptr(gx), stream_ptr())
+    guard = 4096
+    acc = torch.randn(P * K * N + 2 * guard, device="cuda", generator=g)
+    acc0 = acc.clone()
+    call("ee_wgrad_accum_stacked", ptr(x), ptr(gy), T, K, N, P, ptr(acc[guard:]), stream_ptr())
+    torch.cuda.synchronize()
+    ry = x.float() @ wcat
+    rgx = gy.float() @ wcat.t() + r.float()
+    assert _rel(y.double().cpu().numpy(), ry.double().cpu().numpy()) < 1e-2
+    assert _rel(gx.double().cpu().numpy(), rgx.double().cpu().numpy()) < 1e-2
+    dw = acc[guard:guard + P * K * N].view(P, K, N).double()
+    for j in range(P):
+        ref = acc0[guard + j * K * N:guard + (j + 1) * K * N].view(K, N).double() + \
+            x.double().t() @ gy[:, j * N:(j + 1) * N].double()
+        assert _rel(dw[j].cpu().numpy(), ref.cpu().numpy()) < 1e-3, j
+    assert torch.equal(acc[:guard], acc0[:guard]) and torch.equal(acc[-guard:], acc0[-guard:])
+
+
+def test_stacked_qkv_training_path_matches_separate():
+    """The training block with q / k / v fused (one stacked GEMM each way, q /
+    k / v and their gradients as column blocks of one buffer read in place by
+    the attention kernels) against the three-GEMM path (EE_STACKED_QKV=0
+    semantics): loss and every float32 gradient sum within bf16 tolerance
+    (2e-2 relative per tensor)."""
+    import torch
+    from paper_2312_04916_b200 import training as TR
+    from paper_2312_04916_b200.model import ExitSpec, ModelConfig, build_model
+    cfg = ModelConfig(2, 512, 4, 1024, 256, exits=(ExitSpec(1, "minimalistic", 0.5),))
+    model = build_model(cfg, 0)
+    tokens = np.random.default_rng(3).integers(0, 1024, size=(2, 257))
+    out = {}
+    for stacked in (True, False):
+        TR._STACKED_QKV = stacked
+        uses0 = TR._STACKED_USES[0]
+        try:
+            tm = TR.TrainModel(model, master_dtype=torch.float32)
+            tm.zero_grad()
+            total, per_exit = TR.weighted_loss(tm, tokens, [1.0] * len(tm.heads))
+            total.backward()
+            TR.join_wgrad()
+            assert TR._STACKED_USES[0] - uses0 == (cfg.num_layers if stacked else 0)
+            torch.cuda.synchronize()
+            out[stacked] = (dict(enumerate(per_exit)),
+                            {k: v.detach().cpu().clone() for k, v in tm.main_grads.items()})
+        finally:
+            TR._STACKED_QKV = True
+    (la, ga), (lb, gb) = out[True], out[False]
+    for k in lb:
+        assert abs(la[k] - lb[k]) <= 1e-2 * abs(lb[k]), k
+    for k in gb:
+        if "wq" in k or "wk" in k or "wv" in k or "wo" in k or "w1" in k:
+            assert _rel(ga[k].numpy().astype(np.float64), gb[k].numpy().astype(np.float64)) < 2e-2, k
+
+
 @pytest.mark.parametrize("n,h", [(37, 264), (4096, 2048), (1000, 5120)])
 def test_rmsnorm_fork_joins_residual_gradient(n, h):
     """`rmsnorm_fork` (ee_rmsnorm_bwd with gres): the residual branch's
