@@ -426,6 +426,7 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
         asm volatile("cp.async.wait_group 1;" ::: "memory");  // this slab's group landed
         __syncthreads();
         EE_TMAX(5);
+        if (li == 0) EE_TMAX(4);
         // scores: thread (position jl = tid & 63, quarter qt = tid >> 6)
         {
             const int jl = tid & (kSlab - 1), qt = tid >> 6;
@@ -523,6 +524,7 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
                 slot[1] = s_l[i];
             }
         }
+        if (li == 0) EE_TMAX(6);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     EE_TMAX(7);

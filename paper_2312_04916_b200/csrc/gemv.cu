@@ -129,11 +129,17 @@ struct TileResidualStats {
 template <int NB>
 constexpr int kGemvStages = NB == 1 ? 4 : 3;
 
-template <int NB, class Epi>
+// single-row passes (most decode passes): one activation row per stage and a
+// 6-deep weight ring in the same ~109 KB (two CTAs per SM), so 6 of a tile's
+// stages stream in before the dependency on the previous kernel resolves
+constexpr int kGemvStages1 = 6;
+
+template <int NB, class Epi, int XR = 0>
 __global__ void __launch_bounds__(tma_gemv::kThreads)
 k_gemv_tma(const bf16* __restrict__ W, int N, int K, const bf16* __restrict__ X, int64_t ldx,
            int m, tma_gemv::RowNorm rn, Epi epi) {
-    tma_gemv::gemv_body<NB, Epi, kGemvStages<NB>>(W, N, K, X, ldx, m, rn, epi);
+    tma_gemv::gemv_body<NB, Epi, XR == 1 ? kGemvStages1 : kGemvStages<NB>, XR>(W, N, K, X, ldx, m,
+                                                                              rn, epi);
 }
 
 // ---- LDG kernels (row-major bf16, fp32 parity mode) ----------------------------
@@ -195,11 +201,11 @@ k_gemv_f32(const float* __restrict__ W, int N, int64_t K, const float* __restric
 }
 
 // ---- launchers ------------------------------------------------------------
-template <int NB, class Epi>
+template <int NB, class Epi, int XR = 0>
 int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K,
                tma_gemv::RowNorm rn, Epi epi, cudaStream_t s) {
-    auto kern = k_gemv_tma<NB, Epi>;
-    const size_t smem = tma_gemv::smem_bytes(NB, kGemvStages<NB>);
+    auto kern = k_gemv_tma<NB, Epi, XR>;
+    const size_t smem = tma_gemv::smem_bytes(NB, XR == 1 ? kGemvStages1 : kGemvStages<NB>, XR);
     static bool configured[16] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -208,7 +214,8 @@ int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, 
         configured[dev & 15] = true;
     }
     const int64_t tiles = (N + tma_gemv::kRows - 1) / tma_gemv::kRows;
-    const int64_t groups = (m + 8 * NB - 1) / (8 * NB);
+    const int64_t rows_per_item = XR ? XR : 8 * NB;
+    const int64_t groups = (m + rows_per_item - 1) / rows_per_item;
     const int64_t items = tiles * groups;
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
     const unsigned grid = (unsigned)std::min<int64_t>(items, (int64_t)ee_sm_count() * per_sm);
@@ -222,6 +229,10 @@ static bool gemv_nb1_only() {  // EE_GEMV_NB1=1: 8-row groups only (A/B runs)
     static const bool v = getenv("EE_GEMV_NB1") && atoi(getenv("EE_GEMV_NB1")) != 0;
     return v;
 }
+static bool gemv_deep1() {  // EE_GEMV_DEEP1=0: single-row passes on the 8-row ring (A/B runs)
+    static const bool v = !getenv("EE_GEMV_DEEP1") || atoi(getenv("EE_GEMV_DEEP1")) != 0;
+    return v;
+}
 
 template <class Epi>
 int run_tma_epi(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K,
@@ -231,6 +242,7 @@ int run_tma_epi(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N,
     // 16-row groups for m > 8 (each weight stage serves 16 rows; a 3-deep
     // ring keeps it at two CTAs per SM).  A row's result does not depend on
     // the group width: the reduction order is per (n, k).
+    if (m == 1 && gemv_deep1()) return run_tma_nb<1, Epi, 1>(X, ldx, m, W, N, K, rn, epi, s);
     if (m <= 8 || gemv_nb1_only()) return run_tma_nb<1>(X, ldx, m, W, N, K, rn, epi, s);
     return run_tma_nb<2>(X, ldx, m, W, N, K, rn, epi, s);
 }

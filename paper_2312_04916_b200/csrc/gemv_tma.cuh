@@ -37,9 +37,14 @@ constexpr int kWBytes = kRows * KS * 2;       // 16 KB weight block per stage
 constexpr int kXPitch = KS * 2 + 16;          // padded activation row
 constexpr int kMaxCols = 16;                  // activation rows per work item (NB = 2)
 
-__host__ __device__ constexpr int stage_bytes(int NB) { return kWBytes + 8 * NB * kXPitch; }
-__host__ inline size_t smem_bytes(int NB, int stages = kStages) {
-    return (size_t)stages * stage_bytes(NB) + 3 * stages * 8 +
+// a stage = the 16 KB weight block + the activation rows it serves (xrows
+// reserved: 8 NB by default; a single-row pass reserves 1 and spends the
+// room on a deeper weight ring)
+__host__ __device__ constexpr int stage_bytes(int NB, int xrows = 0) {
+    return kWBytes + (xrows ? xrows : 8 * NB) * kXPitch;
+}
+__host__ inline size_t smem_bytes(int NB, int stages = kStages, int xrows = 0) {
+    return (size_t)stages * stage_bytes(NB, xrows) + 3 * stages * 8 +
            (size_t)kConsumers * kRows * kMaxCols * 4 + kMaxCols * 4 + 64;
 }
 
@@ -101,13 +106,13 @@ struct RowNorm {
 // cols, inv) and finish(), both called by the 128 consumer threads (inv is
 // the per-column 1/rms or nullptr).  K must be a multiple of 512, W in the
 // tiled layout.
-template <int NB, class Epi, int kStages = tma_gemv::kStages>
+template <int NB, class Epi, int kStages = tma_gemv::kStages, int kXRows = 0>
 __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int K,
                                           const bf16* __restrict__ X, int64_t ldx, int m,
                                           RowNorm rn, Epi& epi) {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr int cols = 8 * NB;
-    constexpr int sbytes = stage_bytes(NB);
+    constexpr int cols = kXRows ? kXRows : 8 * NB;  // rows per work item
+    constexpr int sbytes = stage_bytes(NB, kXRows);
     uint8_t* ring = smem;
     uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + kStages * sbytes);
     uint64_t* xfull = wfull + kStages;

@@ -550,6 +550,27 @@ def _matmul(params, name, x, residual=None):
     return x @ w if residual is None else residual + x @ w
 
 
+def _flat_order(names):
+    """Flat-buffer order of the parameters: as given, except that a block's
+    q / k / v projections are placed back to back (wq, wk, wv) at the first
+    of them, so the stacked GEMMs read them as one operand (stage partitions
+    list their names sorted, which interleaves wo)."""
+    have = set(names)
+    out, done = [], set()
+    for n in names:
+        if n in done:
+            continue
+        prefix, _, leaf = n.rpartition(".")
+        trio = [f"{prefix}.{w}" for w in ("wq", "wk", "wv")]
+        if leaf in ("wq", "wk", "wv") and all(t in have for t in trio):
+            out.extend(trio)
+            done.update(trio)
+        else:
+            out.append(n)
+            done.add(n)
+    return out
+
+
 class TrainModel:
     """Device-resident trainable copy of an `EarlyExitModel`: parameters as
     torch tensors (requires_grad) keyed by the reference names, compute dtype
@@ -578,6 +599,7 @@ class TrainModel:
             a = model.params[name].data
             srcs[name] = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
         if self.mixed:
+            names = _flat_order(names)
             total = sum(srcs[n].numel() for n in names)
             self._flat = torch.empty(total, dtype=self.dtype, device=self.device)
             self._flat_grad = torch.zeros(total, dtype=torch.float32, device=self.device)
