@@ -426,7 +426,6 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
         asm volatile("cp.async.wait_group 1;" ::: "memory");  // this slab's group landed
         __syncthreads();
         EE_TMAX(5);
-        if (li == 0) EE_TMAX(4);
         // scores: thread (position jl = tid & 63, quarter qt = tid >> 6)
         {
             const int jl = tid & (kSlab - 1), qt = tid >> 6;
@@ -457,6 +456,7 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
             }
         }
         __syncthreads();
+        if (li == 0) EE_TMAX(11);
         // slab softmax per row: warp per row, lane owns positions lane, lane + 32
         for (int i = warp; i < mr; i += kSlabWarps) {
             const int p = pos[r0 + i];
@@ -488,6 +488,7 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
             }
         }
         __syncthreads();
+        if (li == 0) EE_TMAX(13);
         // P V: thread (dim d, position half ph), 4 interleaved chains per half
         {
             const int d = tid & (dh - 1), ph = tid >> 7;
@@ -512,6 +513,7 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
             }
         }
         __syncthreads();  // buffer b and sS free from here on
+        if (li == 0) EE_TMAX(15);
         if (li + 2 < nloc) issue(b, rank + (li + 2) * C);
         asm volatile("cp.async.commit_group;" ::: "memory");
         // the slab's partials -> this CTA's shared memory
@@ -524,11 +526,11 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
                 slot[1] = s_l[i];
             }
         }
-        if (li == 0) EE_TMAX(6);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     EE_TMAX(7);
     cl_sync();  // every slab partial of the cluster is in place
+    EE_TMAX(1);
     if (rank == 0) {
         const uint32_t part_u = (uint32_t)__cvta_generic_to_shared(sPart);
         for (int i = warp; i < mr; i += kSlabWarps) {

@@ -133,13 +133,18 @@ constexpr int kGemvStages = NB == 1 ? 4 : 3;
 // 6-deep weight ring in the same ~109 KB (two CTAs per SM), so 6 of a tile's
 // stages stream in before the dependency on the previous kernel resolves
 constexpr int kGemvStages1 = 6;
+// 2-4 rows: four activation rows per stage, a 5-deep ring (~107 KB)
+constexpr int kGemvStages4 = 5;
+template <int NB, int XR>
+constexpr int gemv_stages() {
+    return XR == 1 ? kGemvStages1 : XR == 4 ? kGemvStages4 : kGemvStages<NB>;
+}
 
 template <int NB, class Epi, int XR = 0>
 __global__ void __launch_bounds__(tma_gemv::kThreads)
 k_gemv_tma(const bf16* __restrict__ W, int N, int K, const bf16* __restrict__ X, int64_t ldx,
            int m, tma_gemv::RowNorm rn, Epi epi) {
-    tma_gemv::gemv_body<NB, Epi, XR == 1 ? kGemvStages1 : kGemvStages<NB>, XR>(W, N, K, X, ldx, m,
-                                                                              rn, epi);
+    tma_gemv::gemv_body<NB, Epi, gemv_stages<NB, XR>(), XR>(W, N, K, X, ldx, m, rn, epi);
 }
 
 // ---- LDG kernels (row-major bf16, fp32 parity mode) ----------------------------
@@ -205,7 +210,7 @@ template <int NB, class Epi, int XR = 0>
 int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, int64_t K,
                tma_gemv::RowNorm rn, Epi epi, cudaStream_t s) {
     auto kern = k_gemv_tma<NB, Epi, XR>;
-    const size_t smem = tma_gemv::smem_bytes(NB, XR == 1 ? kGemvStages1 : kGemvStages<NB>, XR);
+    const size_t smem = tma_gemv::smem_bytes(NB, gemv_stages<NB, XR>(), XR);
     static bool configured[16] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -229,6 +234,10 @@ static bool gemv_nb1_only() {  // EE_GEMV_NB1=1: 8-row groups only (A/B runs)
     static const bool v = getenv("EE_GEMV_NB1") && atoi(getenv("EE_GEMV_NB1")) != 0;
     return v;
 }
+static bool gemv_deep4() {  // EE_GEMV_DEEP4=0: 2-4-row passes on the 8-row ring (A/B runs)
+    static const bool v = !getenv("EE_GEMV_DEEP4") || atoi(getenv("EE_GEMV_DEEP4")) != 0;
+    return v;
+}
 static bool gemv_deep1() {  // EE_GEMV_DEEP1=0: single-row passes on the 8-row ring (A/B runs)
     static const bool v = !getenv("EE_GEMV_DEEP1") || atoi(getenv("EE_GEMV_DEEP1")) != 0;
     return v;
@@ -243,6 +252,7 @@ int run_tma_epi(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N,
     // ring keeps it at two CTAs per SM).  A row's result does not depend on
     // the group width: the reduction order is per (n, k).
     if (m == 1 && gemv_deep1()) return run_tma_nb<1, Epi, 1>(X, ldx, m, W, N, K, rn, epi, s);
+    if (m <= 4 && gemv_deep4()) return run_tma_nb<1, Epi, 4>(X, ldx, m, W, N, K, rn, epi, s);
     if (m <= 8 || gemv_nb1_only()) return run_tma_nb<1>(X, ldx, m, W, N, K, rn, epi, s);
     return run_tma_nb<2>(X, ldx, m, W, N, K, rn, epi, s);
 }

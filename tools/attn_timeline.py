@@ -23,7 +23,8 @@ NAMES_G = {0: "qkv entry", 2: "qkv post-wait", 1: "qkv exit", 4: "wo entry", 6: 
            5: "wo exit", 8: "w1 entry", 10: "w1 post-wait", 9: "w1 exit", 12: "w2 entry",
            14: "w2 post-wait", 13: "w2 exit"}
 NAMES_A = {0: "attn entry", 2: "attn post-wait first", 3: "attn post-wait last",
-           4: "attn first slab loaded last", 6: "attn first slab done last",
+           11: "attn slab0 scores last", 13: "attn slab0 softmax last", 15: "attn slab0 PV last",
+           1: "attn cluster barrier last",
            5: "attn K/V loaded last", 7: "attn block merge done last", 9: "attn chunk merge last"}
 
 
