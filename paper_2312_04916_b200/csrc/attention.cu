@@ -367,7 +367,23 @@ __device__ __forceinline__ float4 ld_dsmem4(uint32_t a) {
     return v;
 }
 
-__global__ void __launch_bounds__(kSlabThreads)
+// A/B variants (profiling builds only, -DEE_ATTN_V=n): 0 = rolled PV loop,
+// two-trip fold; 1 = unrolled PV + one-trip fold, <= 85 registers (3 CTAs
+// per SM); 2 = the same, <= 64 registers; 3 = the same, no register cap
+#ifndef EE_ATTN_V
+#define EE_ATTN_V 1
+#endif
+#define EE_PV_UNROLL (EE_ATTN_V != 0)
+#define EE_FOLD_HOIST (EE_ATTN_V != 0)
+#if EE_ATTN_V == 1
+#define EE_SLAB_BOUNDS __launch_bounds__(kSlabThreads, 3)
+#elif EE_ATTN_V == 2
+#define EE_SLAB_BOUNDS __launch_bounds__(kSlabThreads, 4)
+#else
+#define EE_SLAB_BOUNDS __launch_bounds__(kSlabThreads)
+#endif
+
+__global__ void EE_SLAB_BOUNDS
 k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int m,
                const bf16* __restrict__ kc, const bf16* __restrict__ vc, int nh, float scale,
                bf16* __restrict__ out, int g) {
@@ -500,15 +516,35 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
                 const float* pr = sS + i * 4 * kSlab + jb;
                 const bf16* vb = sV + jb * dh + d;
                 float a[4] = {0.f, 0.f, 0.f, 0.f};
-                int jl = 0;
-                for (; jl + 4 <= nj; jl += 4) {
+#if EE_PV_UNROLL
+                if (nj == 32) {
+                    // full half-slab: unrolled, so all 64 shared loads issue
+                    // ahead of the FMA chains (same chains, same order)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        a[u] = fmaf(pr[jl + u], __bfloat162float(vb[(jl + u) * dh]), a[u]);
+                    for (int jh = 0; jh < 32; jh += 16) {
+                        float pv[16], vv[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            pv[j] = pr[jh + j];
+                            vv[j] = __bfloat162float(vb[(jh + j) * dh]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) a[j & 3] = fmaf(pv[j], vv[j], a[j & 3]);
+                    }
+                } else
+#endif
+                {
+                    int jl = 0;
+                    for (; jl + 4 <= nj; jl += 4) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            a[u] = fmaf(pr[jl + u], __bfloat162float(vb[(jl + u) * dh]), a[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 3; ++u)  // tail: at most 3 positions
+                        if (jl + u < nj)
+                            a[u] = fmaf(pr[jl + u], __bfloat162float(vb[(jl + u) * dh]), a[u]);
                 }
-#pragma unroll
-                for (int u = 0; u < 3; ++u)  // tail: at most 3 positions
-                    if (jl + u < nj) a[u] = fmaf(pr[jl + u], __bfloat162float(vb[(jl + u) * dh]), a[u]);
                 sO[(i * 2 + ph) * dh + d] = (a[0] + a[1]) + (a[2] + a[3]);
             }
         }
@@ -546,6 +582,14 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
                 Mc = ld_dsmem(a);
                 Lc = ld_dsmem(a + 4);
             }
+            // the first 8 slabs' o slices travel with (m, l): one DSMEM round
+            // trip instead of two for contexts up to 512
+#if EE_FOLD_HOIST
+            float4 oc0[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                oc0[u] = u < ns ? ld_dsmem4(slot_addr(u) + 16 + 16 * lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
             float MM = Mc;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) MM = fmaxf(MM, __shfl_xor_sync(0xffffffffu, MM, o));
@@ -558,8 +602,14 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
                 float4 oc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
+#if EE_FOLD_HOIST
+                    oc[u] = c0 == 0 ? oc0[u]
+                            : c0 + u < ns ? ld_dsmem4(slot_addr(c0 + u) + 16 + 16 * lane)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#else
                     oc[u] = c0 + u < ns ? ld_dsmem4(slot_addr(c0 + u) + 16 + 16 * lane)
                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const float wc = __shfl_sync(0xffffffffu, w, (c0 + u) & 31);
