@@ -79,6 +79,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Weight stages carry an L2 evict-first hint: every weight byte is read once
+// per pass, so its lines should go first and leave the L2 to the data that
+// is re-read (the KV cache rows of earlier positions, the activation rows).
+// EE_GEMV_EVICT_FIRST=0 (profiling A/B builds) drops the hint.
+#ifndef EE_GEMV_EVICT_FIRST
+#define EE_GEMV_EVICT_FIRST 1
+#endif
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t pol) {
+#if EE_GEMV_EVICT_FIRST
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+        "[%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+#else
+    (void)pol;
+    bulk_g2s(dst, src, bytes, bar);
+#endif
+}
 __device__ __forceinline__ void consumers_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
 }
@@ -147,13 +172,14 @@ __device__ __forceinline__ void gemv_body(const bf16* __restrict__ W, int N, int
         const int my_items =
             items > (int)blockIdx.x ? (items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
         const int total = my_items * nks;
+        const uint64_t pol = policy_evict_first();
         auto issue_w = [&](int q) {
             const int it = (int)blockIdx.x + (q / nks) * (int)gridDim.x;
             const int ks = q % nks;
             const int slot = q % kStages;
             mbar_expect_tx(&wfull[slot], kWBytes);
-            bulk_g2s(ring + slot * sbytes, W + ((int64_t)(it / groups) * nks + ks) * (kRows * KS),
-                     kWBytes, &wfull[slot]);
+            bulk_g2s_hint(ring + slot * sbytes, W + ((int64_t)(it / groups) * nks + ks) * (kRows * KS),
+                          kWBytes, &wfull[slot], pol);
         };
         auto issue_x = [&](int q) {
             const int it = (int)blockIdx.x + (q / nks) * (int)gridDim.x;

@@ -288,6 +288,8 @@ k_gw_reduce(const float* __restrict__ part, int nparts, int h, int accumulate,
     if (j < h) {
         float s4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains, combined in order
         int p = v;
+        // unrolled: 16 partial loads in flight per thread (same per-chain order)
+#pragma unroll 4
         for (; p + 3 * kRedWarps < nparts; p += 4 * kRedWarps) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) s4[k] += part[(int64_t)(p + k * kRedWarps) * h + j];
