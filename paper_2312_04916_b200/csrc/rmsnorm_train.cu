@@ -129,9 +129,6 @@ __device__ __forceinline__ void acc_gw8(float* a, const float* gv, const float* 
     p[0] = u0;
     p[1] = u1;
 }
-#ifndef EE_RMS_PREFETCH
-#define EE_RMS_PREFETCH 1
-#endif
 #ifndef EE_RMS_BWD_MINB
 #define EE_RMS_BWD_MINB 1
 #endif
@@ -157,17 +154,6 @@ k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* 
         const uint4* gr = reinterpret_cast<const uint4*>(g + row * h);
         const uint4* rr = gres ? reinterpret_cast<const uint4*>(gres + row * h) : nullptr;
         uint4* gxr = reinterpret_cast<uint4*>(gx + row * h);
-#if EE_RMS_PREFETCH
-        // the warp's next row streams into L2 while this one is processed
-        if (lane == 0 && i + 1 < rpw && row + 1 < n) {
-            const uint32_t rb = (uint32_t)h * 2;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (row + 1) * h), "r"(rb));
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g + (row + 1) * h), "r"(rb));
-            if (gres)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gres + (row + 1) * h),
-                             "r"(rb));
-        }
-#endif
         const float inv = inv_in[row];
         float dot = 0.f;
         if (held) {
