@@ -620,16 +620,54 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
         cl_sync();  // every slab partial of the cluster is in place
     }
     EE_TMAX(1);
-    if (rank == 0) {
+    if (rank == 0 && push) {
+        // push mode (<= 8 slabs): every slab's partial sits in this CTA's own
+        // shared memory; the same fold arithmetic as the pull path below
         for (int i = warp; i < mr; i += kSlabWarps) {
             const int r = r0 + i;
             const int ns = pos[r] / kSlab + 1;
-            // pull: slab c lives in rank c % C, local index c / C; push: all
-            // slabs in rank 0's own area (ld.shared::cluster on a local address)
+            const float* base = sPart + i * kSlot;  // slab c at base + c * mr * kSlot
+            const int cs = mr * kSlot;
+            float Mc = -INFINITY, Lc = 0.f;
+            if (lane < ns) {
+                Mc = base[lane * cs];
+                Lc = base[lane * cs + 1];
+            }
+            float4 oc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                oc[u] = u < ns ? reinterpret_cast<const float4*>(base + u * cs + 4)[lane]
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            float MM = Mc;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) MM = fmaxf(MM, __shfl_xor_sync(0xffffffffu, MM, o));
+            const float w = lane < ns ? expf(Mc - MM) : 0.f;
+            float LL = Lc * w;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) LL += __shfl_xor_sync(0xffffffffu, LL, o);
+            float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float wc = __shfl_sync(0xffffffffu, w, u);
+                if (u < ns) {
+                    o4.x = fmaf(oc[u].x, wc, o4.x);
+                    o4.y = fmaf(oc[u].y, wc, o4.y);
+                    o4.z = fmaf(oc[u].z, wc, o4.z);
+                    o4.w = fmaf(oc[u].w, wc, o4.w);
+                }
+            }
+            const float inv = 1.f / LL;
+            bf16* orow = out + (int64_t)r * h + hoff + 4 * lane;
+            *reinterpret_cast<__nv_bfloat162*>(orow) = __floats2bfloat162_rn(o4.x * inv, o4.y * inv);
+            *reinterpret_cast<__nv_bfloat162*>(orow + 2) = __floats2bfloat162_rn(o4.z * inv, o4.w * inv);
+        }
+    } else if (rank == 0) {
+        for (int i = warp; i < mr; i += kSlabWarps) {
+            const int r = r0 + i;
+            const int ns = pos[r] / kSlab + 1;
+            // slab c lives in rank c % C, local index c / C
             auto slot_addr = [&](int c) {
-                return push ? part_u + (uint32_t)(((c * mr + i) * kSlot) * 4)
-                            : cl_map(part_u + (uint32_t)((((c / C) * mr + i) * kSlot) * 4),
-                                     (uint32_t)(c % C));
+                return cl_map(part_u + (uint32_t)((((c / C) * mr + i) * kSlot) * 4), (uint32_t)(c % C));
             };
             float Mc = -INFINITY, Lc = 0.f;
             if (lane < ns) {
