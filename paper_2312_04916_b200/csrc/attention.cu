@@ -621,8 +621,8 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
     }
     EE_TMAX(1);
     if (rank == 0 && push) {
-        // push mode (<= 8 slabs): every slab's partial sits in this CTA's own
-        // shared memory; the same fold arithmetic as the pull path below
+        // push mode: every slab's partial sits in this CTA's own shared
+        // memory; the same fold arithmetic as the pull path below
         for (int i = warp; i < mr; i += kSlabWarps) {
             const int r = r0 + i;
             const int ns = pos[r] / kSlab + 1;
@@ -633,11 +633,6 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
                 Mc = base[lane * cs];
                 Lc = base[lane * cs + 1];
             }
-            float4 oc[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                oc[u] = u < ns ? reinterpret_cast<const float4*>(base + u * cs + 4)[lane]
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
             float MM = Mc;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) MM = fmaxf(MM, __shfl_xor_sync(0xffffffffu, MM, o));
@@ -646,14 +641,21 @@ k_attn_slab128(const float* __restrict__ q, const int32_t* __restrict__ pos, int
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) LL += __shfl_xor_sync(0xffffffffu, LL, o);
             float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int c0 = 0; c0 < ns; c0 += 8) {
+                float4 oc[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const float wc = __shfl_sync(0xffffffffu, w, u);
-                if (u < ns) {
-                    o4.x = fmaf(oc[u].x, wc, o4.x);
-                    o4.y = fmaf(oc[u].y, wc, o4.y);
-                    o4.z = fmaf(oc[u].z, wc, o4.z);
-                    o4.w = fmaf(oc[u].w, wc, o4.w);
+                for (int u = 0; u < 8; ++u)
+                    oc[u] = c0 + u < ns ? reinterpret_cast<const float4*>(base + (c0 + u) * cs + 4)[lane]
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const float wc = __shfl_sync(0xffffffffu, w, (c0 + u) & 31);
+                    if (c0 + u < ns) {
+                        o4.x = fmaf(oc[u].x, wc, o4.x);
+                        o4.y = fmaf(oc[u].y, wc, o4.y);
+                        o4.z = fmaf(oc[u].z, wc, o4.z);
+                        o4.w = fmaf(oc[u].w, wc, o4.w);
+                    }
                 }
             }
             const float inv = 1.f / LL;
@@ -734,6 +736,7 @@ size_t attention_ws_bytes(int64_t /*m*/, int64_t nh, int64_t dh, int64_t /*s_max
 }
 
 // EE_ATTN_PUSH=0 (A/B): slab partials always pulled by rank 0 through DSMEM
+constexpr int kPushMaxSlabs = 12;
 static bool attn_push() {
     static const bool v = !getenv("EE_ATTN_PUSH") || atoi(getenv("EE_ATTN_PUSH")) != 0;
     return v;
@@ -778,10 +781,12 @@ int launch_attention(const float* q, int64_t m, const int32_t* pos, int32_t max_
             const int g = (int)(want < 1 ? 1 : (want > kSlabRows ? kSlabRows : want));
             const int groups = (int)((mr + g - 1) / g);
             // push mode (partials stored straight into rank 0, no cluster
-            // barriers at the end) for short contexts (<= 8 slabs: measured
-            // 0.7% faster per pass at ctx 192-320, slower at ctx >= 1024)
+            // barriers at the end) up to 12 slabs: per pass -1.5..-2.3% at
+            // ctx 64-320, -3..-6% at ctx 640, but +1.4..+6% at ctx 1024 and
+            // +2.6% at 2000 (1 row), where pull mode stays
+            // (profiles/r2_attn_push_ab.txt)
             const int gr = (int)(mr < g ? mr : g);
-            const bool push = attn_push() && ns <= kMaxCluster &&
+            const bool push = attn_push() && ns <= kPushMaxSlabs &&
                               slab_smem(gr, ns) <= slab_smem(kSlabRows, kLocalSlabs);
             const int local = push ? ns : (ns + C - 1) / C;
             static bool configured[16] = {};
