@@ -66,3 +66,50 @@ def test_attention_matches_oracle_all_context_lengths(dtype, nh, dh):
         assert np.array_equal(one[0], out[r]), pos[r]
     five = _run(q[3:8], pos[3:8], kc, vc, nh, dt)
     assert np.array_equal(five, out[3:8])
+
+
+_PUSH_PROBE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2312_04916_b200 import _lib
+from paper_2312_04916_b200._lib import call, ptr, stream_ptr
+lib = _lib.load()
+rng = np.random.default_rng(11)
+nh, dh, smax = 32, 128, 2048
+h = nh * dh
+kc = torch.tensor(rng.normal(size=(smax, h)), dtype=torch.bfloat16, device="cuda")
+vc = torch.tensor(rng.normal(size=(smax, h)), dtype=torch.bfloat16, device="cuda")
+outs = []
+for pos in ([0], [63], [191], [320, 321, 322, 323, 324], [700], [767, 760]):
+    m = len(pos)
+    q = torch.tensor(rng.normal(size=(m, h)) * 0.3, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(lib.ee_workspace_bytes(_lib.EE_OP_ATTENTION, m, h, 0, nh, smax),
+                     dtype=torch.uint8, device="cuda")
+    pd = torch.tensor(pos, dtype=torch.int32, device="cuda")
+    out = torch.empty((m, h), dtype=torch.bfloat16, device="cuda")
+    call("ee_decode_attention", ptr(q), m, ptr(pd), int(max(pos)), ptr(kc), ptr(vc), nh, dh,
+         _lib.EE_BF16, ptr(out), ptr(ws), ws.numel(), stream_ptr())
+    torch.cuda.synchronize()
+    outs.append(out.view(torch.int16).cpu().numpy())
+np.save(sys.argv[2], np.concatenate([o.ravel() for o in outs]))
+"""
+
+
+def test_attention_push_and_pull_fold_bitwise_equal(tmp_path):
+    """The slab kernel's two fold modes -- partials pushed into rank 0's
+    shared memory (<= 12 slabs, default) and pulled by rank 0 through DSMEM
+    (EE_ATTN_PUSH=0) -- give identical bits (same fold arithmetic), so the
+    mode a launch picks never changes a row's result."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for push in ("1", "0"):
+        out = tmp_path / f"o{push}.npy"
+        env = dict(os.environ, EE_ATTN_PUSH=push)
+        subprocess.run([sys.executable, "-c", _PUSH_PROBE, root, str(out)], check=True, env=env,
+                       timeout=600)
+        res[push] = np.load(out)
+    assert res["1"].shape == res["0"].shape
+    assert np.array_equal(res["1"], res["0"])
