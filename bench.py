@@ -423,7 +423,7 @@ def bench_pipeline_stages(model, prompt, local, new_tokens=64, thresholds=(1.0, 
     return out
 
 
-def bench_train_step(local, steps=3, warmup=2, M=4, mb=4, seq=2048, cfg=None, workload=None):
+def bench_train_step(local, steps=3, warmup=4, M=4, mb=4, seq=2048, cfg=None, workload=None):
     """One training step: by default C2 (BASELINE configs[1]): EE-GPT 1.3B
     (L=24, h=2048, 16 heads, V=50304, tied exits at 6 (w 0.25) / 12 (w 0.5)),
     global batch 16 x 2048 as M=4 microbatches of 4 sequences (the

@@ -129,15 +129,18 @@ __device__ __forceinline__ void acc_gw8(float* a, const float* gv, const float* 
     p[0] = u0;
     p[1] = u1;
 }
+#ifndef EE_RMS_SW
+#define EE_RMS_SW 1
+#endif
 #ifndef EE_RMS_BWD_MINB
 #define EE_RMS_BWD_MINB 1
 #endif
 __global__ void __launch_bounds__(kBwdThreads, EE_RMS_BWD_MINB)
-k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* __restrict__ inv_in,
+k_rms_bwd(const bf16* __restrict__ x, const float* w, const float* __restrict__ inv_in,
           const bf16* __restrict__ g, const bf16* __restrict__ gres, int64_t n, int h, int rpw,
           bf16* __restrict__ gx, float* __restrict__ gw_part) {
     extern __shared__ float4 acc_raw[];
-    float* acc = reinterpret_cast<float*>(acc_raw);  // [kBwdWarps][h]
+    float* acc = reinterpret_cast<float*>(acc_raw);  // [kBwdWarps][h], then w (h)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nvec = h / 8;
     float* my = acc + (size_t)warp * h;
@@ -145,6 +148,15 @@ k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* 
         reinterpret_cast<float4*>(my)[2 * c] = make_float4(0.f, 0.f, 0.f, 0.f);
         reinterpret_cast<float4*>(my)[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+#if EE_RMS_SW
+    // the norm weight once per CTA in shared memory: the row loops read it
+    // with shared loads instead of a dependent global load per chunk
+    float* sw = acc + (size_t)kBwdWarps * h;
+    for (int j4 = threadIdx.x; j4 < h / 4; j4 += kBwdThreads)
+        reinterpret_cast<float4*>(sw)[j4] = reinterpret_cast<const float4*>(w)[j4];
+    __syncthreads();
+    w = sw;
+#endif
     const bool held = nvec <= 32 * kHeld;
     const int64_t r0 = ((int64_t)blockIdx.x * kBwdWarps + warp) * rpw;
     for (int i = 0; i < rpw; ++i) {
@@ -275,9 +287,12 @@ k_rms_bwd(const bf16* __restrict__ x, const float* __restrict__ w, const float* 
 }
 
 // gw_j (+)= sum over the CTA partials in CTA order (deterministic): a CTA per
-// 32 columns, warp v sums partials v, v + 8, v + 16, ... (lane = column), then
-// the 8 warp sums are added in warp order
-constexpr int kRedWarps = 8;
+// 32 columns, warp v sums partials v, v + W, v + 2W, ... (lane = column; W =
+// kRedWarps), then the W warp sums are added in warp order
+#ifndef EE_RED_WARPS
+#define EE_RED_WARPS 32
+#endif
+constexpr int kRedWarps = EE_RED_WARPS;  // 32: ~9 partials per warp (latency-bound sums)
 __global__ void __launch_bounds__(kRedWarps * 32)
 k_gw_reduce(const float* __restrict__ part, int nparts, int h, int accumulate,
             float* __restrict__ gw) {
@@ -317,7 +332,7 @@ struct BwdGrid {
 };
 BwdGrid bwd_grid(int64_t n, int64_t h) {
     BwdGrid gr;
-    gr.smem = (size_t)kBwdWarps * h * sizeof(float);
+    gr.smem = (size_t)(kBwdWarps + (EE_RMS_SW ? 1 : 0)) * h * sizeof(float);
     static int64_t cached_h = -1;  // occupancy of the last width asked for
     static int cached_per_sm = 1;
     int per_sm = cached_per_sm;
@@ -367,7 +382,7 @@ extern "C" int ee_rmsnorm_bwd(const void* x, const float* w, const float* inv_rm
                (long long)h);
     EE_REQUIRE(ws_bytes >= rmsnorm_train_ws_bytes(n, h), EE_ESHAPE,
                "rmsnorm_bwd: workspace too small");
-    EE_REQUIRE((size_t)kBwdWarps * h * sizeof(float) <= 227 * 1024, EE_ESHAPE,
+    EE_REQUIRE((size_t)(kBwdWarps + 1) * h * sizeof(float) <= 227 * 1024, EE_ESHAPE,
                "rmsnorm_bwd: h too large (%lld)", (long long)h);
     cudaStream_t s = as_stream(stream);
     int nparts = 0;

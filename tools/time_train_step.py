@@ -21,7 +21,7 @@ def c2_config():
                        tie_embeddings=True)
 
 
-def train_step_bench(M=8, mb=2, seq=2048, steps=3, warmup=2, stages=1):
+def train_step_bench(M=8, mb=2, seq=2048, steps=3, warmup=int(os.environ.get("TS_WARMUP", "4")), stages=1):
     cfg = c2_config()
     master = build_model(cfg, 0, init="device", dtype=torch.float32)
     opt = Adam(3e-4)
