@@ -223,7 +223,20 @@ int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, 
     const int64_t groups = (m + rows_per_item - 1) / rows_per_item;
     const int64_t items = tiles * groups;
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (226 * 1024) / (smem + 1024)));
-    const unsigned grid = (unsigned)std::min<int64_t>(items, (int64_t)ee_sm_count() * per_sm);
+    const int64_t slots = (int64_t)ee_sm_count() * per_sm;
+    int64_t g = std::min<int64_t>(items, slots);
+    // EE_GEMV_BALANCE (A/B): a grid that divides the items evenly (e.g. 768
+    // QKV tiles on 256 CTAs x 3 instead of 296 CTAs x 2.6) when one exists
+    // within 5/6 of the slots
+    static const bool balance = getenv("EE_GEMV_BALANCE") && atoi(getenv("EE_GEMV_BALANCE")) != 0;
+    if (balance && items > slots) {
+        for (int64_t c = slots; c >= slots * 5 / 6; --c)
+            if (items % c == 0) {
+                g = c;
+                break;
+            }
+    }
+    const unsigned grid = (unsigned)g;
     cudaError_t e = launch_ex(kern, dim3(grid), dim3(tma_gemv::kThreads), smem, s,
                               (const bf16*)W, (int)N, (int)K, X, ldx, (int)m, rn, epi);
     if (e != cudaSuccess) return ee_fail(EE_ECUDA, "gemv_tma launch: %s", cudaGetErrorString(e));
