@@ -227,10 +227,12 @@ int run_tma_nb(const bf16* X, int64_t ldx, int64_t m, const void* W, int64_t N, 
     int64_t g = std::min<int64_t>(items, slots);
     // a grid that divides the items evenly (e.g. 768 QKV tiles on 256 CTAs x
     // 3 instead of 296 CTAs x 2.6) when one exists within 5/6 of the slots:
-    // no CTA runs a last item alone (5-row pass -2.4%, 1 row unchanged;
-    // EE_GEMV_BALANCE=0 for A/B).  Reduction orders do not depend on the grid.
+    // no CTA runs a last item alone (C3 5-row pass -2.4%, 1 row unchanged;
+    // only up to 4 items per CTA: the C5 W1, 1792 tiles on 256 x 7, measured
+    // slower than 296 x 6.05; EE_GEMV_BALANCE=0 for A/B).  Reduction orders
+    // do not depend on the grid.
     static const bool balance = !getenv("EE_GEMV_BALANCE") || atoi(getenv("EE_GEMV_BALANCE")) != 0;
-    if (balance && items > slots) {
+    if (balance && items > slots && items <= 4 * slots) {  // few items per CTA: the tail matters
         for (int64_t c = slots; c >= slots * 5 / 6; --c)
             if (items % c == 0) {
                 g = c;
